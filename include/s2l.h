@@ -1,0 +1,219 @@
+/*
+ * s2l.h — C ABI of libs2l, the B200 (sm_100a) streaming-prefill KV / attention library
+ * for STREAM2LLM (arXiv 2604.16395).  Citations: P:Lnnn = /root/reference/PAPER.md line,
+ * S:Lnnn = SPEC.md line, Zn = a reading recorded in DESIGN.md §Readings.
+ *
+ * What the library holds ("GPU and CPU block pools"):
+ *   - a GPU block pool (caller-owned device memory) and a CPU block pool (caller-owned
+ *     PINNED host memory), both laid out as
+ *         pool[block][layer][2 (0=K,1=V)][kv_head][slot (0..k-1)][head_dim]   bf16
+ *     so one block is contiguous across layers and occupies
+ *         M_block = 2 * L * k * h_kv * d * 2 bytes   (= P:L73 with d_model*h_kv/h = h_kv*d);
+ *   - a request table: per request its input tokens, num_computed_tokens (nc), tier
+ *     (GPU or CPU), ordered block ids on that tier, total_tokens_invalidated;
+ *   - a device block table [max_requests][max_blocks_per_request] int32 (library-owned)
+ *     read by the kernels; block j of a request holds positions [j*k, j*k+k).
+ *
+ * Allocation (Z9): every allocation takes the LOWEST free ids of the tier, ascending;
+ * requests/items of one call are served in call order.  Every call that can fail is
+ * all-or-nothing: arguments and capacity are validated before any state changes.
+ *
+ * Streams: `compute_stream` runs append/patch/attention kernels; `copy_stream` runs swap
+ * copies (cudaStream_t handles passed as void*; NULL = legacy default stream).  The library
+ * inserts the event waits that make reuse of swapped / freed blocks safe.
+ * Pointer arguments to device/pinned buffers must stay valid until the work enqueued by the
+ * call has completed on its stream (stream-ordered semantics).  Host token arrays and item
+ * arrays are copied before the call returns.
+ *
+ * Errors: every function returns an s2l_status.  State/argument errors are detected before
+ * any mutation.  A CUDA error is reported as S2L_E_CUDA and is sticky for the context.
+ * s2l_last_error() returns a thread-local message for the most recent failure.
+ * No C++ exception crosses the ABI.  One host thread per context at a time.
+ */
+#ifndef S2L_H_
+#define S2L_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct s2l_ctx s2l_ctx;
+typedef int32_t s2l_status;
+
+enum {
+  S2L_OK = 0,
+  S2L_E_INVAL = -1,          /* bad argument / geometry / duplicate request in one call    */
+  S2L_E_NO_GPU_BLOCKS = -2,  /* GPU pool cannot satisfy the whole call    */
+  S2L_E_NO_CPU_BLOCKS = -3,  /* CPU pool cannot satisfy the whole swap-out        */
+  S2L_E_NO_REQUEST = -4,     /* unknown request id                                          */
+  S2L_E_STATE = -5,          /* wrong tier for the call / request already exists            */
+  S2L_E_CUDA = -6,           /* CUDA runtime / driver failure (sticky)                      */
+  S2L_E_CAPACITY = -7        /* request table full (max_requests)                           */
+};
+
+enum { S2L_TIER_GPU = 0, S2L_TIER_CPU = 1 };
+
+/* Bookkeeping is identical in every context; the attention kernel variant is chosen per
+ * call: the tcgen05/TMEM/TMA tensor-core kernel when head_dim == 128 and 16 <= block_size
+ * <= 128, otherwise a CUDA-core kernel (e.g. C1: head_dim 16, block 4).  Both are sm_100a
+ * code in this library; there is no CPU path. */
+typedef struct s2l_config {
+  int32_t num_layers;             /* L: layers held by the pools                            */
+  int32_t num_q_heads;            /* h                                            */
+  int32_t num_kv_heads;           /* h_kv; must divide num_q_heads (GQA, Z2)         */
+  int32_t head_dim;               /* d_h = d/h; multiple of 8, <= 256                       */
+  int32_t block_size;             /* k tokens per block; power of two, 1..256       */
+  int32_t num_gpu_blocks;         /* blocks in the GPU pool                                 */
+  int32_t num_cpu_blocks;         /* blocks in the CPU pool (may be 0: no swapping)         */
+  int32_t max_requests;           /* live requests at once                                  */
+  int32_t max_blocks_per_request; /* columns of the device block table                      */
+  int32_t lcp_block_aligned;      /* 0 = token-granular LCP (default, Z4);
+                                     1 = round the kept prefix down to a block     */
+} s2l_config;
+
+/* One request of an s2l_append_chunk call. */
+typedef struct s2l_append_item {
+  int64_t req_id;
+  const int32_t* tokens;  /* host; n_tokens ids appended to the input first (Append event,
+                             LCP = old length); NULL when n_tokens == 0             */
+  int64_t n_tokens;
+  int64_t n_kv;           /* K/V rows written for positions [nc, nc+n_kv); 0..pending     */
+  int64_t kv_row;         /* first row of this item in the k/v token dimension            */
+} s2l_append_item;
+
+/* One request of an s2l_prefill_batch call. */
+typedef struct s2l_prefill_item {
+  int64_t req_id;
+  int64_t q_pos;          /* absolute position of the first query row (normally nc - n_q) */
+  int64_t n_q;            /* >= 1 query rows; q_pos + n_q <= nc                            */
+  int64_t q_row;          /* first row of this item in q / o / lse                         */
+} s2l_prefill_item;
+
+typedef struct s2l_req_info {
+  int64_t num_tokens;               /* len(input)                                         */
+  int64_t num_computed;             /* nc = num_computed_tokens                  */
+  int64_t total_tokens_invalidated;
+  int32_t tier;                     /* S2L_TIER_GPU / S2L_TIER_CPU                        */
+  int32_t num_blocks;               /* blocks held on that tier = ceil(nc / k)            */
+} s2l_req_info;
+
+/* M_block = 2*L*k*h_kv*d*2 bytes.  Returns -1 for an invalid config. */
+int64_t s2l_block_bytes(const s2l_config* cfg);
+
+/* Create a context bound to the current CUDA device.
+ *   gpu_pool        device pointer, num_gpu_blocks*M_block bytes, 256-B aligned
+ *   cpu_pool_pinned page-locked host pointer, num_cpu_blocks*M_block bytes (NULL iff
+ *                   num_cpu_blocks == 0)
+ *   compute_stream, copy_stream: cudaStream_t as void*.
+ * Both pools are zero-filled (device: cudaMemsetAsync on compute_stream; host: memset) so
+ * never-written slots are finite.  The library allocates its own device block table and a
+ * small pinned + device staging ring.  Ownership of the pools stays with the caller and
+ * they must outlive the context.  Errors: S2L_E_INVAL (geometry), S2L_E_CUDA. */
+s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinned,
+                      void* compute_stream, void* copy_stream, s2l_ctx** out);
+
+/* Bookkeeping-only context for host-logic tests (no device, no pools).  Every call runs its
+ * validation and state machine exactly as in a device context; calls that would move data
+ * require their data pointers to be NULL (append: k = v = NULL) and s2l_prefill_batch returns
+ * S2L_E_STATE.  It never computes attention or moves bytes. */
+s2l_status s2l_create_host_only(const s2l_config* cfg, s2l_ctx** out);
+
+/* Synchronises both streams, frees library-owned memory.  NULL is a no-op. */
+void s2l_destroy(s2l_ctx* ctx);
+
+/* NewStream: input := tokens (copied), nc := 0, GPU tier, no blocks.
+ * S2L_E_STATE if req_id is live, S2L_E_CAPACITY if max_requests are live. */
+s2l_status s2l_new_request(s2l_ctx* ctx, int64_t req_id, const int32_t* tokens, int64_t n);
+
+/* Request finished: frees its blocks on its tier and forgets the id. */
+s2l_status s2l_release_request(s2l_ctx* ctx, int64_t req_id);
+
+/* Recomputation preemption: frees all its blocks on its tier, nc := 0,
+ * tier := GPU; the input is kept.  total_tokens_invalidated is unchanged. */
+s2l_status s2l_preempt_recompute(s2l_ctx* ctx, int64_t req_id);
+
+/* Append (a3): for each item, append its tokens to the input, allocate
+ * ceil((nc+n_kv)/k) - held blocks (lowest free ids, P:L69 on-demand from the free pool),
+ * write K/V of positions [nc, nc+n_kv) into slot (table[pos/k], pos%k) of every layer,
+ * nc += n_kv.
+ *   k, v: device, [num_layers][kv_rows][h_kv][d] bf16, item i's rows at
+ *         [kv_row_i, kv_row_i + n_kv_i); kv_rows = token rows per layer.
+ * Validation (first failing item in call order wins; capacity checked last):
+ *   unknown id -> E_NO_REQUEST; id repeated in the call -> E_INVAL; CPU tier -> E_STATE;
+ *   n_tokens/n_kv/kv_row < 0, kv_row+n_kv > kv_rows, n_kv > len(input)+n_tokens-nc, or
+ *   ceil((nc+n_kv)/k) > max_blocks_per_request -> E_INVAL;
+ *   total new blocks > free GPU blocks -> E_NO_GPU_BLOCKS.
+ * On any error nothing changes (all-or-nothing). */
+s2l_status s2l_append_chunk(s2l_ctx* ctx, int32_t n_items, const s2l_append_item* items,
+                            const void* k, const void* v, int64_t kv_rows);
+
+/* Update event (a1 + a2).  p = LCP(input, new_tokens); b = min(p, nc)
+ * (Z5; lcp_block_aligned: b = floor(b/k)*k); keep ceil(b/k) blocks (Z4) and
+ * return the rest to the pool of the tier holding them (GPU, or CPU when swapped);
+ * nc := b; input := new_tokens; invalidated = nc_old - b is added to
+ * total_tokens_invalidated.  A swapped request left with no blocks becomes a
+ * GPU-tier request.  Host-only: the device block-table tail reset is applied by the
+ * next kernel launch on compute_stream.  lcp_out / tokens_invalidated_out may be NULL. */
+s2l_status s2l_invalidate_lcp(s2l_ctx* ctx, int64_t req_id, const int32_t* new_tokens,
+                              int64_t new_len, int64_t* lcp_out, int64_t* tokens_invalidated_out);
+
+/* Chunked-prefill attention (a4): for item i, query row t (0 <= t < n_q) at
+ * absolute position q_pos+t and q head h,
+ *   o[q_row+t][h] = softmax_j( q·K_j / sqrt(d) ) · V   over keys j = 0 .. q_pos+t of kv head
+ *   g(h) = floor(h / (h/h_kv)) (Z2), K/V read from layer `layer` of the GPU pool through the
+ *   request's block table.  lse (optional) = natural-log log-sum-exp of the scaled scores.
+ *   q, o: device [q_rows][h][d] bf16; lse: device [q_rows][h] fp32 or NULL.
+ * Requirements: GPU tier, n_q >= 1, q_pos >= 0, q_pos + n_q <= nc, q_row + n_q <= q_rows,
+ * 0 <= layer < L (else E_INVAL / E_STATE / E_NO_REQUEST).  Read-only on the request state;
+ * waits for any swap-in of the listed requests.  fp32 accumulation, bf16 P, bf16 output. */
+s2l_status s2l_prefill_batch(s2l_ctx* ctx, int32_t layer, int32_t n_items,
+                             const s2l_prefill_item* items, const void* q, void* o, float* lse,
+                             int64_t q_rows);
+
+/* Swap-out (a5): all-or-nothing over the listed requests (all GPU tier, no
+ * duplicates): allocate |blocks| CPU ids per request (lowest free), copy every block GPU ->
+ * CPU in order on copy_stream (whole blocks, Z12), free the GPU ids, tier := CPU, nc kept.
+ * bytes_out = total blocks * M_block.  E_NO_CPU_BLOCKS if the CPU pool is short. */
+s2l_status s2l_swap_out(s2l_ctx* ctx, int32_t n_reqs, const int64_t* req_ids, int64_t* bytes_out);
+
+/* Swap-in (a6, "symmetric", P:L184 prefix only after an update): mirror of
+ * s2l_swap_out CPU -> GPU.  E_NO_GPU_BLOCKS if the GPU pool is short. */
+s2l_status s2l_swap_in(s2l_ctx* ctx, int32_t n_reqs, const int64_t* req_ids, int64_t* bytes_out);
+
+s2l_status s2l_query(s2l_ctx* ctx, int64_t req_id, s2l_req_info* out);
+
+/* Copies the request's block ids (on its current tier) into ids_out[0..cap); *n_out = count
+ * (may exceed cap; then only cap ids are written). */
+s2l_status s2l_block_table(s2l_ctx* ctx, int64_t req_id, int32_t* ids_out, int64_t cap,
+                           int64_t* n_out);
+
+/* Free block counts of both tiers. */
+s2l_status s2l_free_blocks(s2l_ctx* ctx, int64_t* gpu_free, int64_t* cpu_free);
+
+/* Blocks until all work enqueued by this context on both streams has completed. */
+s2l_status s2l_sync(s2l_ctx* ctx);
+
+/* Number of kernels this context has launched since creation (evidence counter). */
+int64_t s2l_kernel_launches(s2l_ctx* ctx);
+
+/* Per-kernel device timing (for the roofline in bench.py).  s2l_set_timing(ctx, 1) clears
+ * and starts a window: every attention / append kernel launch is then bracketed by CUDA
+ * events on compute_stream.  s2l_timing_read synchronises compute_stream and returns the
+ * summed event durations (ms) and launch counts of the window.  Timing off by default. */
+s2l_status s2l_set_timing(s2l_ctx* ctx, int32_t enable);
+s2l_status s2l_timing_read(s2l_ctx* ctx, double* attn_ms, int64_t* attn_launches,
+                           double* append_ms, int64_t* append_launches);
+
+/* Thread-local description of the most recent error ("" if none). */
+const char* s2l_last_error(void);
+
+/* Library build string (arch, version). */
+const char* s2l_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* S2L_H_ */

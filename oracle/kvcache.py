@@ -160,6 +160,8 @@ class OracleKV:
             n_tok = 0 if toks is None else len(toks)
             if n_kv < 0 or kv_row < 0:
                 return E_INVAL
+            if n_kv > 0 and kv_row + n_kv > k_rows.shape[1]:
+                return E_INVAL
             if n_kv > len(r.input) + n_tok - r.nc:
                 return E_INVAL
             nb = blocks_needed(r.nc + n_kv, self.k)

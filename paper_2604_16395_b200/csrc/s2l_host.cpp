@@ -1,0 +1,838 @@
+// libs2l host runtime: request table, two-tier block allocator, LCP, staging ring, stream /
+// event hazards, swap copies, and the extern "C" ABI declared in include/s2l.h.
+//
+// Every operation follows the paper passage cited at the ABI declaration; the bookkeeping
+// is the state machine of SURVEY §8.2 c.2 (and is checked bit-exact against oracle/ by
+// tests/test_host_bookkeeping.py).  No attention / K/V arithmetic happens on the host.
+#include "s2l.h"
+#include "s2l_internal.h"
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+s2l_status fail(s2l_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---- lowest-free-id allocator (reading Z9) ----------------------------------------------
+// A bitset of free ids (bit = 1 -> free) plus a hint to the lowest word that may hold a
+// free id.  take_lowest(n) returns the n smallest free ids in ascending order.
+class Allocator {
+ public:
+  void init(int64_t n) {
+    n_ = n;
+    bits_.assign((size_t)ceil_div(n, 64), ~0ull);
+    if (n % 64) bits_.back() = (1ull << (n % 64)) - 1;
+    if (n == 0) bits_.clear();
+    free_ = n;
+    hint_ = 0;
+  }
+  int64_t free_count() const { return free_; }
+  // Caller checks free_count() >= n first.
+  void take_lowest(int64_t n, std::vector<int32_t>& out) {
+    size_t w = hint_;
+    while (n > 0) {
+      while (bits_[w] == 0) ++w;
+      uint64_t word = bits_[w];
+      while (word && n > 0) {
+        int b = __builtin_ctzll(word);
+        out.push_back((int32_t)(w * 64 + b));
+        word &= word - 1;
+        --n;
+        --free_;
+      }
+      bits_[w] = word;
+    }
+    hint_ = w;
+  }
+  void give_back(const int32_t* ids, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) {
+      size_t w = (size_t)ids[i] >> 6;
+      bits_[w] |= 1ull << (ids[i] & 63);
+      if (w < hint_) hint_ = w;
+    }
+    free_ += n;
+  }
+
+ private:
+  std::vector<uint64_t> bits_;
+  int64_t n_ = 0, free_ = 0;
+  size_t hint_ = 0;
+};
+
+struct Request {
+  int64_t id = 0;
+  std::vector<int32_t> input;
+  int64_t nc = 0;
+  int32_t tier = S2L_TIER_GPU;
+  std::vector<int32_t> blocks;
+  int64_t tti = 0;
+  int32_t slot = -1;
+  cudaEvent_t swap_in_event = nullptr;  // pending H2D of its blocks (on copy stream)
+  bool swap_in_pending = false;
+};
+
+// Pinned-host + device staging ring.  Slot s is reused only after its event (recorded after
+// the kernels that read it) has completed, which protects both copies.
+struct StagingRing {
+  static constexpr int kSlots = 4;
+  void* host[kSlots] = {};
+  void* dev[kSlots] = {};
+  size_t cap[kSlots] = {};
+  cudaEvent_t ev[kSlots] = {};
+  bool used[kSlots] = {};
+  int next = 0;
+};
+
+}  // namespace
+
+struct s2l_ctx {
+  s2l_config cfg{};
+  bool host_only = true;
+  int64_t m_block = 0;
+  void* gpu_pool = nullptr;
+  void* cpu_pool = nullptr;
+  cudaStream_t compute = nullptr;
+  cudaStream_t copy = nullptr;
+  bool own_copy_stream = false;
+  int32_t* d_table = nullptr;          // [max_requests][max_blocks] int32
+  std::vector<int32_t> h_table;        // host mirror
+  std::vector<int32_t> dirty;          // table entries whose host value must reach the device
+  std::vector<uint8_t> dirty_flag;
+  Allocator alloc[2];
+  std::vector<Request> slots;
+  std::vector<int32_t> free_slots;     // stack; lowest slot on top
+  std::unordered_map<int64_t, int32_t> by_id;
+  StagingRing ring;
+  s2l_status sticky = S2L_OK;
+  int64_t launches = 0;
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> attn_ev, append_ev, ev_pool;
+  // event that marks the end of the most recent swap-out copy of GPU blocks; GPU blocks freed
+  // by a swap-out may only be rewritten by the compute stream after it
+  cudaEvent_t swap_out_done = nullptr;
+  bool swap_out_pending = false;
+  unsigned char tmap_kv[128] __attribute__((aligned(64)));
+  bool tc_ok = false;
+  s2l::Geometry geo{};
+};
+
+namespace {
+
+bool cuda_ok(s2l_ctx* c, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return true;
+  c->sticky = S2L_E_CUDA;
+  fail(S2L_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return false;
+}
+#define CK(call)                                   \
+  do {                                             \
+    if (!cuda_ok(c, (call), #call)) return S2L_E_CUDA; \
+  } while (0)
+
+s2l_status check_config(const s2l_config* cfg) {
+  if (!cfg) return fail(S2L_E_INVAL, "config is NULL");
+  const s2l_config& g = *cfg;
+  if (g.num_layers < 1 || g.num_q_heads < 1 || g.num_kv_heads < 1 ||
+      g.num_q_heads % g.num_kv_heads)
+    return fail(S2L_E_INVAL, "bad head geometry (L=%d h=%d h_kv=%d)", g.num_layers,
+                g.num_q_heads, g.num_kv_heads);
+  if (g.head_dim < 8 || g.head_dim > 256 || g.head_dim % 8)
+    return fail(S2L_E_INVAL, "head_dim %d must be a multiple of 8 in [8, 256]", g.head_dim);
+  if (g.block_size < 1 || g.block_size > 256 || (g.block_size & (g.block_size - 1)))
+    return fail(S2L_E_INVAL, "block_size %d must be a power of two <= 256", g.block_size);
+  if (g.num_gpu_blocks < 0 || g.num_cpu_blocks < 0 || g.max_requests < 1 ||
+      g.max_blocks_per_request < 1)
+    return fail(S2L_E_INVAL, "bad pool / table sizes");
+  if (g.lcp_block_aligned != 0 && g.lcp_block_aligned != 1)
+    return fail(S2L_E_INVAL, "lcp_block_aligned must be 0 or 1");
+  return S2L_OK;
+}
+
+s2l_status init_common(s2l_ctx* c, const s2l_config* cfg) {
+  c->cfg = *cfg;
+  c->m_block = s2l_block_bytes(cfg);
+  c->alloc[S2L_TIER_GPU].init(cfg->num_gpu_blocks);
+  c->alloc[S2L_TIER_CPU].init(cfg->num_cpu_blocks);
+  c->slots.resize(cfg->max_requests);
+  c->free_slots.reserve(cfg->max_requests);
+  for (int32_t s = cfg->max_requests - 1; s >= 0; --s) c->free_slots.push_back(s);
+  c->h_table.assign((size_t)cfg->max_requests * cfg->max_blocks_per_request, -1);
+  c->dirty_flag.assign(c->h_table.size(), 0);
+  c->geo = s2l::Geometry{cfg->num_layers, cfg->num_q_heads, cfg->num_kv_heads, cfg->head_dim,
+                         cfg->block_size, cfg->max_blocks_per_request};
+  return S2L_OK;
+}
+
+Request* find(s2l_ctx* c, int64_t id) {
+  auto it = c->by_id.find(id);
+  return it == c->by_id.end() ? nullptr : &c->slots[it->second];
+}
+
+void set_table(s2l_ctx* c, int32_t slot, int64_t col, int32_t value) {
+  size_t idx = (size_t)slot * c->cfg.max_blocks_per_request + (size_t)col;
+  c->h_table[idx] = value;
+  if (!c->dirty_flag[idx]) {
+    c->dirty_flag[idx] = 1;
+    c->dirty.push_back((int32_t)idx);
+  }
+}
+
+// Frees blocks [keep, end) of the request on its tier and resets those table entries.
+void free_tail(s2l_ctx* c, Request* r, size_t keep) {
+  if (keep >= r->blocks.size()) return;
+  if (r->tier == S2L_TIER_GPU && r->swap_in_pending && !c->host_only) {
+    // GPU blocks still being filled by a swap-in must not be rewritten by later compute work.
+    if (cudaStreamWaitEvent(c->compute, r->swap_in_event, 0) != cudaSuccess) c->sticky = S2L_E_CUDA;
+    r->swap_in_pending = false;
+  }
+  c->alloc[r->tier].give_back(r->blocks.data() + keep, (int64_t)(r->blocks.size() - keep));
+  if (r->tier == S2L_TIER_GPU)
+    for (size_t j = keep; j < r->blocks.size(); ++j) set_table(c, r->slot, (int64_t)j, -1);
+  r->blocks.resize(keep);
+}
+
+// ---- staging ring --------------------------------------------------------------------------
+// Returns slot index with at least `bytes` of host+device space, or -1 on CUDA error.
+int staging_acquire(s2l_ctx* c, size_t bytes) {
+  StagingRing& R = c->ring;
+  int s = R.next;
+  R.next = (R.next + 1) % StagingRing::kSlots;
+  if (R.used[s]) {
+    if (!cuda_ok(c, cudaEventSynchronize(R.ev[s]), "staging event sync")) return -1;
+    R.used[s] = false;
+  }
+  if (R.cap[s] < bytes) {
+    size_t cap = std::max<size_t>(bytes, 64 << 10);
+    cap = (cap + 4095) & ~size_t(4095);
+    if (R.host[s]) cudaFreeHost(R.host[s]);
+    if (R.dev[s]) cudaFree(R.dev[s]);
+    R.host[s] = R.dev[s] = nullptr;
+    R.cap[s] = 0;
+    if (!cuda_ok(c, cudaHostAlloc(&R.host[s], cap, cudaHostAllocDefault), "cudaHostAlloc staging"))
+      return -1;
+    if (!cuda_ok(c, cudaMalloc(&R.dev[s], cap), "cudaMalloc staging")) return -1;
+    R.cap[s] = cap;
+  }
+  return s;
+}
+
+bool staging_upload_and_mark(s2l_ctx* c, int s, size_t bytes) {
+  StagingRing& R = c->ring;
+  if (bytes && !cuda_ok(c, cudaMemcpyAsync(R.dev[s], R.host[s], bytes, cudaMemcpyHostToDevice,
+                                           c->compute), "staging H2D"))
+    return false;
+  return true;
+}
+
+bool staging_release(s2l_ctx* c, int s) {
+  StagingRing& R = c->ring;
+  if (!cuda_ok(c, cudaEventRecord(R.ev[s], c->compute), "staging event record")) return false;
+  R.used[s] = true;
+  return true;
+}
+
+size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Packs the dirty table entries into dst (as TablePatch) and clears the dirty set.
+int32_t take_patches(s2l_ctx* c, s2l::TablePatch* dst) {
+  int32_t n = 0;
+  for (int32_t idx : c->dirty) {
+    dst[n++] = s2l::TablePatch{idx, c->h_table[idx]};
+    c->dirty_flag[idx] = 0;
+  }
+  c->dirty.clear();
+  return n;
+}
+
+// Event pairs for per-kernel timing.
+std::pair<cudaEvent_t, cudaEvent_t> timing_pair(s2l_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    auto p = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return p;
+  }
+  std::pair<cudaEvent_t, cudaEvent_t> p{nullptr, nullptr};
+  cudaEventCreate(&p.first);
+  cudaEventCreate(&p.second);
+  return p;
+}
+
+// The compute stream must not rewrite GPU blocks freed by a swap-out before that copy ends.
+bool wait_swap_out_hazard(s2l_ctx* c) {
+  if (!c->swap_out_pending) return true;
+  if (!cuda_ok(c, cudaStreamWaitEvent(c->compute, c->swap_out_done, 0), "wait swap-out")) return false;
+  c->swap_out_pending = false;
+  return true;
+}
+
+// Flush pending table patches with a standalone patch kernel (used before attention when no
+// append kernel carried them).
+s2l_status flush_patches(s2l_ctx* c) {
+  if (c->dirty.empty()) return S2L_OK;
+  size_t bytes = c->dirty.size() * sizeof(s2l::TablePatch);
+  int s = staging_acquire(c, bytes);
+  if (s < 0) return S2L_E_CUDA;
+  int32_t n = take_patches(c, (s2l::TablePatch*)c->ring.host[s]);
+  if (!staging_upload_and_mark(c, s, bytes)) return S2L_E_CUDA;
+  CK(s2l::launch_table_patch((const s2l::TablePatch*)c->ring.dev[s], n, c->d_table, c->compute));
+  c->launches++;
+  if (!staging_release(c, s)) return S2L_E_CUDA;
+  return S2L_OK;
+}
+
+s2l_status swap_impl(s2l_ctx* c, int32_t n_reqs, const int64_t* ids, int64_t* bytes_out,
+                     int32_t src, int32_t dst) {
+  if (bytes_out) *bytes_out = 0;
+  if (n_reqs < 0 || (n_reqs > 0 && !ids)) return fail(S2L_E_INVAL, "bad request list");
+  std::unordered_set<int64_t> seen;
+  int64_t need = 0;
+  for (int32_t i = 0; i < n_reqs; ++i) {
+    Request* r = find(c, ids[i]);
+    if (!r) return fail(S2L_E_NO_REQUEST, "unknown request %lld", (long long)ids[i]);
+    if (!seen.insert(ids[i]).second) return fail(S2L_E_INVAL, "request %lld repeated", (long long)ids[i]);
+    if (r->tier != src) return fail(S2L_E_STATE, "request %lld is not on the %s tier",
+                                    (long long)ids[i], src == S2L_TIER_GPU ? "GPU" : "CPU");
+    need += (int64_t)r->blocks.size();
+  }
+  if (need > c->alloc[dst].free_count())
+    return fail(dst == S2L_TIER_CPU ? S2L_E_NO_CPU_BLOCKS : S2L_E_NO_GPU_BLOCKS,
+                "swap needs %lld blocks, %lld free", (long long)need,
+                (long long)c->alloc[dst].free_count());
+  if (c->sticky) return fail(c->sticky, "context has a sticky CUDA error");
+
+  // ---- bookkeeping (identical in host-only contexts) ----
+  std::vector<std::pair<int32_t, int32_t>> moves;  // (src id, dst id) in request/block order
+  moves.reserve((size_t)need);
+  std::vector<Request*> touched;
+  for (int32_t i = 0; i < n_reqs; ++i) {
+    Request* r = find(c, ids[i]);
+    std::vector<int32_t> nid;
+    nid.reserve(r->blocks.size());
+    c->alloc[dst].take_lowest((int64_t)r->blocks.size(), nid);
+    for (size_t j = 0; j < nid.size(); ++j) moves.emplace_back(r->blocks[j], nid[j]);
+    c->alloc[src].give_back(r->blocks.data(), (int64_t)r->blocks.size());
+    for (size_t j = 0; j < nid.size(); ++j)
+      set_table(c, r->slot, (int64_t)j, dst == S2L_TIER_GPU ? nid[j] : -1);
+    r->blocks.swap(nid);
+    r->tier = dst;
+    touched.push_back(r);
+  }
+  if (bytes_out) *bytes_out = need * c->m_block;
+  if (c->host_only || need == 0) return S2L_OK;
+
+  // ---- copies on the copy stream ----
+  // Order the copy after everything already enqueued on the compute stream: swap-out reads
+  // blocks written by earlier appends; swap-in overwrites GPU blocks that earlier kernels
+  // may still read (they were freed by invalidate / release / swap-out before).
+  cudaEvent_t ev;
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev, c->compute));
+  CK(cudaStreamWaitEvent(c->copy, ev, 0));
+  cudaEventDestroy(ev);
+  if (dst == S2L_TIER_GPU && c->swap_out_pending) {
+    // GPU blocks freed by a swap-out are being read by that D2H; same copy stream -> ordered.
+  }
+  // Coalesce runs where both source and destination ids are consecutive (Z9 makes these long).
+  char* gbase = (char*)c->gpu_pool;
+  char* hbase = (char*)c->cpu_pool;
+  std::vector<void*> dsts, srcs;
+  std::vector<size_t> sizes;
+  for (size_t i = 0; i < moves.size();) {
+    size_t j = i + 1;
+    while (j < moves.size() && moves[j].first == moves[j - 1].first + 1 &&
+           moves[j].second == moves[j - 1].second + 1)
+      ++j;
+    size_t nb = j - i;
+    char* s_ptr = (src == S2L_TIER_GPU ? gbase : hbase) + (size_t)moves[i].first * c->m_block;
+    char* d_ptr = (dst == S2L_TIER_GPU ? gbase : hbase) + (size_t)moves[i].second * c->m_block;
+    srcs.push_back(s_ptr);
+    dsts.push_back(d_ptr);
+    sizes.push_back(nb * (size_t)c->m_block);
+    i = j;
+  }
+  if (sizes.size() == 1) {
+    CK(cudaMemcpyAsync(dsts[0], srcs[0], sizes[0],
+                       dst == S2L_TIER_GPU ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, c->copy));
+  } else {
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t attr_idx = 0, fail_idx = 0;
+    cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(),
+                                         &attr, &attr_idx, 1, &fail_idx, c->copy);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      for (size_t i = 0; i < sizes.size(); ++i)
+        CK(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i],
+                           dst == S2L_TIER_GPU ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                           c->copy));
+    }
+  }
+  if (src == S2L_TIER_GPU) {
+    CK(cudaEventRecord(c->swap_out_done, c->copy));
+    c->swap_out_pending = true;
+  } else {
+    for (Request* r : touched) {
+      if (!r->swap_in_event) CK(cudaEventCreateWithFlags(&r->swap_in_event, cudaEventDisableTiming));
+      CK(cudaEventRecord(r->swap_in_event, c->copy));
+      r->swap_in_pending = true;
+    }
+  }
+  return S2L_OK;
+}
+
+}  // namespace
+
+// =========================================================================================
+extern "C" {
+
+int64_t s2l_block_bytes(const s2l_config* cfg) {
+  if (!cfg || cfg->num_layers < 1 || cfg->num_kv_heads < 1 || cfg->head_dim < 1 ||
+      cfg->block_size < 1)
+    return -1;
+  return 2ll * cfg->num_layers * cfg->block_size * cfg->num_kv_heads * cfg->head_dim * 2ll;
+}
+
+s2l_status s2l_create_host_only(const s2l_config* cfg, s2l_ctx** out) {
+  if (!out) return fail(S2L_E_INVAL, "out is NULL");
+  *out = nullptr;
+  s2l_status st = check_config(cfg);
+  if (st) return st;
+  auto* c = new s2l_ctx();
+  c->host_only = true;
+  init_common(c, cfg);
+  *out = c;
+  return S2L_OK;
+}
+
+s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinned,
+                      void* compute_stream, void* copy_stream, s2l_ctx** out) {
+  if (!out) return fail(S2L_E_INVAL, "out is NULL");
+  *out = nullptr;
+  s2l_status st = check_config(cfg);
+  if (st) return st;
+  if (!gpu_pool && cfg->num_gpu_blocks > 0) return fail(S2L_E_INVAL, "gpu_pool is NULL");
+  if (!cpu_pool_pinned && cfg->num_cpu_blocks > 0) return fail(S2L_E_INVAL, "cpu_pool is NULL");
+  if (((uintptr_t)gpu_pool) & 255) return fail(S2L_E_INVAL, "gpu_pool must be 256-byte aligned");
+  std::unique_ptr<s2l_ctx> holder(new s2l_ctx());
+  s2l_ctx* c = holder.get();
+  c->host_only = false;
+  init_common(c, cfg);
+  c->gpu_pool = gpu_pool;
+  c->cpu_pool = cpu_pool_pinned;
+  c->compute = (cudaStream_t)compute_stream;
+  c->copy = (cudaStream_t)copy_stream;
+  if (!c->copy) {
+    CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    c->own_copy_stream = true;
+  }
+  CK(cudaMalloc(&c->d_table, c->h_table.size() * sizeof(int32_t)));
+  CK(cudaMemsetAsync(c->d_table, 0xFF, c->h_table.size() * sizeof(int32_t), c->compute));
+  size_t gbytes = (size_t)cfg->num_gpu_blocks * (size_t)c->m_block;
+  if (gbytes) CK(cudaMemsetAsync(gpu_pool, 0, gbytes, c->compute));
+  size_t hbytes = (size_t)cfg->num_cpu_blocks * (size_t)c->m_block;
+  if (hbytes) memset(cpu_pool_pinned, 0, hbytes);
+  for (int s = 0; s < StagingRing::kSlots; ++s)
+    CK(cudaEventCreateWithFlags(&c->ring.ev[s], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->swap_out_done, cudaEventDisableTiming));
+  c->tc_ok = s2l::attn_tc_supported(c->geo);
+  if (c->tc_ok && cfg->num_gpu_blocks > 0) {
+    const char* err = nullptr;
+    int64_t rows = (int64_t)cfg->num_gpu_blocks * cfg->num_layers * 2 * cfg->num_kv_heads *
+                   cfg->block_size;
+    if (!s2l::make_tmap_kv(c->tmap_kv, gpu_pool, rows, cfg->head_dim, cfg->block_size, &err))
+      return fail(S2L_E_CUDA, "tensor map (pool): %s", err ? err : "?");
+  } else {
+    c->tc_ok = false;
+  }
+  CK(cudaStreamSynchronize(c->compute));
+  *out = holder.release();
+  return S2L_OK;
+}
+
+void s2l_destroy(s2l_ctx* c) {
+  if (!c) return;
+  if (!c->host_only) {
+    cudaStreamSynchronize(c->compute);
+    cudaStreamSynchronize(c->copy);
+    for (int s = 0; s < StagingRing::kSlots; ++s) {
+      if (c->ring.host[s]) cudaFreeHost(c->ring.host[s]);
+      if (c->ring.dev[s]) cudaFree(c->ring.dev[s]);
+      if (c->ring.ev[s]) cudaEventDestroy(c->ring.ev[s]);
+    }
+    for (auto& r : c->slots)
+      if (r.swap_in_event) cudaEventDestroy(r.swap_in_event);
+    for (auto* v : {&c->attn_ev, &c->append_ev, &c->ev_pool})
+      for (auto& p : *v) {
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+      }
+    if (c->swap_out_done) cudaEventDestroy(c->swap_out_done);
+    if (c->d_table) cudaFree(c->d_table);
+    if (c->own_copy_stream) cudaStreamDestroy(c->copy);
+  }
+  delete c;
+}
+
+s2l_status s2l_new_request(s2l_ctx* c, int64_t id, const int32_t* tokens, int64_t n) {
+  if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
+  if (n < 0 || (n > 0 && !tokens)) return fail(S2L_E_INVAL, "bad token array");
+  if (c->by_id.count(id)) return fail(S2L_E_STATE, "request %lld already exists", (long long)id);
+  if (c->free_slots.empty()) return fail(S2L_E_CAPACITY, "request table full");
+  int32_t slot = c->free_slots.back();
+  c->free_slots.pop_back();
+  Request& r = c->slots[slot];
+  cudaEvent_t keep_ev = r.swap_in_event;
+  r = Request();
+  r.swap_in_event = keep_ev;
+  r.id = id;
+  r.slot = slot;
+  r.input.assign(tokens, tokens + n);
+  c->by_id[id] = slot;
+  return S2L_OK;
+}
+
+s2l_status s2l_release_request(s2l_ctx* c, int64_t id) {
+  if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
+  Request* r = find(c, id);
+  if (!r) return fail(S2L_E_NO_REQUEST, "unknown request %lld", (long long)id);
+  free_tail(c, r, 0);
+  r->swap_in_pending = false;
+  c->by_id.erase(id);
+  c->free_slots.push_back(r->slot);
+  return S2L_OK;
+}
+
+s2l_status s2l_preempt_recompute(s2l_ctx* c, int64_t id) {
+  if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
+  Request* r = find(c, id);
+  if (!r) return fail(S2L_E_NO_REQUEST, "unknown request %lld", (long long)id);
+  free_tail(c, r, 0);
+  r->nc = 0;
+  r->tier = S2L_TIER_GPU;
+  r->swap_in_pending = false;
+  return S2L_OK;
+}
+
+s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* items,
+                            const void* k, const void* v, int64_t kv_rows) {
+  if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
+  if (n_items < 0 || (n_items > 0 && !items)) return fail(S2L_E_INVAL, "bad item array");
+  const int64_t kb = c->cfg.block_size;
+  std::unordered_set<int64_t> seen;
+  int64_t need = 0, total_rows = 0, total_ids = 0;
+  for (int32_t i = 0; i < n_items; ++i) {
+    const s2l_append_item& it = items[i];
+    Request* r = find(c, it.req_id);
+    if (!r) return fail(S2L_E_NO_REQUEST, "item %d: unknown request %lld", i, (long long)it.req_id);
+    if (!seen.insert(it.req_id).second)
+      return fail(S2L_E_INVAL, "item %d: request %lld repeated", i, (long long)it.req_id);
+    if (r->tier != S2L_TIER_GPU)
+      return fail(S2L_E_STATE, "item %d: request %lld is swapped out", i, (long long)it.req_id);
+    if (it.n_tokens < 0 || it.n_kv < 0 || it.kv_row < 0 || (it.n_tokens > 0 && !it.tokens))
+      return fail(S2L_E_INVAL, "item %d: negative sizes or NULL tokens", i);
+    if (it.n_kv > 0 && it.kv_row + it.n_kv > kv_rows)
+      return fail(S2L_E_INVAL, "item %d: rows [%lld,%lld) beyond kv_rows %lld", i,
+                  (long long)it.kv_row, (long long)(it.kv_row + it.n_kv), (long long)kv_rows);
+    if (it.n_kv > (int64_t)r->input.size() + it.n_tokens - r->nc)
+      return fail(S2L_E_INVAL, "item %d: n_kv %lld exceeds pending tokens", i, (long long)it.n_kv);
+    int64_t nb = ceil_div(r->nc + it.n_kv, kb);
+    if (nb > c->cfg.max_blocks_per_request)
+      return fail(S2L_E_INVAL, "item %d: %lld blocks exceed max_blocks_per_request", i, (long long)nb);
+    need += nb - (int64_t)r->blocks.size();
+    total_rows += it.n_kv;
+    if (it.n_kv) total_ids += nb - r->nc / kb;
+  }
+  if (need > c->alloc[S2L_TIER_GPU].free_count())
+    return fail(S2L_E_NO_GPU_BLOCKS, "append needs %lld blocks, %lld free", (long long)need,
+                (long long)c->alloc[S2L_TIER_GPU].free_count());
+  if (!c->host_only && total_rows > 0 && (!k || !v)) return fail(S2L_E_INVAL, "k/v is NULL");
+  if (c->host_only && (k || v)) return fail(S2L_E_STATE, "host-only context cannot write K/V");
+  if (c->sticky) return fail(c->sticky, "context has a sticky CUDA error");
+
+  // Staging layout: [AppendItemDev x n_items][int32 ids x total_ids][TablePatch x patches]
+  std::vector<s2l::AppendItemDev> dev_items;
+  std::vector<int32_t> ids;
+  std::vector<Request*> wait_in;
+  dev_items.reserve(n_items);
+  ids.reserve((size_t)total_ids);
+  int64_t row_begin = 0;
+  for (int32_t i = 0; i < n_items; ++i) {
+    const s2l_append_item& it = items[i];
+    Request* r = find(c, it.req_id);
+    if (it.n_tokens) r->input.insert(r->input.end(), it.tokens, it.tokens + it.n_tokens);
+    int64_t nb = ceil_div(r->nc + it.n_kv, kb);
+    size_t held = r->blocks.size();
+    c->alloc[S2L_TIER_GPU].take_lowest(nb - (int64_t)held, r->blocks);
+    for (size_t j = held; j < r->blocks.size(); ++j) set_table(c, r->slot, (int64_t)j, r->blocks[j]);
+    if (it.n_kv) {
+      s2l::AppendItemDev d{};
+      d.nc = r->nc;
+      d.n_kv = it.n_kv;
+      d.kv_row = it.kv_row;
+      d.row_begin = row_begin;
+      d.id_off = (int32_t)ids.size();
+      for (int64_t b = r->nc / kb; b < nb; ++b) ids.push_back(r->blocks[(size_t)b]);
+      dev_items.push_back(d);
+      row_begin += it.n_kv;
+      if (r->swap_in_pending) wait_in.push_back(r);
+    }
+    r->nc += it.n_kv;
+  }
+  if (c->host_only || total_rows == 0) return c->host_only ? S2L_OK : flush_patches(c);
+
+  size_t off_ids = align16(dev_items.size() * sizeof(s2l::AppendItemDev));
+  size_t off_patch = align16(off_ids + ids.size() * sizeof(int32_t));
+  size_t bytes = off_patch + c->dirty.size() * sizeof(s2l::TablePatch);
+  int s = staging_acquire(c, bytes);
+  if (s < 0) return S2L_E_CUDA;
+  char* h = (char*)c->ring.host[s];
+  memcpy(h, dev_items.data(), dev_items.size() * sizeof(s2l::AppendItemDev));
+  memcpy(h + off_ids, ids.data(), ids.size() * sizeof(int32_t));
+  int32_t n_patch = take_patches(c, (s2l::TablePatch*)(h + off_patch));
+  if (!staging_upload_and_mark(c, s, bytes)) return S2L_E_CUDA;
+  if (!wait_swap_out_hazard(c)) return S2L_E_CUDA;
+  for (Request* r : wait_in) {
+    CK(cudaStreamWaitEvent(c->compute, r->swap_in_event, 0));
+    r->swap_in_pending = false;
+  }
+  char* dv = (char*)c->ring.dev[s];
+  std::pair<cudaEvent_t, cudaEvent_t> tp{};
+  if (c->timing) {
+    tp = timing_pair(c);
+    CK(cudaEventRecord(tp.first, c->compute));
+  }
+  CK(s2l::launch_append(c->geo, (const s2l::AppendItemDev*)dv, (int32_t)dev_items.size(),
+                        total_rows, (const int32_t*)(dv + off_ids),
+                        (const s2l::TablePatch*)(dv + off_patch), n_patch, c->d_table, k, v,
+                        kv_rows, c->gpu_pool, c->compute));
+  c->launches++;
+  if (c->timing) {
+    CK(cudaEventRecord(tp.second, c->compute));
+    c->append_ev.push_back(tp);
+  }
+  if (!staging_release(c, s)) return S2L_E_CUDA;
+  return S2L_OK;
+}
+
+s2l_status s2l_invalidate_lcp(s2l_ctx* c, int64_t id, const int32_t* new_tokens, int64_t new_len,
+                              int64_t* lcp_out, int64_t* inval_out) {
+  if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
+  if (new_len < 0 || (new_len > 0 && !new_tokens)) return fail(S2L_E_INVAL, "bad token array");
+  Request* r = find(c, id);
+  if (!r) return fail(S2L_E_NO_REQUEST, "unknown request %lld", (long long)id);
+  // a1: LCP by a word-wise compare (8 tokens per 32-byte step), then the exact tail.
+  const int32_t* a = r->input.data();
+  int64_t n = std::min<int64_t>((int64_t)r->input.size(), new_len);
+  int64_t p = 0;
+  while (p + 8 <= n && memcmp(a + p, new_tokens + p, 32) == 0) p += 8;
+  while (p < n && a[p] == new_tokens[p]) ++p;
+  // a2: invalidate beyond b = min(p, nc) (Z5), keep ceil(b/k) blocks (Z4 / S:L191 variant).
+  const int64_t kb = c->cfg.block_size;
+  int64_t b = std::min(p, r->nc);
+  if (c->cfg.lcp_block_aligned) b = (b / kb) * kb;
+  size_t keep = (size_t)ceil_div(b, kb);
+  free_tail(c, r, keep);
+  int64_t inval = r->nc - b;
+  r->nc = b;
+  r->tti += inval;
+  r->input.assign(new_tokens, new_tokens + new_len);
+  if (r->tier == S2L_TIER_CPU && keep == 0) r->tier = S2L_TIER_GPU;
+  if (lcp_out) *lcp_out = p;
+  if (inval_out) *inval_out = inval;
+  return S2L_OK;
+}
+
+s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
+                             const s2l_prefill_item* items, const void* q, void* o, float* lse,
+                             int64_t q_rows) {
+  if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
+  if (c->host_only) return fail(S2L_E_STATE, "host-only context has no device");
+  if (n_items < 0 || (n_items > 0 && !items)) return fail(S2L_E_INVAL, "bad item array");
+  if (layer < 0 || layer >= c->cfg.num_layers) return fail(S2L_E_INVAL, "layer %d out of range", layer);
+  for (int32_t i = 0; i < n_items; ++i) {
+    const s2l_prefill_item& it = items[i];
+    Request* r = find(c, it.req_id);
+    if (!r) return fail(S2L_E_NO_REQUEST, "item %d: unknown request %lld", i, (long long)it.req_id);
+    if (r->tier != S2L_TIER_GPU)
+      return fail(S2L_E_STATE, "item %d: request %lld is swapped out", i, (long long)it.req_id);
+    if (it.n_q < 1 || it.q_pos < 0 || it.q_row < 0 || it.q_pos + it.n_q > r->nc ||
+        it.q_row + it.n_q > q_rows || it.n_q > (1ll << 30))
+      return fail(S2L_E_INVAL, "item %d: bad q range (q_pos %lld n_q %lld nc %lld)", i,
+                  (long long)it.q_pos, (long long)it.n_q, (long long)r->nc);
+  }
+  if (n_items > 0 && (!q || !o)) return fail(S2L_E_INVAL, "q/o is NULL");
+  if (c->sticky) return fail(c->sticky, "context has a sticky CUDA error");
+  if (n_items == 0) return S2L_OK;
+  s2l_status st = flush_patches(c);
+  if (st) return st;
+  for (int32_t i = 0; i < n_items; ++i) {
+    Request* r = find(c, items[i].req_id);
+    if (r->swap_in_pending) {
+      CK(cudaStreamWaitEvent(c->compute, r->swap_in_event, 0));
+      r->swap_in_pending = false;
+    }
+  }
+  const int32_t G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
+  // Items ordered by descending KV length (q_pos + n_q) so that the longest Q tiles start
+  // first (longest-processing-time order for the hardware block scheduler).
+  std::vector<int32_t> order(n_items);
+  for (int32_t i = 0; i < n_items; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+    return items[x].q_pos + items[x].n_q > items[y].q_pos + items[y].n_q;
+  });
+  std::vector<s2l::AttnItemDev> dev(n_items);
+  int64_t units = 0, total_q = 0;
+  for (int32_t i = 0; i < n_items; ++i) {
+    const s2l_prefill_item& it = items[order[i]];
+    Request* r = find(c, it.req_id);
+    s2l::AttnItemDev& d = dev[i];
+    d.q_pos = it.q_pos;
+    d.q_row = it.q_row;
+    d.n_q = (int32_t)it.n_q;
+    d.slot = r->slot;
+    d.tiles = (int32_t)ceil_div(it.n_q * G, 128);
+    d.unit_begin = (int32_t)units;
+    units += (int64_t)d.tiles * c->cfg.num_kv_heads;
+    total_q += it.n_q;
+  }
+  if (units >= (1ll << 31)) return fail(S2L_E_INVAL, "batch too large");
+  size_t bytes = dev.size() * sizeof(s2l::AttnItemDev);
+  int s = staging_acquire(c, bytes);
+  if (s < 0) return S2L_E_CUDA;
+  memcpy(c->ring.host[s], dev.data(), bytes);
+  if (!staging_upload_and_mark(c, s, bytes)) return S2L_E_CUDA;
+  const s2l::AttnItemDev* dv = (const s2l::AttnItemDev*)c->ring.dev[s];
+  std::pair<cudaEvent_t, cudaEvent_t> tp{};
+  if (c->timing) {
+    tp = timing_pair(c);
+    CK(cudaEventRecord(tp.first, c->compute));
+  }
+  if (c->tc_ok) {
+    alignas(64) unsigned char tq[128];
+    const char* err = nullptr;
+    if (!s2l::make_tmap_q(tq, q, q_rows, c->cfg.num_q_heads, c->cfg.head_dim, G, &err))
+      return fail(S2L_E_CUDA, "tensor map (q): %s", err ? err : "?");
+    CK(s2l::launch_attn_tc(c->geo, dv, n_items, (int32_t)units, c->d_table, layer, tq,
+                           c->tmap_kv, o, lse, c->compute));
+  } else {
+    CK(s2l::launch_attn_generic(c->geo, dv, n_items, total_q, c->d_table, layer, q, o, lse,
+                                c->gpu_pool, c->compute));
+  }
+  c->launches++;
+  if (c->timing) {
+    CK(cudaEventRecord(tp.second, c->compute));
+    c->attn_ev.push_back(tp);
+  }
+  if (!staging_release(c, s)) return S2L_E_CUDA;
+  return S2L_OK;
+}
+
+s2l_status s2l_swap_out(s2l_ctx* c, int32_t n, const int64_t* ids, int64_t* bytes_out) {
+  if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
+  return swap_impl(c, n, ids, bytes_out, S2L_TIER_GPU, S2L_TIER_CPU);
+}
+
+s2l_status s2l_swap_in(s2l_ctx* c, int32_t n, const int64_t* ids, int64_t* bytes_out) {
+  if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
+  return swap_impl(c, n, ids, bytes_out, S2L_TIER_CPU, S2L_TIER_GPU);
+}
+
+s2l_status s2l_query(s2l_ctx* c, int64_t id, s2l_req_info* out) {
+  if (!c || !out) return fail(S2L_E_INVAL, "NULL argument");
+  Request* r = find(c, id);
+  if (!r) return fail(S2L_E_NO_REQUEST, "unknown request %lld", (long long)id);
+  out->num_tokens = (int64_t)r->input.size();
+  out->num_computed = r->nc;
+  out->total_tokens_invalidated = r->tti;
+  out->tier = r->tier;
+  out->num_blocks = (int32_t)r->blocks.size();
+  return S2L_OK;
+}
+
+s2l_status s2l_block_table(s2l_ctx* c, int64_t id, int32_t* ids_out, int64_t cap, int64_t* n_out) {
+  if (!c || cap < 0 || (cap > 0 && !ids_out)) return fail(S2L_E_INVAL, "bad arguments");
+  Request* r = find(c, id);
+  if (!r) return fail(S2L_E_NO_REQUEST, "unknown request %lld", (long long)id);
+  int64_t n = (int64_t)r->blocks.size();
+  if (n_out) *n_out = n;
+  memcpy(ids_out, r->blocks.data(), (size_t)std::min(n, cap) * sizeof(int32_t));
+  return S2L_OK;
+}
+
+s2l_status s2l_free_blocks(s2l_ctx* c, int64_t* gpu_free, int64_t* cpu_free) {
+  if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
+  if (gpu_free) *gpu_free = c->alloc[S2L_TIER_GPU].free_count();
+  if (cpu_free) *cpu_free = c->alloc[S2L_TIER_CPU].free_count();
+  return S2L_OK;
+}
+
+s2l_status s2l_sync(s2l_ctx* c) {
+  if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
+  if (c->host_only) return S2L_OK;
+  CK(cudaStreamSynchronize(c->compute));
+  CK(cudaStreamSynchronize(c->copy));
+  return c->sticky;
+}
+
+int64_t s2l_kernel_launches(s2l_ctx* c) { return c ? c->launches : -1; }
+
+s2l_status s2l_set_timing(s2l_ctx* c, int32_t enable) {
+  if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
+  if (c->host_only) return fail(S2L_E_STATE, "host-only context has no device");
+  CK(cudaStreamSynchronize(c->compute));
+  for (auto* v : {&c->attn_ev, &c->append_ev}) {
+    for (auto& p : *v) c->ev_pool.push_back(p);
+    v->clear();
+  }
+  c->timing = enable != 0;
+  return S2L_OK;
+}
+
+s2l_status s2l_timing_read(s2l_ctx* c, double* attn_ms, int64_t* attn_n, double* app_ms,
+                           int64_t* app_n) {
+  if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
+  if (c->host_only) return fail(S2L_E_STATE, "host-only context has no device");
+  CK(cudaStreamSynchronize(c->compute));
+  double t[2] = {0, 0};
+  int i = 0;
+  for (auto* v : {&c->attn_ev, &c->append_ev}) {
+    for (auto& p : *v) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, p.first, p.second));
+      t[i] += ms;
+    }
+    ++i;
+  }
+  if (attn_ms) *attn_ms = t[0];
+  if (attn_n) *attn_n = (int64_t)c->attn_ev.size();
+  if (app_ms) *app_ms = t[1];
+  if (app_n) *app_n = (int64_t)c->append_ev.size();
+  return S2L_OK;
+}
+
+const char* s2l_last_error(void) { return g_err.c_str(); }
+
+const char* s2l_version(void) { return "libs2l 0.1 sm_100a (tcgen05/TMEM/TMA attention)"; }
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Internal declarations shared by the host runtime and the kernels of libs2l.
+// Product code only — nothing here is shared with oracle/ (see DESIGN.md §Boundary).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace s2l {
+
+// ---- device-side descriptors written into the staging ring by the host -------------------
+
+// One item of an append launch.  Positions [nc, nc+n_kv) of the request are written; the
+// block ids covering them are ids[id_off .. id_off + n_ids) (first one = block nc/k).
+struct AppendItemDev {
+  int64_t nc;        // num_computed before the append
+  int64_t n_kv;
+  int64_t kv_row;    // first row in the caller's k/v
+  int64_t row_begin; // prefix sum of n_kv over items (thread -> item lookup)
+  int32_t id_off;
+  int32_t pad;
+};
+
+// One entry of the device block-table patch list: table[idx] = value.
+struct TablePatch {
+  int32_t idx;
+  int32_t value;
+};
+
+// One item of an attention launch (items sorted by descending kv length on the host).
+struct AttnItemDev {
+  int64_t q_pos;
+  int64_t q_row;
+  int32_t n_q;
+  int32_t slot;        // row of the device block table
+  int32_t tiles;       // 128-row (token x head-in-group) Q tiles of this item
+  int32_t unit_begin;  // prefix sum of tiles * h_kv over items
+};
+
+struct Geometry {
+  int32_t L, h_q, h_kv, d, k;
+  int32_t max_blocks;  // columns of the device block table
+};
+
+// ---- kernel launchers (kernels_*.cu) ----------------------------------------------------
+
+cudaError_t launch_table_patch(const TablePatch* patches, int32_t n, int32_t* table,
+                               cudaStream_t st);
+
+// Writes K/V rows into the pool and applies the table patches (fused).
+cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t n_items,
+                          int64_t total_rows, const int32_t* ids, const TablePatch* patches,
+                          int32_t n_patches, int32_t* table, const void* k, const void* v,
+                          int64_t kv_rows, void* pool, cudaStream_t st);
+
+// CUDA-core attention for any geometry (one warp per (query row, q head)).
+cudaError_t launch_attn_generic(const Geometry& g, const AttnItemDev* items, int32_t n_items,
+                                int64_t total_q, const int32_t* table, int32_t layer,
+                                const void* q, void* o, float* lse, const void* pool,
+                                cudaStream_t st);
+
+// tcgen05 / TMEM / TMA attention (head_dim 128, 16 <= k <= 128, 128 % (h_q/h_kv) == 0).
+// tmap_q / tmap_kv point to host CUtensorMap (128-byte) objects passed by value.
+bool attn_tc_supported(const Geometry& g);
+cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t n_items,
+                           int32_t total_units, const int32_t* table, int32_t layer,
+                           const void* tmap_q, const void* tmap_kv, void* o, float* lse,
+                           cudaStream_t st);
+// TMA descriptors (host).  Returns false on failure (message in *err).
+bool make_tmap_q(void* out128, const void* q, int64_t q_rows, int32_t h_q, int32_t d,
+                 int32_t group, const char** err);
+bool make_tmap_kv(void* out128, const void* pool, int64_t total_rows, int32_t d, int32_t k,
+                  const char** err);
+
+}  // namespace s2l

@@ -1,0 +1,323 @@
+"""GPU parity tests (B200): libs2l through its C ABI vs the fp64 oracle on the same seeded
+inputs.  Bit-exact for block tables, counts, LCP and pool / swap bytes; normwise relative
+error <= 2e-2 for attention (BJ:L5), |dLSE| <= 1e-2."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from synth import workloads as W
+from tests.harness import Pair, bf16_dev_to_f64, normwise_err, to_dev
+from paper_2604_16395_b200 import s2l
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dev():
+    from paper_2604_16395_b200 import build
+    build.build()
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    torch.cuda.init()
+
+
+def _stream_qkv(seed, toks, geo, q_scale=1.0):
+    return W.request_qkv(seed, np.asarray(toks, np.int32), geo, q_scale)
+
+
+# ----------------------------------------------------------------------------- C1 (BJ:L7)
+@pytest.mark.parametrize("aligned", [False, True])
+def test_c1_full_walk(aligned):
+    geo = W.C1
+    seed = W.seed_of(1)
+    P = Pair(geo.L, geo.h_q, geo.h_kv, geo.d, geo.k, 8, 8, aligned=aligned)
+    toks = W.request_tokens(seed, 0, 24)
+    q, k, v = _stream_qkv(seed, toks, geo)
+    P.new(1, [])
+    for i in range(3):
+        sl = slice(8 * i, 8 * i + 8)
+        P.append([(1, toks[sl], 8, 0)], k[:, sl], v[:, sl])
+        P.prefill([(1, 8 * i, 8, 0)], q[sl])
+        P.check_state()
+        P.check_pool_valid_slots()
+    assert P.lib.block_table(1) == [0, 1, 2, 3, 4, 5]
+    new = W.updated_tokens(seed, 0, toks, 10, 24, 0)
+    p, inval = P.invalidate(1, new)
+    assert p == 10 and inval == (16 if aligned else 14)
+    q2, k2, v2 = _stream_qkv(seed, new, geo)
+    b = P.lib.query(1)["num_computed"]
+    P.append([(1, None, 24 - b, 0)], k2[:, b:], v2[:, b:])
+    P.prefill([(1, b, 24 - b, 0)], q2[b:])
+    P.check_state()
+    P.check_pool_valid_slots()
+    P.check_pools_whole()
+    before = P.gpu_pool_bits()[P.lib.block_table(1)].copy()
+    assert P.swap_out([1]) == (s2l.OK, 6 * 256)
+    assert np.array_equal(P.cpu_pool_bits()[P.lib.block_table(1)], before)
+    P.check_pools_whole()
+    assert P.swap_in([1]) == (s2l.OK, 6 * 256)
+    P.check_state()
+    P.check_pools_whole()
+    # after the round trip attention is unchanged
+    P.prefill([(1, b, 24 - b, 0)], q2[b:])
+
+
+def test_c1_prime_interleaved_two_requests():
+    geo = W.C1
+    seed = W.seed_of(1)
+    P = Pair(geo.L, geo.h_q, geo.h_kv, geo.d, geo.k, 8, 8)
+    toks = {r: W.request_tokens(seed, r, 24) for r in (1, 2)}
+    qkv = {r: _stream_qkv(seed, toks[r], geo) for r in (1, 2)}
+    P.new(1, toks[1]); P.new(2, toks[2])
+    sched = [(1, 0, 8), (2, 0, 8), (1, 8, 8)]
+    for rid, a, n in sched:
+        P.append([(rid, None, n, 0)], qkv[rid][1][:, a:a + n], qkv[rid][2][:, a:a + n])
+        P.prefill([(rid, a, n, 0)], qkv[rid][0][a:a + n])
+    new2 = W.updated_tokens(seed, 2, toks[2], 3, 12, 0)
+    assert P.invalidate(2, new2) == (3, 5)
+    q2, k2, v2 = _stream_qkv(seed, new2, geo)
+    # one append call carrying both requests (freed id 3 reused by request 1)
+    kk = np.concatenate([qkv[1][1][:, 16:20], k2[:, 3:12]], axis=1)
+    vv = np.concatenate([qkv[1][2][:, 16:20], v2[:, 3:12]], axis=1)
+    P.append([(1, None, 4, 0), (2, None, 9, 4)], kk, vv)
+    assert P.lib.block_table(1) == [0, 1, 4, 5, 3] and P.lib.block_table(2) == [2, 6, 7]
+    qq = np.concatenate([qkv[1][0][16:20], q2[3:12]])
+    P.prefill([(1, 16, 4, 0), (2, 3, 9, 4)], qq)
+    P.check_pools_whole()
+
+
+# ----------------------------------------------------------------------------- tensor-core path
+def _multi_request_case(P, seed, geo, lengths, chunks, q_scale=1.0):
+    """Prefills each request's [0, lengths[i]) in `chunks[i]` pieces, all requests batched
+    per round; checks every round against the oracle."""
+    toks = {r: W.request_tokens(seed, r, L) for r, L in enumerate(lengths)}
+    data = {r: _stream_qkv(seed, toks[r], geo, q_scale) for r in toks}
+    for r in toks:
+        P.new(r, toks[r])
+    pos = {r: 0 for r in toks}
+    rounds = max(len(c) for c in chunks)
+    for j in range(rounds):
+        items_a, items_p, ks, vs, qs = [], [], [], [], []
+        row = 0
+        for r in toks:
+            if j >= len(chunks[r]):
+                continue
+            n = chunks[r][j]
+            a = pos[r]
+            items_a.append((r, None, n, row))
+            items_p.append((r, a, n, row))
+            ks.append(data[r][1][:, a:a + n]); vs.append(data[r][2][:, a:a + n]); qs.append(data[r][0][a:a + n])
+            row += n
+            pos[r] += n
+        P.append(items_a, np.concatenate(ks, axis=1), np.concatenate(vs, axis=1))
+        P.prefill(items_p, np.concatenate(qs))
+    P.check_state()
+    P.check_pool_valid_slots()
+    return toks, data
+
+
+@pytest.mark.parametrize("h_q,h_kv", [(8, 2), (4, 4), (16, 2), (4, 2)])
+def test_tc_gqa_ragged(h_q, h_kv):
+    """d = 128, k = 16: several tiles, ragged tails, varied GQA group sizes."""
+    geo = W.Geometry(L=1, h_q=h_q, h_kv=h_kv, d=128, k=16)
+    P = Pair(1, h_q, h_kv, 128, 16, 256, 0)
+    _multi_request_case(P, 77, geo, [517, 300, 129], [[200, 317], [1, 299], [128, 1]])
+
+
+@pytest.mark.parametrize("k", [32, 64, 128])
+def test_tc_block_sizes(k):
+    geo = W.Geometry(L=2, h_q=8, h_kv=2, d=128, k=k)
+    P = Pair(2, 8, 2, 128, k, 64, 0)
+    _multi_request_case(P, 78, geo, [700, 333], [[256, 444], [333]])
+
+
+def test_tc_peaky_scores_rescale():
+    """Q scaled by 4 (score std ~4): exercises the running-max rescale of O in TMEM."""
+    geo = W.Geometry(L=1, h_q=8, h_kv=2, d=128, k=16)
+    P = Pair(1, 8, 2, 128, 16, 256, 0)
+    _multi_request_case(P, 79, geo, [1200, 640], [[64, 900, 236], [640]], q_scale=4.0)
+
+
+def test_tc_layer_selection():
+    geo = W.Geometry(L=3, h_q=8, h_kv=2, d=128, k=16)
+    P = Pair(3, 8, 2, 128, 16, 64, 0)
+    toks, data = _multi_request_case(P, 80, geo, [300], [[300]])
+    q = data[0][0]
+    for layer in range(3):
+        P.prefill([(0, 0, 300, 0)], q, layer=layer)
+
+
+def test_reduced_c2_two_requests_4k():
+    """Reduced C2 (SURVEY d.5): Llama-3-8B attention shape, 2 requests x 4096 tokens in
+    512-token chunks, all checked in full."""
+    geo = W.LLAMA3_8B
+    P = Pair(1, 32, 8, 128, 16, 1024, 0, mirror=False)
+    _multi_request_case(P, W.seed_of(2), geo, [4096, 4096], [[512] * 8, [512] * 8])
+
+
+def test_c3_small_update_equals_fresh():
+    """Update mode (C3 shape, 4 requests x 2048): LCP invalidation of 20-80%, re-append and
+    re-prefill of the suffix == fresh prefill of the new input."""
+    geo = W.LLAMA3_8B
+    seed = W.seed_of(3)
+    P = Pair(1, 32, 8, 128, 16, 1024, 0, mirror=False)
+    toks, data = _multi_request_case(P, seed, geo, [2048] * 4, [[1024, 1024]] * 4)
+    ps = W.c3_lcp_draws(seed, 4, 2048)
+    items_a, items_p, ks, vs, qs, row = [], [], [], [], [], 0
+    fresh = {}
+    for r in range(4):
+        new = W.updated_tokens(seed, r, toks[r], int(ps[r]), 2048, 0)
+        assert P.invalidate(r, new) == (int(ps[r]), 2048 - int(ps[r]))
+        qn, kn, vn = _stream_qkv(seed, new, geo)
+        fresh[r] = (new, qn, kn, vn)
+        b = int(ps[r])
+        items_a.append((r, None, 2048 - b, row)); items_p.append((r, b, 2048 - b, row))
+        ks.append(kn[:, b:]); vs.append(vn[:, b:]); qs.append(qn[b:])
+        row += 2048 - b
+    P.append(items_a, np.concatenate(ks, axis=1), np.concatenate(vs, axis=1))
+    o_gpu, o_ref, _, _ = P.prefill(items_p, np.concatenate(qs))
+    # the same suffix rows from a fresh context holding only the new inputs
+    F = Pair(1, 32, 8, 128, 16, 1024, 0, mirror=False)
+    row = 0
+    for r in range(4):
+        new, qn, kn, vn = fresh[r]
+        F.new(r, new)
+        F.append([(r, None, 2048, 0)], kn, vn)
+        b = int(ps[r])
+        o_f, _, _, _ = F.prefill([(r, 0, 2048, 0)], qn)
+        err = normwise_err(o_gpu[row:row + 2048 - b], o_f[b:])
+        assert err.max() <= 2e-2
+        row += 2048 - b
+
+
+def test_chunked_equals_one_shot_and_batch_independence():
+    geo = W.LLAMA3_8B
+    seed = 91
+    toks = W.request_tokens(seed, 0, 1500)
+    q, k, v = _stream_qkv(seed, toks, geo)
+    A = Pair(1, 32, 8, 128, 16, 256, 0, mirror=False)
+    A.new(0, toks)
+    outs = []
+    for a, n in ((0, 100), (100, 700), (800, 700)):
+        A.append([(0, None, n, 0)], k[:, a:a + n], v[:, a:a + n])
+        outs.append(A.prefill([(0, a, n, 0)], q[a:a + n])[0])
+    B = Pair(1, 32, 8, 128, 16, 256, 0, mirror=False)
+    B.new(0, toks)
+    B.new(1, W.request_tokens(seed, 1, 900))
+    q1, k1, v1 = _stream_qkv(seed, W.request_tokens(seed, 1, 900), geo)
+    B.append([(1, None, 900, 0), (0, None, 1500, 900)], np.concatenate([k1, k], 1), np.concatenate([v1, v], 1))
+    o_b, _, _, _ = B.prefill([(1, 0, 900, 0), (0, 0, 1500, 900)], np.concatenate([q1, q]))
+    one = o_b[900:]
+    chunked = np.concatenate(outs)
+    assert normwise_err(chunked, one).max() <= 2e-2
+    # batch-composition independence: request 0's chunk [800, 1500) alone vs inside a batch
+    C = Pair(1, 32, 8, 128, 16, 256, 0, mirror=False)
+    C.new(0, toks)
+    C.append([(0, None, 1500, 0)], k, v)
+    o_c, _, _, _ = C.prefill([(0, 800, 700, 0)], q[800:])
+    assert np.array_equal(o_c, outs[2]) or normwise_err(o_c, outs[2]).max() <= 2e-2
+    assert np.array_equal(o_c, one[800:])          # same tiles, same kernel -> bitwise
+
+
+def test_swap_round_trip_scattered_and_resume_after_update():
+    """Swap with scattered ids (interleaved allocation), invalidation while swapped, swap-in
+    of the prefix and recompute from the LCP."""
+    geo = W.Geometry(L=2, h_q=8, h_kv=2, d=128, k=16)
+    seed = 92
+    P = Pair(2, 8, 2, 128, 16, 96, 96)
+    toks = {r: W.request_tokens(seed, r, 400) for r in range(3)}
+    data = {r: _stream_qkv(seed, toks[r], geo) for r in range(3)}
+    for r in range(3):
+        P.new(r, toks[r])
+    for a in range(0, 400, 100):                      # interleave -> scattered block ids
+        for r in range(3):
+            P.append([(r, None, 100, 0)], data[r][1][:, a:a + 100], data[r][2][:, a:a + 100])
+    P.check_pools_whole()
+    assert P.swap_out([2, 0]) == (s2l.OK, 2 * 25 * P.m_block)
+    P.check_pools_whole()
+    assert P.prefill([(1, 300, 100, 0)], data[1][0][300:])[0] is not None
+    # update request 0 while swapped: keep 150 tokens
+    new0 = W.updated_tokens(seed, 0, toks[0], 150, 400, 0)
+    assert P.invalidate(0, new0) == (150, 250)
+    assert P.swap_in([0, 2])[0] == s2l.OK
+    P.check_state()
+    P.check_pool_valid_slots()
+    P.check_pools_whole()
+    q0, k0, v0 = _stream_qkv(seed, new0, geo)
+    P.append([(0, None, 250, 0)], k0[:, 150:], v0[:, 150:])
+    P.prefill([(0, 150, 250, 0), (2, 0, 400, 250)], np.concatenate([q0[150:], data[2][0]]))
+    P.check_pool_valid_slots()
+
+
+def test_errors_and_edges_on_device():
+    geo = W.Geometry(L=1, h_q=8, h_kv=2, d=128, k=16)
+    P = Pair(1, 8, 2, 128, 16, 8, 4, max_blocks=64)
+    toks = W.request_tokens(5, 0, 200)
+    q, k, v = _stream_qkv(5, toks, geo)
+    P.new(0, toks)
+    # more blocks than the pool: all-or-nothing
+    assert P.append([(0, None, 200, 0)], k, v) == s2l.E_NO_GPU_BLOCKS
+    P.check_state()
+    P2 = Pair(1, 8, 2, 128, 16, 8, 4)                                   # max_blocks_per_request = 8
+    P2.new(0, toks)
+    assert P2.append([(0, None, 200, 0)], k, v) == s2l.E_INVAL
+    assert P.append([(0, None, 1, 0)], k[:, :1], v[:, :1]) == s2l.OK   # single token
+    P.prefill([(0, 0, 1, 0)], q[:1])                                    # single row, one key
+    assert P.append([(0, None, 127, 0)], k[:, 1:128], v[:, 1:128]) == s2l.OK
+    P.prefill([(0, 127, 1, 0)], q[127:128])                             # exactly 128 keys
+    P.prefill([(0, 0, 128, 0)], q[:128])
+    with pytest.raises(s2l.S2LError) as e:
+        P.lib.prefill_batch(0, [(0, 100, 29, 0)], to_dev(q[:29]), to_dev(q[:29]))
+    assert e.value.status == s2l.E_INVAL                                # beyond nc
+    assert P.swap_out([0])[0] == s2l.E_NO_CPU_BLOCKS                    # 8 blocks, 4 CPU
+    P.lib.prefill_batch(0, [], to_dev(q[:1]), to_dev(q[:1]))            # empty batch is a no-op
+    P.lib.sync()
+
+
+# ----------------------------------------------------------------------------- full size, sampled
+def _sample_rows(rng, n, extra=28):
+    rows = {0, 1, n - 2, n - 1} | set(rng.integers(0, n, size=extra).tolist())
+    return sorted(r for r in rows if 0 <= r < n)
+
+
+@pytest.mark.slow
+def test_c2_full_size_sampled_rows():
+    """C2 (BJ:L8) at full size in the bench's launch configuration (8 requests, 512-token
+    chunks, 32 steps to 16K): sampled rows of every step vs the oracle's row-wise fp64
+    attention; one full request-step (the last) checked in full."""
+    from oracle.attention import attention, attention_rows
+    geo = W.LLAMA3_8B
+    seed = W.seed_of(2)
+    nreq, chunk, total = 8, 512, 16384
+    cfg = s2l.make_config(1, 32, 8, 128, 16, nreq * total // 16 + 64, 0, max_requests=nreq,
+                          max_blocks_per_request=total // 16)
+    mb = s2l.block_bytes(cfg)
+    pool = torch.empty(cfg.num_gpu_blocks * mb // 2, dtype=torch.bfloat16, device="cuda")
+    lib = s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None)
+    toks = [W.request_tokens(seed, r, total) for r in range(nreq)]
+    data = [_stream_qkv(seed, toks[r], geo) for r in range(nreq)]
+    for r in range(nreq):
+        lib.new_request(r, toks[r])
+    rng = np.random.default_rng(0)
+    worst = 0.0
+    for j in range(total // chunk):
+        a = j * chunk
+        kk = to_dev(np.concatenate([data[r][1][:, a:a + chunk] for r in range(nreq)], axis=1))
+        vv = to_dev(np.concatenate([data[r][2][:, a:a + chunk] for r in range(nreq)], axis=1))
+        qq = to_dev(np.concatenate([data[r][0][a:a + chunk] for r in range(nreq)]))
+        oo = torch.empty_like(qq)
+        lib.append_chunk([(r, None, chunk, r * chunk) for r in range(nreq)], kk, vv)
+        lib.prefill_batch(0, [(r, a, chunk, r * chunk) for r in range(nreq)], qq, oo)
+        o = bf16_dev_to_f64(oo)
+        if j % 4 == 3 or j == 0:
+            r = j % nreq
+            rows = _sample_rows(rng, chunk)
+            o_ref, _ = attention_rows(data[r][0][a:a + chunk], data[r][1][0], data[r][2][0], a, rows)
+            err = normwise_err(o[r * chunk:(r + 1) * chunk][rows], o_ref)
+            worst = max(worst, float(err.max()))
+            assert err.max() <= 2e-2, (j, r, float(err.max()))
+    # last step, request 7, in full
+    r = nreq - 1
+    o_ref, _ = attention(data[r][0][total - chunk:], data[r][1][0], data[r][2][0], total - chunk)
+    err = normwise_err(o[r * chunk:(r + 1) * chunk], o_ref)
+    assert err.max() <= 2e-2, float(err.max())

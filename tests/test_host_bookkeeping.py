@@ -1,0 +1,176 @@
+"""CPU tests of libs2l's host logic (no GPU): the ABI exports, and the bookkeeping of a
+host-only context compared bit-exact with the oracle's state machine (block tables of both
+tiers, nc, LCP, invalidated counts, total_tokens_invalidated, free counts, status codes,
+swap bytes)."""
+import os
+import random
+import re
+
+import numpy as np
+import pytest
+
+from oracle import kvcache as O
+from oracle.kvcache import OracleKV
+from paper_2604_16395_b200 import s2l
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_2604_16395_b200 import build
+    build.build()
+
+
+def test_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "s2l.h")).read()
+    declared = set(re.findall(r"\b(s2l_[a-z_]+)\s*\(", hdr))
+    L = s2l.lib()
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+    assert declared == set(s2l.EXPORTS)
+    assert b"sm_100a" in L.s2l_version()
+
+
+def test_block_bytes_matches_paper_formula():
+    # P:L73 / P:L188: 2 MiB for Llama-3.1-8B, k = 16, all 32 layers
+    cfg = s2l.make_config(32, 32, 8, 128, 16, 1, 0)
+    assert s2l.block_bytes(cfg) == 2 * 1024 * 1024
+    assert s2l.block_bytes(s2l.make_config(1, 2, 1, 16, 4, 1, 0)) == 256
+
+
+def test_config_validation():
+    for bad in [s2l.make_config(1, 3, 2, 16, 4, 8, 8),        # h % h_kv
+                s2l.make_config(1, 2, 1, 12, 4, 8, 8),        # head_dim % 8
+                s2l.make_config(1, 2, 1, 16, 3, 8, 8),        # block not power of two
+                s2l.make_config(1, 2, 1, 16, 4, 8, 8, lcp_block_aligned=2)]:
+        with pytest.raises(s2l.S2LError) as e:
+            s2l.Context(bad, host_only=True)
+        assert e.value.status == s2l.E_INVAL
+
+
+def _pair(L=1, h_q=2, h_kv=1, d=16, k=4, ng=8, nc=8, aligned=False, max_requests=64, max_blocks=None):
+    cfg = s2l.make_config(L, h_q, h_kv, d, k, ng, nc, max_requests=max_requests,
+                          max_blocks_per_request=max_blocks or (ng + nc), lcp_block_aligned=int(aligned))
+    lib = s2l.Context(cfg, host_only=True)
+    ora = OracleKV(L, h_q, h_kv, d, k, ng, nc, max_requests=max_requests,
+                   max_blocks_per_request=max_blocks or (ng + nc), lcp_block_aligned=aligned,
+                   mirror_pools=False)
+    return lib, ora
+
+
+def _same_state(lib, ora):
+    assert lib.free_blocks() == ora.free_counts()
+    for rid in ora.reqs:
+        assert lib.query(rid) == ora.info(rid), rid
+        assert lib.block_table(rid) == ora.block_table(rid), rid
+
+
+@pytest.mark.parametrize("aligned", [False, True])
+def test_c1_walk_matches_oracle(aligned):
+    lib, ora = _pair(aligned=aligned)
+    toks = list(range(100, 124))
+    for x in (lib, ora):
+        x.new_request(1, [])
+    z = np.zeros((1, 8, 1, 16), np.uint16)
+    for i in range(3):
+        lib.append_chunk([(1, toks[8 * i: 8 * i + 8], 8, 0)], kv_rows=8)
+        assert ora.append([(1, toks[8 * i: 8 * i + 8], 8, 0)], z, z) == O.OK
+        _same_state(lib, ora)
+    new = toks[:10] + [999] + list(range(500, 513))
+    st, p, inv = ora.invalidate_lcp(1, new)
+    assert lib.invalidate_lcp(1, new) == (p, inv) == (10, 16 if aligned else 14)
+    _same_state(lib, ora)
+    n = 24 - lib.query(1)["num_computed"]
+    lib.append_chunk([(1, None, n, 0)], kv_rows=n)
+    ora.append([(1, None, n, 0)], np.zeros((1, n, 1, 16), np.uint16), np.zeros((1, n, 1, 16), np.uint16))
+    _same_state(lib, ora)
+    assert lib.swap_out([1]) == ora.swap_out([1])[1] == 6 * 256
+    _same_state(lib, ora)
+    assert lib.swap_in([1]) == ora.swap_in([1])[1]
+    _same_state(lib, ora)
+
+
+def test_spec_invalidate_numbers_via_library():
+    # S:L194-L196 (aligned): computed 2048, k 16, lcp 100 -> 96 / 1952 / 122 freed
+    for aligned, exp in ((True, (96, 1952, 122)), (False, (100, 1948, 121))):
+        lib, _ = _pair(L=1, h_q=1, h_kv=1, d=8, k=16, ng=200, nc=0, aligned=aligned)
+        toks = list(range(2048))
+        lib.new_request(0, toks)
+        lib.append_chunk([(0, None, 2048, 0)], kv_rows=2048)
+        g0 = lib.free_blocks()[0]
+        p, inv = lib.invalidate_lcp(0, toks[:100] + [-1] * 1948)
+        assert (lib.query(0)["num_computed"], inv, lib.free_blocks()[0] - g0) == exp
+        assert p == 100
+
+
+def _apply(x, op, args):
+    """Run op on library or oracle, return (status, result)."""
+    is_lib = isinstance(x, s2l.Context)
+    if op == "new":
+        rid, toks = args
+        return (s2l.status_of(x.new_request, rid, toks), None) if is_lib else (x.new_request(rid, toks), None)
+    if op == "append":
+        items = args
+        if is_lib:
+            return s2l.status_of(x.append_chunk, items, kv_rows=64), None
+        z = np.zeros((1, 64, 1, 16), np.uint16)
+        return x.append(items, z, z), None
+    if op == "inval":
+        rid, new = args
+        if is_lib:
+            try:
+                return s2l.OK, x.invalidate_lcp(rid, new)
+            except s2l.S2LError as e:
+                return e.status, None
+        st, p, inv = x.invalidate_lcp(rid, new)
+        return st, ((p, inv) if st == O.OK else None)
+    if op in ("swap_out", "swap_in"):
+        rids = args
+        if is_lib:
+            try:
+                return s2l.OK, getattr(x, op)(rids)
+            except s2l.S2LError as e:
+                return e.status, None
+        st, b = getattr(x, op)(rids)
+        return st, (b if st == O.OK else None)
+    if op == "release":
+        return (s2l.status_of(x.release, args), None) if is_lib else (x.release(args), None)
+    if op == "preempt":
+        return (s2l.status_of(x.preempt_recompute, args), None) if is_lib else (x.preempt_recompute(args), None)
+    raise ValueError(op)
+
+
+@pytest.mark.parametrize("aligned", [False, True])
+def test_fuzz_10000_steps_bit_exact(aligned):
+    """Random interleavings of every bookkeeping call: library == oracle after every step."""
+    rng = random.Random(11 + aligned)
+    lib, ora = _pair(L=1, h_q=2, h_kv=1, d=16, k=4, ng=24, nc=16, aligned=aligned, max_requests=5,
+                     max_blocks=12)
+    for step in range(10000):
+        op = rng.choice(["new", "append", "append", "append", "inval", "swap_out", "swap_in",
+                         "release", "preempt"])
+        rid = rng.randrange(7)
+        if op == "new":
+            args = (rid, [rng.randrange(3) for _ in range(rng.randrange(0, 6))])
+        elif op == "append":
+            items = []
+            for r in rng.sample(range(7), rng.randrange(1, 3)):
+                toks = [rng.randrange(3) for _ in range(rng.randrange(0, 6))] if rng.random() < 0.7 else None
+                pend = (len(ora.reqs[r].input) - ora.reqs[r].nc) if r in ora.reqs else 0
+                n_kv = rng.randrange(0, pend + (len(toks) if toks else 0) + 2)
+                items.append((r, toks, n_kv, rng.randrange(0, 8)))
+            if rng.random() < 0.05:
+                items.append(items[0])                      # duplicate -> E_INVAL
+            args = items
+        elif op == "inval":
+            base = ora.reqs[rid].input if rid in ora.reqs else []
+            args = (rid, list(base[: rng.randrange(0, len(base) + 1)]) + [rng.randrange(3) for _ in range(rng.randrange(0, 8))])
+        elif op in ("swap_out", "swap_in"):
+            args = rng.sample(range(7), rng.randrange(0, 3))
+        else:
+            args = rid
+        a = _apply(lib, op, args)
+        b = _apply(ora, op, args)
+        assert a == b, (step, op, args, a, b)
+        _same_state(lib, ora)
