@@ -31,6 +31,9 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+#include <cstring>
+
 namespace s2l {
 namespace {
 
@@ -162,6 +165,24 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
       "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
       "%28, %29, %30, %31, %32};" ::"r"(taddr),
       S2L_W32(r)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() {
@@ -436,6 +457,306 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ======================================================================================
+// v2: two Q tiles per CTA ping-ponged through the tensor core (the softmax of one tile runs
+// while the MMAs of the other execute), P kept in TMEM (TS-MMA: A operand = P from TMEM,
+// aliasing the first 64 columns of that tile's S buffer), one unified K/V TMA ring of 5
+// 32-KB slots, packed f32x2 FMA / ADD in the softmax, setmaxnreg to give the two softmax
+// warpgroups 224 registers.  384 threads: warpgroup 0 = producer (warp 0), MMA issuer
+// (warp 1), TMEM allocator (warp 2); warpgroup 1 = softmax/epilogue of Q tile 0;
+// warpgroup 2 = softmax/epilogue of Q tile 1.
+// Hand-offs per tile i: MMA commits S_full[i] after S_i(j) (which also covers PV_i(j-1));
+// softmax_i writes P_i(j) into TMEM and arrives P_full[i]; MMA issues PV_i(j) then S_i(j+1)
+// (in-order tensor pipe: PV_i(j) reads P_i(j) before S_i(j+1) overwrites those columns).
+namespace v2 {
+constexpr int kThreads = 320;
+constexpr int WNST = 5;
+constexpr uint32_t WOFF_Q0 = 0;
+constexpr uint32_t WOFF_Q1 = kTileBytes;
+constexpr uint32_t WOFF_RING = 2 * kTileBytes;
+constexpr uint32_t WOFF_BAR = WOFF_RING + WNST * kTileBytes;
+// barriers: 0 Q_full, 1..WNST ring_full, WNST+1..2NST ring_empty, then S_full[2], P_full[2], O_fin[2]
+constexpr uint32_t WB_QF = 0, WB_RF = 1, WB_RE = 1 + WNST, WB_SF = 1 + 2 * WNST, WB_PF = WB_SF + 2,
+                   WB_OF = WB_PF + 2, WNBARS = WB_OF + 2;
+constexpr uint32_t WOFF_TMEM = WOFF_BAR + WNBARS * 8;
+constexpr uint32_t SMEM = WOFF_TMEM + 16 + 1024;
+}  // namespace v2
+
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__global__ void __launch_bounds__(v2::kThreads, 1)
+    attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                    const __grid_constant__ CUtensorMap tmap_kv, const TcParams p) {
+  using namespace v2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sb = smem_u32(smem);
+  auto bar = [&](uint32_t i) { return sb + WOFF_BAR + 8u * i; };
+  uint32_t* tmem_holder = (uint32_t*)(smem + WOFF_TMEM);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- work unit: (item, kv head, pair of Q tiles), longest first
+  const int32_t unit = blockIdx.x;
+  int32_t lo = 0, hi = p.n_items - 1;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (p.items[mid].unit_begin <= unit) lo = mid; else hi = mid - 1;
+  }
+  const AttnItemDev it = p.items[lo];
+  const int32_t local = unit - it.unit_begin;
+  const int32_t pairs = (it.tiles + 1) >> 1;
+  const int32_t pair = pairs - 1 - local / p.h_kv;
+  const int32_t kvh = local % p.h_kv;
+  const int32_t G = p.group;
+  const int32_t toks = kBM / G;
+  const int32_t tok0 = pair * 2 * toks;               // first token of tile 0; tile 1 at +toks
+  const int32_t tok_last = min(tok0 + 2 * toks, it.n_q) - 1;
+  const int64_t key_last = it.q_pos + tok_last;
+  const int32_t nT = (int32_t)(key_last / kBN) + 1;
+  const int64_t kv_len = it.q_pos + it.n_q;
+  const int32_t nblk_valid = (int32_t)((kv_len + p.kb - 1) / p.kb);
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar(WB_QF), 1);
+    for (int s = 0; s < WNST; ++s) {
+      mbar_init(bar(WB_RF + s), 1);
+      mbar_init(bar(WB_RE + s), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(WB_SF + i), 1);
+      mbar_init(bar(WB_PF + i), 128);
+      mbar_init(bar(WB_OF + i), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp < 2) {
+    if (warp == 0) {
+      // ================= TMA producer =================
+      if (lane == 0) {
+        mbar_expect_tx(bar(WB_QF), 2 * kTileBytes);
+        const int32_t z = (int32_t)(it.q_row + tok0);
+        tma_load_3d(sb + WOFF_Q0, &tmap_q, bar(WB_QF), 0, kvh * G, z);
+        tma_load_3d(sb + WOFF_Q0 + kAtom, &tmap_q, bar(WB_QF), 64, kvh * G, z);
+        tma_load_3d(sb + WOFF_Q1, &tmap_q, bar(WB_QF), 0, kvh * G, z + toks);
+        tma_load_3d(sb + WOFF_Q1 + kAtom, &tmap_q, bar(WB_QF), 64, kvh * G, z + toks);
+      }
+      const int32_t nb_tile = kBN / p.kb;
+      const int32_t* trow = p.table + (int64_t)it.slot * p.max_blocks;
+      const int32_t rows_per_block = p.L * 2 * p.h_kv * p.kb;
+      const int32_t row_kv[2] = {((p.layer * 2 + 0) * p.h_kv + kvh) * p.kb,
+                                 ((p.layer * 2 + 1) * p.h_kv + kvh) * p.kb};
+      const int32_t blk_i = lane >> 1, half = lane & 1;
+      uint32_t rp = 0;
+      for (int32_t j = 0; j < nT; ++j) {
+        int32_t bid = 0;
+        if (lane < nb_tile) {
+          const int32_t b = j * nb_tile + lane;
+          bid = __ldg(trow + (b < nblk_valid ? b : 0));
+        }
+        const int32_t id = __shfl_sync(0xffffffffu, bid, blk_i);
+#pragma unroll
+        for (int kind = 0; kind < 2; ++kind, ++rp) {
+          const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
+          mbar_wait(bar(WB_RE + s), ph ^ 1);
+          if (lane == 0) mbar_expect_tx(bar(WB_RF + s), kTileBytes);
+          __syncwarp();
+          if (lane < 2 * nb_tile)
+            tma_load_2d(sb + WOFF_RING + s * kTileBytes + half * kAtom + blk_i * p.kb * 128,
+                        &tmap_kv, bar(WB_RF + s), half * 64, id * rows_per_block + row_kv[kind]);
+        }
+      }
+    } else if (warp == 1) {
+      // ================= MMA issuer (one thread) =================
+      if (lane == 0) {
+        constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);
+        constexpr uint32_t idesc_o = idesc_bf16(kBM, kD, 0, 1);
+        uint32_t rp = 0;
+        auto next_full = [&]() {
+          const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
+          ++rp;
+          mbar_wait(bar(WB_RF + s), ph);
+          tc_fence_after();
+          return s;
+        };
+        auto issue_s = [&](int i, uint32_t kslot) {
+          const uint32_t qb = sb + (i ? WOFF_Q1 : WOFF_Q0);
+          const uint32_t kbase = sb + WOFF_RING + kslot * kTileBytes;
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
+            mma_bf16(tmem + i * 128, sdesc(qb + off, 16, 1024), sdesc(kbase + off, 16, 1024),
+                     idesc_s, kk > 0);
+          }
+          mma_commit(bar(WB_SF + i));
+        };
+        auto issue_pv = [&](int i, uint32_t vslot, int32_t j) {
+          const uint32_t vbase = sb + WOFF_RING + vslot * kTileBytes;
+#pragma unroll
+          for (int kk = 0; kk < kBN / 16; ++kk)
+            mma_bf16_ts(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8,
+                        sdesc(vbase + kk * 16 * 128, kAtom, 1024), idesc_o, (j > 0 || kk > 0));
+        };
+        mbar_wait(bar(WB_QF), 0);
+        tc_fence_after();
+        uint32_t kslot = next_full();
+        issue_s(0, kslot);
+        issue_s(1, kslot);
+        mma_commit(bar(WB_RE + kslot));
+        for (int32_t j = 0; j < nT; ++j) {
+          const uint32_t vslot = next_full();
+          mbar_wait(bar(WB_PF + 0), j & 1);
+          tc_fence_after();
+          issue_pv(0, vslot, j);
+          const bool more = j + 1 < nT;
+          if (more) {
+            kslot = next_full();
+            issue_s(0, kslot);
+          } else {
+            mma_commit(bar(WB_OF + 0));
+          }
+          mbar_wait(bar(WB_PF + 1), j & 1);
+          tc_fence_after();
+          issue_pv(1, vslot, j);
+          mma_commit(bar(WB_RE + vslot));
+          if (more) {
+            issue_s(1, kslot);
+            mma_commit(bar(WB_RE + kslot));
+          } else {
+            mma_commit(bar(WB_OF + 1));
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    // ================= softmax / correction / epilogue of Q tile i =================
+    const int i = (warp - 2) >> 2;                   // 0: warps 2-5, 1: warps 6-9
+    const int r = (warp & 3) * 32 + lane;            // tile row == TMEM lane
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane_off + i * 128;
+    const uint32_t tO = tmem + lane_off + TMEM_O + i * 128;
+    const int32_t tok = tok0 + i * toks + r / G;
+    const int32_t hq = kvh * G + r % G;
+    const bool valid = tok < it.n_q;
+    const int64_t limit = it.q_pos + (valid ? tok : tok_last);
+    const float sl2 = p.scale_log2;
+    float m_run = -INFINITY, l_run = 0.f;
+    uint32_t sv[128];
+    for (int32_t j = 0; j < nT; ++j) {
+      mbar_wait(bar(WB_SF + i), j & 1);
+      tc_fence_after();
+      tmem_ld32(tS, sv);
+      tmem_ld32(tS + 32, sv + 32);
+      tmem_ld32(tS + 64, sv + 64);
+      tmem_ld32(tS + 96, sv + 96);
+      tmem_wait_ld();
+      const int64_t key0 = (int64_t)j * kBN;
+      if (key0 + kBN - 1 > limit) {
+        const int32_t vis = (int32_t)(limit - key0);
+#pragma unroll
+        for (int c = 0; c < kBN; ++c)
+          if (c > vis) sv[c] = __float_as_uint(-INFINITY);
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kBN; ++c) mx = fmaxf(mx, __uint_as_float(sv[c]));
+      mx *= sl2;
+      const float m_new = (mx > m_run + kRescaleThresh) ? mx : m_run;
+      if (j > 0) {
+        const bool resc = m_new != m_run;
+        if (__any_sync(0xffffffffu, resc)) {
+          const float alpha = resc ? fast_exp2(m_run - m_new) : 1.f;
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            uint32_t ov[16];
+            tmem_ld16(tO + c * 16, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              float2 x = __fmul2_rn(make_float2(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])),
+                                    make_float2(alpha, alpha));
+              ov[e] = __float_as_uint(x.x);
+              ov[e + 1] = __float_as_uint(x.y);
+            }
+            tmem_st16(tO + c * 16, ov);
+          }
+          l_run *= alpha;
+        }
+      }
+      m_run = m_new;
+      const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_run, -m_run);
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int e = cc * 32 + 2 * c;
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])),
+                                      sc2, nm2);
+          const float p0 = fast_exp2(x.x), p1 = fast_exp2(x.y);
+          acc = __fadd2_rn(acc, make_float2(p0, p1));
+          pk[c] = pack_bf16(p0, p1);
+        }
+        tmem_st16(tS + cc * 16, pk);
+      }
+      l_run += acc.x + acc.y;
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar(WB_PF + i));
+    }
+    // epilogue
+    mbar_wait(bar(WB_OF + i), 0);
+    tc_fence_after();
+    const float inv = 1.f / l_run;
+    __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      uint32_t ov[16];
+      tmem_ld16(tO + c * 16, ov);
+      tmem_wait_ld();
+      if (valid) {
+        uint32_t w[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          w[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      }
+    }
+    if (valid && p.lse)
+      p.lse[(it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn(const char** err) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -499,16 +820,27 @@ bool make_tmap_q(void* out, const void* q, int64_t q_rows, int32_t h_q, int32_t 
   return true;
 }
 
+int attn_tc_tiles_per_cta() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("S2L_ATTN_V1");
+    v = (e && e[0] == '1') ? 1 : 2;
+  }
+  return v;
+}
+
 cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t n_items,
                            int32_t total_units, const int32_t* table, int32_t layer,
                            const void* tmap_q, const void* tmap_kv, void* o, float* lse,
                            cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  const int variant = attn_tc_tiles_per_cta();
+  static bool attr_set[3] = {false, false, false};
+  if (!attr_set[variant]) {
+    cudaError_t e = variant == 2
+        ? cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM)
+        : cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[variant] = true;
   }
   if (total_units <= 0) return cudaSuccess;
   TcParams p{};
@@ -528,7 +860,10 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
   CUtensorMap tq, tkv;
   memcpy(&tq, tmap_q, sizeof(CUtensorMap));
   memcpy(&tkv, tmap_kv, sizeof(CUtensorMap));
-  attn_tc_kernel<<<total_units, kThreads, SMEM_BYTES, st>>>(tq, tkv, p);
+  if (variant == 2)
+    attn_tc2_kernel<<<total_units, v2::kThreads, v2::SMEM, st>>>(tq, tkv, p);
+  else
+    attn_tc_kernel<<<total_units, kThreads, SMEM_BYTES, st>>>(tq, tkv, p);
   return cudaGetLastError();
 }
 

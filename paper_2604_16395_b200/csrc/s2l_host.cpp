@@ -702,6 +702,7 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
     return items[x].q_pos + items[x].n_q > items[y].q_pos + items[y].n_q;
   });
   std::vector<s2l::AttnItemDev> dev(n_items);
+  const int64_t tiles_per_cta = c->tc_ok ? s2l::attn_tc_tiles_per_cta() : 1;
   int64_t units = 0, total_q = 0;
   for (int32_t i = 0; i < n_items; ++i) {
     const s2l_prefill_item& it = items[order[i]];
@@ -713,7 +714,7 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
     d.slot = r->slot;
     d.tiles = (int32_t)ceil_div(it.n_q * G, 128);
     d.unit_begin = (int32_t)units;
-    units += (int64_t)d.tiles * c->cfg.num_kv_heads;
+    units += ceil_div(d.tiles, tiles_per_cta) * c->cfg.num_kv_heads;
     total_q += it.n_q;
   }
   if (units >= (1ll << 31)) return fail(S2L_E_INVAL, "batch too large");

@@ -61,6 +61,8 @@ cudaError_t launch_attn_generic(const Geometry& g, const AttnItemDev* items, int
 // tcgen05 / TMEM / TMA attention (head_dim 128, 16 <= k <= 128, 128 % (h_q/h_kv) == 0).
 // tmap_q / tmap_kv point to host CUtensorMap (128-byte) objects passed by value.
 bool attn_tc_supported(const Geometry& g);
+// Q tiles per CTA of the tensor-core kernel (2 = ping-pong v2, default; 1 = v1 via S2L_ATTN_V1=1).
+int attn_tc_tiles_per_cta();
 cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t n_items,
                            int32_t total_units, const int32_t* table, int32_t layer,
                            const void* tmap_q, const void* tmap_kv, void* o, float* lse,
