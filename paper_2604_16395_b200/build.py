@@ -45,6 +45,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(bdir, exist_ok=True)
     common = [nvcc(), "-std=c++17", "-O3", ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O3",
               "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(PKG, "csrc")]
+    common += os.environ.get("S2L_NVCC_FLAGS", "").split()   # experiments only (e.g. -DS2L_POLY_PAIRS=2)
     procs = []
     for src in sources():
         obj = os.path.join(bdir, os.path.basename(src) + ".o")

@@ -66,6 +66,12 @@ struct TcParams {
   float* lse;
   int32_t n_items, max_blocks, layer, L, h_q, h_kv, kb, group;
   float scale_log2;
+  // tail-wave KV split (v2): CTAs >= split_begin are pieces of units split into split_s
+  // contiguous KV ranges; partials go to ws, the last piece of a unit merges (ws_cnt).
+  int32_t split_begin, split_s;
+  float* ws;       // [pieces][2][128][128] partial O (unnormalised, fp32)
+  float* ws_ml;    // [pieces][2][128][2] running max (log2 units) and row sum
+  int32_t* ws_cnt;
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -82,16 +88,25 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
-      "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE;\n\t"
-      "bra LAB_WAIT;\n\t"
-      "DONE:\n\t}" ::"r"(bar),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// Blocking wait with a watchdog: a protocol bug traps (kernel error) after ~2^26 timed-out
+// try_waits (seconds) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
+  uint32_t n = 0;
+  while (!mbar_try(bar, parity)) {
+    if (++n == (1u << 26)) __trap();
+  }
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint32_t bar,
                                             int32_t x, int32_t y) {
@@ -195,6 +210,25 @@ __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA pipe for a pair (offloads MUFU.EX2, the softmax bottleneck at d = 128):
+// round-to-nearest split x = n + f with the 1.5*2^23 trick, f in [-0.5, 0.5], degree-3
+// polynomial for 2^f (relative error <= 7.6e-5, fitted to 2^f on [-0.5, 0.5]), exponent
+// added as an integer (n << 23).  x is clamped to >= -127 (result ~0 there); callers use it
+// only on tiles without masked (-inf) scores.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 y = __fadd2_rn(x, magic);
+  const float2 t = __fadd2_rn(y, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-t.x, -t.y));
+  float2 q = __ffma2_rn(f, make_float2(0.0551704f, 0.0551704f), make_float2(0.24260826f, 0.24260826f));
+  q = __ffma2_rn(q, f, make_float2(0.69326098f, 0.69326098f));
+  q = __ffma2_rn(q, f, make_float2(0.99992833f, 0.99992833f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(y.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(y.y) << 23)));
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
@@ -457,6 +491,94 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ---- softmax helpers for v2 (two passes over a 128-column S row in 32-column chunks) ----
+template <bool kMasked>
+__device__ __forceinline__ float chunk_max(const uint32_t (&v)[32], float mx, int vis, int base) {
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    float x = __uint_as_float(v[c]);
+    if (kMasked && base + c > vis) x = -INFINITY;
+    mx = fmaxf(mx, x);
+  }
+  return mx;
+}
+// p = 2^(s*scale - m) for 32 columns; returns the running pair sum, writes 16 packed bf16x2.
+template <bool kMasked, int kPolyPer8>
+__device__ __forceinline__ float2 chunk_p(const uint32_t (&v)[32], float2 acc, int vis, int base,
+                                          float2 sc2, float2 nm2, uint32_t (&pk)[16]) {
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    float s0 = __uint_as_float(v[2 * c]), s1 = __uint_as_float(v[2 * c + 1]);
+    if (kMasked) {
+      if (base + 2 * c > vis) s0 = -INFINITY;
+      if (base + 2 * c + 1 > vis) s1 = -INFINITY;
+    }
+    const float2 x = __ffma2_rn(make_float2(s0, s1), sc2, nm2);
+    float2 pp;
+    if (!kMasked && (c & 7) < kPolyPer8) pp = exp2_poly2(x);
+    else pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+    acc = __fadd2_rn(acc, pp);
+    pk[c] = pack_bf16(pp.x, pp.y);
+  }
+  return acc;
+}
+// Row max of the tile (pass 1) with the next chunk's TMEM load in flight.
+template <bool kMasked>
+__device__ __forceinline__ float tile_max(uint32_t tS, int vis) {
+  uint32_t a[32], b[32];
+  float mx = -INFINITY;
+  tmem_ld32(tS, a);
+  tmem_wait_ld();
+  tmem_ld32(tS + 32, b);
+  mx = chunk_max<kMasked>(a, mx, vis, 0);
+  tmem_wait_ld();
+  tmem_ld32(tS + 64, a);
+  mx = chunk_max<kMasked>(b, mx, vis, 32);
+  tmem_wait_ld();
+  tmem_ld32(tS + 96, b);
+  mx = chunk_max<kMasked>(a, mx, vis, 64);
+  tmem_wait_ld();
+  return chunk_max<kMasked>(b, mx, vis, 96);
+}
+// P of the tile (pass 2): re-reads S, writes P (bf16) over S columns [0, 64) of this lane.
+template <bool kMasked, int kPolyPer8>
+__device__ __forceinline__ float tile_p(uint32_t tS, int vis, float2 sc2, float2 nm2) {
+  uint32_t a[32], b[32], pk[16];
+  float2 acc = make_float2(0.f, 0.f);
+  tmem_ld32(tS, a);
+  tmem_wait_ld();
+  tmem_ld32(tS + 32, b);
+  acc = chunk_p<kMasked, kPolyPer8>(a, acc, vis, 0, sc2, nm2, pk);
+  tmem_st16(tS, pk);
+  tmem_wait_ld();
+  tmem_ld32(tS + 64, a);
+  acc = chunk_p<kMasked, kPolyPer8>(b, acc, vis, 32, sc2, nm2, pk);
+  tmem_st16(tS + 16, pk);
+  tmem_wait_ld();
+  tmem_ld32(tS + 96, b);
+  acc = chunk_p<kMasked, kPolyPer8>(a, acc, vis, 64, sc2, nm2, pk);
+  tmem_st16(tS + 32, pk);
+  tmem_wait_ld();
+  acc = chunk_p<kMasked, kPolyPer8>(b, acc, vis, 96, sc2, nm2, pk);
+  tmem_st16(tS + 48, pk);
+  return acc.x + acc.y;
+}
+
+// Single-pass variant: the whole 128-column row is in registers (needs ~200 registers; the
+// softmax warpgroups get kRegSoftmax via setmaxnreg).
+template <bool kMasked, int kPolyPer8>
+__device__ __forceinline__ float row_p(uint32_t (&sv)[128], uint32_t tS, int vis, float2 sc2, float2 nm2) {
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) {
+    uint32_t pk[16];
+    acc = chunk_p<kMasked, kPolyPer8>(*reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc), acc, vis,
+                                      32 * cc, sc2, nm2, pk);
+    tmem_st16(tS + 16 * cc, pk);
+  }
+  return acc.x + acc.y;
+}
 // ======================================================================================
 // v2: two Q tiles per CTA ping-ponged through the tensor core (the softmax of one tile runs
 // while the MMAs of the other execute), P kept in TMEM (TS-MMA: A operand = P from TMEM,
@@ -469,7 +591,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 // softmax_i writes P_i(j) into TMEM and arrives P_full[i]; MMA issues PV_i(j) then S_i(j+1)
 // (in-order tensor pipe: PV_i(j) reads P_i(j) before S_i(j+1) overwrites those columns).
 namespace v2 {
-constexpr int kThreads = 320;
+constexpr int kThreads = 384;
+// setmaxnreg moves registers inside the CTA's launch allocation (384 x 168): the control
+// warpgroup releases first, the softmax warpgroups then grow; the sums must fit the pool or
+// setmaxnreg.inc waits forever.
+constexpr int kRegLaunch = 168, kRegCtrl = 88, kRegSoftmax = 208;
+static_assert(128 * kRegCtrl + 256 * kRegSoftmax <= kThreads * kRegLaunch, "register pool");
+#ifndef S2L_POLY_PAIRS
+#define S2L_POLY_PAIRS 2
+#endif
+constexpr int kPolyPairsPer8 = S2L_POLY_PAIRS;   // of every 8 exp2 pairs, this many on the FMA pipe
 constexpr int WNST = 5;
 constexpr uint32_t WOFF_Q0 = 0;
 constexpr uint32_t WOFF_Q1 = kTileBytes;
@@ -491,6 +622,35 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+
+// Warp-wide MMA issue: every lane of the MMA warp executes the loop with warp-uniform
+// operands (kept in uniform registers); elect.sync picks one lane (always the same, lane 0,
+// with the full warp converged) to issue tcgen05.mma / tcgen05.commit.
+__device__ __forceinline__ void mma_ss_elect(uint32_t d_tmem, uint64_t a, uint64_t b,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+      : "memory");
+}
 __global__ void __launch_bounds__(v2::kThreads, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_kv, const TcParams p) {
@@ -503,7 +663,13 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // ---- work unit: (item, kv head, pair of Q tiles), longest first
-  const int32_t unit = blockIdx.x;
+  int32_t unit = blockIdx.x, piece = 0, npieces = 1;
+  if (unit >= p.split_begin) {
+    const int32_t b = unit - p.split_begin;
+    unit = p.split_begin + b / p.split_s;
+    piece = b % p.split_s;
+    npieces = p.split_s;
+  }
   int32_t lo = 0, hi = p.n_items - 1;
   while (lo < hi) {
     const int32_t mid = (lo + hi + 1) >> 1;
@@ -519,7 +685,9 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
   const int32_t tok0 = pair * 2 * toks;               // first token of tile 0; tile 1 at +toks
   const int32_t tok_last = min(tok0 + 2 * toks, it.n_q) - 1;
   const int64_t key_last = it.q_pos + tok_last;
-  const int32_t nT = (int32_t)(key_last / kBN) + 1;
+  const int32_t nT_all = (int32_t)(key_last / kBN) + 1;
+  const int32_t jb = (int32_t)((int64_t)nT_all * piece / npieces);   // this CTA's KV tiles
+  const int32_t nT = (int32_t)((int64_t)nT_all * (piece + 1) / npieces) - jb;
   const int64_t kv_len = it.q_pos + it.n_q;
   const int32_t nblk_valid = (int32_t)((kv_len + p.kb - 1) / p.kb);
 
@@ -549,7 +717,8 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  if (warp < 2) {
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtrl));
     if (warp == 0) {
       // ================= TMA producer =================
       if (lane == 0) {
@@ -570,7 +739,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       for (int32_t j = 0; j < nT; ++j) {
         int32_t bid = 0;
         if (lane < nb_tile) {
-          const int32_t b = j * nb_tile + lane;
+          const int32_t b = (jb + j) * nb_tile + lane;
           bid = __ldg(trow + (b < nblk_valid ? b : 0));
         }
         const int32_t id = __shfl_sync(0xffffffffu, bid, blk_i);
@@ -586,71 +755,73 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         }
       }
     } else if (warp == 1) {
-      // ================= MMA issuer (one thread) =================
-      if (lane == 0) {
-        constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);
-        constexpr uint32_t idesc_o = idesc_bf16(kBM, kD, 0, 1);
-        uint32_t rp = 0;
-        auto next_full = [&]() {
-          const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
-          ++rp;
-          mbar_wait(bar(WB_RF + s), ph);
-          tc_fence_after();
-          return s;
-        };
-        auto issue_s = [&](int i, uint32_t kslot) {
-          const uint32_t qb = sb + (i ? WOFF_Q1 : WOFF_Q0);
-          const uint32_t kbase = sb + WOFF_RING + kslot * kTileBytes;
-#pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
-            mma_bf16(tmem + i * 128, sdesc(qb + off, 16, 1024), sdesc(kbase + off, 16, 1024),
-                     idesc_s, kk > 0);
-          }
-          mma_commit(bar(WB_SF + i));
-        };
-        auto issue_pv = [&](int i, uint32_t vslot, int32_t j) {
-          const uint32_t vbase = sb + WOFF_RING + vslot * kTileBytes;
-#pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk)
-            mma_bf16_ts(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8,
-                        sdesc(vbase + kk * 16 * 128, kAtom, 1024), idesc_o, (j > 0 || kk > 0));
-        };
-        mbar_wait(bar(WB_QF), 0);
+      // ================= MMA issuer (whole warp, one elected lane issues) =================
+      constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16(kBM, kD, 0, 1);
+      // descriptors of the buffer bases; the start-address field (bits 0-13, 16-byte units)
+      // is advanced by adding (byte offset >> 4) — smem addresses stay below 256 KB
+      const uint64_t dq[2] = {sdesc(sb + WOFF_Q0, 16, 1024), sdesc(sb + WOFF_Q1, 16, 1024)};
+      const uint64_t dk0 = sdesc(sb + WOFF_RING, 16, 1024);
+      const uint64_t dv0 = sdesc(sb + WOFF_RING, kAtom, 1024);
+      uint32_t rp = 0;
+      auto next_full = [&]() {
+        const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
+        ++rp;
+        mbar_wait(bar(WB_RF + s), ph);
         tc_fence_after();
-        uint32_t kslot = next_full();
-        issue_s(0, kslot);
-        issue_s(1, kslot);
-        mma_commit(bar(WB_RE + kslot));
-        for (int32_t j = 0; j < nT; ++j) {
-          const uint32_t vslot = next_full();
-          mbar_wait(bar(WB_PF + 0), j & 1);
-          tc_fence_after();
-          issue_pv(0, vslot, j);
-          const bool more = j + 1 < nT;
-          if (more) {
-            kslot = next_full();
-            issue_s(0, kslot);
-          } else {
-            mma_commit(bar(WB_OF + 0));
-          }
-          mbar_wait(bar(WB_PF + 1), j & 1);
-          tc_fence_after();
-          issue_pv(1, vslot, j);
-          mma_commit(bar(WB_RE + vslot));
-          if (more) {
-            issue_s(1, kslot);
-            mma_commit(bar(WB_RE + kslot));
-          } else {
-            mma_commit(bar(WB_OF + 1));
-          }
+        return s;
+      };
+      auto issue_s = [&](int i, uint32_t kslot) {
+        const uint64_t kd = dk0 + ((kslot * kTileBytes) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const uint32_t off = ((kk >> 2) * kAtom + (kk & 3) * 32) >> 4;
+          mma_ss_elect(tmem + i * 128, dq[i] + off, kd + off, idesc_s, kk > 0);
+        }
+        mma_commit_elect(bar(WB_SF + i));
+      };
+      auto issue_pv = [&](int i, uint32_t vslot, int32_t j) {
+        const uint64_t vd = dv0 + ((vslot * kTileBytes) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
+                       idesc_o, (j > 0 || kk > 0));
+      };
+      mbar_wait(bar(WB_QF), 0);
+      tc_fence_after();
+      uint32_t kslot = next_full();
+      issue_s(0, kslot);
+      issue_s(1, kslot);
+      mma_commit_elect(bar(WB_RE + kslot));
+      for (int32_t j = 0; j < nT; ++j) {
+        const uint32_t vslot = next_full();
+        mbar_wait(bar(WB_PF + 0), j & 1);
+        tc_fence_after();
+        issue_pv(0, vslot, j);
+        const bool more = j + 1 < nT;
+        if (more) {
+          kslot = next_full();
+          issue_s(0, kslot);
+        } else {
+          mma_commit_elect(bar(WB_OF + 0));
+        }
+        mbar_wait(bar(WB_PF + 1), j & 1);
+        tc_fence_after();
+        issue_pv(1, vslot, j);
+        mma_commit_elect(bar(WB_RE + vslot));
+        if (more) {
+          issue_s(1, kslot);
+          mma_commit_elect(bar(WB_RE + kslot));
+        } else {
+          mma_commit_elect(bar(WB_OF + 1));
         }
       }
       __syncwarp();
     }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
     // ================= softmax / correction / epilogue of Q tile i =================
-    const int i = (warp - 2) >> 2;                   // 0: warps 2-5, 1: warps 6-9
+    const int i = (warp - 4) >> 2;                   // 0: warps 4-7, 1: warps 8-11
     const int r = (warp & 3) * 32 + lane;            // tile row == TMEM lane
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t tS = tmem + lane_off + i * 128;
@@ -661,25 +832,34 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     const int64_t limit = it.q_pos + (valid ? tok : tok_last);
     const float sl2 = p.scale_log2;
     float m_run = -INFINITY, l_run = 0.f;
-    uint32_t sv[128];
     for (int32_t j = 0; j < nT; ++j) {
       mbar_wait(bar(WB_SF + i), j & 1);
       tc_fence_after();
+#ifdef S2L_EXP_MMA_ONLY   // timing experiment only: tensor-core / TMA pipeline without softmax
+      tc_fence_before();
+      mbar_arrive(bar(WB_PF + i));
+      continue;
+#endif
+      const int64_t key0 = (int64_t)(jb + j) * kBN;
+      const int64_t vis64 = limit - key0;                 // keys c <= vis of this tile visible
+      const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBN ? kBN : vis64));
+      const bool masked_tile = __any_sync(0xffffffffu, vis < kBN - 1);
+      uint32_t sv[128];
       tmem_ld32(tS, sv);
       tmem_ld32(tS + 32, sv + 32);
       tmem_ld32(tS + 64, sv + 64);
       tmem_ld32(tS + 96, sv + 96);
       tmem_wait_ld();
-      const int64_t key0 = (int64_t)j * kBN;
-      if (key0 + kBN - 1 > limit) {
-        const int32_t vis = (int32_t)(limit - key0);
-#pragma unroll
-        for (int c = 0; c < kBN; ++c)
-          if (c > vis) sv[c] = __float_as_uint(-INFINITY);
-      }
       float mx = -INFINITY;
+      if (masked_tile) {
 #pragma unroll
-      for (int c = 0; c < kBN; ++c) mx = fmaxf(mx, __uint_as_float(sv[c]));
+        for (int cc = 0; cc < 4; ++cc)
+          mx = chunk_max<true>(*reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc), mx, vis, 32 * cc);
+      } else {
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+          mx = chunk_max<false>(*reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc), mx, vis, 32 * cc);
+      }
       mx *= sl2;
       const float m_new = (mx > m_run + kRescaleThresh) ? mx : m_run;
       if (j > 0) {
@@ -704,23 +884,11 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         }
       }
       m_run = m_new;
-      const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_run, -m_run);
-      float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const int e = cc * 32 + 2 * c;
-          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[e]), __uint_as_float(sv[e + 1])),
-                                      sc2, nm2);
-          const float p0 = fast_exp2(x.x), p1 = fast_exp2(x.y);
-          acc = __fadd2_rn(acc, make_float2(p0, p1));
-          pk[c] = pack_bf16(p0, p1);
-        }
-        tmem_st16(tS + cc * 16, pk);
-      }
-      l_run += acc.x + acc.y;
+      // a row with no visible key yet (possible in a split piece) keeps m = -inf and p = 0
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_use, -m_use);
+      l_run += masked_tile ? row_p<true, 0>(sv, tS, vis, sc2, nm2)
+                           : row_p<false, kPolyPairsPer8>(sv, tS, vis, sc2, nm2);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(bar(WB_PF + i));
@@ -728,25 +896,105 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     // epilogue
     mbar_wait(bar(WB_OF + i), 0);
     tc_fence_after();
-    const float inv = 1.f / l_run;
     __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
+    if (npieces == 1) {
+      const float inv = 1.f / l_run;
 #pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
-      uint32_t ov[16];
-      tmem_ld16(tO + c * 16, ov);
-      tmem_wait_ld();
-      if (valid) {
-        uint32_t w[8];
+      for (int c = 0; c < 8; ++c) {
+        uint32_t ov[16];
+        tmem_ld16(tO + c * 16, ov);
+        tmem_wait_ld();
+        if (valid) {
+          uint32_t w[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          w[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
-        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          for (int e = 0; e < 8; ++e)
+            w[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      }
+      if (valid && p.lse)
+        p.lse[(it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+    } else {
+      // partial (unnormalised O, m, l) of this KV range -> workspace; the last piece merges
+      const int32_t su = unit - p.split_begin;                 // split-unit index
+      const int64_t prow = (((int64_t)su * npieces + piece) * 2 + i) * 128 + r;
+      float* wo = p.ws + prow * kD;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t ov[16];
+        tmem_ld16(tO + c * 16, ov);
+        tmem_wait_ld();
+        float4* dst = reinterpret_cast<float4*>(wo + c * 16);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
+                               __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
+      }
+      p.ws_ml[prow * 2] = m_run;
+      p.ws_ml[prow * 2 + 1] = l_run;
+      __threadfence();
+      asm volatile("bar.sync 1, 256;" ::: "memory");       // both softmax warpgroups wrote
+      uint32_t* flag = (uint32_t*)(smem + WOFF_TMEM + 8);
+      if (threadIdx.x == 128) {
+        const int32_t old = atomicAdd(p.ws_cnt + su, 1);
+        const uint32_t last = (old == npieces - 1) ? 1u : 0u;
+        if (last) p.ws_cnt[su] = 0;                          // ready for the next launch
+        *flag = last;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (*flag) {
+        __threadfence();
+        float M = -INFINITY;
+        for (int k = 0; k < npieces; ++k) {
+          const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
+          M = fmaxf(M, __ldcg(p.ws_ml + pr * 2));
+        }
+        constexpr int kMaxPieces = 8;
+        float wk[kMaxPieces];
+        float Lsum = 0.f;
+#pragma unroll
+        for (int k = 0; k < kMaxPieces; ++k) {
+          wk[k] = 0.f;
+          if (k < npieces) {
+            const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
+            wk[k] = fast_exp2(__ldcg(p.ws_ml + pr * 2) - M);
+            Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
+          }
+        }
+        const float inv = 1.f / Lsum;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kD; c0 += 32) {
+          float acc[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+#pragma unroll
+          for (int k = 0; k < kMaxPieces; ++k) {
+            if (k < npieces) {
+              const float* po = p.ws + ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * kD + c0;
+#pragma unroll
+              for (int c = 0; c < 32; c += 2) {
+                const float2 x = __ldcg(reinterpret_cast<const float2*>(po + c));
+                acc[c] += wk[k] * x.x;
+                acc[c + 1] += wk[k] * x.y;
+              }
+            }
+          }
+          if (valid) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) {
+              uint4 v4 = make_uint4(pack_bf16(acc[c] * inv, acc[c + 1] * inv), pack_bf16(acc[c + 2] * inv, acc[c + 3] * inv),
+                                    pack_bf16(acc[c + 4] * inv, acc[c + 5] * inv), pack_bf16(acc[c + 6] * inv, acc[c + 7] * inv));
+              *reinterpret_cast<uint4*>(orow + c0 + c) = v4;
+            }
+          }
+        }
+        if (valid) {
+          if (p.lse) p.lse[(it.q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
+        }
       }
     }
-    if (valid && p.lse)
-      p.lse[(it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
     tc_fence_before();
   }
   __syncthreads();
@@ -830,9 +1078,10 @@ int attn_tc_tiles_per_cta() {
 }
 
 cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t n_items,
-                           int32_t total_units, const int32_t* table, int32_t layer,
-                           const void* tmap_q, const void* tmap_kv, void* o, float* lse,
-                           cudaStream_t st) {
+                           int32_t total_units, int32_t split_begin, int32_t split_s,
+                           float* ws, int32_t max_pieces, int32_t* ws_cnt,
+                           const int32_t* table, int32_t layer, const void* tmap_q,
+                           const void* tmap_kv, void* o, float* lse, cudaStream_t st) {
   const int variant = attn_tc_tiles_per_cta();
   static bool attr_set[3] = {false, false, false};
   if (!attr_set[variant]) {
@@ -860,8 +1109,19 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
   CUtensorMap tq, tkv;
   memcpy(&tq, tmap_q, sizeof(CUtensorMap));
   memcpy(&tkv, tmap_kv, sizeof(CUtensorMap));
+  p.split_begin = total_units;
+  p.split_s = 1;
+  int32_t grid = total_units;
+  if (variant == 2 && split_s > 1 && split_begin < total_units) {
+    p.split_begin = split_begin;
+    p.split_s = split_s;
+    grid = split_begin + (total_units - split_begin) * split_s;
+  }
+  p.ws = ws;
+  p.ws_ml = ws ? ws + (int64_t)max_pieces * 2 * 128 * kD : nullptr;
+  p.ws_cnt = ws_cnt;
   if (variant == 2)
-    attn_tc2_kernel<<<total_units, v2::kThreads, v2::SMEM, st>>>(tq, tkv, p);
+    attn_tc2_kernel<<<grid, v2::kThreads, v2::SMEM, st>>>(tq, tkv, p);
   else
     attn_tc_kernel<<<total_units, kThreads, SMEM_BYTES, st>>>(tq, tkv, p);
   return cudaGetLastError();

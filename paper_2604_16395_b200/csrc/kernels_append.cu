@@ -21,40 +21,58 @@ __global__ void table_patch_kernel(const TablePatch* __restrict__ patches, int32
     table[patches[i].idx] = patches[i].value;
 }
 
+constexpr int kVecPerThread = 8;   // 8 x 16-byte loads in flight per thread, then 8 stores
+
+__device__ __forceinline__ int32_t find_item(const AppendItemDev* __restrict__ items, int32_t n,
+                                             int64_t row) {
+  int32_t lo = 0, hi = n - 1;     // last item with row_begin <= row
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (items[mid].row_begin <= row) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 __global__ void __launch_bounds__(256) append_kernel(
     const AppendItemDev* __restrict__ items, int32_t n_items, int64_t total_vecs_per_lk,
     const int32_t* __restrict__ ids, const TablePatch* __restrict__ patches, int32_t n_patches,
     int32_t* __restrict__ table, const uint4* __restrict__ k, const uint4* __restrict__ v,
     int64_t kv_rows, uint4* __restrict__ pool, int32_t L, int32_t h_kv, int32_t vec_per_row,
-    int32_t kb) {
+    int32_t kb_log2) {
   const int32_t lk = blockIdx.y;          // layer * 2 + kind
   const int32_t layer = lk >> 1, kind = lk & 1;
   if (lk == 0 && blockIdx.x == 0) {
     for (int32_t i = threadIdx.x; i < n_patches; i += blockDim.x) table[patches[i].idx] = patches[i].value;
   }
   const uint4* src = (kind ? v : k) + (int64_t)layer * kv_rows * h_kv * vec_per_row;
-  const int64_t vecs_per_token = (int64_t)h_kv * vec_per_row;
-  const int32_t total = (int32_t)total_vecs_per_lk;   // host checks < 2^31
-  const int32_t vpt = (int32_t)vecs_per_token;
-  for (int32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
-    const int32_t row = g / vpt;                      // token row in the concatenated items
-    const int32_t rem = g - row * vpt;
-    const int32_t head = rem / vec_per_row;
-    const int32_t vec = rem - head * vec_per_row;
-    // item lookup: last item with row_begin <= row
-    int32_t lo = 0, hi = n_items - 1;
-    while (lo < hi) {
-      int32_t mid = (lo + hi + 1) >> 1;
-      if (items[mid].row_begin <= row) lo = mid; else hi = mid - 1;
+  const int32_t vpt = h_kv * vec_per_row;                   // vectors per token row
+  const int32_t total = (int32_t)total_vecs_per_lk;        // host checks < 2^31
+  const int32_t kb = 1 << kb_log2;
+  const int32_t stride = gridDim.x * blockDim.x;
+  for (int32_t g0 = blockIdx.x * blockDim.x + threadIdx.x; g0 < total; g0 += stride * kVecPerThread) {
+    uint4 val[kVecPerThread];
+    int64_t dst[kVecPerThread];
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u) {
+      const int32_t g = g0 + u * stride;
+      dst[u] = -1;
+      if (g < total) {
+        const int32_t row = g / vpt;                        // token row of the concatenation
+        const int32_t rem = g - row * vpt;
+        const int32_t head = rem / vec_per_row;
+        const int32_t vec = rem - head * vec_per_row;
+        const AppendItemDev& it = items[find_item(items, n_items, row)];
+        const int64_t t = (int64_t)row - it.row_begin;
+        const int64_t pos = it.nc + t;
+        const int32_t blk = ids[it.id_off + (int32_t)((pos >> kb_log2) - (it.nc >> kb_log2))];
+        const int32_t slot = (int32_t)(pos & (kb - 1));
+        val[u] = src[((it.kv_row + t) * h_kv + head) * vec_per_row + vec];
+        dst[u] = (((((int64_t)blk * L + layer) * 2 + kind) * h_kv + head) * kb + slot) * vec_per_row + vec;
+      }
     }
-    const AppendItemDev it = items[lo];
-    const int64_t t = (int64_t)row - it.row_begin;
-    const int64_t pos = it.nc + t;
-    const int32_t blk = ids[it.id_off + (int32_t)(pos / kb - it.nc / kb)];
-    const int32_t slot = (int32_t)(pos % kb);
-    const uint4 val = src[((it.kv_row + t) * h_kv + head) * vec_per_row + vec];
-    const int64_t dst = ((((int64_t)blk * L + layer) * 2 + kind) * h_kv + head) * kb + slot;
-    pool[dst * vec_per_row + vec] = val;
+#pragma unroll
+    for (int u = 0; u < kVecPerThread; ++u)
+      if (dst[u] >= 0) pool[dst[u]] = val[u];
   }
 }
 
@@ -76,14 +94,17 @@ cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t
   const int32_t vec_per_row = g.d / 8;
   const int64_t total = total_rows * g.h_kv * vec_per_row;
   if (total >= (1ll << 31)) return cudaErrorInvalidValue;
-  int64_t want = (total + 255) / 256;
-  // enough CTAs to cover the data, capped at 8 waves of 148 SMs x 8 CTAs
-  int64_t cap = 148 * 8 * 8;
-  int blocks = (int)(want < cap ? (want > 0 ? want : 1) : cap);
-  dim3 grid(blocks, g.L * 2);
+  int kb_log2 = 0;
+  while ((1 << kb_log2) < g.k) ++kb_log2;
+  // one pass: each thread moves kVecPerThread vectors (grid covers the data exactly once)
+  int64_t threads = (total + kVecPerThread - 1) / kVecPerThread;
+  int64_t blocks = (threads + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 65535) blocks = 65535;
+  dim3 grid((unsigned)blocks, g.L * 2);
   append_kernel<<<grid, 256, 0, st>>>(items, n_items, total, ids, patches, n_patches, table,
                                       (const uint4*)k, (const uint4*)v, kv_rows, (uint4*)pool,
-                                      g.L, g.h_kv, vec_per_row, g.k);
+                                      g.L, g.h_kv, vec_per_row, kb_log2);
   return cudaGetLastError();
 }
 

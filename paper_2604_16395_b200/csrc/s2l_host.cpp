@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -132,6 +133,10 @@ struct s2l_ctx {
   cudaEvent_t swap_out_done = nullptr;
   bool swap_out_pending = false;
   unsigned char tmap_kv[128] __attribute__((aligned(64)));
+  int32_t num_sms = 148;
+  float* split_ws = nullptr;          // tail-wave split partials (num_sms pieces)
+  int32_t* split_cnt = nullptr;       // per split unit arrival counters (self-resetting)
+  bool split_enabled = true;
   bool tc_ok = false;
   s2l::Geometry geo{};
 };
@@ -465,6 +470,16 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
   } else {
     c->tc_ok = false;
   }
+  if (c->tc_ok) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaMalloc(&c->split_ws, (size_t)c->num_sms * s2l::kSplitPieceFloats * sizeof(float)));
+    CK(cudaMalloc(&c->split_cnt, (size_t)c->num_sms * sizeof(int32_t)));
+    CK(cudaMemsetAsync(c->split_cnt, 0, (size_t)c->num_sms * sizeof(int32_t), c->compute));
+    const char* e = getenv("S2L_NO_SPLIT");
+    c->split_enabled = !(e && e[0] == '1');
+  }
   CK(cudaStreamSynchronize(c->compute));
   *out = holder.release();
   return S2L_OK;
@@ -488,6 +503,8 @@ void s2l_destroy(s2l_ctx* c) {
         cudaEventDestroy(p.second);
       }
     if (c->swap_out_done) cudaEventDestroy(c->swap_out_done);
+    if (c->split_ws) cudaFree(c->split_ws);
+    if (c->split_cnt) cudaFree(c->split_cnt);
     if (c->d_table) cudaFree(c->d_table);
     if (c->own_copy_stream) cudaStreamDestroy(c->copy);
   }
@@ -734,7 +751,36 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
     const char* err = nullptr;
     if (!s2l::make_tmap_q(tq, q, q_rows, c->cfg.num_q_heads, c->cfg.head_dim, G, &err))
       return fail(S2L_E_CUDA, "tensor map (q): %s", err ? err : "?");
-    CK(s2l::launch_attn_tc(c->geo, dv, n_items, (int32_t)units, c->d_table, layer, tq,
+    // Tail-wave split (hybrid stream-K): whole units fill the full waves; the units of the
+    // last partial wave are cut into s contiguous KV ranges so that wave is ~full as well.
+    const int64_t P = c->num_sms;
+    const int64_t rem = units % P;
+    int32_t split_begin = (int32_t)units, split_s = 1;
+    if (tiles_per_cta == 2 && c->split_enabled && rem > 0 && rem * 2 <= P) {
+      int64_t s_want = std::min<int64_t>(P / rem, 8);
+      // no piece may be empty: s <= the smallest KV-tile count among the split units
+      const int64_t first = units - rem;
+      for (int32_t i = n_items - 1; i >= 0 && s_want > 1; --i) {
+        const s2l::AttnItemDev& d = dev[i];
+        const int64_t pairs = ceil_div(d.tiles, 2);
+        const int64_t u0 = d.unit_begin, u1 = u0 + pairs * c->cfg.num_kv_heads;
+        if (u1 <= first) break;
+        for (int64_t pr = 0; pr < pairs; ++pr) {       // pair index; its units are >= first?
+          const int64_t local0 = (pairs - 1 - pr) * c->cfg.num_kv_heads;
+          if (u0 + local0 + c->cfg.num_kv_heads <= first) continue;
+          const int64_t toks = 128 / G;
+          const int64_t tok_last = std::min<int64_t>((pr * 2 + 2) * toks, d.n_q) - 1;
+          const int64_t nT = (d.q_pos + tok_last) / 128 + 1;
+          s_want = std::min(s_want, nT);
+        }
+      }
+      if (s_want > 1) {
+        split_begin = (int32_t)(units - rem);
+        split_s = (int32_t)s_want;
+      }
+    }
+    CK(s2l::launch_attn_tc(c->geo, dv, n_items, (int32_t)units, split_begin, split_s,
+                           c->split_ws, c->num_sms, c->split_cnt, c->d_table, layer, tq,
                            c->tmap_kv, o, lse, c->compute));
   } else {
     CK(s2l::launch_attn_generic(c->geo, dv, n_items, total_q, c->d_table, layer, q, o, lse,

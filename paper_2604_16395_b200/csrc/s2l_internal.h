@@ -63,10 +63,15 @@ cudaError_t launch_attn_generic(const Geometry& g, const AttnItemDev* items, int
 bool attn_tc_supported(const Geometry& g);
 // Q tiles per CTA of the tensor-core kernel (2 = ping-pong v2, default; 1 = v1 via S2L_ATTN_V1=1).
 int attn_tc_tiles_per_cta();
+// Grid = split_begin + (total_units - split_begin) * split_s CTAs: units below split_begin
+// run whole, the remaining (tail-wave) units run as split_s KV-range pieces whose partials
+// (ws: O partials of max_pieces pieces, then their (m, l)) are merged by the last piece (ws_cnt).
 cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t n_items,
-                           int32_t total_units, const int32_t* table, int32_t layer,
-                           const void* tmap_q, const void* tmap_kv, void* o, float* lse,
-                           cudaStream_t st);
+                           int32_t total_units, int32_t split_begin, int32_t split_s,
+                           float* ws, int32_t max_pieces, int32_t* ws_cnt,
+                           const int32_t* table, int32_t layer, const void* tmap_q,
+                           const void* tmap_kv, void* o, float* lse, cudaStream_t st);
+constexpr int64_t kSplitPieceFloats = 2 * 128 * 130;   // O [2][128][128] + (m, l) [2][128][2]
 // TMA descriptors (host).  Returns false on failure (message in *err).
 bool make_tmap_q(void* out128, const void* q, int64_t q_rows, int32_t h_q, int32_t d,
                  int32_t group, const char** err);

@@ -321,3 +321,54 @@ def test_c2_full_size_sampled_rows():
     o_ref, _ = attention(data[r][0][total - chunk:], data[r][1][0], data[r][2][0], total - chunk)
     err = normwise_err(o[r * chunk:(r + 1) * chunk], o_ref)
     assert err.max() <= 2e-2, float(err.max())
+
+
+def test_tc_tail_wave_kv_split_matches_unsplit(monkeypatch):
+    """Few work units (< #SMs) -> the kernel splits each unit's KV range into pieces and the
+    last piece merges the partial (O, m, l); must match the oracle and the unsplit kernel."""
+    geo = W.LLAMA3_8B
+    seed = 93
+    toks = W.request_tokens(seed, 0, 3256)
+    q, k, v = _stream_qkv(seed, toks, geo, q_scale=2.0)
+    outs = []
+    for no_split in ("1", "0"):
+        monkeypatch.setenv("S2L_NO_SPLIT", no_split)
+        P = Pair(1, 32, 8, 128, 16, 256, 0, mirror=False)
+        P.new(0, toks)
+        P.append([(0, None, 3256, 0)], k, v)
+        # 256 rows at p0 = 3000: 8 tiles -> 4 pairs x 8 heads = 32 units, ~24 KV tiles each
+        o, _, l, _ = P.prefill([(0, 3000, 256, 0)], q[3000:])
+        outs.append((o, l))
+        # a second launch reuses the (self-resetting) arrival counters
+        P.prefill([(0, 3000, 256, 0)], q[3000:])
+    assert normwise_err(outs[0][0], outs[1][0]).max() <= 1e-2
+    assert np.abs(outs[0][1] - outs[1][1]).max() <= 1e-3
+
+
+def test_c5_shape_reduced_long_request():
+    """C5 shape (BJ:L11): Llama-3-70B attention (64 q / 8 kv heads, GQA group 8), one long
+    request streamed in 2K-token chunks (reduced to 8K context so every row is checked)."""
+    geo = W.LLAMA3_70B
+    seed = W.seed_of(5)
+    P = Pair(1, 64, 8, 128, 16, 600, 0, mirror=False)
+    _multi_request_case(P, seed, geo, [8192], [[2048] * 4])
+
+
+def test_c5_kv_head_sharding_on_device():
+    """KV-head sharding: a context holding only kv heads {2,3} (q heads 16..31)
+    reproduces the matching slice of the full-head computation."""
+    from paper_2604_16395_b200 import shard
+    geo = W.Geometry(L=1, h_q=64, h_kv=8, d=128, k=16)
+    seed = 95
+    toks = W.request_tokens(seed, 0, 1024)
+    q, k, v = _stream_qkv(seed, toks, geo)
+    kv_h, q_h = shard.kv_head_shard(1, 4, 64, 8)
+    S = Pair(1, 16, 2, 128, 16, 128, 0, mirror=False)
+    S.new(0, toks)
+    S.append([(0, None, 1024, 0)], np.ascontiguousarray(k[:, :, kv_h]), np.ascontiguousarray(v[:, :, kv_h]))
+    o_s, o_ref_s, _, _ = S.prefill([(0, 512, 512, 0)], np.ascontiguousarray(q[512:, q_h]))
+    F = Pair(1, 64, 8, 128, 16, 128, 0, mirror=False)
+    F.new(0, toks)
+    F.append([(0, None, 1024, 0)], k, v)
+    o_f, _, _, _ = F.prefill([(0, 512, 512, 0)], q[512:])
+    assert normwise_err(o_s, o_f[:, q_h]).max() <= 2e-2

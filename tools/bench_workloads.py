@@ -1,0 +1,166 @@
+"""Extra measurements for the other BASELINE configs (not the driver's bench line):
+
+  C3 (BJ:L9)  update mode: 32 requests x 8192 tokens prefilled (2 x 4096), then an update
+              round: s2l_invalidate_lcp with LCP uniform in 20-80% (Z14), one append of all
+              suffixes, one prefill_batch of all suffixes.  Reports the update round's
+              attention TFLOP/s and the invalidate latency.
+  C5 (BJ:L11) one 128K request of Llama-3-70B attention shape (64 q / 8 kv heads) in 2K-token
+              chunks on one GPU (all 8 kv heads; the 8-GPU run shards kv heads, one per GPU).
+  C4 (BJ:L10) swap microbench: B in {1, 8, 64, 512} blocks x M_block in {64 KiB, 512 KiB,
+              2 MiB}, scattered (interleaved requests) ids, out and in, vs the measured link.
+
+    python tools/bench_workloads.py [c3] [c5] [c4]   -> one JSON line per workload
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from bench import attn_flops, measure_link  # noqa: E402
+from paper_2604_16395_b200 import s2l  # noqa: E402
+from synth import workloads as W  # noqa: E402
+
+
+def dev(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits)).view(torch.bfloat16).cuda()
+
+
+def c3():
+    geo = W.LLAMA3_8B
+    seed = W.seed_of(3)
+    R, T = 32, 8192
+    cfg = s2l.make_config(1, 32, 8, 128, 16, R * T // 16 + 64, 0, max_requests=R, max_blocks_per_request=T // 16)
+    pool = torch.empty(cfg.num_gpu_blocks * s2l.block_bytes(cfg) // 2, dtype=torch.bfloat16, device="cuda")
+    ctx = s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None)
+    toks = [W.request_tokens(seed, r, T) for r in range(R)]
+    for r in range(R):
+        ctx.new_request(r, toks[r])
+    for half in range(2):
+        a = half * 4096
+        for r0 in range(0, R, 8):
+            qs, ks, vs = [], [], []
+            for r in range(r0, r0 + 8):
+                q, k, v = W.request_qkv(seed, toks[r][: a + 4096], geo)
+                qs.append(q[a:]); ks.append(k[:, a:]); vs.append(v[:, a:])
+            kk, vv, qq = dev(np.concatenate(ks, 1)), dev(np.concatenate(vs, 1)), dev(np.concatenate(qs))
+            ctx.append_chunk([(r, None, 4096, i * 4096) for i, r in enumerate(range(r0, r0 + 8))], kk, vv)
+            ctx.prefill_batch(0, [(r, a, 4096, i * 4096) for i, r in enumerate(range(r0, r0 + 8))], qq, torch.empty_like(qq))
+    ctx.sync()
+    ps = W.c3_lcp_draws(seed, R)
+    news = [W.updated_tokens(seed, r, toks[r], int(ps[r]), T, 0) for r in range(R)]
+    data = [W.request_qkv(seed, news[r], geo) for r in range(R)]
+    rows = [T - int(ps[r]) for r in range(R)]
+    off = np.concatenate([[0], np.cumsum(rows)])
+    kk = dev(np.concatenate([data[r][1][:, int(ps[r]):] for r in range(R)], 1))
+    vv = dev(np.concatenate([data[r][2][:, int(ps[r]):] for r in range(R)], 1))
+    qq = dev(np.concatenate([data[r][0][int(ps[r]):] for r in range(R)]))
+    oo = torch.empty_like(qq)
+    flops = sum(attn_flops(rows[r], int(ps[r])) for r in range(R))
+    t = time.perf_counter()
+    for r in range(R):
+        p, inv = ctx.invalidate_lcp(r, news[r])
+        assert p == ps[r]
+    inval_us = (time.perf_counter() - t) / R * 1e6
+    ctx.set_timing(True)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    ctx.append_chunk([(r, None, rows[r], int(off[r])) for r in range(R)], kk, vv)
+    ctx.prefill_batch(0, [(r, int(ps[r]), rows[r], int(off[r])) for r in range(R)], qq, oo)
+    s1.record()
+    torch.cuda.synchronize()
+    ti = ctx.timing_read()
+    ms = s0.elapsed_time(s1)
+    return {"workload": "C3 update round (BJ:L9)", "requests": R, "tokens_recomputed": int(sum(rows)),
+            "attn_flops": flops, "round_ms": ms, "round_tflops": flops / (ms * 1e-3) / 1e12,
+            "attn_kernel_tflops": flops / (ti["attn_ms"] * 1e-3) / 1e12, "append_ms": ti["append_ms"],
+            "invalidate_us_per_request": inval_us}
+
+
+def c5():
+    geo = W.LLAMA3_70B
+    seed = W.seed_of(5)
+    T, chunk = 131072, 2048
+    cfg = s2l.make_config(1, 64, 8, 128, 16, T // 16 + 64, 0, max_requests=1, max_blocks_per_request=T // 16)
+    pool = torch.empty(cfg.num_gpu_blocks * s2l.block_bytes(cfg) // 2, dtype=torch.bfloat16, device="cuda")
+    ctx = s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None)
+    toks = W.request_tokens(seed, 0, T)
+    q, k, v = W.request_qkv(seed, toks, geo)
+    Q = [dev(q[a:a + chunk]) for a in range(0, T, chunk)]
+    K = [dev(k[:, a:a + chunk]) for a in range(0, T, chunk)]
+    V = [dev(v[:, a:a + chunk]) for a in range(0, T, chunk)]
+    O = [torch.empty_like(x) for x in Q]
+    flops = sum(attn_flops(chunk, a, h_q=64) for a in range(0, T, chunk))
+
+    def step():
+        ctx.new_request(0, toks)
+        for j in range(T // chunk):
+            ctx.append_chunk([(0, None, chunk, 0)], K[j], V[j])
+            ctx.prefill_batch(0, [(0, j * chunk, chunk, 0)], Q[j], O[j])
+        ctx.release(0)
+
+    step()
+    torch.cuda.synchronize()
+    ctx.set_timing(True)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(3):
+        step()
+    s1.record()
+    torch.cuda.synchronize()
+    ti = ctx.timing_read()
+    ms = s0.elapsed_time(s1) / 3
+    return {"workload": "C5 single 128K request, 2K chunks, 64q/8kv (BJ:L11), 1 GPU all heads", "stream_ms": ms,
+            "attn_flops": flops, "tflops": flops / (ms * 1e-3) / 1e12,
+            "attn_kernel_tflops": 3 * flops / (ti["attn_ms"] * 1e-3) / 1e12,
+            "prefill_tokens_per_s": T / (ms * 1e-3)}
+
+
+def c4():
+    link = measure_link("cuda")
+    out = {"workload": "C4 swap microbench (BJ:L10)", "link_h2d_gbs": link["h2d"], "link_d2h_gbs": link["d2h"], "cells": []}
+    for L in (1, 8, 32):
+        for B in (1, 8, 64, 512):
+            cfg = s2l.make_config(L, 32, 8, 128, 16, 2 * B + 8, 2 * B + 8, max_requests=4, max_blocks_per_request=2 * B + 8)
+            mb = s2l.block_bytes(cfg)
+            if B * mb > (1 << 30) + 1:
+                continue
+            gp = torch.empty((2 * B + 8) * mb // 2, dtype=torch.bfloat16, device="cuda")
+            cp = torch.empty((2 * B + 8) * mb // 2, dtype=torch.bfloat16).pin_memory()
+            cs = torch.cuda.Stream()
+            ctx = s2l.Context(cfg, gp, cp, torch.cuda.current_stream(), cs)
+            # two interleaved requests -> scattered ids for request 0 (B blocks)
+            kv = torch.zeros(L, 32, 8, 128, dtype=torch.bfloat16, device="cuda")
+            ctx.new_request(0, np.zeros(B * 16, np.int32))
+            ctx.new_request(1, np.zeros(B * 16, np.int32))
+            for _ in range(B // 2 if B > 1 else 1):
+                ctx.append_chunk([(0, None, min(32, B * 16 - ctx.query(0)["num_computed"]), 0),
+                                  (1, None, min(32, B * 16 - ctx.query(1)["num_computed"]), 0)], kv, kv)
+            ctx.sync()
+            nblk = ctx.query(0)["num_blocks"]
+            best = {}
+            for _ in range(3):
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record(cs)
+                b_out = ctx.swap_out([0])
+                e1.record(cs)
+                ctx.swap_in([0])
+                e2.record(cs)
+                ctx.sync()
+                for key, ms in (("out", e0.elapsed_time(e1)), ("in", e1.elapsed_time(e2))):
+                    best[key] = max(best.get(key, 0), b_out / (ms * 1e-3) / 1e9)
+            out["cells"].append({"L": L, "m_block": mb, "blocks": nblk, "bytes": b_out, "out_gbs": best["out"],
+                                 "in_gbs": best["in"], "out_frac": best["out"] / link["d2h"], "in_frac": best["in"] / link["h2d"]})
+            ctx.close()
+    return out
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["c3", "c5", "c4"]
+    for w in which:
+        print(json.dumps(globals()[w]()), flush=True)
