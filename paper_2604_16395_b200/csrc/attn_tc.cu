@@ -34,6 +34,14 @@
 #include <cstdlib>
 #include <cstring>
 
+// Build-time variants (experiments; defaults are the measured best).
+#ifndef S2L_EXP_MODE
+#define S2L_EXP_MODE 0   // 0: f32 MUFU.EX2 + FMA-pipe polynomial share; 1: MUFU.EX2 f16x2
+#endif
+#ifndef S2L_POLY_PAIRS
+#define S2L_POLY_PAIRS 2
+#endif
+
 namespace s2l {
 namespace {
 
@@ -229,6 +237,19 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   q = __ffma2_rn(q, f, make_float2(0.99992833f, 0.99992833f));
   return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(y.x) << 23)),
                      __int_as_float(__float_as_int(q.y) + (__float_as_int(y.y) << 23)));
+}
+
+// 2^x for a pair through MUFU.EX2 in packed f16x2 (two exponentials per MUFU slot).  x is
+// rounded to f16 first (|x| < 2^4 for every term that matters: relative error of the result
+// <= ~2^-7 only where 2^x < 2^-8 of the row max); results below 2^-24 flush to 0.
+__device__ __forceinline__ float2 exp2_f16x2(float2 x) {
+  uint32_t hx, he;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hx) : "f"(x.y), "f"(x.x));
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(he) : "r"(hx));
+  float lo, hi;
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+      : "=f"(lo), "=f"(hi) : "r"(he));
+  return make_float2(lo, hi);
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
@@ -507,6 +528,7 @@ __device__ __forceinline__ float chunk_max(const uint32_t (&v)[32], float mx, in
 template <bool kMasked, int kPolyPer8>
 __device__ __forceinline__ float2 chunk_p(const uint32_t (&v)[32], float2 acc, int vis, int base,
                                           float2 sc2, float2 nm2, uint32_t (&pk)[16]) {
+  float2 acc2 = make_float2(0.f, 0.f);   // second chain: halves the FADD2 dependency latency
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
     float s0 = __uint_as_float(v[2 * c]), s1 = __uint_as_float(v[2 * c + 1]);
@@ -516,12 +538,28 @@ __device__ __forceinline__ float2 chunk_p(const uint32_t (&v)[32], float2 acc, i
     }
     const float2 x = __ffma2_rn(make_float2(s0, s1), sc2, nm2);
     float2 pp;
+#if S2L_EXP_MODE == 1
+    pp = exp2_f16x2(x);
+#else
     if (!kMasked && (c & 7) < kPolyPer8) pp = exp2_poly2(x);
     else pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
-    acc = __fadd2_rn(acc, pp);
+#endif
+    if (c & 1) acc2 = __fadd2_rn(acc2, pp); else acc = __fadd2_rn(acc, pp);
     pk[c] = pack_bf16(pp.x, pp.y);
   }
-  return acc;
+  return __fadd2_rn(acc, acc2);
+}
+// Row max with 4 independent chains (short dependency latency).
+template <bool kMasked>
+__device__ __forceinline__ float row_max(const uint32_t (&sv)[128], int vis) {
+  float t[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int c = 0; c < 128; ++c) {
+    float x = __uint_as_float(sv[c]);
+    if (kMasked && c > vis) x = -INFINITY;
+    t[c & 3] = fmaxf(t[c & 3], x);
+  }
+  return fmaxf(fmaxf(t[0], t[1]), fmaxf(t[2], t[3]));
 }
 // Row max of the tile (pass 1) with the next chunk's TMEM load in flight.
 template <bool kMasked>
@@ -597,9 +635,6 @@ constexpr int kThreads = 384;
 // setmaxnreg.inc waits forever.
 constexpr int kRegLaunch = 168, kRegCtrl = 88, kRegSoftmax = 208;
 static_assert(128 * kRegCtrl + 256 * kRegSoftmax <= kThreads * kRegLaunch, "register pool");
-#ifndef S2L_POLY_PAIRS
-#define S2L_POLY_PAIRS 2
-#endif
 constexpr int kPolyPairsPer8 = S2L_POLY_PAIRS;   // of every 8 exp2 pairs, this many on the FMA pipe
 constexpr int WNST = 5;
 constexpr uint32_t WOFF_Q0 = 0;
@@ -607,8 +642,10 @@ constexpr uint32_t WOFF_Q1 = kTileBytes;
 constexpr uint32_t WOFF_RING = 2 * kTileBytes;
 constexpr uint32_t WOFF_BAR = WOFF_RING + WNST * kTileBytes;
 // barriers: 0 Q_full, 1..WNST ring_full, WNST+1..2NST ring_empty, then S_full[2], P_full[2], O_fin[2]
+// P_full is split in two halves (keys 0-63 / 64-127) so the PV MMAs of the first half start
+// while the softmax still computes the second half.
 constexpr uint32_t WB_QF = 0, WB_RF = 1, WB_RE = 1 + WNST, WB_SF = 1 + 2 * WNST, WB_PF = WB_SF + 2,
-                   WB_OF = WB_PF + 2, WNBARS = WB_OF + 2;
+                   WB_PH = WB_PF + 2, WB_OF = WB_PH + 2, WNBARS = WB_OF + 2;
 constexpr uint32_t WOFF_TMEM = WOFF_BAR + WNBARS * 8;
 constexpr uint32_t SMEM = WOFF_TMEM + 16 + 1024;
 }  // namespace v2
@@ -700,6 +737,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(WB_SF + i), 1);
       mbar_init(bar(WB_PF + i), 128);
+      mbar_init(bar(WB_PH + i), 128);
       mbar_init(bar(WB_OF + i), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -729,29 +767,41 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         tma_load_3d(sb + WOFF_Q1, &tmap_q, bar(WB_QF), 0, kvh * G, z + toks);
         tma_load_3d(sb + WOFF_Q1 + kAtom, &tmap_q, bar(WB_QF), 64, kvh * G, z + toks);
       }
-      const int32_t nb_tile = kBN / p.kb;
+      const int32_t nb_tile = kBN / p.kb;               // 1..8 blocks per 128-key tile
       const int32_t* trow = p.table + (int64_t)it.slot * p.max_blocks;
       const int32_t rows_per_block = p.L * 2 * p.h_kv * p.kb;
       const int32_t row_kv[2] = {((p.layer * 2 + 0) * p.h_kv + kvh) * p.kb,
                                  ((p.layer * 2 + 1) * p.h_kv + kvh) * p.kb};
-      const int32_t blk_i = lane >> 1, half = lane & 1;
+      auto load_id = [&](int32_t jt) {                  // lane b < nb_tile: block b of tile jt
+        const int32_t b = (jb + jt) * nb_tile + lane;
+        return __ldg(trow + (b < nblk_valid ? b : 0));
+      };
+      int32_t next_id = (lane < nb_tile) ? load_id(0) : 0;
       uint32_t rp = 0;
       for (int32_t j = 0; j < nT; ++j) {
-        int32_t bid = 0;
-        if (lane < nb_tile) {
-          const int32_t b = (jb + j) * nb_tile + lane;
-          bid = __ldg(trow + (b < nblk_valid ? b : 0));
-        }
-        const int32_t id = __shfl_sync(0xffffffffu, bid, blk_i);
+        const int32_t cur_id = next_id;
+        if (j + 1 < nT && lane < nb_tile) next_id = load_id(j + 1);   // prefetch the next ids
+        int32_t ids[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) ids[b] = __shfl_sync(0xffffffffu, cur_id, b);
 #pragma unroll
         for (int kind = 0; kind < 2; ++kind, ++rp) {
           const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
           mbar_wait(bar(WB_RE + s), ph ^ 1);
-          if (lane == 0) mbar_expect_tx(bar(WB_RF + s), kTileBytes);
+          if (lane == 0) {
+            // one lane issues the whole tile: 2 boxes {64, k} (d halves) per block
+            mbar_expect_tx(bar(WB_RF + s), kTileBytes);
+            const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+              if (b < nb_tile) {
+                const int32_t y = ids[b] * rows_per_block + row_kv[kind];
+                tma_load_2d(dst + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
+                tma_load_2d(dst + kAtom + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
+              }
+            }
+          }
           __syncwarp();
-          if (lane < 2 * nb_tile)
-            tma_load_2d(sb + WOFF_RING + s * kTileBytes + half * kAtom + blk_i * p.kb * 128,
-                        &tmap_kv, bar(WB_RF + s), half * 64, id * rows_per_block + row_kv[kind]);
         }
       }
     } else if (warp == 1) {
@@ -782,10 +832,18 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       };
       auto issue_pv = [&](int i, uint32_t vslot, int32_t j) {
         const uint64_t vd = dv0 + ((vslot * kTileBytes) >> 4);
+        mbar_wait(bar(WB_PF + i), j & 1);               // P keys 0-63 in TMEM
+        tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk)
+        for (int kk = 0; kk < kBN / 32; ++kk)
           mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
                        idesc_o, (j > 0 || kk > 0));
+        mbar_wait(bar(WB_PH + i), j & 1);               // P keys 64-127
+        tc_fence_after();
+#pragma unroll
+        for (int kk = kBN / 32; kk < kBN / 16; ++kk)
+          mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
+                       idesc_o, 1);
       };
       mbar_wait(bar(WB_QF), 0);
       tc_fence_after();
@@ -795,8 +853,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       mma_commit_elect(bar(WB_RE + kslot));
       for (int32_t j = 0; j < nT; ++j) {
         const uint32_t vslot = next_full();
-        mbar_wait(bar(WB_PF + 0), j & 1);
-        tc_fence_after();
         issue_pv(0, vslot, j);
         const bool more = j + 1 < nT;
         if (more) {
@@ -805,8 +861,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         } else {
           mma_commit_elect(bar(WB_OF + 0));
         }
-        mbar_wait(bar(WB_PF + 1), j & 1);
-        tc_fence_after();
         issue_pv(1, vslot, j);
         mma_commit_elect(bar(WB_RE + vslot));
         if (more) {
@@ -838,6 +892,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
 #ifdef S2L_EXP_MMA_ONLY   // timing experiment only: tensor-core / TMA pipeline without softmax
       tc_fence_before();
       mbar_arrive(bar(WB_PF + i));
+      mbar_arrive(bar(WB_PH + i));
       continue;
 #endif
       const int64_t key0 = (int64_t)(jb + j) * kBN;
@@ -850,16 +905,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       tmem_ld32(tS + 64, sv + 64);
       tmem_ld32(tS + 96, sv + 96);
       tmem_wait_ld();
-      float mx = -INFINITY;
-      if (masked_tile) {
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-          mx = chunk_max<true>(*reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc), mx, vis, 32 * cc);
-      } else {
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-          mx = chunk_max<false>(*reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc), mx, vis, 32 * cc);
-      }
+      float mx = masked_tile ? row_max<true>(sv, vis) : row_max<false>(sv, vis);
       mx *= sl2;
       const float m_new = (mx > m_run + kRescaleThresh) ? mx : m_run;
       if (j > 0) {
@@ -887,11 +933,21 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       // a row with no visible key yet (possible in a split piece) keeps m = -inf and p = 0
       const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
       const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_use, -m_use);
-      l_run += masked_tile ? row_p<true, 0>(sv, tS, vis, sc2, nm2)
-                           : row_p<false, kPolyPairsPer8>(sv, tS, vis, sc2, nm2);
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(bar(WB_PF + i));
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t pk[16];
+        uint32_t(&v32)[32] = *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc);
+        acc = masked_tile ? chunk_p<true, 0>(v32, acc, vis, 32 * cc, sc2, nm2, pk)
+                          : chunk_p<false, kPolyPairsPer8>(v32, acc, vis, 32 * cc, sc2, nm2, pk);
+        tmem_st16(tS + 16 * cc, pk);
+        if (cc == 1 || cc == 3) {      // keys 0-63 / 64-127 of P are in TMEM
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(bar((cc == 1 ? WB_PF : WB_PH) + i));
+        }
+      }
+      l_run += acc.x + acc.y;
     }
     // epilogue
     mbar_wait(bar(WB_OF + i), 0);

@@ -54,17 +54,18 @@ EXPORTS = ["s2l_block_bytes", "s2l_create", "s2l_create_host_only", "s2l_destroy
            "s2l_free_blocks", "s2l_sync", "s2l_kernel_launches", "s2l_set_timing", "s2l_timing_read",
            "s2l_last_error", "s2l_version"]
 
-_lib = None
+_libs: dict = {}
 
 
-def lib() -> C.CDLL:
-    """Loads libs2l.so (raises FileNotFoundError if it has not been built)."""
-    global _lib
-    if _lib is not None:
-        return _lib
-    if not os.path.exists(LIB_PATH):
-        raise FileNotFoundError(f"{LIB_PATH} not built: run `python -m paper_2604_16395_b200.build`")
-    L = C.CDLL(LIB_PATH)
+def lib(path: str | None = None) -> C.CDLL:
+    """Loads libs2l.so (raises FileNotFoundError if it has not been built).  `path` selects
+    another build of the same library (A/B timing experiments load several side by side)."""
+    path = path or LIB_PATH
+    if path in _libs:
+        return _libs[path]
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} not built: run `python -m paper_2604_16395_b200.build`")
+    L = C.CDLL(path)
     P, I32, I64, VP = C.POINTER, C.c_int32, C.c_int64, C.c_void_p
     sig = {
         "s2l_block_bytes": (I64, [P(Config)]),
@@ -92,7 +93,7 @@ def lib() -> C.CDLL:
     for name, (res, args) in sig.items():
         f = getattr(L, name)
         f.restype, f.argtypes = res, args
-    _lib = L
+    _libs[path] = L
     return L
 
 
@@ -127,8 +128,8 @@ class Context:
     """One libs2l context (one device).  Methods raise S2LError on a non-OK status."""
 
     def __init__(self, cfg: Config, gpu_pool=None, cpu_pool=None, compute_stream=None,
-                 copy_stream=None, host_only=False):
-        self._L = lib()
+                 copy_stream=None, host_only=False, lib_path=None):
+        self._L = lib(lib_path)
         self.cfg = cfg
         self.host_only = host_only
         h = C.c_void_p()
