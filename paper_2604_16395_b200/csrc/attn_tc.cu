@@ -77,6 +77,7 @@ struct TcParams {
   // tail-wave KV split (v2): CTAs >= split_begin are pieces of units split into split_s
   // contiguous KV ranges; partials go to ws, the last piece of a unit merges (ws_cnt).
   int32_t split_begin, split_s;
+  int32_t n_work;  // v3: work items = split_begin + (units - split_begin) * split_s
   float* ws;       // [pieces][2][128][128] partial O (unnormalised, fp32)
   float* ws_ml;    // [pieces][2][128][2] running max (log2 units) and row sum
   int32_t* ws_cnt;
@@ -645,7 +646,7 @@ constexpr uint32_t WOFF_BAR = WOFF_RING + WNST * kTileBytes;
 // P_full is split in two halves (keys 0-63 / 64-127) so the PV MMAs of the first half start
 // while the softmax still computes the second half.
 constexpr uint32_t WB_QF = 0, WB_RF = 1, WB_RE = 1 + WNST, WB_SF = 1 + 2 * WNST, WB_PF = WB_SF + 2,
-                   WB_PH = WB_PF + 2, WB_OF = WB_PH + 2, WNBARS = WB_OF + 2;
+                   WB_PH = WB_PF + 2, WB_OF = WB_PH + 2, WB_QE = WB_OF + 2, WNBARS = WB_QE + 1;
 constexpr uint32_t WOFF_TMEM = WOFF_BAR + WNBARS * 8;
 constexpr uint32_t SMEM = WOFF_TMEM + 16 + 1024;
 }  // namespace v2
@@ -1061,6 +1062,411 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
   }
 }
 
+// ======================================================================================
+// v3 = v2 made persistent: each CTA loops over work items (whole units, then the tail-wave
+// split pieces) with a static stride of gridDim.x, so the TMEM allocation / barrier setup is
+// paid once per SM and the next item's Q load, K/V loads and first S MMAs overlap the current
+// item's epilogue.  Barrier phases run on per-CTA counters (KV steps g, items n) instead of
+// per-item indices.  Q_empty (committed after an item's last S MMAs) lets the producer load
+// the next Q; O reuse is ordered by the softmax warps themselves (their epilogue precedes
+// their next P_full arrival, which gates the next item's first PV).
+struct WorkInfo {
+  AttnItemDev it;
+  int32_t unit, piece, npieces, kvh, tok0, tok_last, jb, nT, nblk_valid;
+};
+
+__device__ __forceinline__ WorkInfo decode_work(const TcParams& p, int32_t w) {
+  WorkInfo wk;
+  wk.unit = w;
+  wk.piece = 0;
+  wk.npieces = 1;
+  if (w >= p.split_begin) {
+    const int32_t b = w - p.split_begin;
+    wk.unit = p.split_begin + b / p.split_s;
+    wk.piece = b % p.split_s;
+    wk.npieces = p.split_s;
+  }
+  int32_t lo = 0, hi = p.n_items - 1;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (p.items[mid].unit_begin <= wk.unit) lo = mid; else hi = mid - 1;
+  }
+  wk.it = p.items[lo];
+  const int32_t local = wk.unit - wk.it.unit_begin;
+  const int32_t pairs = (wk.it.tiles + 1) >> 1;
+  const int32_t pair = pairs - 1 - local / p.h_kv;
+  wk.kvh = local % p.h_kv;
+  const int32_t toks = kBM / p.group;
+  wk.tok0 = pair * 2 * toks;
+  wk.tok_last = min(wk.tok0 + 2 * toks, wk.it.n_q) - 1;
+  const int32_t nT_all = (int32_t)((wk.it.q_pos + wk.tok_last) / kBN) + 1;
+  wk.jb = (int32_t)((int64_t)nT_all * wk.piece / wk.npieces);
+  wk.nT = (int32_t)((int64_t)nT_all * (wk.piece + 1) / wk.npieces) - wk.jb;
+  wk.nblk_valid = (int32_t)((wk.it.q_pos + wk.it.n_q + p.kb - 1) / p.kb);
+  return wk;
+}
+
+__global__ void __launch_bounds__(v2::kThreads, 1)
+    attn_tc3_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                    const __grid_constant__ CUtensorMap tmap_kv, const TcParams p) {
+  using namespace v2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sb = smem_u32(smem);
+  auto bar = [&](uint32_t i) { return sb + WOFF_BAR + 8u * i; };
+  uint32_t* tmem_holder = (uint32_t*)(smem + WOFF_TMEM);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t G = p.group;
+  const int32_t toks = kBM / G;
+  const int32_t W = p.n_work;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar(WB_QF), 1);
+    mbar_init(bar(WB_QE), 1);
+    for (int s = 0; s < WNST; ++s) {
+      mbar_init(bar(WB_RF + s), 1);
+      mbar_init(bar(WB_RE + s), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(WB_SF + i), 1);
+      mbar_init(bar(WB_PF + i), 128);
+      mbar_init(bar(WB_PH + i), 128);
+      mbar_init(bar(WB_OF + i), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtrl));
+    if (warp == 0) {
+      // ================= TMA producer =================
+      const int32_t nb_tile = kBN / p.kb;
+      const int32_t rows_per_block = p.L * 2 * p.h_kv * p.kb;
+      uint32_t rp = 0, n = 0;
+      for (int32_t w = blockIdx.x; w < W; w += gridDim.x, ++n) {
+        const WorkInfo wk = decode_work(p, w);
+        if (lane == 0) {
+          mbar_wait(bar(WB_QE), (n & 1) ^ 1);          // previous item's S MMAs are done
+          mbar_expect_tx(bar(WB_QF), 2 * kTileBytes);
+          const int32_t z = (int32_t)(wk.it.q_row + wk.tok0);
+          tma_load_3d(sb + WOFF_Q0, &tmap_q, bar(WB_QF), 0, wk.kvh * G, z);
+          tma_load_3d(sb + WOFF_Q0 + kAtom, &tmap_q, bar(WB_QF), 64, wk.kvh * G, z);
+          tma_load_3d(sb + WOFF_Q1, &tmap_q, bar(WB_QF), 0, wk.kvh * G, z + toks);
+          tma_load_3d(sb + WOFF_Q1 + kAtom, &tmap_q, bar(WB_QF), 64, wk.kvh * G, z + toks);
+        }
+        __syncwarp();
+        const int32_t* trow = p.table + (int64_t)wk.it.slot * p.max_blocks;
+        const int32_t row_kv[2] = {((p.layer * 2 + 0) * p.h_kv + wk.kvh) * p.kb,
+                                   ((p.layer * 2 + 1) * p.h_kv + wk.kvh) * p.kb};
+        auto load_id = [&](int32_t jt) {
+          const int32_t b = (wk.jb + jt) * nb_tile + lane;
+          return __ldg(trow + (b < wk.nblk_valid ? b : 0));
+        };
+        int32_t next_id = (lane < nb_tile) ? load_id(0) : 0;
+        for (int32_t j = 0; j < wk.nT; ++j) {
+          const int32_t cur_id = next_id;
+          if (j + 1 < wk.nT && lane < nb_tile) next_id = load_id(j + 1);
+          int32_t ids[8];
+#pragma unroll
+          for (int b = 0; b < 8; ++b) ids[b] = __shfl_sync(0xffffffffu, cur_id, b);
+#pragma unroll
+          for (int kind = 0; kind < 2; ++kind, ++rp) {
+            const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
+            mbar_wait(bar(WB_RE + s), ph ^ 1);
+            if (lane == 0) {
+              mbar_expect_tx(bar(WB_RF + s), kTileBytes);
+              const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
+#pragma unroll
+              for (int b = 0; b < 8; ++b) {
+                if (b < nb_tile) {
+                  const int32_t y = ids[b] * rows_per_block + row_kv[kind];
+                  tma_load_2d(dst + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
+                  tma_load_2d(dst + kAtom + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
+                }
+              }
+            }
+            __syncwarp();
+          }
+        }
+      }
+    } else if (warp == 1) {
+      // ================= MMA issuer (whole warp, one elected lane issues) =================
+      constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16(kBM, kD, 0, 1);
+      const uint64_t dq[2] = {sdesc(sb + WOFF_Q0, 16, 1024), sdesc(sb + WOFF_Q1, 16, 1024)};
+      const uint64_t dk0 = sdesc(sb + WOFF_RING, 16, 1024);
+      const uint64_t dv0 = sdesc(sb + WOFF_RING, kAtom, 1024);
+      uint32_t rp = 0, g = 0, n = 0;
+      auto next_full = [&]() {
+        const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
+        ++rp;
+        mbar_wait(bar(WB_RF + s), ph);
+        tc_fence_after();
+        return s;
+      };
+      auto issue_s = [&](int i, uint32_t kslot) {
+        const uint64_t kd = dk0 + ((kslot * kTileBytes) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const uint32_t off = ((kk >> 2) * kAtom + (kk & 3) * 32) >> 4;
+          mma_ss_elect(tmem + i * 128, dq[i] + off, kd + off, idesc_s, kk > 0);
+        }
+        mma_commit_elect(bar(WB_SF + i));
+      };
+      auto issue_pv = [&](int i, uint32_t vslot, int32_t j, uint32_t gj) {
+        const uint64_t vd = dv0 + ((vslot * kTileBytes) >> 4);
+        mbar_wait(bar(WB_PF + i), gj & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kBN / 32; ++kk)
+          mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
+                       idesc_o, (j > 0 || kk > 0));
+        mbar_wait(bar(WB_PH + i), gj & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = kBN / 32; kk < kBN / 16; ++kk)
+          mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
+                       idesc_o, 1);
+      };
+      for (int32_t w = blockIdx.x; w < W; w += gridDim.x, ++n) {
+        const int32_t nT = decode_work(p, w).nT;
+        mbar_wait(bar(WB_QF), n & 1);
+        tc_fence_after();
+        uint32_t kslot = next_full();
+        issue_s(0, kslot);
+        issue_s(1, kslot);
+        mma_commit_elect(bar(WB_RE + kslot));
+        if (nT == 1) mma_commit_elect(bar(WB_QE));      // last S of this item issued
+        for (int32_t j = 0; j < nT; ++j) {
+          const uint32_t gj = g + j;
+          const uint32_t vslot = next_full();
+          issue_pv(0, vslot, j, gj);
+          const bool more = j + 1 < nT;
+          if (more) {
+            kslot = next_full();
+            issue_s(0, kslot);
+          } else {
+            mma_commit_elect(bar(WB_OF + 0));
+          }
+          issue_pv(1, vslot, j, gj);
+          mma_commit_elect(bar(WB_RE + vslot));
+          if (more) {
+            issue_s(1, kslot);
+            mma_commit_elect(bar(WB_RE + kslot));
+            if (j + 2 == nT) mma_commit_elect(bar(WB_QE));
+          } else {
+            mma_commit_elect(bar(WB_OF + 1));
+          }
+        }
+        g += nT;
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
+    // ================= softmax / correction / epilogue of Q tile i =================
+    const int i = (warp - 4) >> 2;
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane_off + i * 128;
+    const uint32_t tO = tmem + lane_off + TMEM_O + i * 128;
+    const float sl2 = p.scale_log2;
+    uint32_t g = 0, n = 0;
+    for (int32_t w = blockIdx.x; w < W; w += gridDim.x, ++n) {
+      const WorkInfo wk = decode_work(p, w);
+      const int32_t tok = wk.tok0 + i * toks + r / G;
+      const int32_t hq = wk.kvh * G + r % G;
+      const bool valid = tok < wk.it.n_q;
+      const int64_t limit = wk.it.q_pos + (valid ? tok : wk.tok_last);
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int32_t j = 0; j < wk.nT; ++j) {
+        mbar_wait(bar(WB_SF + i), (g + j) & 1);
+        tc_fence_after();
+#ifdef S2L_EXP_MMA_ONLY
+        tc_fence_before();
+        mbar_arrive(bar(WB_PF + i));
+        mbar_arrive(bar(WB_PH + i));
+        continue;
+#endif
+        const int64_t key0 = (int64_t)(wk.jb + j) * kBN;
+        const int64_t vis64 = limit - key0;
+        const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBN ? kBN : vis64));
+        const bool masked_tile = __any_sync(0xffffffffu, vis < kBN - 1);
+        uint32_t sv[128];
+        tmem_ld32(tS, sv);
+        tmem_ld32(tS + 32, sv + 32);
+        tmem_ld32(tS + 64, sv + 64);
+        tmem_ld32(tS + 96, sv + 96);
+        tmem_wait_ld();
+        float mx = masked_tile ? row_max<true>(sv, vis) : row_max<false>(sv, vis);
+        mx *= sl2;
+        const float m_new = (mx > m_run + kRescaleThresh) ? mx : m_run;
+        if (j > 0) {
+          const bool resc = m_new != m_run;
+          if (__any_sync(0xffffffffu, resc)) {
+            const float alpha = resc ? fast_exp2(m_run - m_new) : 1.f;
+#pragma unroll 1
+            for (int c = 0; c < 8; ++c) {
+              uint32_t ov[16];
+              tmem_ld16(tO + c * 16, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 16; e += 2) {
+                float2 x = __fmul2_rn(make_float2(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])),
+                                      make_float2(alpha, alpha));
+                ov[e] = __float_as_uint(x.x);
+                ov[e + 1] = __float_as_uint(x.y);
+              }
+              tmem_st16(tO + c * 16, ov);
+            }
+            l_run *= alpha;
+          }
+        }
+        m_run = m_new;
+        const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+        const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_use, -m_use);
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t pk[16];
+          uint32_t(&v32)[32] = *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc);
+          acc = masked_tile ? chunk_p<true, 0>(v32, acc, vis, 32 * cc, sc2, nm2, pk)
+                            : chunk_p<false, kPolyPairsPer8>(v32, acc, vis, 32 * cc, sc2, nm2, pk);
+          tmem_st16(tS + 16 * cc, pk);
+          if (cc == 1 || cc == 3) {
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(bar((cc == 1 ? WB_PF : WB_PH) + i));
+          }
+        }
+        l_run += acc.x + acc.y;
+      }
+      g += wk.nT;
+      // ---- epilogue of this item (overlaps the next item's first S MMAs)
+      mbar_wait(bar(WB_OF + i), n & 1);
+      tc_fence_after();
+      __nv_bfloat16* orow = p.o + ((wk.it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
+      if (wk.npieces == 1) {
+        const float inv = 1.f / l_run;
+#pragma unroll 1
+        for (int c = 0; c < 8; ++c) {
+          uint32_t ov[16];
+          tmem_ld16(tO + c * 16, ov);
+          tmem_wait_ld();
+          if (valid) {
+            uint32_t wv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              wv[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+            dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+          }
+        }
+        if (valid && p.lse)
+          p.lse[(wk.it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+      } else {
+        const int32_t su = wk.unit - p.split_begin;
+        const int32_t npieces = wk.npieces;
+        const int64_t prow = (((int64_t)su * npieces + wk.piece) * 2 + i) * 128 + r;
+        float* wo = p.ws + prow * kD;
+#pragma unroll 1
+        for (int c = 0; c < 8; ++c) {
+          uint32_t ov[16];
+          tmem_ld16(tO + c * 16, ov);
+          tmem_wait_ld();
+          float4* dst = reinterpret_cast<float4*>(wo + c * 16);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
+                                 __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
+        }
+        p.ws_ml[prow * 2] = m_run;
+        p.ws_ml[prow * 2 + 1] = l_run;
+        __threadfence();
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        uint32_t* flag = (uint32_t*)(smem + WOFF_TMEM + 8);
+        if (threadIdx.x == 128) {
+          const int32_t old = atomicAdd(p.ws_cnt + su, 1);
+          const uint32_t last = (old == npieces - 1) ? 1u : 0u;
+          if (last) p.ws_cnt[su] = 0;
+          *flag = last;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const bool is_last = *flag != 0;
+        asm volatile("bar.sync 1, 256;" ::: "memory");   // flag is reused by the next item
+        if (is_last) {
+          __threadfence();
+          float M = -INFINITY;
+          for (int k = 0; k < npieces; ++k) {
+            const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
+            M = fmaxf(M, __ldcg(p.ws_ml + pr * 2));
+          }
+          constexpr int kMaxPieces = 8;
+          float wk8[kMaxPieces];
+          float Lsum = 0.f;
+#pragma unroll
+          for (int k = 0; k < kMaxPieces; ++k) {
+            wk8[k] = 0.f;
+            if (k < npieces) {
+              const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
+              wk8[k] = fast_exp2(__ldcg(p.ws_ml + pr * 2) - M);
+              Lsum += wk8[k] * __ldcg(p.ws_ml + pr * 2 + 1);
+            }
+          }
+          const float inv = 1.f / Lsum;
+#pragma unroll 1
+          for (int c0 = 0; c0 < kD; c0 += 32) {
+            float acc[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+#pragma unroll
+            for (int k = 0; k < kMaxPieces; ++k) {
+              if (k < npieces) {
+                const float* po = p.ws + ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * kD + c0;
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                  const float2 x = __ldcg(reinterpret_cast<const float2*>(po + c));
+                  acc[c] += wk8[k] * x.x;
+                  acc[c + 1] += wk8[k] * x.y;
+                }
+              }
+            }
+            if (valid) {
+#pragma unroll
+              for (int c = 0; c < 32; c += 8) {
+                uint4 v4 = make_uint4(pack_bf16(acc[c] * inv, acc[c + 1] * inv), pack_bf16(acc[c + 2] * inv, acc[c + 3] * inv),
+                                      pack_bf16(acc[c + 4] * inv, acc[c + 5] * inv), pack_bf16(acc[c + 6] * inv, acc[c + 7] * inv));
+                *reinterpret_cast<uint4*>(orow + c0 + c) = v4;
+              }
+            }
+          }
+          if (valid && p.lse)
+            p.lse[(wk.it.q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
+        }
+      }
+      tc_fence_before();
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn(const char** err) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -1137,14 +1543,20 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
                            int32_t total_units, int32_t split_begin, int32_t split_s,
                            float* ws, int32_t max_pieces, int32_t* ws_cnt,
                            const int32_t* table, int32_t layer, const void* tmap_q,
-                           const void* tmap_kv, void* o, float* lse, cudaStream_t st) {
+                           const void* tmap_kv, void* o, float* lse, int32_t num_sms,
+                           int32_t flags, cudaStream_t st) {
   const int variant = attn_tc_tiles_per_cta();
+  const bool persistent = (flags & kAttnPersistent) != 0;
   static bool attr_set[3] = {false, false, false};
   if (!attr_set[variant]) {
     cudaError_t e = variant == 2
         ? cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM)
         : cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
+    if (variant == 2) {
+      e = cudaFuncSetAttribute(attn_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM);
+      if (e != cudaSuccess) return e;
+    }
     attr_set[variant] = true;
   }
   if (total_units <= 0) return cudaSuccess;
@@ -1176,7 +1588,11 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
   p.ws = ws;
   p.ws_ml = ws ? ws + (int64_t)max_pieces * 2 * 128 * kD : nullptr;
   p.ws_cnt = ws_cnt;
-  if (variant == 2)
+  p.n_work = grid;
+  if (variant == 2 && persistent) {
+    const int32_t g = grid < num_sms ? grid : num_sms;
+    attn_tc3_kernel<<<g, v2::kThreads, v2::SMEM, st>>>(tq, tkv, p);
+  } else if (variant == 2)
     attn_tc2_kernel<<<grid, v2::kThreads, v2::SMEM, st>>>(tq, tkv, p);
   else
     attn_tc_kernel<<<total_units, kThreads, SMEM_BYTES, st>>>(tq, tkv, p);

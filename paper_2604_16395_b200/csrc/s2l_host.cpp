@@ -137,6 +137,7 @@ struct s2l_ctx {
   float* split_ws = nullptr;          // tail-wave split partials (num_sms pieces)
   int32_t* split_cnt = nullptr;       // per split unit arrival counters (self-resetting)
   bool split_enabled = true;
+  bool persistent = false;            // persistent attention kernel (S2L_PERSIST=1); off: measured slower
   bool tc_ok = false;
   s2l::Geometry geo{};
 };
@@ -479,6 +480,8 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
     CK(cudaMemsetAsync(c->split_cnt, 0, (size_t)c->num_sms * sizeof(int32_t), c->compute));
     const char* e = getenv("S2L_NO_SPLIT");
     c->split_enabled = !(e && e[0] == '1');
+    e = getenv("S2L_PERSIST");
+    c->persistent = (e && e[0] == '1');
   }
   CK(cudaStreamSynchronize(c->compute));
   *out = holder.release();
@@ -781,7 +784,8 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
     }
     CK(s2l::launch_attn_tc(c->geo, dv, n_items, (int32_t)units, split_begin, split_s,
                            c->split_ws, c->num_sms, c->split_cnt, c->d_table, layer, tq,
-                           c->tmap_kv, o, lse, c->compute));
+                           c->tmap_kv, o, lse, c->num_sms,
+                           c->persistent ? s2l::kAttnPersistent : 0, c->compute));
   } else {
     CK(s2l::launch_attn_generic(c->geo, dv, n_items, total_q, c->d_table, layer, q, o, lse,
                                 c->gpu_pool, c->compute));

@@ -70,7 +70,10 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
                            int32_t total_units, int32_t split_begin, int32_t split_s,
                            float* ws, int32_t max_pieces, int32_t* ws_cnt,
                            const int32_t* table, int32_t layer, const void* tmap_q,
-                           const void* tmap_kv, void* o, float* lse, cudaStream_t st);
+                           const void* tmap_kv, void* o, float* lse, int32_t num_sms,
+                           int32_t flags, cudaStream_t st);
+// flags of launch_attn_tc
+constexpr int32_t kAttnPersistent = 1;   // v2 only: grid = min(work items, SMs), CTAs loop
 constexpr int64_t kSplitPieceFloats = 2 * 128 * 130;   // O [2][128][128] + (m, l) [2][128][2]
 // TMA descriptors (host).  Returns false on failure (message in *err).
 bool make_tmap_q(void* out128, const void* q, int64_t q_rows, int32_t h_q, int32_t d,

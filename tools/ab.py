@@ -19,27 +19,42 @@ from paper_2604_16395_b200 import s2l  # noqa: E402
 
 
 def main():
-    libs = [a for a in sys.argv[1:] if a.endswith(".so")]
-    rounds = int(([a for a in sys.argv[1:] if not a.endswith(".so")] or ["6"])[0])
+    # specs: path.so[:ENV=VAL[,ENV=VAL]] (env applied while that context is created)
+    specs = [a for a in sys.argv[1:] if ".so" in a]
+    rounds = int(([a for a in sys.argv[1:] if ".so" not in a] or ["8"])[0])
+    libs = specs
     torch.cuda.set_device(0)
     rids, toks, data = bench.make_stream_data(0)
     S = bench.Stream(rids, toks, data, "cuda:0")
     ctxs = []
-    for path in libs:
+    for spec in libs:
+        path, _, envs = spec.partition(":")
+        saved = {}
+        for kv in filter(None, envs.split(",")):
+            k, v = kv.split("=")
+            saved[k] = os.environ.get(k)
+            os.environ[k] = v
         nblk = bench.NREQ * bench.TOTAL // bench.KB
         cfg = s2l.make_config(1, bench.H_Q, bench.H_KV, bench.D, bench.KB, nblk, 0, max_requests=bench.NREQ,
                               max_blocks_per_request=bench.TOTAL // bench.KB)
         pool = torch.empty(nblk * s2l.block_bytes(cfg) // 2, dtype=torch.bfloat16, device="cuda")
         ctxs.append((s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None, lib_path=path), pool))
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     flops = bench.step_flops()
     res = {p: [] for p in libs}
+    for path, (ctx, _) in zip(libs, ctxs):       # warm every context (clocks, caches)
+        bench.timed(lambda: bench.run_step(ctx, S), 1, 4)
     for r in range(rounds):
         for path, (ctx, _) in zip(libs, ctxs):
-            ms = bench.timed(lambda: bench.run_step(ctx, S), 3, 2 if r == 0 else 1)
+            ms = bench.timed(lambda: bench.run_step(ctx, S), 3, 1)
             res[path].append(flops * 3 / (ms * 1e-3) / 1e12)
     for path in libs:
         v = res[path]
-        print(f"{os.path.basename(path):24s} median {statistics.median(v):8.1f}  min {min(v):8.1f}  max {max(v):8.1f} TFLOP/s")
+        print(f"{path.split('/')[-1]:40s} median {statistics.median(v):8.1f}  min {min(v):8.1f}  max {max(v):8.1f} TFLOP/s")
 
 
 if __name__ == "__main__":
