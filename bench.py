@@ -473,11 +473,13 @@ def main():
     attn_launches = tinfo["attn_launches"]
     attn_ms_avg = tinfo["attn_ms"] / max(1, attn_launches)
     achieved = flops_rank * args.steps / (tinfo["attn_ms"] * 1e-3) / 1e12
-    traffic = None
+    traffic, traffic_note = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("attn_tc_kernel_bytes_per_launch")
+            tj = json.load(open(tpath))
+            traffic = tj.get("attn_tc_kernel_bytes_per_launch")
+            traffic_note = tj.get("attn_launch")
         except Exception:
             traffic = None
     new_tokens = NREQ * TOTAL * world
@@ -494,7 +496,8 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16"], "unit": "TFLOP/s",
                      "frac": achieved / pk["bf16"], "traffic": traffic,
-                     "kernel": "attn_tc_kernel (tcgen05 chunked-prefill attention)",
+                     "traffic_launch": traffic_note,
+                     "kernel": "attn_tc2_kernel (tcgen05/TMEM/TMA chunked-prefill attention)",
                      "peak_source": f"{pk['source']} bf16_tflops (burst)",
                      "frac_vs_sustained": (achieved / pk["bf16_sus"]) if pk.get("bf16_sus") else None,
                      "launches": attn_launches, "avg_launch_ms": attn_ms_avg,

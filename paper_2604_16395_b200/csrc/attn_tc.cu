@@ -824,17 +824,20 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       };
       auto issue_s = [&](int i, uint32_t kslot) {
         const uint64_t kd = dk0 + ((kslot * kTileBytes) >> 4);
+#ifndef S2L_EXP_NO_S
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
           const uint32_t off = ((kk >> 2) * kAtom + (kk & 3) * 32) >> 4;
           mma_ss_elect(tmem + i * 128, dq[i] + off, kd + off, idesc_s, kk > 0);
         }
+#endif
         mma_commit_elect(bar(WB_SF + i));
       };
       auto issue_pv = [&](int i, uint32_t vslot, int32_t j) {
         const uint64_t vd = dv0 + ((vslot * kTileBytes) >> 4);
         mbar_wait(bar(WB_PF + i), j & 1);               // P keys 0-63 in TMEM
         tc_fence_after();
+#ifndef S2L_EXP_NO_PV
 #pragma unroll
         for (int kk = 0; kk < kBN / 32; ++kk)
           mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
@@ -845,6 +848,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         for (int kk = kBN / 32; kk < kBN / 16; ++kk)
           mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
                        idesc_o, 1);
+#endif
       };
       mbar_wait(bar(WB_QF), 0);
       tc_fence_after();
