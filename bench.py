@@ -200,20 +200,25 @@ def timed(fn, steps, warmup, dist=None):
     return ms
 
 
+E2E_BUFS = 4   # device staging buffers per input: H2D of chunk j+3 overlaps compute of j and D2H of j-1
+
+
 def e2e_run(ctx, S_host: "Stream", dev_bufs, streams):
-    """One step with inputs in pinned host memory: per chunk H2D of Q/K/V (copy stream),
-    append + attention (compute stream), D2H of O (d2h stream); double-buffered."""
+    """One step with inputs in pinned host memory: per chunk H2D of Q/K/V (h2d stream),
+    append + attention (compute stream), D2H of O (d2h stream); E2E_BUFS-deep buffering so
+    both PCIe directions and the compute run concurrently."""
     import torch
     comp = torch.cuda.current_stream()
     h2d, d2h = streams
     qd, kd, vd, od = dev_bufs
-    ev_loaded = [torch.cuda.Event() for _ in range(2)]
-    ev_done = [torch.cuda.Event() for _ in range(2)]
-    ev_free = [None, None]
+    nb = len(qd)
+    ev_loaded = [torch.cuda.Event() for _ in range(nb)]
+    ev_done = [torch.cuda.Event() for _ in range(nb)]
+    ev_free = [None] * nb
     for r, t in zip(S_host.rids, S_host.toks):
         ctx.new_request(r, t)
     for j in range(S_host.steps):
-        b = j & 1
+        b = j % nb
         with torch.cuda.stream(h2d):
             if ev_free[b] is not None:
                 h2d.wait_event(ev_free[b])
@@ -510,8 +515,8 @@ def main():
     if not args.no_side and rank == 0:
         # e2e through the C ABI with host buffers
         S_host = Stream(rids, toks, data, dev, pinned=True)
-        dev_bufs = tuple([torch.empty_like(S.q[0]), torch.empty_like(S.q[0])] if i in (0, 3) else
-                         [torch.empty_like(S.k[0]), torch.empty_like(S.k[0])] for i in range(4))
+        dev_bufs = tuple([torch.empty_like(S.q[0] if i in (0, 3) else S.k[0]) for _ in range(E2E_BUFS)]
+                         for i in range(4))
         streams = (torch.cuda.Stream(), torch.cuda.Stream())
         efn = lambda: e2e_run(ctx, S_host, dev_bufs, streams)
         ems = timed(efn, max(2, args.steps // 2), 1, None) / max(2, args.steps // 2)

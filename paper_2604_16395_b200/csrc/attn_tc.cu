@@ -133,6 +133,14 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, uint
       "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const void* tmap, uint32_t bar,
+                                            int32_t x, int32_t y, int32_t z, int32_t w) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(w), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -691,7 +699,8 @@ __device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
 }
 __global__ void __launch_bounds__(v2::kThreads, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                    const __grid_constant__ CUtensorMap tmap_kv, const TcParams p) {
+                    const __grid_constant__ CUtensorMap tmap_kv,
+                    const __grid_constant__ CUtensorMap tmap_kv4, const TcParams p) {
   using namespace v2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -744,6 +753,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv4) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -773,6 +783,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       const int32_t rows_per_block = p.L * 2 * p.h_kv * p.kb;
       const int32_t row_kv[2] = {((p.layer * 2 + 0) * p.h_kv + kvh) * p.kb,
                                  ((p.layer * 2 + 1) * p.h_kv + kvh) * p.kb};
+      const int32_t lkh[2] = {(p.layer * 2 + 0) * p.h_kv + kvh, (p.layer * 2 + 1) * p.h_kv + kvh};
       auto load_id = [&](int32_t jt) {                  // lane b < nb_tile: block b of tile jt
         const int32_t b = (jb + jt) * nb_tile + lane;
         return __ldg(trow + (b < nblk_valid ? b : 0));
@@ -785,20 +796,47 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         int32_t ids[8];
 #pragma unroll
         for (int b = 0; b < 8; ++b) ids[b] = __shfl_sync(0xffffffffu, cur_id, b);
+        bool run = (jb + j + 1) * nb_tile <= nblk_valid;   // whole tile inside the table
+#pragma unroll
+        for (int b = 1; b < 8; ++b)
+          if (b < nb_tile) run = run && (ids[b] == ids[0] + b);
 #pragma unroll
         for (int kind = 0; kind < 2; ++kind, ++rp) {
           const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
           mbar_wait(bar(WB_RE + s), ph ^ 1);
-          if (lane == 0) {
-            // one lane issues the whole tile: 2 boxes {64, k} (d halves) per block
+          if (lane == 0 && run) {
+            // consecutive block ids: two 4-D boxes (d halves) cover the whole 128-key tile
             mbar_expect_tx(bar(WB_RF + s), kTileBytes);
             const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
+            tma_load_4d(dst, &tmap_kv4, bar(WB_RF + s), 0, 0, lkh[kind], ids[0]);
+            tma_load_4d(dst + kAtom, &tmap_kv4, bar(WB_RF + s), 64, 0, lkh[kind], ids[0]);
+          } else if (lane == 0) {
+            // one lane issues the whole tile: 2 boxes {64, k} (d halves) per block
+#ifdef S2L_EXP_HALF_LOAD   // timing experiment only: load one d-half of each K/V tile
+            mbar_expect_tx(bar(WB_RF + s), kTileBytes / 2);
+#else
+            mbar_expect_tx(bar(WB_RF + s), kTileBytes);
+#endif
+            const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
+#ifdef S2L_EXP_BOX32   // timing experiment only: boxes of 2 blocks (wrong rows, same bytes)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              if (b < nb_tile / 2) {
+                const int32_t y = ids[2 * b] * rows_per_block + row_kv[kind];
+                tma_load_2d(dst + b * 2 * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
+                tma_load_2d(dst + kAtom + b * 2 * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
+              }
+            }
+            if (false)
+#endif
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
               if (b < nb_tile) {
                 const int32_t y = ids[b] * rows_per_block + row_kv[kind];
                 tma_load_2d(dst + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
+#ifndef S2L_EXP_HALF_LOAD
                 tma_load_2d(dst + kAtom + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
+#endif
               }
             }
           }
@@ -1112,7 +1150,8 @@ __device__ __forceinline__ WorkInfo decode_work(const TcParams& p, int32_t w) {
 
 __global__ void __launch_bounds__(v2::kThreads, 1)
     attn_tc3_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                    const __grid_constant__ CUtensorMap tmap_kv, const TcParams p) {
+                    const __grid_constant__ CUtensorMap tmap_kv,
+                    const __grid_constant__ CUtensorMap tmap_kv4, const TcParams p) {
   using namespace v2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -1140,6 +1179,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv4) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -1178,6 +1218,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
           const int32_t b = (wk.jb + jt) * nb_tile + lane;
           return __ldg(trow + (b < wk.nblk_valid ? b : 0));
         };
+        const int32_t lkh[2] = {(p.layer * 2 + 0) * p.h_kv + wk.kvh, (p.layer * 2 + 1) * p.h_kv + wk.kvh};
         int32_t next_id = (lane < nb_tile) ? load_id(0) : 0;
         for (int32_t j = 0; j < wk.nT; ++j) {
           const int32_t cur_id = next_id;
@@ -1185,11 +1226,20 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
           int32_t ids[8];
 #pragma unroll
           for (int b = 0; b < 8; ++b) ids[b] = __shfl_sync(0xffffffffu, cur_id, b);
+          bool run = (wk.jb + j + 1) * nb_tile <= wk.nblk_valid;
+#pragma unroll
+          for (int b = 1; b < 8; ++b)
+            if (b < nb_tile) run = run && (ids[b] == ids[0] + b);
 #pragma unroll
           for (int kind = 0; kind < 2; ++kind, ++rp) {
             const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
             mbar_wait(bar(WB_RE + s), ph ^ 1);
-            if (lane == 0) {
+            if (lane == 0 && run) {
+              mbar_expect_tx(bar(WB_RF + s), kTileBytes);
+              const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
+              tma_load_4d(dst, &tmap_kv4, bar(WB_RF + s), 0, 0, lkh[kind], ids[0]);
+              tma_load_4d(dst + kAtom, &tmap_kv4, bar(WB_RF + s), 64, 0, lkh[kind], ids[0]);
+            } else if (lane == 0) {
               mbar_expect_tx(bar(WB_RF + s), kTileBytes);
               const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
 #pragma unroll
@@ -1494,24 +1544,46 @@ bool attn_tc_supported(const Geometry& g) {
   return g.d == kD && g.k >= 16 && g.k <= 128 && (kBM % G) == 0;
 }
 
-bool make_tmap_kv(void* out, const void* pool, int64_t total_rows, int32_t d, int32_t k,
-                  const char** err) {
+bool make_tmap_kv(void* out, const void* pool, int64_t num_blocks, int32_t L, int32_t h_kv,
+                  int32_t d, int32_t k, const char** err) {
   auto fn = encode_fn(err);
   if (!fn) return false;
+  const int64_t total_rows = num_blocks * L * 2 * h_kv * k;
   if (total_rows >= (1ll << 31)) {
     *err = "pool has >= 2^31 rows";
     return false;
   }
-  cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)total_rows};
-  cuuint64_t strides[1] = {(cuuint64_t)d * 2};
-  cuuint32_t box[2] = {64, (cuuint32_t)k};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn((CUtensorMap*)out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)pool, dims,
-                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    *err = "cuTensorMapEncodeTiled(pool) failed";
-    return false;
+  // (1) per-block map: the pool as [rows][d], box {64, k} = one (block, layer, K|V, head) d-half
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)total_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)k};
+    if (const char* e = getenv("S2L_EXP_BOX_ROWS")) box[1] = (cuuint32_t)atoi(e);   // experiments only
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn((CUtensorMap*)out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)pool, dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      *err = "cuTensorMapEncodeTiled(pool, per block) failed";
+      return false;
+    }
+  }
+  // (2) run map: the pool as [block][L*2*h_kv][k][d], box {64, k, 1, 128/k} = one d-half of a
+  //     whole 128-key tile when the tile's blocks have consecutive ids (the common case with
+  //     the lowest-free-id allocator): rows land contiguous, exactly like 128/k per-block boxes.
+  {
+    const int32_t R = 128 / k;
+    cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)k, (cuuint64_t)L * 2 * h_kv, (cuuint64_t)num_blocks};
+    cuuint64_t strides[3] = {(cuuint64_t)d * 2, (cuuint64_t)k * d * 2, (cuuint64_t)L * 2 * h_kv * k * d * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)k, 1, (cuuint32_t)(R > 0 ? R : 1)};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn((CUtensorMap*)((char*)out + 128), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)pool,
+                    dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      *err = "cuTensorMapEncodeTiled(pool, block runs) failed";
+      return false;
+    }
   }
   return true;
 }
@@ -1578,9 +1650,10 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
   p.kb = g.k;
   p.group = g.h_q / g.h_kv;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)kD);
-  CUtensorMap tq, tkv;
+  CUtensorMap tq, tkv, tkv4;
   memcpy(&tq, tmap_q, sizeof(CUtensorMap));
   memcpy(&tkv, tmap_kv, sizeof(CUtensorMap));
+  memcpy(&tkv4, (const char*)tmap_kv + 128, sizeof(CUtensorMap));
   p.split_begin = total_units;
   p.split_s = 1;
   int32_t grid = total_units;
@@ -1595,9 +1668,9 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
   p.n_work = grid;
   if (variant == 2 && persistent) {
     const int32_t g = grid < num_sms ? grid : num_sms;
-    attn_tc3_kernel<<<g, v2::kThreads, v2::SMEM, st>>>(tq, tkv, p);
+    attn_tc3_kernel<<<g, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, p);
   } else if (variant == 2)
-    attn_tc2_kernel<<<grid, v2::kThreads, v2::SMEM, st>>>(tq, tkv, p);
+    attn_tc2_kernel<<<grid, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, p);
   else
     attn_tc_kernel<<<total_units, kThreads, SMEM_BYTES, st>>>(tq, tkv, p);
   return cudaGetLastError();

@@ -22,9 +22,10 @@ __global__ void table_patch_kernel(const TablePatch* __restrict__ patches, int32
 }
 
 constexpr int kVecPerThread = 8;   // 8 x 16-byte loads in flight per thread, then 8 stores
+constexpr int kSmemItems = 256;    // items / ids staged in shared memory when they fit (38 KB)
+constexpr int kSmemIds = 6144;
 
-__device__ __forceinline__ int32_t find_item(const AppendItemDev* __restrict__ items, int32_t n,
-                                             int64_t row) {
+__device__ __forceinline__ int32_t find_item(const AppendItemDev* items, int32_t n, int64_t row) {
   int32_t lo = 0, hi = n - 1;     // last item with row_begin <= row
   while (lo < hi) {
     const int32_t mid = (lo + hi + 1) >> 1;
@@ -33,12 +34,26 @@ __device__ __forceinline__ int32_t find_item(const AppendItemDev* __restrict__ i
   return lo;
 }
 
+// One thread moves kVecPerThread 16-byte vectors of the concatenated [rows][h_kv][d] input of
+// one (layer, K|V) (blockIdx.y) to their (block, slot) in the pool.  The item descriptors and
+// the block ids are staged in shared memory first, so the only global load on each vector's
+// critical path is the data itself.
 __global__ void __launch_bounds__(256) append_kernel(
-    const AppendItemDev* __restrict__ items, int32_t n_items, int64_t total_vecs_per_lk,
-    const int32_t* __restrict__ ids, const TablePatch* __restrict__ patches, int32_t n_patches,
-    int32_t* __restrict__ table, const uint4* __restrict__ k, const uint4* __restrict__ v,
-    int64_t kv_rows, uint4* __restrict__ pool, int32_t L, int32_t h_kv, int32_t vec_per_row,
-    int32_t kb_log2) {
+    const AppendItemDev* __restrict__ items_g, int32_t n_items, int64_t total_vecs_per_lk,
+    const int32_t* __restrict__ ids_g, int32_t n_ids, const TablePatch* __restrict__ patches,
+    int32_t n_patches, int32_t* __restrict__ table, const uint4* __restrict__ k,
+    const uint4* __restrict__ v, int64_t kv_rows, uint4* __restrict__ pool, int32_t L,
+    int32_t h_kv, int32_t vec_per_row, int32_t kb_log2, int32_t vpt_log2) {
+  __shared__ AppendItemDev s_items[kSmemItems];
+  __shared__ int32_t s_ids[kSmemIds];
+  const bool staged = n_items <= kSmemItems && n_ids <= kSmemIds;
+  if (staged) {
+    for (int32_t i = threadIdx.x; i < n_items; i += blockDim.x) s_items[i] = items_g[i];
+    for (int32_t i = threadIdx.x; i < n_ids; i += blockDim.x) s_ids[i] = ids_g[i];
+    __syncthreads();
+  }
+  const AppendItemDev* items = staged ? s_items : items_g;
+  const int32_t* ids = staged ? s_ids : ids_g;
   const int32_t lk = blockIdx.y;          // layer * 2 + kind
   const int32_t layer = lk >> 1, kind = lk & 1;
   if (lk == 0 && blockIdx.x == 0) {
@@ -57,7 +72,7 @@ __global__ void __launch_bounds__(256) append_kernel(
       const int32_t g = g0 + u * stride;
       dst[u] = -1;
       if (g < total) {
-        const int32_t row = g / vpt;                        // token row of the concatenation
+        const int32_t row = vpt_log2 >= 0 ? (g >> vpt_log2) : g / vpt;   // token row
         const int32_t rem = g - row * vpt;
         const int32_t head = rem / vec_per_row;
         const int32_t vec = rem - head * vec_per_row;
@@ -88,7 +103,8 @@ cudaError_t launch_table_patch(const TablePatch* patches, int32_t n, int32_t* ta
 }
 
 cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t n_items,
-                          int64_t total_rows, const int32_t* ids, const TablePatch* patches,
+                          int64_t total_rows, const int32_t* ids, int32_t n_ids,
+                          const TablePatch* patches,
                           int32_t n_patches, int32_t* table, const void* k, const void* v,
                           int64_t kv_rows, void* pool, cudaStream_t st) {
   const int32_t vec_per_row = g.d / 8;
@@ -96,15 +112,27 @@ cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t
   if (total >= (1ll << 31)) return cudaErrorInvalidValue;
   int kb_log2 = 0;
   while ((1 << kb_log2) < g.k) ++kb_log2;
-  // one pass: each thread moves kVecPerThread vectors (grid covers the data exactly once)
+  const int32_t vpt = g.h_kv * vec_per_row;
+  int vpt_log2 = -1;
+  if ((vpt & (vpt - 1)) == 0) {
+    vpt_log2 = 0;
+    while ((1 << vpt_log2) < vpt) ++vpt_log2;
+  }
+  // one pass: each thread moves kVecPerThread vectors; at most one wave of resident CTAs
   int64_t threads = (total + kVecPerThread - 1) / kVecPerThread;
   int64_t blocks = (threads + 255) / 256;
+  const int64_t wave = 148 * 4;                 // 4 x 256-thread CTAs resident per SM (64 regs)
+  const int64_t per_lk = blocks;
+  if (blocks * g.L * 2 > wave && per_lk > 1) {
+    blocks = (wave + g.L * 2 - 1) / (g.L * 2);
+    if (blocks < 1) blocks = 1;
+  }
   if (blocks < 1) blocks = 1;
   if (blocks > 65535) blocks = 65535;
   dim3 grid((unsigned)blocks, g.L * 2);
-  append_kernel<<<grid, 256, 0, st>>>(items, n_items, total, ids, patches, n_patches, table,
+  append_kernel<<<grid, 256, 0, st>>>(items, n_items, total, ids, n_ids, patches, n_patches, table,
                                       (const uint4*)k, (const uint4*)v, kv_rows, (uint4*)pool,
-                                      g.L, g.h_kv, vec_per_row, kb_log2);
+                                      g.L, g.h_kv, vec_per_row, kb_log2, vpt_log2);
   return cudaGetLastError();
 }
 

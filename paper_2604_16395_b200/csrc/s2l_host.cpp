@@ -132,7 +132,7 @@ struct s2l_ctx {
   // by a swap-out may only be rewritten by the compute stream after it
   cudaEvent_t swap_out_done = nullptr;
   bool swap_out_pending = false;
-  unsigned char tmap_kv[128] __attribute__((aligned(64)));
+  unsigned char tmap_kv[256] __attribute__((aligned(64)));
   int32_t num_sms = 148;
   float* split_ws = nullptr;          // tail-wave split partials (num_sms pieces)
   int32_t* split_cnt = nullptr;       // per split unit arrival counters (self-resetting)
@@ -464,9 +464,8 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
   c->tc_ok = s2l::attn_tc_supported(c->geo);
   if (c->tc_ok && cfg->num_gpu_blocks > 0) {
     const char* err = nullptr;
-    int64_t rows = (int64_t)cfg->num_gpu_blocks * cfg->num_layers * 2 * cfg->num_kv_heads *
-                   cfg->block_size;
-    if (!s2l::make_tmap_kv(c->tmap_kv, gpu_pool, rows, cfg->head_dim, cfg->block_size, &err))
+    if (!s2l::make_tmap_kv(c->tmap_kv, gpu_pool, cfg->num_gpu_blocks, cfg->num_layers,
+                           cfg->num_kv_heads, cfg->head_dim, cfg->block_size, &err))
       return fail(S2L_E_CUDA, "tensor map (pool): %s", err ? err : "?");
   } else {
     c->tc_ok = false;
@@ -643,7 +642,7 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
     CK(cudaEventRecord(tp.first, c->compute));
   }
   CK(s2l::launch_append(c->geo, (const s2l::AppendItemDev*)dv, (int32_t)dev_items.size(),
-                        total_rows, (const int32_t*)(dv + off_ids),
+                        total_rows, (const int32_t*)(dv + off_ids), (int32_t)ids.size(),
                         (const s2l::TablePatch*)(dv + off_patch), n_patch, c->d_table, k, v,
                         kv_rows, c->gpu_pool, c->compute));
   c->launches++;

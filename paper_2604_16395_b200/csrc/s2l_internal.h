@@ -48,7 +48,8 @@ cudaError_t launch_table_patch(const TablePatch* patches, int32_t n, int32_t* ta
 
 // Writes K/V rows into the pool and applies the table patches (fused).
 cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t n_items,
-                          int64_t total_rows, const int32_t* ids, const TablePatch* patches,
+                          int64_t total_rows, const int32_t* ids, int32_t n_ids,
+                          const TablePatch* patches,
                           int32_t n_patches, int32_t* table, const void* k, const void* v,
                           int64_t kv_rows, void* pool, cudaStream_t st);
 
@@ -59,7 +60,7 @@ cudaError_t launch_attn_generic(const Geometry& g, const AttnItemDev* items, int
                                 cudaStream_t st);
 
 // tcgen05 / TMEM / TMA attention (head_dim 128, 16 <= k <= 128, 128 % (h_q/h_kv) == 0).
-// tmap_q / tmap_kv point to host CUtensorMap (128-byte) objects passed by value.
+// tmap_q points to one host CUtensorMap (128 bytes), tmap_kv to the two pool maps (256 bytes).
 bool attn_tc_supported(const Geometry& g);
 // Q tiles per CTA of the tensor-core kernel (2 = ping-pong v2, default; 1 = v1 via S2L_ATTN_V1=1).
 int attn_tc_tiles_per_cta();
@@ -78,7 +79,8 @@ constexpr int64_t kSplitPieceFloats = 2 * 128 * 130;   // O [2][128][128] + (m, 
 // TMA descriptors (host).  Returns false on failure (message in *err).
 bool make_tmap_q(void* out128, const void* q, int64_t q_rows, int32_t h_q, int32_t d,
                  int32_t group, const char** err);
-bool make_tmap_kv(void* out128, const void* pool, int64_t total_rows, int32_t d, int32_t k,
-                  const char** err);
+// Two maps of the pool into out256: [0,128) per-block boxes, [128,256) 4-D block-run boxes.
+bool make_tmap_kv(void* out256, const void* pool, int64_t num_blocks, int32_t L, int32_t h_kv,
+                  int32_t d, int32_t k, const char** err);
 
 }  // namespace s2l
