@@ -81,6 +81,7 @@ struct TcParams {
   float* ws;       // [pieces][2][128][128] partial O (unnormalised, fp32)
   float* ws_ml;    // [pieces][2][128][2] running max (log2 units) and row sum
   int32_t* ws_cnt;
+  uint32_t* trace;   // S2L_TRACE builds only: per-event SM clock stamps of CTA 0
 };
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -537,7 +538,9 @@ __device__ __forceinline__ float chunk_max(const uint32_t (&v)[32], float mx, in
 template <bool kMasked, int kPolyPer8>
 __device__ __forceinline__ float2 chunk_p(const uint32_t (&v)[32], float2 acc, int vis, int base,
                                           float2 sc2, float2 nm2, uint32_t (&pk)[16]) {
-  float2 acc2 = make_float2(0.f, 0.f);   // second chain: halves the FADD2 dependency latency
+  // Phase-ordered so a single warp has 16 independent pairs in flight per phase (the softmax
+  // of a tile runs one warp per SMSP, so latency is hidden only by this ILP).
+  float2 x[16];
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
     float s0 = __uint_as_float(v[2 * c]), s1 = __uint_as_float(v[2 * c + 1]);
@@ -545,30 +548,43 @@ __device__ __forceinline__ float2 chunk_p(const uint32_t (&v)[32], float2 acc, i
       if (base + 2 * c > vis) s0 = -INFINITY;
       if (base + 2 * c + 1 > vis) s1 = -INFINITY;
     }
-    const float2 x = __ffma2_rn(make_float2(s0, s1), sc2, nm2);
-    float2 pp;
-#if S2L_EXP_MODE == 1
-    pp = exp2_f16x2(x);
-#else
-    if (!kMasked && (c & 7) < kPolyPer8) pp = exp2_poly2(x);
-    else pp = make_float2(fast_exp2(x.x), fast_exp2(x.y));
-#endif
-    if (c & 1) acc2 = __fadd2_rn(acc2, pp); else acc = __fadd2_rn(acc, pp);
-    pk[c] = pack_bf16(pp.x, pp.y);
+    x[c] = __ffma2_rn(make_float2(s0, s1), sc2, nm2);
   }
-  return __fadd2_rn(acc, acc2);
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+#if S2L_EXP_MODE == 1
+    x[c] = exp2_f16x2(x[c]);
+#else
+    if (!kMasked && (c & 7) < kPolyPer8) x[c] = exp2_poly2(x[c]);
+    else x[c] = make_float2(fast_exp2(x[c].x), fast_exp2(x[c].y));
+#endif
+  }
+  float2 a[4] = {acc, make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    a[c & 3] = __fadd2_rn(a[c & 3], x[c]);
+    pk[c] = pack_bf16(x[c].x, x[c].y);
+  }
+  return __fadd2_rn(__fadd2_rn(a[0], a[1]), __fadd2_rn(a[2], a[3]));
 }
-// Row max with 4 independent chains (short dependency latency).
+// Row max of 32 columns with 8 independent chains (short dependency latency).
+template <bool kMasked>
+__device__ __forceinline__ void max32(const uint32_t* sv, int vis, int base, float (&t)[8]) {
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    float x = __uint_as_float(sv[c]);
+    if (kMasked && base + c > vis) x = -INFINITY;
+    t[c & 7] = fmaxf(t[c & 7], x);
+  }
+}
 template <bool kMasked>
 __device__ __forceinline__ float row_max(const uint32_t (&sv)[128], int vis) {
-  float t[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  float t[8];
 #pragma unroll
-  for (int c = 0; c < 128; ++c) {
-    float x = __uint_as_float(sv[c]);
-    if (kMasked && c > vis) x = -INFINITY;
-    t[c & 3] = fmaxf(t[c & 3], x);
-  }
-  return fmaxf(fmaxf(t[0], t[1]), fmaxf(t[2], t[3]));
+  for (int i = 0; i < 8; ++i) t[i] = -INFINITY;
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) max32<kMasked>(sv + 32 * cc, vis, 32 * cc, t);
+  return fmaxf(fmaxf(fmaxf(t[0], t[1]), fmaxf(t[2], t[3])), fmaxf(fmaxf(t[4], t[5]), fmaxf(t[6], t[7])));
 }
 // Row max of the tile (pass 1) with the next chunk's TMEM load in flight.
 template <bool kMasked>
@@ -626,6 +642,25 @@ __device__ __forceinline__ float row_p(uint32_t (&sv)[128], uint32_t tS, int vis
   }
   return acc.x + acc.y;
 }
+
+#ifdef S2L_TRACE
+// Timing experiment: CTA 0 records (event, tile, step, clock); each writer thread has its own
+// region and counter, so a stamp is two fire-and-forget global stores.
+__device__ __forceinline__ void trace_ev(const TcParams& p, uint32_t& n, uint32_t writer, uint32_t ev,
+                                         uint32_t tile, uint32_t j) {
+  if (blockIdx.x != 0 || p.trace == nullptr || n >= 4000) return;
+  uint32_t c;
+  asm volatile("mov.u32 %0, %%clock;" : "=r"(c));
+  uint32_t* e = p.trace + 16 + (writer * 4096 + n) * 2;
+  e[0] = (ev << 24) | (tile << 16) | (j & 0xffff);
+  e[1] = c;
+  ++n;
+  p.trace[writer] = n;
+}
+#define TRACE(ev, tile, j) trace_ev(p, tr_n, tr_w, ev, tile, j)
+#else
+#define TRACE(ev, tile, j)
+#endif
 // ======================================================================================
 // v2: two Q tiles per CTA ping-ponged through the tensor core (the softmax of one tile runs
 // while the MMAs of the other execute), P kept in TMEM (TS-MMA: A operand = P from TMEM,
@@ -702,6 +737,457 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
                     const __grid_constant__ CUtensorMap tmap_kv,
                     const __grid_constant__ CUtensorMap tmap_kv4, const TcParams p) {
   using namespace v2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sb = smem_u32(smem);
+  auto bar = [&](uint32_t i) { return sb + WOFF_BAR + 8u * i; };
+  uint32_t* tmem_holder = (uint32_t*)(smem + WOFF_TMEM);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef S2L_TRACE
+  uint32_t tr_n = 0;
+  const uint32_t tr_w = warp == 1 ? 0u : (warp == 4 ? 1u : (warp == 8 ? 2u : 3u));
+#endif
+
+  // ---- work unit: (item, kv head, pair of Q tiles), longest first
+  int32_t unit = blockIdx.x, piece = 0, npieces = 1;
+  if (unit >= p.split_begin) {
+    const int32_t b = unit - p.split_begin;
+    unit = p.split_begin + b / p.split_s;
+    piece = b % p.split_s;
+    npieces = p.split_s;
+  }
+  int32_t lo = 0, hi = p.n_items - 1;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (p.items[mid].unit_begin <= unit) lo = mid; else hi = mid - 1;
+  }
+  const AttnItemDev it = p.items[lo];
+  const int32_t local = unit - it.unit_begin;
+  const int32_t pairs = (it.tiles + 1) >> 1;
+  const int32_t pair = pairs - 1 - local / p.h_kv;
+  const int32_t kvh = local % p.h_kv;
+  const int32_t G = p.group;
+  const int32_t toks = kBM / G;
+  const int32_t tok0 = pair * 2 * toks;               // first token of tile 0; tile 1 at +toks
+  const int32_t tok_last = min(tok0 + 2 * toks, it.n_q) - 1;
+  const int64_t key_last = it.q_pos + tok_last;
+  const int32_t nT_all = (int32_t)(key_last / kBN) + 1;
+  const int32_t jb = (int32_t)((int64_t)nT_all * piece / npieces);   // this CTA's KV tiles
+  const int32_t nT = (int32_t)((int64_t)nT_all * (piece + 1) / npieces) - jb;
+  const int64_t kv_len = it.q_pos + it.n_q;
+  const int32_t nblk_valid = (int32_t)((kv_len + p.kb - 1) / p.kb);
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar(WB_QF), 1);
+    for (int s = 0; s < WNST; ++s) {
+      mbar_init(bar(WB_RF + s), 1);
+      mbar_init(bar(WB_RE + s), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(WB_SF + i), 1);
+      mbar_init(bar(WB_PF + i), 128);
+      mbar_init(bar(WB_PH + i), 128);
+      mbar_init(bar(WB_OF + i), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv4) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtrl));
+    if (warp == 0) {
+      // ================= TMA producer =================
+      if (lane == 0) {
+        mbar_expect_tx(bar(WB_QF), 2 * kTileBytes);
+        const int32_t z = (int32_t)(it.q_row + tok0);
+        tma_load_3d(sb + WOFF_Q0, &tmap_q, bar(WB_QF), 0, kvh * G, z);
+        tma_load_3d(sb + WOFF_Q0 + kAtom, &tmap_q, bar(WB_QF), 64, kvh * G, z);
+        tma_load_3d(sb + WOFF_Q1, &tmap_q, bar(WB_QF), 0, kvh * G, z + toks);
+        tma_load_3d(sb + WOFF_Q1 + kAtom, &tmap_q, bar(WB_QF), 64, kvh * G, z + toks);
+      }
+      const int32_t nb_tile = kBN / p.kb;               // 1..8 blocks per 128-key tile
+      const int32_t* trow = p.table + (int64_t)it.slot * p.max_blocks;
+      const int32_t rows_per_block = p.L * 2 * p.h_kv * p.kb;
+      const int32_t row_kv[2] = {((p.layer * 2 + 0) * p.h_kv + kvh) * p.kb,
+                                 ((p.layer * 2 + 1) * p.h_kv + kvh) * p.kb};
+      const int32_t lkh[2] = {(p.layer * 2 + 0) * p.h_kv + kvh, (p.layer * 2 + 1) * p.h_kv + kvh};
+      auto load_id = [&](int32_t jt) {                  // lane b < nb_tile: block b of tile jt
+        const int32_t b = (jb + jt) * nb_tile + lane;
+        return __ldg(trow + (b < nblk_valid ? b : 0));
+      };
+      int32_t next_id = (lane < nb_tile) ? load_id(0) : 0;
+      uint32_t rp = 0;
+      for (int32_t j = 0; j < nT; ++j) {
+        const int32_t cur_id = next_id;
+        if (j + 1 < nT && lane < nb_tile) next_id = load_id(j + 1);   // prefetch the next ids
+        int32_t ids[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) ids[b] = __shfl_sync(0xffffffffu, cur_id, b);
+        bool run = (jb + j + 1) * nb_tile <= nblk_valid;   // whole tile inside the table
+#pragma unroll
+        for (int b = 1; b < 8; ++b)
+          if (b < nb_tile) run = run && (ids[b] == ids[0] + b);
+#pragma unroll
+        for (int kind = 0; kind < 2; ++kind, ++rp) {
+          const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
+          mbar_wait(bar(WB_RE + s), ph ^ 1);
+          if (lane == 0 && run) {
+            // consecutive block ids: two 4-D boxes (d halves) cover the whole 128-key tile
+            mbar_expect_tx(bar(WB_RF + s), kTileBytes);
+            const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
+            tma_load_4d(dst, &tmap_kv4, bar(WB_RF + s), 0, 0, lkh[kind], ids[0]);
+            tma_load_4d(dst + kAtom, &tmap_kv4, bar(WB_RF + s), 64, 0, lkh[kind], ids[0]);
+          } else if (lane == 0) {
+            // one lane issues the whole tile: 2 boxes {64, k} (d halves) per block
+#ifdef S2L_EXP_HALF_LOAD   // timing experiment only: load one d-half of each K/V tile
+            mbar_expect_tx(bar(WB_RF + s), kTileBytes / 2);
+#else
+            mbar_expect_tx(bar(WB_RF + s), kTileBytes);
+#endif
+            const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
+#ifdef S2L_EXP_BOX32   // timing experiment only: boxes of 2 blocks (wrong rows, same bytes)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              if (b < nb_tile / 2) {
+                const int32_t y = ids[2 * b] * rows_per_block + row_kv[kind];
+                tma_load_2d(dst + b * 2 * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
+                tma_load_2d(dst + kAtom + b * 2 * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
+              }
+            }
+            if (false)
+#endif
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+              if (b < nb_tile) {
+                const int32_t y = ids[b] * rows_per_block + row_kv[kind];
+                tma_load_2d(dst + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
+#ifndef S2L_EXP_HALF_LOAD
+                tma_load_2d(dst + kAtom + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
+#endif
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
+    } else if (warp == 1) {
+      // ================= MMA issuer (whole warp, one elected lane issues) =================
+      constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16(kBM, kD, 0, 1);
+      // descriptors of the buffer bases; the start-address field (bits 0-13, 16-byte units)
+      // is advanced by adding (byte offset >> 4) — smem addresses stay below 256 KB
+      const uint64_t dq[2] = {sdesc(sb + WOFF_Q0, 16, 1024), sdesc(sb + WOFF_Q1, 16, 1024)};
+      const uint64_t dk0 = sdesc(sb + WOFF_RING, 16, 1024);
+      const uint64_t dv0 = sdesc(sb + WOFF_RING, kAtom, 1024);
+      uint32_t rp = 0;
+      auto next_full = [&]() {
+        const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
+        ++rp;
+        mbar_wait(bar(WB_RF + s), ph);
+        tc_fence_after();
+        return s;
+      };
+      auto issue_s = [&](int i, uint32_t kslot) {
+        if (lane == 0) TRACE(13, i, 0);
+        const uint64_t kd = dk0 + ((kslot * kTileBytes) >> 4);
+#ifndef S2L_EXP_NO_S
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const uint32_t off = ((kk >> 2) * kAtom + (kk & 3) * 32) >> 4;
+          mma_ss_elect(tmem + i * 128, dq[i] + off, kd + off, idesc_s, kk > 0);
+        }
+#endif
+        mma_commit_elect(bar(WB_SF + i));
+        if (lane == 0) TRACE(14, i, 0);
+      };
+      auto issue_pv = [&](int i, uint32_t vslot, int32_t j) {
+        const uint64_t vd = dv0 + ((vslot * kTileBytes) >> 4);
+        if (lane == 0) TRACE(10, i, j);
+        mbar_wait(bar(WB_PF + i), j & 1);               // P keys 0-63 in TMEM
+        tc_fence_after();
+        if (lane == 0) TRACE(11, i, j);
+#ifndef S2L_EXP_NO_PV
+#pragma unroll
+        for (int kk = 0; kk < kBN / 32; ++kk)
+          mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
+                       idesc_o, (j > 0 || kk > 0));
+        mbar_wait(bar(WB_PH + i), j & 1);               // P keys 64-127
+        tc_fence_after();
+        if (lane == 0) TRACE(12, i, j);
+#pragma unroll
+        for (int kk = kBN / 32; kk < kBN / 16; ++kk)
+          mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
+                       idesc_o, 1);
+#endif
+      };
+      mbar_wait(bar(WB_QF), 0);
+      tc_fence_after();
+      uint32_t kslot = next_full();
+      issue_s(0, kslot);
+      issue_s(1, kslot);
+      mma_commit_elect(bar(WB_RE + kslot));
+      for (int32_t j = 0; j < nT; ++j) {
+        const uint32_t vslot = next_full();
+        issue_pv(0, vslot, j);
+        const bool more = j + 1 < nT;
+        if (more) {
+          kslot = next_full();
+          issue_s(0, kslot);
+        } else {
+          mma_commit_elect(bar(WB_OF + 0));
+        }
+        issue_pv(1, vslot, j);
+        mma_commit_elect(bar(WB_RE + vslot));
+        if (more) {
+          issue_s(1, kslot);
+          mma_commit_elect(bar(WB_RE + kslot));
+        } else {
+          mma_commit_elect(bar(WB_OF + 1));
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
+    // ================= softmax / correction / epilogue of Q tile i =================
+    const int i = (warp - 4) >> 2;                   // 0: warps 4-7, 1: warps 8-11
+    const int r = (warp & 3) * 32 + lane;            // tile row == TMEM lane
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane_off + i * 128;
+    const uint32_t tO = tmem + lane_off + TMEM_O + i * 128;
+    const int32_t tok = tok0 + i * toks + r / G;
+    const int32_t hq = kvh * G + r % G;
+    const bool valid = tok < it.n_q;
+    const int64_t limit = it.q_pos + (valid ? tok : tok_last);
+    const float sl2 = p.scale_log2;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int32_t j = 0; j < nT; ++j) {
+      const bool tr = (warp & 3) == 0 && lane == 0;
+      if (tr) TRACE(20, i, j);
+      mbar_wait(bar(WB_SF + i), j & 1);
+      tc_fence_after();
+      if (tr) TRACE(21, i, j);
+#ifdef S2L_EXP_MMA_ONLY   // timing experiment only: tensor-core / TMA pipeline without softmax
+      tc_fence_before();
+      mbar_arrive(bar(WB_PF + i));
+      mbar_arrive(bar(WB_PH + i));
+      continue;
+#endif
+      const int64_t key0 = (int64_t)(jb + j) * kBN;
+      const int64_t vis64 = limit - key0;                 // keys c <= vis of this tile visible
+      const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBN ? kBN : vis64));
+      const bool masked_tile = __any_sync(0xffffffffu, vis < kBN - 1);
+      uint32_t sv[128];
+      float mt[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) mt[q] = -INFINITY;
+      tmem_ld32(tS, sv);
+      tmem_ld32(tS + 32, sv + 32);
+      tmem_wait_ld();
+      tmem_ld32(tS + 64, sv + 64);                      // in flight during the first max half
+      tmem_ld32(tS + 96, sv + 96);
+      if (masked_tile) { max32<true>(sv, vis, 0, mt); max32<true>(sv + 32, vis, 32, mt); }
+      else { max32<false>(sv, vis, 0, mt); max32<false>(sv + 32, vis, 32, mt); }
+      tmem_wait_ld();
+      if (masked_tile) { max32<true>(sv + 64, vis, 64, mt); max32<true>(sv + 96, vis, 96, mt); }
+      else { max32<false>(sv + 64, vis, 64, mt); max32<false>(sv + 96, vis, 96, mt); }
+      float mx = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])), fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7])));
+      mx *= sl2;
+      if (tr) TRACE(22, i, j);
+      const float m_new = (mx > m_run + kRescaleThresh) ? mx : m_run;
+      if (j > 0) {
+        const bool resc = m_new != m_run;
+        if (__any_sync(0xffffffffu, resc)) {
+          const float alpha = resc ? fast_exp2(m_run - m_new) : 1.f;
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            uint32_t ov[16];
+            tmem_ld16(tO + c * 16, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              float2 x = __fmul2_rn(make_float2(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])),
+                                    make_float2(alpha, alpha));
+              ov[e] = __float_as_uint(x.x);
+              ov[e + 1] = __float_as_uint(x.y);
+            }
+            tmem_st16(tO + c * 16, ov);
+          }
+          l_run *= alpha;
+        }
+      }
+      m_run = m_new;
+      // a row with no visible key yet (possible in a split piece) keeps m = -inf and p = 0
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_use, -m_use);
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t pk[16];
+        uint32_t(&v32)[32] = *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc);
+        acc = masked_tile ? chunk_p<true, 0>(v32, acc, vis, 32 * cc, sc2, nm2, pk)
+                          : chunk_p<false, kPolyPairsPer8>(v32, acc, vis, 32 * cc, sc2, nm2, pk);
+        tmem_st16(tS + 16 * cc, pk);
+        if (cc == 1 || cc == 3) {      // keys 0-63 / 64-127 of P are in TMEM
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(bar((cc == 1 ? WB_PF : WB_PH) + i));
+          if (tr) TRACE(cc == 1 ? 23 : 24, i, j);
+        }
+      }
+      l_run += acc.x + acc.y;
+    }
+    // epilogue
+    mbar_wait(bar(WB_OF + i), 0);
+    tc_fence_after();
+    __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
+    if (npieces == 1) {
+      const float inv = 1.f / l_run;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t ov[16];
+        tmem_ld16(tO + c * 16, ov);
+        tmem_wait_ld();
+        if (valid) {
+          uint32_t w[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            w[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      }
+      if (valid && p.lse)
+        p.lse[(it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+    } else {
+      // partial (unnormalised O, m, l) of this KV range -> workspace; the last piece merges
+      const int32_t su = unit - p.split_begin;                 // split-unit index
+      const int64_t prow = (((int64_t)su * npieces + piece) * 2 + i) * 128 + r;
+      float* wo = p.ws + prow * kD;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t ov[16];
+        tmem_ld16(tO + c * 16, ov);
+        tmem_wait_ld();
+        float4* dst = reinterpret_cast<float4*>(wo + c * 16);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
+                               __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
+      }
+      p.ws_ml[prow * 2] = m_run;
+      p.ws_ml[prow * 2 + 1] = l_run;
+      __threadfence();
+      asm volatile("bar.sync 1, 256;" ::: "memory");       // both softmax warpgroups wrote
+      uint32_t* flag = (uint32_t*)(smem + WOFF_TMEM + 8);
+      if (threadIdx.x == 128) {
+        const int32_t old = atomicAdd(p.ws_cnt + su, 1);
+        const uint32_t last = (old == npieces - 1) ? 1u : 0u;
+        if (last) p.ws_cnt[su] = 0;                          // ready for the next launch
+        *flag = last;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (*flag) {
+        __threadfence();
+        float M = -INFINITY;
+        for (int k = 0; k < npieces; ++k) {
+          const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
+          M = fmaxf(M, __ldcg(p.ws_ml + pr * 2));
+        }
+        constexpr int kMaxPieces = 8;
+        float wk[kMaxPieces];
+        float Lsum = 0.f;
+#pragma unroll
+        for (int k = 0; k < kMaxPieces; ++k) {
+          wk[k] = 0.f;
+          if (k < npieces) {
+            const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
+            wk[k] = fast_exp2(__ldcg(p.ws_ml + pr * 2) - M);
+            Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
+          }
+        }
+        const float inv = 1.f / Lsum;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kD; c0 += 32) {
+          float acc[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+#pragma unroll
+          for (int k = 0; k < kMaxPieces; ++k) {
+            if (k < npieces) {
+              const float* po = p.ws + ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * kD + c0;
+#pragma unroll
+              for (int c = 0; c < 32; c += 2) {
+                const float2 x = __ldcg(reinterpret_cast<const float2*>(po + c));
+                acc[c] += wk[k] * x.x;
+                acc[c + 1] += wk[k] * x.y;
+              }
+            }
+          }
+          if (valid) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) {
+              uint4 v4 = make_uint4(pack_bf16(acc[c] * inv, acc[c + 1] * inv), pack_bf16(acc[c + 2] * inv, acc[c + 3] * inv),
+                                    pack_bf16(acc[c + 4] * inv, acc[c + 5] * inv), pack_bf16(acc[c + 6] * inv, acc[c + 7] * inv));
+              *reinterpret_cast<uint4*>(orow + c0 + c) = v4;
+            }
+          }
+        }
+        if (valid) {
+          if (p.lse) p.lse[(it.q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ======================================================================================
+// v4 = v2 with the softmax of each Q tile split by columns over two warps per SMSP (eight
+// warps per tile, 640 threads): a tile's exponentials are issued by two warps in parallel,
+// halving the softmax latency that bounds the ping-pong (profiles/r01: one warp per SMSP
+// needed ~2200 cycles per tile vs 1024 cycles of the other tile's MMAs).
+namespace v4 {
+constexpr int kThreads = 640;
+constexpr int kRegLaunch = 96, kRegCtrl = 64, kRegSoftmax = 104;
+static_assert(128 * kRegCtrl + 512 * kRegSoftmax <= kThreads * kRegLaunch, "register pool");
+constexpr int WNST = 4;
+constexpr uint32_t WOFF_Q0 = 0;
+constexpr uint32_t WOFF_Q1 = kTileBytes;
+constexpr uint32_t WOFF_RING = 2 * kTileBytes;
+constexpr uint32_t WOFF_RED = WOFF_RING + WNST * kTileBytes;      // 3 x [2][128][2] floats
+constexpr uint32_t WOFF_BAR = WOFF_RED + 3 * 2 * 128 * 2 * 4;
+constexpr uint32_t WB_QF = 0, WB_RF = 1, WB_RE = 1 + WNST, WB_SF = 1 + 2 * WNST, WB_PF = WB_SF + 2,
+                   WB_PH = WB_PF + 2, WB_OF = WB_PH + 2, WNBARS = WB_OF + 2;
+constexpr uint32_t WOFF_TMEM = WOFF_BAR + WNBARS * 8;
+constexpr uint32_t SMEM = WOFF_TMEM + 16 + 1024;
+constexpr int kPolyPairsPer8 = v2::kPolyPairsPer8;
+}  // namespace v4
+
+__global__ void __launch_bounds__(v4::kThreads, 1)
+    attn_tc4_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                    const __grid_constant__ CUtensorMap tmap_kv,
+                    const __grid_constant__ CUtensorMap tmap_kv4, const TcParams p) {
+  using namespace v4;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sb = smem_u32(smem);
@@ -917,12 +1403,21 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
-    // ================= softmax / correction / epilogue of Q tile i =================
-    const int i = (warp - 4) >> 2;                   // 0: warps 4-7, 1: warps 8-11
-    const int r = (warp & 3) * 32 + lane;            // tile row == TMEM lane
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    // ===== softmax / correction / epilogue: tile i, column half h, lane quarter q =====
+    // Each row's 128 scores are split between two warps of the same SMSP (half h handles keys
+    // 64h .. 64h+63); the row max is exchanged through shared memory and a 64-thread named
+    // barrier; each half writes its half of P (and arrives on P_lo / P_hi), rescales and
+    // stores its 64 columns of O.
+    const int t = warp - 4;                          // 0..15
+    const int i = t >> 3;                            // Q tile
+    const int h = (t >> 2) & 1;                      // column half
+    const int q = warp & 3;                          // TMEM lane quarter
+    const int r = q * 32 + lane;                     // tile row == TMEM lane
+    const uint32_t bar_pair = 1 + i * 4 + q;         // named barrier of the two halves of rows q*32..
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const uint32_t tS = tmem + lane_off + i * 128;
-    const uint32_t tO = tmem + lane_off + TMEM_O + i * 128;
+    const uint32_t tO = tmem + lane_off + TMEM_O + i * 128 + 64 * h;
+    float* red = reinterpret_cast<float*>(smem + WOFF_RED);   // [2 parity][2 tiles][128 rows][2 halves]
     const int32_t tok = tok0 + i * toks + r / G;
     const int32_t hq = kvh * G + r % G;
     const bool valid = tok < it.n_q;
@@ -932,31 +1427,36 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     for (int32_t j = 0; j < nT; ++j) {
       mbar_wait(bar(WB_SF + i), j & 1);
       tc_fence_after();
-#ifdef S2L_EXP_MMA_ONLY   // timing experiment only: tensor-core / TMA pipeline without softmax
+#ifdef S2L_EXP_MMA_ONLY
       tc_fence_before();
-      mbar_arrive(bar(WB_PF + i));
-      mbar_arrive(bar(WB_PH + i));
+      mbar_arrive(bar((h ? WB_PH : WB_PF) + i));
       continue;
 #endif
-      const int64_t key0 = (int64_t)(jb + j) * kBN;
-      const int64_t vis64 = limit - key0;                 // keys c <= vis of this tile visible
-      const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBN ? kBN : vis64));
-      const bool masked_tile = __any_sync(0xffffffffu, vis < kBN - 1);
-      uint32_t sv[128];
-      tmem_ld32(tS, sv);
-      tmem_ld32(tS + 32, sv + 32);
-      tmem_ld32(tS + 64, sv + 64);
-      tmem_ld32(tS + 96, sv + 96);
+      const int64_t key0 = (int64_t)(jb + j) * kBN + 64 * h;
+      const int64_t vis64 = limit - key0;             // this half's columns c <= vis visible
+      const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > 64 ? 64 : vis64));
+      const bool masked = __any_sync(0xffffffffu, vis < 63);
+      uint32_t sv[64];
+      float mt[8];
+#pragma unroll
+      for (int z = 0; z < 8; ++z) mt[z] = -INFINITY;
+      tmem_ld32(tS + 64 * h, sv);
+      tmem_ld32(tS + 64 * h + 32, sv + 32);
       tmem_wait_ld();
-      float mx = masked_tile ? row_max<true>(sv, vis) : row_max<false>(sv, vis);
-      mx *= sl2;
+      if (masked) { max32<true>(sv, vis, 0, mt); max32<true>(sv + 32, vis, 32, mt); }
+      else { max32<false>(sv, vis, 0, mt); max32<false>(sv + 32, vis, 32, mt); }
+      float pm = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])), fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7])));
+      float* slot = red + (((j & 1) * 2 + i) * 128 + r) * 2;
+      slot[h] = pm;
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_pair) : "memory");
+      const float mx = fmaxf(slot[0], slot[1]) * sl2;
       const float m_new = (mx > m_run + kRescaleThresh) ? mx : m_run;
       if (j > 0) {
         const bool resc = m_new != m_run;
         if (__any_sync(0xffffffffu, resc)) {
           const float alpha = resc ? fast_exp2(m_run - m_new) : 1.f;
 #pragma unroll 1
-          for (int c = 0; c < 8; ++c) {
+          for (int c = 0; c < 4; ++c) {
             uint32_t ov[16];
             tmem_ld16(tO + c * 16, ov);
             tmem_wait_ld();
@@ -973,33 +1473,34 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         }
       }
       m_run = m_new;
-      // a row with no visible key yet (possible in a split piece) keeps m = -inf and p = 0
       const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
       const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_use, -m_use);
       float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
+      for (int cc = 0; cc < 2; ++cc) {
         uint32_t pk[16];
         uint32_t(&v32)[32] = *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc);
-        acc = masked_tile ? chunk_p<true, 0>(v32, acc, vis, 32 * cc, sc2, nm2, pk)
-                          : chunk_p<false, kPolyPairsPer8>(v32, acc, vis, 32 * cc, sc2, nm2, pk);
-        tmem_st16(tS + 16 * cc, pk);
-        if (cc == 1 || cc == 3) {      // keys 0-63 / 64-127 of P are in TMEM
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(bar((cc == 1 ? WB_PF : WB_PH) + i));
-        }
+        acc = masked ? chunk_p<true, 0>(v32, acc, vis, 32 * cc, sc2, nm2, pk)
+                     : chunk_p<false, kPolyPairsPer8>(v32, acc, vis, 32 * cc, sc2, nm2, pk);
+        tmem_st16(tS + 32 * h + 16 * cc, pk);
       }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar((h ? WB_PH : WB_PF) + i));
       l_run += acc.x + acc.y;
     }
-    // epilogue
+    // ---- epilogue: row sum of both halves, then this half's 64 columns of O
     mbar_wait(bar(WB_OF + i), 0);
     tc_fence_after();
-    __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
+    float* lsl = red + ((2 * 2 + i) * 128 + r) * 2;   // after the two max parities
+    lsl[h] = l_run;
+    asm volatile("bar.sync %0, 64;" ::"r"(bar_pair) : "memory");
+    const float l_tot = lsl[0] + lsl[1];
+    __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD + 64 * h;
     if (npieces == 1) {
-      const float inv = 1.f / l_run;
+      const float inv = 1.f / l_tot;
 #pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < 4; ++c) {
         uint32_t ov[16];
         tmem_ld16(tO + c * 16, ov);
         tmem_wait_ld();
@@ -1013,15 +1514,14 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
           dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
         }
       }
-      if (valid && p.lse)
-        p.lse[(it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+      if (valid && h == 0 && p.lse)
+        p.lse[(it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_tot)) * 0.69314718055994531f;
     } else {
-      // partial (unnormalised O, m, l) of this KV range -> workspace; the last piece merges
-      const int32_t su = unit - p.split_begin;                 // split-unit index
+      const int32_t su = unit - p.split_begin;
       const int64_t prow = (((int64_t)su * npieces + piece) * 2 + i) * 128 + r;
-      float* wo = p.ws + prow * kD;
+      float* wo = p.ws + prow * kD + 64 * h;
 #pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < 4; ++c) {
         uint32_t ov[16];
         tmem_ld16(tO + c * 16, ov);
         tmem_wait_ld();
@@ -1031,18 +1531,20 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
           dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
                                __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
       }
-      p.ws_ml[prow * 2] = m_run;
-      p.ws_ml[prow * 2 + 1] = l_run;
+      if (h == 0) {
+        p.ws_ml[prow * 2] = m_run;
+        p.ws_ml[prow * 2 + 1] = l_tot;
+      }
       __threadfence();
-      asm volatile("bar.sync 1, 256;" ::: "memory");       // both softmax warpgroups wrote
+      asm volatile("bar.sync 9, 512;" ::: "memory");       // every softmax thread wrote
       uint32_t* flag = (uint32_t*)(smem + WOFF_TMEM + 8);
       if (threadIdx.x == 128) {
         const int32_t old = atomicAdd(p.ws_cnt + su, 1);
         const uint32_t last = (old == npieces - 1) ? 1u : 0u;
-        if (last) p.ws_cnt[su] = 0;                          // ready for the next launch
+        if (last) p.ws_cnt[su] = 0;
         *flag = last;
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 9, 512;" ::: "memory");
       if (*flag) {
         __threadfence();
         float M = -INFINITY;
@@ -1064,14 +1566,14 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         }
         const float inv = 1.f / Lsum;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kD; c0 += 32) {
+        for (int c0 = 0; c0 < 64; c0 += 32) {
           float acc[32];
 #pragma unroll
           for (int c = 0; c < 32; ++c) acc[c] = 0.f;
 #pragma unroll
           for (int k = 0; k < kMaxPieces; ++k) {
             if (k < npieces) {
-              const float* po = p.ws + ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * kD + c0;
+              const float* po = p.ws + ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * kD + 64 * h + c0;
 #pragma unroll
               for (int c = 0; c < 32; c += 2) {
                 const float2 x = __ldcg(reinterpret_cast<const float2*>(po + c));
@@ -1089,9 +1591,8 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
             }
           }
         }
-        if (valid) {
-          if (p.lse) p.lse[(it.q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
-        }
+        if (valid && h == 0 && p.lse)
+          p.lse[(it.q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
       }
     }
     tc_fence_before();
@@ -1103,6 +1604,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
                  "r"(TMEM_COLS));
   }
 }
+
 
 // ======================================================================================
 // v3 = v2 made persistent: each CTA loops over work items (whole units, then the tail-wave
@@ -1358,12 +1860,20 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBN ? kBN : vis64));
         const bool masked_tile = __any_sync(0xffffffffu, vis < kBN - 1);
         uint32_t sv[128];
+        float mt[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mt[q] = -INFINITY;
         tmem_ld32(tS, sv);
         tmem_ld32(tS + 32, sv + 32);
-        tmem_ld32(tS + 64, sv + 64);
-        tmem_ld32(tS + 96, sv + 96);
         tmem_wait_ld();
-        float mx = masked_tile ? row_max<true>(sv, vis) : row_max<false>(sv, vis);
+        tmem_ld32(tS + 64, sv + 64);                      // in flight during the first max half
+        tmem_ld32(tS + 96, sv + 96);
+        if (masked_tile) { max32<true>(sv, vis, 0, mt); max32<true>(sv + 32, vis, 32, mt); }
+        else { max32<false>(sv, vis, 0, mt); max32<false>(sv + 32, vis, 32, mt); }
+        tmem_wait_ld();
+        if (masked_tile) { max32<true>(sv + 64, vis, 64, mt); max32<true>(sv + 96, vis, 96, mt); }
+        else { max32<false>(sv + 64, vis, 64, mt); max32<false>(sv + 96, vis, 96, mt); }
+        float mx = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])), fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7])));
         mx *= sl2;
         const float m_new = (mx > m_run + kRescaleThresh) ? mx : m_run;
         if (j > 0) {
@@ -1606,6 +2116,9 @@ bool make_tmap_q(void* out, const void* q, int64_t q_rows, int32_t h_q, int32_t 
   return true;
 }
 
+static uint32_t* g_trace = nullptr;
+void set_attn_trace(uint32_t* buf) { g_trace = buf; }
+
 int attn_tc_tiles_per_cta() {
   static int v = -1;
   if (v < 0) {
@@ -1631,6 +2144,8 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
     if (e != cudaSuccess) return e;
     if (variant == 2) {
       e = cudaFuncSetAttribute(attn_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(attn_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v4::SMEM);
       if (e != cudaSuccess) return e;
     }
     attr_set[variant] = true;
@@ -1662,11 +2177,14 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
     p.split_s = split_s;
     grid = split_begin + (total_units - split_begin) * split_s;
   }
+  p.trace = g_trace;
   p.ws = ws;
   p.ws_ml = ws ? ws + (int64_t)max_pieces * 2 * 128 * kD : nullptr;
   p.ws_cnt = ws_cnt;
   p.n_work = grid;
-  if (variant == 2 && persistent) {
+  if (variant == 2 && (flags & kAttnSplitSoftmax)) {
+    attn_tc4_kernel<<<grid, v4::kThreads, v4::SMEM, st>>>(tq, tkv, tkv4, p);
+  } else if (variant == 2 && persistent) {
     const int32_t g = grid < num_sms ? grid : num_sms;
     attn_tc3_kernel<<<g, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, p);
   } else if (variant == 2)

@@ -137,7 +137,10 @@ struct s2l_ctx {
   float* split_ws = nullptr;          // tail-wave split partials (num_sms pieces)
   int32_t* split_cnt = nullptr;       // per split unit arrival counters (self-resetting)
   bool split_enabled = true;
-  bool persistent = false;            // persistent attention kernel (S2L_PERSIST=1); off: measured slower
+  bool persistent = false;            // persistent attention kernel (S2L_PERSIST=1)
+  bool split_softmax = false;         // v4 kernel (S2L_ATTN_V4=1)
+  uint32_t* trace_buf = nullptr;      // S2L_TRACE=1: device buffer for kernel timelines (experiments)
+  int64_t trace_launch = -1, attn_launch_no = 0;  // which attention launch to trace (S2L_TRACE_LAUNCH)            // persistent attention kernel (S2L_PERSIST=1); off: measured slower
   bool tc_ok = false;
   s2l::Geometry geo{};
 };
@@ -481,6 +484,15 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
     c->split_enabled = !(e && e[0] == '1');
     e = getenv("S2L_PERSIST");
     c->persistent = (e && e[0] == '1');
+    e = getenv("S2L_ATTN_V4");
+    c->split_softmax = (e && e[0] == '1');
+    e = getenv("S2L_TRACE");
+    if (e && e[0] == '1') {
+      CK(cudaMalloc(&c->trace_buf, (16 + 4 * 4096 * 2) * sizeof(uint32_t)));
+      CK(cudaMemsetAsync(c->trace_buf, 0, (16 + 4 * 4096 * 2) * sizeof(uint32_t), c->compute));
+      const char* tl = getenv("S2L_TRACE_LAUNCH");
+      c->trace_launch = tl ? atoll(tl) : 0;
+    }
   }
   CK(cudaStreamSynchronize(c->compute));
   *out = holder.release();
@@ -505,6 +517,16 @@ void s2l_destroy(s2l_ctx* c) {
         cudaEventDestroy(p.second);
       }
     if (c->swap_out_done) cudaEventDestroy(c->swap_out_done);
+    if (c->trace_buf) {   // experiments: dump the recorded timeline
+      std::vector<uint32_t> h(16 + 4 * 4096 * 2);
+      cudaMemcpy(h.data(), c->trace_buf, h.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+      const char* path = getenv("S2L_TRACE_FILE");
+      if (FILE* f = fopen(path ? path : "s2l_trace.bin", "wb")) {
+        fwrite(h.data(), sizeof(uint32_t), h.size(), f);
+        fclose(f);
+      }
+      cudaFree(c->trace_buf);
+    }
     if (c->split_ws) cudaFree(c->split_ws);
     if (c->split_cnt) cudaFree(c->split_cnt);
     if (c->d_table) cudaFree(c->d_table);
@@ -781,10 +803,13 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
         split_s = (int32_t)s_want;
       }
     }
+    s2l::set_attn_trace(c->attn_launch_no++ == c->trace_launch ? c->trace_buf : nullptr);
     CK(s2l::launch_attn_tc(c->geo, dv, n_items, (int32_t)units, split_begin, split_s,
                            c->split_ws, c->num_sms, c->split_cnt, c->d_table, layer, tq,
                            c->tmap_kv, o, lse, c->num_sms,
-                           c->persistent ? s2l::kAttnPersistent : 0, c->compute));
+                           (c->persistent ? s2l::kAttnPersistent : 0) |
+                               (c->split_softmax ? s2l::kAttnSplitSoftmax : 0),
+                           c->compute));
   } else {
     CK(s2l::launch_attn_generic(c->geo, dv, n_items, total_q, c->d_table, layer, q, o, lse,
                                 c->gpu_pool, c->compute));

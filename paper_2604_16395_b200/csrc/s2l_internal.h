@@ -75,6 +75,9 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
                            int32_t flags, cudaStream_t st);
 // flags of launch_attn_tc
 constexpr int32_t kAttnPersistent = 1;   // v2 only: grid = min(work items, SMs), CTAs loop
+constexpr int32_t kAttnSplitSoftmax = 2; // v4: each tile's softmax split over two warps per SMSP
+// Experiments: device buffer receiving kernel timeline stamps (S2L_TRACE builds); nullptr = off.
+void set_attn_trace(uint32_t* buf);   // v2 only: grid = min(work items, SMs), CTAs loop
 constexpr int64_t kSplitPieceFloats = 2 * 128 * 130;   // O [2][128][128] + (m, l) [2][128][2]
 // TMA descriptors (host).  Returns false on failure (message in *err).
 bool make_tmap_q(void* out128, const void* q, int64_t q_rows, int32_t h_q, int32_t d,
