@@ -372,3 +372,71 @@ def test_c5_kv_head_sharding_on_device():
     F.append([(0, None, 1024, 0)], k, v)
     o_f, _, _, _ = F.prefill([(0, 512, 512, 0)], q[512:])
     assert normwise_err(o_s, o_f[:, q_h]).max() <= 2e-2
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_c4_mixed_stream_under_memory_pressure(seed):
+    """C4-like mix (BJ:L10) at small scale: append-mode and update-mode requests interleaved
+    with swap-out / swap-in under a GPU pool smaller than the working set, recompute
+    preemption and release; every prefill is checked against the oracle and every GPU block
+    and CPU block is compared byte for byte at the end (hazards between the copy stream and
+    the compute stream would show up as stale or torn blocks)."""
+    import random
+    geo = W.Geometry(L=2, h_q=8, h_kv=2, d=128, k=16)
+    rng = random.Random(seed)
+    sd = 2000 + seed
+    P = Pair(2, 8, 2, 128, 16, 48, 96, max_blocks=64)
+    reqs = {}
+    for rid in range(10):
+        n = rng.randrange(200, 700)
+        toks = W.request_tokens(sd, rid, n)
+        reqs[rid] = dict(toks=toks, data=_stream_qkv(sd, toks, geo), mode=("append" if rid % 2 == 0 else "update"),
+                         updates=0)
+        P.new(rid, toks)
+    for step in range(60):
+        rid = rng.randrange(10)
+        if rid not in P.ora.reqs:
+            continue
+        r = reqs[rid]
+        info = P.lib.query(rid)
+        if info["tier"] == s2l.TIER_CPU:
+            st, _ = P.swap_in([rid])
+            if st != s2l.OK:
+                # make room: swap out the GPU-resident request holding the most blocks
+                victims = sorted((x for x in P.ora.reqs if P.ora.reqs[x].tier == 0 and x != rid),
+                                 key=lambda x: -len(P.ora.reqs[x].blocks))
+                if victims:
+                    if P.swap_out([victims[0]])[0] != s2l.OK:
+                        P.lib.preempt_recompute(victims[0]); P.ora.preempt_recompute(victims[0])
+                continue
+        nc = P.lib.query(rid)["num_computed"]
+        total = len(r["toks"])
+        if r["mode"] == "update" and nc == total and r["updates"] < 2:
+            p = rng.randrange(0, total)
+            new = W.updated_tokens(sd, rid, r["toks"], p, total, r["updates"])
+            r["updates"] += 1
+            r["toks"] = new
+            r["data"] = _stream_qkv(sd, new, geo)
+            P.invalidate(rid, new)
+            continue
+        if nc == total:
+            if rng.random() < 0.3:
+                assert P.lib.release(rid) == s2l.OK and P.ora.release(rid) == 0
+            continue
+        n = min(total - nc, rng.choice([64, 128, 200]))
+        q, k, v = r["data"]
+        st = P.append([(rid, None, n, 0)], k[:, nc:nc + n], v[:, nc:nc + n])
+        if st == s2l.E_NO_GPU_BLOCKS:
+            victims = [x for x in P.ora.reqs if P.ora.reqs[x].tier == 0 and x != rid and P.ora.reqs[x].blocks]
+            if victims:
+                vtm = rng.choice(victims)
+                if P.swap_out([vtm])[0] != s2l.OK:
+                    P.lib.preempt_recompute(vtm); P.ora.preempt_recompute(vtm)
+            continue
+        assert st == s2l.OK
+        layer = rng.randrange(2)
+        P.prefill([(rid, nc, n, 0)], q[nc:nc + n], layer=layer)
+        P.check_state()
+    P.check_state()
+    P.check_pool_valid_slots()
+    P.check_pools_whole()
