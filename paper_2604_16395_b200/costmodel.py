@@ -73,9 +73,12 @@ class CostModel:
         blocks = -(-computed_tokens // self.block_size)
         return "recompute" if self.recompute_latency(computed_tokens) <= 2.0 * self.swap_latency(blocks) else "swap"
 
-    def crossover_tokens(self, lo: int = 1, hi: int = 1 << 20) -> int | None:
-        """Smallest ℓ in [lo, hi] at which swapping becomes cheaper, by bisection on the sign of
-        C_recomp(ℓ) - 2·C_swap(ℓ) (assumes one crossing; None if recompute wins throughout)."""
+    def crossover_tokens(self, lo: int | None = None, hi: int | None = None) -> int | None:
+        """Smallest ℓ in [lo, hi] (default: the profiled token range) at which swapping becomes
+        cheaper, by bisection on the sign of C_recomp(ℓ) - 2·C_swap(ℓ) (assumes one crossing
+        in the range; None if recompute wins throughout)."""
+        lo = int(self.recompute_s.xs[0]) if lo is None else lo
+        hi = int(self.recompute_s.xs[-1]) if hi is None else hi
         f = lambda t: self.recompute_latency(t) - 2.0 * self.swap_latency(-(-t // self.block_size))
         if f(hi) <= 0:
             return None

@@ -985,6 +985,23 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       mbar_arrive(bar(WB_PH + i));
       continue;
 #endif
+#ifdef S2L_EXP_TMEM_ONLY  // timing experiment only: the softmax's TMEM traffic without its math
+      {
+        uint32_t tv[128];
+        tmem_ld32(tS, tv);
+        tmem_ld32(tS + 32, tv + 32);
+        tmem_ld32(tS + 64, tv + 64);
+        tmem_ld32(tS + 96, tv + 96);
+        tmem_wait_ld();
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) tmem_st16(tS + 16 * cc, tv + 16 * cc);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(bar(WB_PF + i));
+        mbar_arrive(bar(WB_PH + i));
+        continue;
+      }
+#endif
       const int64_t key0 = (int64_t)(jb + j) * kBN;
       const int64_t vis64 = limit - key0;                 // keys c <= vis of this tile visible
       const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBN ? kBN : vis64));
