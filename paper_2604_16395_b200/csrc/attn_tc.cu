@@ -1211,6 +1211,10 @@ __global__ void __launch_bounds__(v4::kThreads, 1)
   auto bar = [&](uint32_t i) { return sb + WOFF_BAR + 8u * i; };
   uint32_t* tmem_holder = (uint32_t*)(smem + WOFF_TMEM);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef S2L_TRACE
+  uint32_t tr_n = 0;
+  const uint32_t tr_w = warp == 1 ? 0u : (warp == 4 ? 1u : (warp == 12 ? 2u : 3u));
+#endif
 
   // ---- work unit: (item, kv head, pair of Q tiles), longest first
   int32_t unit = blockIdx.x, piece = 0, npieces = 1;
@@ -1376,8 +1380,10 @@ __global__ void __launch_bounds__(v4::kThreads, 1)
       };
       auto issue_pv = [&](int i, uint32_t vslot, int32_t j) {
         const uint64_t vd = dv0 + ((vslot * kTileBytes) >> 4);
+        if (lane == 0) TRACE(10, i, j);
         mbar_wait(bar(WB_PF + i), j & 1);               // P keys 0-63 in TMEM
         tc_fence_after();
+        if (lane == 0) TRACE(11, i, j);
 #ifndef S2L_EXP_NO_PV
 #pragma unroll
         for (int kk = 0; kk < kBN / 32; ++kk)
@@ -1385,6 +1391,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1)
                        idesc_o, (j > 0 || kk > 0));
         mbar_wait(bar(WB_PH + i), j & 1);               // P keys 64-127
         tc_fence_after();
+        if (lane == 0) TRACE(12, i, j);
 #pragma unroll
         for (int kk = kBN / 32; kk < kBN / 16; ++kk)
           mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
@@ -1442,8 +1449,11 @@ __global__ void __launch_bounds__(v4::kThreads, 1)
     const float sl2 = p.scale_log2;
     float m_run = -INFINITY, l_run = 0.f;
     for (int32_t j = 0; j < nT; ++j) {
+      const bool tr = (warp == 4 || warp == 12) && lane == 0;
+      if (tr) TRACE(20, i, j);
       mbar_wait(bar(WB_SF + i), j & 1);
       tc_fence_after();
+      if (tr) TRACE(21, i, j);
 #ifdef S2L_EXP_MMA_ONLY
       tc_fence_before();
       mbar_arrive(bar((h ? WB_PH : WB_PF) + i));
@@ -1467,6 +1477,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1)
       slot[h] = pm;
       asm volatile("bar.sync %0, 64;" ::"r"(bar_pair) : "memory");
       const float mx = fmaxf(slot[0], slot[1]) * sl2;
+      if (tr) TRACE(22, i, j);
       const float m_new = (mx > m_run + kRescaleThresh) ? mx : m_run;
       if (j > 0) {
         const bool resc = m_new != m_run;
@@ -1504,6 +1515,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1)
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(bar((h ? WB_PH : WB_PF) + i));
+      if (tr) TRACE(23, i, j);
       l_run += acc.x + acc.y;
     }
     // ---- epilogue: row sum of both halves, then this half's 64 columns of O

@@ -1,0 +1,69 @@
+// Microbenchmark: the softmax inner loop of attn_tc2 (FFMA2 scale, MUFU/poly exp2, FADD2 row
+// sum, bf16 pack) for 128 columns per thread, W warps per SMSP, no TMEM / barriers.
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ float fast_exp2(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) { uint32_t r; asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo)); return r; }
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f); x.y = fmaxf(x.y, -127.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 y = __fadd2_rn(x, magic);
+  const float2 t = __fadd2_rn(y, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-t.x, -t.y));
+  float2 q = __ffma2_rn(f, make_float2(0.0551704f, 0.0551704f), make_float2(0.24260826f, 0.24260826f));
+  q = __ffma2_rn(q, f, make_float2(0.69326098f, 0.69326098f));
+  q = __ffma2_rn(q, f, make_float2(0.99992833f, 0.99992833f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(y.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(y.y) << 23)));
+}
+
+template <int POLY>
+__global__ void k(const float* __restrict__ in, uint32_t* out, int iters, long long* cycles) {
+  float s[128];
+#pragma unroll
+  for (int c = 0; c < 128; ++c) s[c] = in[(threadIdx.x * 7 + c) & 1023];
+  uint32_t sink = 0;
+  float l = 0.f;
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    float mx = -1e30f;
+#pragma unroll
+    for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
+    const float2 sc = make_float2(0.18f, 0.18f), nm = make_float2(-mx * 0.18f, -mx * 0.18f);
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < 64; ++c) {
+      float2 x = __ffma2_rn(make_float2(s[2 * c], s[2 * c + 1]), sc, nm);
+      float2 p = ((c & 7) < POLY) ? exp2_poly2(x) : make_float2(fast_exp2(x.x), fast_exp2(x.y));
+      acc = __fadd2_rn(acc, p);
+      sink ^= pack_bf16(p.x, p.y);
+    }
+    l += acc.x + acc.y;
+    s[it & 127] += 1e-3f;
+  }
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = sink ^ __float_as_uint(l);
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cycles = (t1 - t0) / iters;
+}
+
+template <int POLY>
+void run(int warps_per_smsp) {
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  float* in; cudaMalloc(&in, 1024 * 4); cudaMemset(in, 0, 4096);
+  uint32_t* out; cudaMalloc(&out, sms * 1024 * 4);
+  long long* cyc; cudaMalloc(&cyc, 8);
+  const int threads = 128 * warps_per_smsp;   // 4 SMSPs
+  k<POLY><<<sms, threads>>>(in, out, 200, cyc);
+  cudaDeviceSynchronize();
+  long long h; cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("poly %d/8, %d warp(s) per SMSP: %lld cycles per 128-column row-tile per warp\n", POLY, warps_per_smsp, h);
+  cudaFree(in); cudaFree(out); cudaFree(cyc);
+}
+
+int main() {
+  run<0>(1); run<2>(1); run<4>(1); run<8>(1);
+  run<0>(2); run<2>(2); run<4>(2);
+  return 0;
+}
