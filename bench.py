@@ -194,7 +194,7 @@ def timed(fn, steps, warmup, dist=None):
         dist.barrier()
     ms = s.elapsed_time(e)
     if dist:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     return ms
@@ -394,6 +394,8 @@ def parity_check(S, data, rank, world, dist):
     rows = [0, 1, 255, 510, 511]
     o = S.o[-1][[0 * CHUNK + r for r in rows]].float()         # request 0 of this rank
     if dist:
+        if dist.get_backend() != "nccl":
+            o = o.cpu()
         bufs = [torch.empty_like(o) for _ in range(world)]
         dist.all_gather(bufs, o)
     else:
@@ -435,12 +437,18 @@ def main():
         return
 
     import torch
+    # S2L_BENCH_DEVICE overrides the device (test plumbing: several ranks on one GPU with gloo)
+    local = int(os.environ.get("S2L_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(dev))
+        backend = os.environ.get("S2L_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(dev))
+        else:
+            dist.init_process_group(backend)
     from paper_2604_16395_b200 import build
     if rank == 0:
         build.build()

@@ -21,7 +21,6 @@ __global__ void table_patch_kernel(const TablePatch* __restrict__ patches, int32
     table[patches[i].idx] = patches[i].value;
 }
 
-constexpr int kVecPerThread = 8;   // 8 x 16-byte loads in flight per thread, then 8 stores
 constexpr int kSmemItems = 256;    // items / ids staged in shared memory when they fit (38 KB)
 constexpr int kSmemIds = 6144;
 
@@ -34,16 +33,21 @@ __device__ __forceinline__ int32_t find_item(const AppendItemDev* items, int32_t
   return lo;
 }
 
-// One thread moves kVecPerThread 16-byte vectors of the concatenated [rows][h_kv][d] input of
-// one (layer, K|V) (blockIdx.y) to their (block, slot) in the pool.  The item descriptors and
-// the block ids are staged in shared memory first, so the only global load on each vector's
-// critical path is the data itself.
+// One warp moves whole token rows: for each of its kRowsPerWarp rows it looks the item up once
+// (items and block ids are staged in shared memory), then each lane loads its 16-byte vectors
+// of the row ([h_kv][d] contiguous, so the warp reads the row coalesced) and stores them to
+// (block, slot) of every kv head (each head's d*2 bytes contiguous in the pool).  All loads of
+// a warp are issued before its stores.  blockIdx.y = layer * 2 + (0: K, 1: V).
+constexpr int kRowsPerWarp = 2;
+
+// kMaxVecPerLane >= vectors per lane per row (vpt/32: 4 at Llama-3 h_kv 8, d 128).
+template <int kMaxVecPerLane>
 __global__ void __launch_bounds__(256) append_kernel(
-    const AppendItemDev* __restrict__ items_g, int32_t n_items, int64_t total_vecs_per_lk,
+    const AppendItemDev* __restrict__ items_g, int32_t n_items, int64_t total_rows,
     const int32_t* __restrict__ ids_g, int32_t n_ids, const TablePatch* __restrict__ patches,
     int32_t n_patches, int32_t* __restrict__ table, const uint4* __restrict__ k,
     const uint4* __restrict__ v, int64_t kv_rows, uint4* __restrict__ pool, int32_t L,
-    int32_t h_kv, int32_t vec_per_row, int32_t kb_log2, int32_t vpt_log2) {
+    int32_t h_kv, int32_t vec_per_row, int32_t kb_log2) {
   __shared__ AppendItemDev s_items[kSmemItems];
   __shared__ int32_t s_ids[kSmemIds];
   const bool staged = n_items <= kSmemItems && n_ids <= kSmemIds;
@@ -54,40 +58,52 @@ __global__ void __launch_bounds__(256) append_kernel(
   }
   const AppendItemDev* items = staged ? s_items : items_g;
   const int32_t* ids = staged ? s_ids : ids_g;
-  const int32_t lk = blockIdx.y;          // layer * 2 + kind
+  const int32_t lk = blockIdx.y;
   const int32_t layer = lk >> 1, kind = lk & 1;
   if (lk == 0 && blockIdx.x == 0) {
     for (int32_t i = threadIdx.x; i < n_patches; i += blockDim.x) table[patches[i].idx] = patches[i].value;
   }
+  const int32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint4* src = (kind ? v : k) + (int64_t)layer * kv_rows * h_kv * vec_per_row;
-  const int32_t vpt = h_kv * vec_per_row;                   // vectors per token row
-  const int32_t total = (int32_t)total_vecs_per_lk;        // host checks < 2^31
+  const int32_t vpt = h_kv * vec_per_row;                 // vectors per token row
   const int32_t kb = 1 << kb_log2;
-  const int32_t stride = gridDim.x * blockDim.x;
-  for (int32_t g0 = blockIdx.x * blockDim.x + threadIdx.x; g0 < total; g0 += stride * kVecPerThread) {
-    uint4 val[kVecPerThread];
-    int64_t dst[kVecPerThread];
+  const int64_t row0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * kRowsPerWarp;
+  const int64_t stride_rows = (int64_t)gridDim.x * (blockDim.x >> 5) * kRowsPerWarp;
+  for (int64_t rb = row0; rb < total_rows; rb += stride_rows) {
+    uint4 val[kRowsPerWarp][kMaxVecPerLane];
+    int64_t dst_row[kRowsPerWarp];        // pool vector index of (block, layer, kind, head 0, slot)
+    int64_t src_row[kRowsPerWarp];
 #pragma unroll
-    for (int u = 0; u < kVecPerThread; ++u) {
-      const int32_t g = g0 + u * stride;
-      dst[u] = -1;
-      if (g < total) {
-        const int32_t row = vpt_log2 >= 0 ? (g >> vpt_log2) : g / vpt;   // token row
-        const int32_t rem = g - row * vpt;
-        const int32_t head = rem / vec_per_row;
-        const int32_t vec = rem - head * vec_per_row;
+    for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+      const int64_t row = rb + rr;
+      dst_row[rr] = -1;
+      if (row < total_rows) {
         const AppendItemDev& it = items[find_item(items, n_items, row)];
-        const int64_t t = (int64_t)row - it.row_begin;
+        const int64_t t = row - it.row_begin;
         const int64_t pos = it.nc + t;
         const int32_t blk = ids[it.id_off + (int32_t)((pos >> kb_log2) - (it.nc >> kb_log2))];
         const int32_t slot = (int32_t)(pos & (kb - 1));
-        val[u] = src[((it.kv_row + t) * h_kv + head) * vec_per_row + vec];
-        dst[u] = (((((int64_t)blk * L + layer) * 2 + kind) * h_kv + head) * kb + slot) * vec_per_row + vec;
+        src_row[rr] = (it.kv_row + t) * vpt;
+        dst_row[rr] = ((((int64_t)blk * L + layer) * 2 + kind) * h_kv * kb + slot) * vec_per_row;
+#pragma unroll
+        for (int u = 0; u < kMaxVecPerLane; ++u) {
+          const int32_t gi = lane + 32 * u;
+          if (gi < vpt) val[rr][u] = src[src_row[rr] + gi];
+        }
       }
     }
 #pragma unroll
-    for (int u = 0; u < kVecPerThread; ++u)
-      if (dst[u] >= 0) pool[dst[u]] = val[u];
+    for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+      if (dst_row[rr] < 0) continue;
+#pragma unroll
+      for (int u = 0; u < kMaxVecPerLane; ++u) {
+        const int32_t gi = lane + 32 * u;
+        if (gi < vpt) {
+          const int32_t head = gi / vec_per_row, vec = gi - head * vec_per_row;
+          pool[dst_row[rr] + (int64_t)head * kb * vec_per_row + vec] = val[rr][u];
+        }
+      }
+    }
   }
 }
 
@@ -108,31 +124,25 @@ cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t
                           int32_t n_patches, int32_t* table, const void* k, const void* v,
                           int64_t kv_rows, void* pool, cudaStream_t st) {
   const int32_t vec_per_row = g.d / 8;
-  const int64_t total = total_rows * g.h_kv * vec_per_row;
-  if (total >= (1ll << 31)) return cudaErrorInvalidValue;
+  const int64_t vpt = (int64_t)g.h_kv * vec_per_row;
   int kb_log2 = 0;
   while ((1 << kb_log2) < g.k) ++kb_log2;
-  const int32_t vpt = g.h_kv * vec_per_row;
-  int vpt_log2 = -1;
-  if ((vpt & (vpt - 1)) == 0) {
-    vpt_log2 = 0;
-    while ((1 << vpt_log2) < vpt) ++vpt_log2;
-  }
-  // one pass: each thread moves kVecPerThread vectors; at most one wave of resident CTAs
-  int64_t threads = (total + kVecPerThread - 1) / kVecPerThread;
-  int64_t blocks = (threads + 255) / 256;
-  const int64_t wave = 148 * 4;                 // 4 x 256-thread CTAs resident per SM (64 regs)
-  const int64_t per_lk = blocks;
-  if (blocks * g.L * 2 > wave && per_lk > 1) {
-    blocks = (wave + g.L * 2 - 1) / (g.L * 2);
-    if (blocks < 1) blocks = 1;
-  }
+  const int64_t warps = (total_rows + kRowsPerWarp - 1) / kRowsPerWarp;
+  int64_t blocks = (warps + 7) / 8;                  // 8 warps per CTA
   if (blocks < 1) blocks = 1;
   if (blocks > 65535) blocks = 65535;
   dim3 grid((unsigned)blocks, g.L * 2);
-  append_kernel<<<grid, 256, 0, st>>>(items, n_items, total, ids, n_ids, patches, n_patches, table,
-                                      (const uint4*)k, (const uint4*)v, kv_rows, (uint4*)pool,
-                                      g.L, g.h_kv, vec_per_row, kb_log2, vpt_log2);
+#define S2L_APPEND(MAXV)                                                                       \
+  append_kernel<MAXV><<<grid, 256, 0, st>>>(items, n_items, total_rows, ids, n_ids, patches,  \
+                                            n_patches, table, (const uint4*)k, (const uint4*)v, \
+                                            kv_rows, (uint4*)pool, g.L, g.h_kv, vec_per_row,    \
+                                            kb_log2)
+  if (vpt <= 32) S2L_APPEND(1);
+  else if (vpt <= 128) S2L_APPEND(4);
+  else if (vpt <= 512) S2L_APPEND(16);
+  else if (vpt <= 2048) S2L_APPEND(64);
+  else return cudaErrorInvalidValue;
+#undef S2L_APPEND
   return cudaGetLastError();
 }
 
