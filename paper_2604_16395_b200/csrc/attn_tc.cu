@@ -1636,6 +1636,430 @@ __global__ void __launch_bounds__(v4::kThreads, 1)
 
 
 // ======================================================================================
+// v5: v2 with 64-key KV steps and a double-buffered S per Q tile (TMEM per tile: S[2] x 64
+// columns + O 128 = 256; two tiles = 512).  The tensor core computes S_i(j+1) while the
+// softmax works on S_i(j), so each tile's softmax runs back to back instead of waiting for its
+// own PV/S MMAs (v2's period was T_softmax + T_mma per tile); the two tiles' softmax warps share
+// each SMSP.  PV_i(j) (4 TS-MMAs, K = 64 keys) follows P_i(j); S_i(j+2) reuses S_i(j)'s buffer
+// after PV_i(j) in the in-order tensor pipe.  A rescale of O waits for PV_i(j-1) (O_done).
+namespace v5 {
+constexpr int kThreads = 384;
+constexpr int kRegLaunch = 168, kRegCtrl = 88, kRegSoftmax = 208;
+static_assert(128 * kRegCtrl + 256 * kRegSoftmax <= kThreads * kRegLaunch, "register pool");
+constexpr int kBS = 64;                                  // keys per KV step
+constexpr uint32_t kKV = kBS * kD * 2;                   // 16 KB K or V tile
+constexpr uint32_t kAtomS = kBS * 128;                   // one d-half [64 keys][64] = 8 KB
+constexpr int WNST = 10;
+constexpr uint32_t WOFF_Q0 = 0;
+constexpr uint32_t WOFF_Q1 = kTileBytes;
+constexpr uint32_t WOFF_RING = 2 * kTileBytes;
+constexpr uint32_t WOFF_BAR = WOFF_RING + WNST * kKV;
+// QF, RF[NST], RE[NST], SF[tile][buf] (4), PF[tile][buf] (4), OD[2], OF[2].  S and P are double
+// buffered by step parity (the softmax may run one step ahead of the MMA warp); O_done has a
+// single phase (after PV_i(nT-2)), so no phase of any barrier is ever skipped by a waiter.
+constexpr uint32_t WB_QF = 0, WB_RF = 1, WB_RE = 1 + WNST, WB_SF = 1 + 2 * WNST, WB_PF = WB_SF + 4,
+                   WB_OD = WB_PF + 4, WB_OF = WB_OD + 2, WNBARS = WB_OF + 2;
+constexpr uint32_t WOFF_TMEM = WOFF_BAR + WNBARS * 8;
+constexpr uint32_t SMEM = WOFF_TMEM + 16 + 1024;
+constexpr int kPolyPairsPer8 = v2::kPolyPairsPer8;
+}  // namespace v5
+
+__global__ void __launch_bounds__(v5::kThreads, 1)
+    attn_tc5_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                    const __grid_constant__ CUtensorMap tmap_kv,
+                    const __grid_constant__ CUtensorMap tmap_kv64, const TcParams p) {
+  using namespace v5;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sb = smem_u32(smem);
+  auto bar = [&](uint32_t i) { return sb + WOFF_BAR + 8u * i; };
+  uint32_t* tmem_holder = (uint32_t*)(smem + WOFF_TMEM);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef S2L_TRACE
+  uint32_t tr_n = 0;
+  const uint32_t tr_w = warp == 1 ? 0u : (warp == 4 ? 1u : (warp == 8 ? 2u : 3u));
+#endif
+
+  // ---- work unit: (item, kv head, pair of Q tiles), longest first (same as v2)
+  int32_t unit = blockIdx.x, piece = 0, npieces = 1;
+  if (unit >= p.split_begin) {
+    const int32_t b = unit - p.split_begin;
+    unit = p.split_begin + b / p.split_s;
+    piece = b % p.split_s;
+    npieces = p.split_s;
+  }
+  int32_t lo = 0, hi = p.n_items - 1;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (p.items[mid].unit_begin <= unit) lo = mid; else hi = mid - 1;
+  }
+  const AttnItemDev it = p.items[lo];
+  const int32_t local = unit - it.unit_begin;
+  const int32_t pairs = (it.tiles + 1) >> 1;
+  const int32_t pair = pairs - 1 - local / p.h_kv;
+  const int32_t kvh = local % p.h_kv;
+  const int32_t G = p.group;
+  const int32_t toks = kBM / G;
+  const int32_t tok0 = pair * 2 * toks;
+  const int32_t tok_last = min(tok0 + 2 * toks, it.n_q) - 1;
+  const int64_t key_last = it.q_pos + tok_last;
+  const int32_t nT_all = (int32_t)(key_last / kBS) + 1;
+  const int32_t jb = (int32_t)((int64_t)nT_all * piece / npieces);
+  const int32_t nT = (int32_t)((int64_t)nT_all * (piece + 1) / npieces) - jb;
+  const int64_t kv_len = it.q_pos + it.n_q;
+  const int32_t nblk_valid = (int32_t)((kv_len + p.kb - 1) / p.kb);
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar(WB_QF), 1);
+    for (int s = 0; s < WNST; ++s) {
+      mbar_init(bar(WB_RF + s), 1);
+      mbar_init(bar(WB_RE + s), 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(bar(WB_SF + i), 1);
+      mbar_init(bar(WB_PF + i), 128);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(WB_OD + i), 1);
+      mbar_init(bar(WB_OF + i), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv64) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtrl));
+    if (warp == 0) {
+      // ================= TMA producer: loads in the MMA's consumption order
+      //   K_0, K_1, then per step j: V_j, K_{j+2}   (one ring, released in the same order)
+      if (lane == 0) {
+        mbar_expect_tx(bar(WB_QF), 2 * kTileBytes);
+        const int32_t z = (int32_t)(it.q_row + tok0);
+        tma_load_3d(sb + WOFF_Q0, &tmap_q, bar(WB_QF), 0, kvh * G, z);
+        tma_load_3d(sb + WOFF_Q0 + kAtom, &tmap_q, bar(WB_QF), 64, kvh * G, z);
+        tma_load_3d(sb + WOFF_Q1, &tmap_q, bar(WB_QF), 0, kvh * G, z + toks);
+        tma_load_3d(sb + WOFF_Q1 + kAtom, &tmap_q, bar(WB_QF), 64, kvh * G, z + toks);
+      }
+      const int32_t nb_tile = kBS / p.kb;               // 1..4 blocks per 64-key tile
+      const int32_t* trow = p.table + (int64_t)it.slot * p.max_blocks;
+      const int32_t rows_per_block = p.L * 2 * p.h_kv * p.kb;
+      const int32_t row_kv[2] = {((p.layer * 2 + 0) * p.h_kv + kvh) * p.kb,
+                                 ((p.layer * 2 + 1) * p.h_kv + kvh) * p.kb};
+      const int32_t lkh[2] = {(p.layer * 2 + 0) * p.h_kv + kvh, (p.layer * 2 + 1) * p.h_kv + kvh};
+      uint32_t rp = 0;
+      auto load_tile = [&](int32_t jt, int kind) {
+        int32_t bid = 0;
+        if (lane < nb_tile) {
+          const int32_t b = (jb + jt) * nb_tile + lane;
+          bid = __ldg(trow + (b < nblk_valid ? b : 0));
+        }
+        int32_t ids[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) ids[b] = __shfl_sync(0xffffffffu, bid, b);
+        bool run = (jb + jt + 1) * nb_tile <= nblk_valid;
+#pragma unroll
+        for (int b = 1; b < 4; ++b)
+          if (b < nb_tile) run = run && (ids[b] == ids[0] + b);
+        const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
+        ++rp;
+        mbar_wait(bar(WB_RE + s), ph ^ 1);
+        if (lane == 0) {
+          mbar_expect_tx(bar(WB_RF + s), kKV);
+          const uint32_t dst = sb + WOFF_RING + s * kKV;
+          if (run) {
+            tma_load_4d(dst, &tmap_kv64, bar(WB_RF + s), 0, 0, lkh[kind], ids[0]);
+            tma_load_4d(dst + kAtomS, &tmap_kv64, bar(WB_RF + s), 64, 0, lkh[kind], ids[0]);
+          } else {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              if (b < nb_tile) {
+                const int32_t y = ids[b] * rows_per_block + row_kv[kind];
+                tma_load_2d(dst + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
+                tma_load_2d(dst + kAtomS + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
+              }
+            }
+          }
+        }
+        __syncwarp();
+      };
+      load_tile(0, 0);
+      if (nT > 1) load_tile(1, 0);
+      for (int32_t j = 0; j < nT; ++j) {
+        load_tile(j, 1);
+        if (j + 2 < nT) load_tile(j + 2, 0);
+      }
+    } else if (warp == 1) {
+      // ================= MMA issuer (whole warp, one elected lane issues) =================
+      constexpr uint32_t idesc_s = idesc_bf16(kBM, kBS, 0, 0);  // S: M 128, N 64 keys
+      constexpr uint32_t idesc_o = idesc_bf16(kBM, kD, 0, 1);   // O: M 128, N 128 d
+      const uint64_t dq[2] = {sdesc(sb + WOFF_Q0, 16, 1024), sdesc(sb + WOFF_Q1, 16, 1024)};
+      const uint64_t dk0 = sdesc(sb + WOFF_RING, 16, 1024);
+      const uint64_t dv0 = sdesc(sb + WOFF_RING, kAtomS, 1024);
+      uint32_t rp = 0;
+      auto next_full = [&]() {
+        const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
+        ++rp;
+        mbar_wait(bar(WB_RF + s), ph);
+        tc_fence_after();
+        return s;
+      };
+      // S_i(jj) into buffer jj & 1 of tile i
+      auto issue_s = [&](int i, uint32_t kslot, int32_t jj) {
+        const uint64_t kd = dk0 + ((kslot * kKV) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const uint32_t qoff = ((kk >> 2) * kAtom + (kk & 3) * 32) >> 4;
+          const uint32_t koff = ((kk >> 2) * kAtomS + (kk & 3) * 32) >> 4;
+          mma_ss_elect(tmem + i * 256 + (jj & 1) * 64, dq[i] + qoff, kd + koff, idesc_s, kk > 0);
+        }
+        mma_commit_elect(bar(WB_SF + i * 2 + (jj & 1)));
+      };
+      auto issue_pv = [&](int i, uint32_t vslot, int32_t j) {
+        const uint64_t vd = dv0 + ((vslot * kKV) >> 4);
+        if (lane == 0) TRACE(10, i, j);
+        mbar_wait(bar(WB_PF + i * 2 + (j & 1)), (j >> 1) & 1);
+        tc_fence_after();
+        if (lane == 0) TRACE(11, i, j);
+#pragma unroll
+        for (int kk = 0; kk < kBS / 16; ++kk)
+          mma_ts_elect(tmem + i * 256 + 128, tmem + i * 256 + (j & 1) * 64 + kk * 8,
+                       vd + ((kk * 16 * 128) >> 4), idesc_o, (j > 0 || kk > 0));
+        if (j + 2 == nT) mma_commit_elect(bar(WB_OD + i));   // PV_i(nT-2) done (one phase)
+      };
+      mbar_wait(bar(WB_QF), 0);
+      tc_fence_after();
+      uint32_t k0 = next_full();
+      issue_s(0, k0, 0);
+      issue_s(1, k0, 0);
+      mma_commit_elect(bar(WB_RE + k0));
+      if (nT > 1) {
+        const uint32_t k1 = next_full();
+        issue_s(0, k1, 1);
+        issue_s(1, k1, 1);
+        mma_commit_elect(bar(WB_RE + k1));
+      }
+      for (int32_t j = 0; j < nT; ++j) {
+        const uint32_t vslot = next_full();
+        const bool more = j + 2 < nT;
+        const uint32_t kslot = more ? next_full() : 0;
+        issue_pv(0, vslot, j);
+        if (more) issue_s(0, kslot, j + 2);
+        if (j + 1 == nT) mma_commit_elect(bar(WB_OF + 0));
+        issue_pv(1, vslot, j);
+        mma_commit_elect(bar(WB_RE + vslot));
+        if (more) {
+          issue_s(1, kslot, j + 2);
+          mma_commit_elect(bar(WB_RE + kslot));
+        }
+        if (j + 1 == nT) mma_commit_elect(bar(WB_OF + 1));
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
+    // ================= softmax / correction / epilogue of Q tile i =================
+    const int i = (warp - 4) >> 2;
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS0 = tmem + lane_off + i * 256;
+    const uint32_t tO = tmem + lane_off + i * 256 + 128;
+    const int32_t tok = tok0 + i * toks + r / G;
+    const int32_t hq = kvh * G + r % G;
+    const bool valid = tok < it.n_q;
+    const int64_t limit = it.q_pos + (valid ? tok : tok_last);
+    const float sl2 = p.scale_log2;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int32_t j = 0; j < nT; ++j) {
+      const uint32_t tS = tS0 + (j & 1) * 64;
+      const bool tr = (warp & 3) == 0 && lane == 0;
+      if (tr) TRACE(20, i, j);
+      mbar_wait(bar(WB_SF + i * 2 + (j & 1)), (j >> 1) & 1);
+      tc_fence_after();
+      if (tr) TRACE(21, i, j);
+      const int64_t key0 = (int64_t)(jb + j) * kBS;
+      const int64_t vis64 = limit - key0;
+      const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBS ? kBS : vis64));
+      const bool masked_tile = __any_sync(0xffffffffu, vis < kBS - 1);
+      uint32_t sv[64];
+      float mt[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) mt[q] = -INFINITY;
+      tmem_ld32(tS, sv);
+      tmem_ld32(tS + 32, sv + 32);
+      tmem_wait_ld();
+      if (masked_tile) { max32<true>(sv, vis, 0, mt); max32<true>(sv + 32, vis, 32, mt); }
+      else { max32<false>(sv, vis, 0, mt); max32<false>(sv + 32, vis, 32, mt); }
+      float mx = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])), fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7])));
+      mx *= sl2;
+      if (tr) TRACE(22, i, j);
+      const float m_new = (mx > m_run + kRescaleThresh) ? mx : m_run;
+      const bool resc = j > 0 && m_new != m_run;
+      const float alpha = resc ? fast_exp2(m_run - m_new) : 1.f;
+      m_run = m_new;
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_use, -m_use);
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        uint32_t pk[16];
+        uint32_t(&v32)[32] = *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc);
+        acc = masked_tile ? chunk_p<true, 0>(v32, acc, vis, 32 * cc, sc2, nm2, pk)
+                          : chunk_p<false, kPolyPairsPer8>(v32, acc, vis, 32 * cc, sc2, nm2, pk);
+        tmem_st16(tS + 16 * cc, pk);
+      }
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+        // O may only be rescaled after PV_i(j-1) has landed: S_i(j+1) was issued after it
+        // (same in-order tensor pipe), and for the last step O_done marks PV_i(nT-2)
+        if (j + 1 < nT) mbar_wait(bar(WB_SF + i * 2 + ((j + 1) & 1)), ((j + 1) >> 1) & 1);
+        else mbar_wait(bar(WB_OD + i), 0);
+        tc_fence_after();
+        if (tr) TRACE(23, i, j);
+        {
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            uint32_t ov[16];
+            tmem_ld16(tO + c * 16, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              float2 x = __fmul2_rn(make_float2(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])),
+                                    make_float2(alpha, alpha));
+              ov[e] = __float_as_uint(x.x);
+              ov[e + 1] = __float_as_uint(x.y);
+            }
+            tmem_st16(tO + c * 16, ov);
+          }
+          l_run *= alpha;
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar(WB_PF + i * 2 + (j & 1)));
+      if (tr) TRACE(24, i, j);
+      l_run += acc.x + acc.y;
+    }
+    // epilogue
+    mbar_wait(bar(WB_OF + i), 0);
+    tc_fence_after();
+    __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
+    if (npieces == 1) {
+      const float inv = 1.f / l_run;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t ov[16];
+        tmem_ld16(tO + c * 16, ov);
+        tmem_wait_ld();
+        if (valid) {
+          uint32_t w[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            w[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+      }
+      if (valid && p.lse)
+        p.lse[(it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+    } else {
+      const int32_t su = unit - p.split_begin;
+      const int64_t prow = (((int64_t)su * npieces + piece) * 2 + i) * 128 + r;
+      float* wo = p.ws + prow * kD;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t ov[16];
+        tmem_ld16(tO + c * 16, ov);
+        tmem_wait_ld();
+        float4* dst = reinterpret_cast<float4*>(wo + c * 16);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
+                               __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
+      }
+      p.ws_ml[prow * 2] = m_run;
+      p.ws_ml[prow * 2 + 1] = l_run;
+      __threadfence();
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      uint32_t* flag = (uint32_t*)(smem + WOFF_TMEM + 8);
+      if (threadIdx.x == 128) {
+        const int32_t old = atomicAdd(p.ws_cnt + su, 1);
+        const uint32_t last = (old == npieces - 1) ? 1u : 0u;
+        if (last) p.ws_cnt[su] = 0;
+        *flag = last;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (*flag) {
+        __threadfence();
+        float M = -INFINITY;
+        for (int k = 0; k < npieces; ++k) {
+          const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
+          M = fmaxf(M, __ldcg(p.ws_ml + pr * 2));
+        }
+        constexpr int kMaxPieces = 8;
+        float wk[kMaxPieces];
+        float Lsum = 0.f;
+#pragma unroll
+        for (int k = 0; k < kMaxPieces; ++k) {
+          wk[k] = 0.f;
+          if (k < npieces) {
+            const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
+            wk[k] = fast_exp2(__ldcg(p.ws_ml + pr * 2) - M);
+            Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
+          }
+        }
+        const float inv = 1.f / Lsum;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kD; c0 += 32) {
+          float acc[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+#pragma unroll
+          for (int k = 0; k < kMaxPieces; ++k) {
+            if (k < npieces) {
+              const float* po = p.ws + ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * kD + c0;
+#pragma unroll
+              for (int c = 0; c < 32; c += 2) {
+                const float2 x = __ldcg(reinterpret_cast<const float2*>(po + c));
+                acc[c] += wk[k] * x.x;
+                acc[c + 1] += wk[k] * x.y;
+              }
+            }
+          }
+          if (valid) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) {
+              uint4 v4 = make_uint4(pack_bf16(acc[c] * inv, acc[c + 1] * inv), pack_bf16(acc[c + 2] * inv, acc[c + 3] * inv),
+                                    pack_bf16(acc[c + 4] * inv, acc[c + 5] * inv), pack_bf16(acc[c + 6] * inv, acc[c + 7] * inv));
+              *reinterpret_cast<uint4*>(orow + c0 + c) = v4;
+            }
+          }
+        }
+        if (valid && p.lse)
+          p.lse[(it.q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ======================================================================================
 // v3 = v2 made persistent: each CTA loops over work items (whole units, then the tail-wave
 // split pieces) with a static stride of gridDim.x, so the TMEM allocation / barrier setup is
 // paid once per SM and the next item's Q load, K/V loads and first S MMAs overlap the current
@@ -2124,6 +2548,21 @@ bool make_tmap_kv(void* out, const void* pool, int64_t num_blocks, int32_t L, in
       return false;
     }
   }
+  // (3) 64-key run map (v5): box {64, k, 1, 64/k} (only for k <= 64)
+  if (k <= 64) {
+    const int32_t R = 64 / k;
+    cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)k, (cuuint64_t)L * 2 * h_kv, (cuuint64_t)num_blocks};
+    cuuint64_t strides[3] = {(cuuint64_t)d * 2, (cuuint64_t)k * d * 2, (cuuint64_t)L * 2 * h_kv * k * d * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)k, 1, (cuuint32_t)R};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn((CUtensorMap*)((char*)out + 256), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)pool,
+                    dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      *err = "cuTensorMapEncodeTiled(pool, 64-key runs) failed";
+      return false;
+    }
+  }
   return true;
 }
 
@@ -2176,6 +2615,8 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
       if (e != cudaSuccess) return e;
       e = cudaFuncSetAttribute(attn_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v4::SMEM);
       if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(attn_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v5::SMEM);
+      if (e != cudaSuccess) return e;
     }
     attr_set[variant] = true;
   }
@@ -2211,7 +2652,11 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
   p.ws_ml = ws ? ws + (int64_t)max_pieces * 2 * 128 * kD : nullptr;
   p.ws_cnt = ws_cnt;
   p.n_work = grid;
-  if (variant == 2 && (flags & kAttnSplitSoftmax)) {
+  if (variant == 2 && (flags & kAttnKV64) && g.k <= 64) {
+    CUtensorMap tkv64;
+    memcpy(&tkv64, (const char*)tmap_kv + 256, sizeof(CUtensorMap));
+    attn_tc5_kernel<<<grid, v5::kThreads, v5::SMEM, st>>>(tq, tkv, tkv64, p);
+  } else if (variant == 2 && (flags & kAttnSplitSoftmax)) {
     attn_tc4_kernel<<<grid, v4::kThreads, v4::SMEM, st>>>(tq, tkv, tkv4, p);
   } else if (variant == 2 && persistent) {
     const int32_t g = grid < num_sms ? grid : num_sms;

@@ -132,13 +132,14 @@ struct s2l_ctx {
   // by a swap-out may only be rewritten by the compute stream after it
   cudaEvent_t swap_out_done = nullptr;
   bool swap_out_pending = false;
-  unsigned char tmap_kv[256] __attribute__((aligned(64)));
+  unsigned char tmap_kv[384] __attribute__((aligned(64)));
   int32_t num_sms = 148;
   float* split_ws = nullptr;          // tail-wave split partials (num_sms pieces)
   int32_t* split_cnt = nullptr;       // per split unit arrival counters (self-resetting)
   bool split_enabled = true;
   bool persistent = false;            // persistent attention kernel (S2L_PERSIST=1)
   bool split_softmax = false;         // v4 kernel (S2L_ATTN_V4=1)
+  bool kv64 = false;                  // v5 kernel (S2L_ATTN_V5=1)
   uint32_t* trace_buf = nullptr;      // S2L_TRACE=1: device buffer for kernel timelines (experiments)
   int64_t trace_launch = -1, attn_launch_no = 0;  // which attention launch to trace (S2L_TRACE_LAUNCH)            // persistent attention kernel (S2L_PERSIST=1); off: measured slower
   bool tc_ok = false;
@@ -486,6 +487,8 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
     c->persistent = (e && e[0] == '1');
     e = getenv("S2L_ATTN_V4");
     c->split_softmax = (e && e[0] == '1');
+    e = getenv("S2L_ATTN_V5");
+    c->kv64 = (e && e[0] == '1');
     e = getenv("S2L_TRACE");
     if (e && e[0] == '1') {
       CK(cudaMalloc(&c->trace_buf, (16 + 4 * 4096 * 2) * sizeof(uint32_t)));
@@ -808,7 +811,8 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
                            c->split_ws, c->num_sms, c->split_cnt, c->d_table, layer, tq,
                            c->tmap_kv, o, lse, c->num_sms,
                            (c->persistent ? s2l::kAttnPersistent : 0) |
-                               (c->split_softmax ? s2l::kAttnSplitSoftmax : 0),
+                               (c->split_softmax ? s2l::kAttnSplitSoftmax : 0) |
+                               (c->kv64 ? s2l::kAttnKV64 : 0),
                            c->compute));
   } else {
     CK(s2l::launch_attn_generic(c->geo, dv, n_items, total_q, c->d_table, layer, q, o, lse,

@@ -76,14 +76,16 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
 // flags of launch_attn_tc
 constexpr int32_t kAttnPersistent = 1;   // v2 only: grid = min(work items, SMs), CTAs loop
 constexpr int32_t kAttnSplitSoftmax = 2; // v4: each tile's softmax split over two warps per SMSP
+constexpr int32_t kAttnKV64 = 4;         // v5: 64-key steps, double-buffered S per tile
 // Experiments: device buffer receiving kernel timeline stamps (S2L_TRACE builds); nullptr = off.
 void set_attn_trace(uint32_t* buf);   // v2 only: grid = min(work items, SMs), CTAs loop
 constexpr int64_t kSplitPieceFloats = 2 * 128 * 130;   // O [2][128][128] + (m, l) [2][128][2]
 // TMA descriptors (host).  Returns false on failure (message in *err).
 bool make_tmap_q(void* out128, const void* q, int64_t q_rows, int32_t h_q, int32_t d,
                  int32_t group, const char** err);
-// Two maps of the pool into out256: [0,128) per-block boxes, [128,256) 4-D block-run boxes.
-bool make_tmap_kv(void* out256, const void* pool, int64_t num_blocks, int32_t L, int32_t h_kv,
+// Maps of the pool into out384: [0,128) per-block boxes, [128,256) 128-key block runs,
+// [256,384) 64-key block runs (k <= 64).
+bool make_tmap_kv(void* out384, const void* pool, int64_t num_blocks, int32_t L, int32_t h_kv,
                   int32_t d, int32_t k, const char** err);
 
 }  // namespace s2l
