@@ -250,7 +250,7 @@ def measure_link(dev):
     out = {}
     for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
         best = 0.0
-        for _ in range(3):
+        for _ in range(10):   # best of 10
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize(); s.record(); fn(); e.record(); torch.cuda.synchronize()
             best = max(best, n / (s.elapsed_time(e) * 1e-3) / 1e9)

@@ -41,6 +41,9 @@
 #ifndef S2L_POLY_PAIRS
 #define S2L_POLY_PAIRS 2
 #endif
+#ifndef S2L_PACK_TRUNC
+#define S2L_PACK_TRUNC 0   // 1: P -> bf16 by truncation (PRMT) with a mean-bias correction of l
+#endif
 
 namespace s2l {
 namespace {
@@ -266,6 +269,24 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+// P -> bf16x2 for the PV MMA.  S2L_PACK_TRUNC=1 keeps the high halves (PRMT, off the
+// F2FP pipe the softmax's FMNMX/FFMA2 also use); truncation lowers each p by 2^-8 * E[1/(1+m)]
+// on average (m = mantissa fraction, log-uniform for 2^x: E = 1/(2 ln 2)), and the epilogues
+// divide by l * (1 - that mean) instead of l (kPNorm), leaving a zero-mean rounding error.
+__device__ __forceinline__ uint32_t pack_p(float lo, float hi) {
+#if S2L_PACK_TRUNC
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(__float_as_uint(lo)), "r"(__float_as_uint(hi)));
+  return r;
+#else
+  return pack_bf16(lo, hi);
+#endif
+}
+#if S2L_PACK_TRUNC
+constexpr float kPNorm = 1.f / (1.f - 0.0028177f);
+#else
+constexpr float kPNorm = 1.f;
+#endif
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                              uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
@@ -480,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float p0 = fast_exp2(fmaf(__uint_as_float(sv[chunk * 8 + 2 * e]), sl2, -m_run));
           const float p1 = fast_exp2(fmaf(__uint_as_float(sv[chunk * 8 + 2 * e + 1]), sl2, -m_run));
           sum += p0 + p1;
-          w[e] = pack_bf16(p0, p1);
+          w[e] = pack_p(p0, p1);
         }
         const uint32_t atom = chunk >> 3, cc = chunk & 7;
         st_shared_v4(prow + atom * kAtom + ((cc ^ (r & 7)) << 4), w[0], w[1], w[2], w[3]);
@@ -493,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // epilogue
     mbar_wait(bar(B_OD), (nT - 1) & 1);
     tc_fence_after();
-    const float inv = 1.f / l_run;
+    const float inv = kPNorm / l_run;
     __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -563,7 +584,7 @@ __device__ __forceinline__ float2 chunk_p(const uint32_t (&v)[32], float2 acc, i
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
     a[c & 3] = __fadd2_rn(a[c & 3], x[c]);
-    pk[c] = pack_bf16(x[c].x, x[c].y);
+    pk[c] = pack_p(x[c].x, x[c].y);
   }
   return __fadd2_rn(__fadd2_rn(a[0], a[1]), __fadd2_rn(a[2], a[3]));
 }
@@ -1071,7 +1092,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     tc_fence_after();
     __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
     if (npieces == 1) {
-      const float inv = 1.f / l_run;
+      const float inv = kPNorm / l_run;
 #pragma unroll 1
       for (int c = 0; c < 8; ++c) {
         uint32_t ov[16];
@@ -1136,7 +1157,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
             Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
           }
         }
-        const float inv = 1.f / Lsum;
+        const float inv = kPNorm / Lsum;
 #pragma unroll 1
         for (int c0 = 0; c0 < kD; c0 += 32) {
           float acc[32];
@@ -1527,7 +1548,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1)
     const float l_tot = lsl[0] + lsl[1];
     __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD + 64 * h;
     if (npieces == 1) {
-      const float inv = 1.f / l_tot;
+      const float inv = kPNorm / l_tot;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t ov[16];
@@ -1593,7 +1614,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1)
             Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
           }
         }
-        const float inv = 1.f / Lsum;
+        const float inv = kPNorm / Lsum;
 #pragma unroll 1
         for (int c0 = 0; c0 < 64; c0 += 32) {
           float acc[32];
@@ -1954,7 +1975,7 @@ __global__ void __launch_bounds__(v5::kThreads, 1)
     tc_fence_after();
     __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
     if (npieces == 1) {
-      const float inv = 1.f / l_run;
+      const float inv = kPNorm / l_run;
 #pragma unroll 1
       for (int c = 0; c < 8; ++c) {
         uint32_t ov[16];
@@ -2018,7 +2039,7 @@ __global__ void __launch_bounds__(v5::kThreads, 1)
             Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
           }
         }
-        const float inv = 1.f / Lsum;
+        const float inv = kPNorm / Lsum;
 #pragma unroll 1
         for (int c0 = 0; c0 < kD; c0 += 32) {
           float acc[32];
@@ -2375,7 +2396,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       tc_fence_after();
       __nv_bfloat16* orow = p.o + ((wk.it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
       if (wk.npieces == 1) {
-        const float inv = 1.f / l_run;
+        const float inv = kPNorm / l_run;
 #pragma unroll 1
         for (int c = 0; c < 8; ++c) {
           uint32_t ov[16];
@@ -2442,7 +2463,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
               Lsum += wk8[k] * __ldcg(p.ws_ml + pr * 2 + 1);
             }
           }
-          const float inv = 1.f / Lsum;
+          const float inv = kPNorm / Lsum;
 #pragma unroll 1
           for (int c0 = 0; c0 < kD; c0 += 32) {
             float acc[32];

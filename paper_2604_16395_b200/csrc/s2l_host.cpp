@@ -88,14 +88,25 @@ struct Request {
   std::vector<int32_t> blocks;
   int64_t tti = 0;
   int32_t slot = -1;
-  cudaEvent_t swap_in_event = nullptr;  // pending H2D of its blocks (on copy stream)
-  bool swap_in_pending = false;
+  uint64_t swap_in_seq = 0;   // copy-ring record after the H2D that filled its blocks (0: none)
+  uint64_t write_seq = 0;     // compute-ring record after the last append that wrote its blocks
+  uint64_t use_seq = 0;       // compute-ring record after the last append / attention using them
+};
+
+// Events re-recorded round-robin on ONE stream.  record() returns a sequence number (1, 2,
+// ...); a wait on seq uses slot seq % kN.  If that slot has since been re-recorded by a newer
+// operation of the same in-order stream, the wait only lasts longer (never too short), and it
+// still refers to work enqueued before the wait, so no cycle between streams can form.
+struct EventRing {
+  static constexpr int kN = 64;
+  cudaEvent_t ev[kN] = {};
+  uint64_t seq = 0;
 };
 
 // Pinned-host + device staging ring.  Slot s is reused only after its event (recorded after
 // the kernels that read it) has completed, which protects both copies.
 struct StagingRing {
-  static constexpr int kSlots = 4;
+  static constexpr int kSlots = 16;
   void* host[kSlots] = {};
   void* dev[kSlots] = {};
   size_t cap[kSlots] = {};
@@ -128,10 +139,17 @@ struct s2l_ctx {
   int64_t launches = 0;
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> attn_ev, append_ev, ev_pool;
-  // event that marks the end of the most recent swap-out copy of GPU blocks; GPU blocks freed
-  // by a swap-out may only be rewritten by the compute stream after it
-  cudaEvent_t swap_out_done = nullptr;
-  bool swap_out_pending = false;
+  // Stream hazards (DESIGN.md §5 "Stream hazards"), tracked per request and per GPU block so
+  // that swaps on the copy stream overlap the compute work they do not conflict with:
+  //  * compute_ring: one record after every append / attention launch; Request::write_seq
+  //    (a swap-out's D2H waits for it) and Request::use_seq;
+  //  * copy_ring: one record after every swap call; Request::swap_in_seq (compute waits for
+  //    it before touching the request);
+  //  * per free GPU block: freed_use = the previous owner's use_seq (an H2D that reuses the
+  //    block waits for it) and quar = the copy-ring record of a D2H / H2D still touching it
+  //    (an append that reuses the block waits for it).  Both are cleared on allocation.
+  EventRing compute_ring, copy_ring;
+  std::vector<uint64_t> freed_use, quar;
   unsigned char tmap_kv[384] __attribute__((aligned(64)));
   int32_t num_sms = 148;
   float* split_ws = nullptr;          // tail-wave split partials (num_sms pieces)
@@ -158,6 +176,18 @@ bool cuda_ok(s2l_ctx* c, cudaError_t e, const char* what) {
   do {                                             \
     if (!cuda_ok(c, (call), #call)) return S2L_E_CUDA; \
   } while (0)
+
+bool ring_record(s2l_ctx* c, EventRing& R, cudaStream_t st, uint64_t* seq) {
+  const uint64_t n = R.seq + 1;
+  if (!cuda_ok(c, cudaEventRecord(R.ev[n % EventRing::kN], st), "event ring record")) return false;
+  R.seq = n;
+  *seq = n;
+  return true;
+}
+bool ring_wait(s2l_ctx* c, EventRing& R, cudaStream_t st, uint64_t seq) {
+  if (seq == 0) return true;
+  return cuda_ok(c, cudaStreamWaitEvent(st, R.ev[seq % EventRing::kN], 0), "event ring wait");
+}
 
 s2l_status check_config(const s2l_config* cfg) {
   if (!cfg) return fail(S2L_E_INVAL, "config is NULL");
@@ -210,14 +240,20 @@ void set_table(s2l_ctx* c, int32_t slot, int64_t col, int32_t value) {
 // Frees blocks [keep, end) of the request on its tier and resets those table entries.
 void free_tail(s2l_ctx* c, Request* r, size_t keep) {
   if (keep >= r->blocks.size()) return;
-  if (r->tier == S2L_TIER_GPU && r->swap_in_pending && !c->host_only) {
-    // GPU blocks still being filled by a swap-in must not be rewritten by later compute work.
-    if (cudaStreamWaitEvent(c->compute, r->swap_in_event, 0) != cudaSuccess) c->sticky = S2L_E_CUDA;
-    r->swap_in_pending = false;
+  if (r->tier == S2L_TIER_GPU && r->swap_in_seq && !c->host_only) {
+    // blocks possibly still being filled by a swap-in: an append reusing them waits for it
+    for (size_t j = keep; j < r->blocks.size(); ++j)
+      c->quar[(size_t)r->blocks[j]] = std::max(c->quar[(size_t)r->blocks[j]], r->swap_in_seq);
+    if (keep == 0) r->swap_in_seq = 0;
   }
   c->alloc[r->tier].give_back(r->blocks.data() + keep, (int64_t)(r->blocks.size() - keep));
   if (r->tier == S2L_TIER_GPU)
-    for (size_t j = keep; j < r->blocks.size(); ++j) set_table(c, r->slot, (int64_t)j, -1);
+    for (size_t j = keep; j < r->blocks.size(); ++j) {
+      set_table(c, r->slot, (int64_t)j, -1);
+      // kernels of this request enqueued so far may still use the block: an H2D reusing it
+      // waits for them (an append reusing it is ordered on the compute stream anyway)
+      if (!c->host_only) c->freed_use[(size_t)r->blocks[j]] = r->use_seq;
+    }
   r->blocks.resize(keep);
 }
 
@@ -287,13 +323,6 @@ std::pair<cudaEvent_t, cudaEvent_t> timing_pair(s2l_ctx* c) {
   return p;
 }
 
-// The compute stream must not rewrite GPU blocks freed by a swap-out before that copy ends.
-bool wait_swap_out_hazard(s2l_ctx* c) {
-  if (!c->swap_out_pending) return true;
-  if (!cuda_ok(c, cudaStreamWaitEvent(c->compute, c->swap_out_done, 0), "wait swap-out")) return false;
-  c->swap_out_pending = false;
-  return true;
-}
 
 // Flush pending table patches with a standalone patch kernel (used before attention when no
 // append kernel carried them).
@@ -340,6 +369,8 @@ s2l_status swap_impl(s2l_ctx* c, int32_t n_reqs, const int64_t* ids, int64_t* by
     nid.reserve(r->blocks.size());
     c->alloc[dst].take_lowest((int64_t)r->blocks.size(), nid);
     for (size_t j = 0; j < nid.size(); ++j) moves.emplace_back(r->blocks[j], nid[j]);
+    if (src == S2L_TIER_GPU && !c->host_only)
+      for (int32_t b : r->blocks) c->freed_use[(size_t)b] = r->use_seq;
     c->alloc[src].give_back(r->blocks.data(), (int64_t)r->blocks.size());
     for (size_t j = 0; j < nid.size(); ++j)
       set_table(c, r->slot, (int64_t)j, dst == S2L_TIER_GPU ? nid[j] : -1);
@@ -350,18 +381,22 @@ s2l_status swap_impl(s2l_ctx* c, int32_t n_reqs, const int64_t* ids, int64_t* by
   if (bytes_out) *bytes_out = need * c->m_block;
   if (c->host_only || need == 0) return S2L_OK;
 
-  // ---- copies on the copy stream ----
-  // Order the copy after everything already enqueued on the compute stream: swap-out reads
-  // blocks written by earlier appends; swap-in overwrites GPU blocks that earlier kernels
-  // may still read (they were freed by invalidate / release / swap-out before).
-  cudaEvent_t ev;
-  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  CK(cudaEventRecord(ev, c->compute));
-  CK(cudaStreamWaitEvent(c->copy, ev, 0));
-  cudaEventDestroy(ev);
-  if (dst == S2L_TIER_GPU && c->swap_out_pending) {
-    // GPU blocks freed by a swap-out are being read by that D2H; same copy stream -> ordered.
+  // ---- copies on the copy stream: order only against the compute work they conflict with --
+  uint64_t w = 0;
+  if (src == S2L_TIER_GPU) {
+    // D2H reads blocks written by earlier appends of these requests (wait for the newest one;
+    // the compute ring is in order).  Blocks filled by an earlier swap-in: same copy stream.
+    for (Request* r : touched) w = std::max(w, r->write_seq);
+  } else {
+    // H2D overwrites free GPU blocks that kernels of their previous owner may still use
+    // (freed_use); blocks freed by a swap-out are read by a D2H earlier on this stream.
+    for (const auto& m : moves) {
+      w = std::max(w, c->freed_use[(size_t)m.second]);
+      c->freed_use[(size_t)m.second] = 0;
+      c->quar[(size_t)m.second] = 0;
+    }
   }
+  if (!ring_wait(c, c->compute_ring, c->copy, w)) return S2L_E_CUDA;
   // Coalesce runs where both source and destination ids are consecutive (Z9 makes these long).
   char* gbase = (char*)c->gpu_pool;
   char* hbase = (char*)c->cpu_pool;
@@ -398,15 +433,12 @@ s2l_status swap_impl(s2l_ctx* c, int32_t n_reqs, const int64_t* ids, int64_t* by
                            c->copy));
     }
   }
+  uint64_t seq = 0;
+  if (!ring_record(c, c->copy_ring, c->copy, &seq)) return S2L_E_CUDA;
   if (src == S2L_TIER_GPU) {
-    CK(cudaEventRecord(c->swap_out_done, c->copy));
-    c->swap_out_pending = true;
+    for (const auto& m : moves) c->quar[(size_t)m.first] = seq;   // freed GPU ids: quarantined
   } else {
-    for (Request* r : touched) {
-      if (!r->swap_in_event) CK(cudaEventCreateWithFlags(&r->swap_in_event, cudaEventDisableTiming));
-      CK(cudaEventRecord(r->swap_in_event, c->copy));
-      r->swap_in_pending = true;
-    }
+    for (Request* r : touched) r->swap_in_seq = seq;
   }
   return S2L_OK;
 }
@@ -464,7 +496,10 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
   if (hbytes) memset(cpu_pool_pinned, 0, hbytes);
   for (int s = 0; s < StagingRing::kSlots; ++s)
     CK(cudaEventCreateWithFlags(&c->ring.ev[s], cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&c->swap_out_done, cudaEventDisableTiming));
+  for (EventRing* R : {&c->compute_ring, &c->copy_ring})
+    for (int i = 0; i < EventRing::kN; ++i) CK(cudaEventCreateWithFlags(&R->ev[i], cudaEventDisableTiming));
+  c->quar.assign((size_t)cfg->num_gpu_blocks, 0);
+  c->freed_use.assign((size_t)cfg->num_gpu_blocks, 0);
   c->tc_ok = s2l::attn_tc_supported(c->geo);
   if (c->tc_ok && cfg->num_gpu_blocks > 0) {
     const char* err = nullptr;
@@ -512,14 +547,14 @@ void s2l_destroy(s2l_ctx* c) {
       if (c->ring.dev[s]) cudaFree(c->ring.dev[s]);
       if (c->ring.ev[s]) cudaEventDestroy(c->ring.ev[s]);
     }
-    for (auto& r : c->slots)
-      if (r.swap_in_event) cudaEventDestroy(r.swap_in_event);
+    for (EventRing* R : {&c->compute_ring, &c->copy_ring})
+      for (int i = 0; i < EventRing::kN; ++i)
+        if (R->ev[i]) cudaEventDestroy(R->ev[i]);
     for (auto* v : {&c->attn_ev, &c->append_ev, &c->ev_pool})
       for (auto& p : *v) {
         cudaEventDestroy(p.first);
         cudaEventDestroy(p.second);
       }
-    if (c->swap_out_done) cudaEventDestroy(c->swap_out_done);
     if (c->trace_buf) {   // experiments: dump the recorded timeline
       std::vector<uint32_t> h(16 + 4 * 4096 * 2);
       cudaMemcpy(h.data(), c->trace_buf, h.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost);
@@ -546,9 +581,7 @@ s2l_status s2l_new_request(s2l_ctx* c, int64_t id, const int32_t* tokens, int64_
   int32_t slot = c->free_slots.back();
   c->free_slots.pop_back();
   Request& r = c->slots[slot];
-  cudaEvent_t keep_ev = r.swap_in_event;
   r = Request();
-  r.swap_in_event = keep_ev;
   r.id = id;
   r.slot = slot;
   r.input.assign(tokens, tokens + n);
@@ -561,7 +594,7 @@ s2l_status s2l_release_request(s2l_ctx* c, int64_t id) {
   Request* r = find(c, id);
   if (!r) return fail(S2L_E_NO_REQUEST, "unknown request %lld", (long long)id);
   free_tail(c, r, 0);
-  r->swap_in_pending = false;
+  r->swap_in_seq = 0;
   c->by_id.erase(id);
   c->free_slots.push_back(r->slot);
   return S2L_OK;
@@ -574,7 +607,7 @@ s2l_status s2l_preempt_recompute(s2l_ctx* c, int64_t id) {
   free_tail(c, r, 0);
   r->nc = 0;
   r->tier = S2L_TIER_GPU;
-  r->swap_in_pending = false;
+  r->swap_in_seq = 0;
   return S2L_OK;
 }
 
@@ -617,7 +650,8 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
   // Staging layout: [AppendItemDev x n_items][int32 ids x total_ids][TablePatch x patches]
   std::vector<s2l::AppendItemDev> dev_items;
   std::vector<int32_t> ids;
-  std::vector<Request*> wait_in;
+  std::vector<Request*> wait_in, written;
+  uint64_t quar_wait = 0;   // newest swap-out D2H still reading a block reallocated here
   dev_items.reserve(n_items);
   ids.reserve((size_t)total_ids);
   int64_t row_begin = 0;
@@ -629,6 +663,13 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
     size_t held = r->blocks.size();
     c->alloc[S2L_TIER_GPU].take_lowest(nb - (int64_t)held, r->blocks);
     for (size_t j = held; j < r->blocks.size(); ++j) set_table(c, r->slot, (int64_t)j, r->blocks[j]);
+    if (!c->host_only)
+      for (size_t j = held; j < r->blocks.size(); ++j) {
+        uint64_t& q = c->quar[(size_t)r->blocks[j]];
+        quar_wait = std::max(quar_wait, q);
+        q = 0;
+        c->freed_use[(size_t)r->blocks[j]] = 0;
+      }
     if (it.n_kv) {
       s2l::AppendItemDev d{};
       d.nc = r->nc;
@@ -639,11 +680,16 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
       for (int64_t b = r->nc / kb; b < nb; ++b) ids.push_back(r->blocks[(size_t)b]);
       dev_items.push_back(d);
       row_begin += it.n_kv;
-      if (r->swap_in_pending) wait_in.push_back(r);
+      if (r->swap_in_seq) wait_in.push_back(r);
+      written.push_back(r);
     }
     r->nc += it.n_kv;
   }
-  if (c->host_only || total_rows == 0) return c->host_only ? S2L_OK : flush_patches(c);
+  if (c->host_only) return S2L_OK;
+  if (total_rows == 0) {
+    if (!ring_wait(c, c->copy_ring, c->compute, quar_wait)) return S2L_E_CUDA;
+    return flush_patches(c);
+  }
 
   size_t off_ids = align16(dev_items.size() * sizeof(s2l::AppendItemDev));
   size_t off_patch = align16(off_ids + ids.size() * sizeof(int32_t));
@@ -655,10 +701,10 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
   memcpy(h + off_ids, ids.data(), ids.size() * sizeof(int32_t));
   int32_t n_patch = take_patches(c, (s2l::TablePatch*)(h + off_patch));
   if (!staging_upload_and_mark(c, s, bytes)) return S2L_E_CUDA;
-  if (!wait_swap_out_hazard(c)) return S2L_E_CUDA;
+  if (!ring_wait(c, c->copy_ring, c->compute, quar_wait)) return S2L_E_CUDA;
   for (Request* r : wait_in) {
-    CK(cudaStreamWaitEvent(c->compute, r->swap_in_event, 0));
-    r->swap_in_pending = false;
+    if (!ring_wait(c, c->copy_ring, c->compute, r->swap_in_seq)) return S2L_E_CUDA;
+    r->swap_in_seq = 0;
   }
   char* dv = (char*)c->ring.dev[s];
   std::pair<cudaEvent_t, cudaEvent_t> tp{};
@@ -675,6 +721,9 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
     CK(cudaEventRecord(tp.second, c->compute));
     c->append_ev.push_back(tp);
   }
+  uint64_t wseq = 0;
+  if (!ring_record(c, c->compute_ring, c->compute, &wseq)) return S2L_E_CUDA;
+  for (Request* r : written) r->write_seq = r->use_seq = wseq;
   if (!staging_release(c, s)) return S2L_E_CUDA;
   return S2L_OK;
 }
@@ -732,9 +781,9 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
   if (st) return st;
   for (int32_t i = 0; i < n_items; ++i) {
     Request* r = find(c, items[i].req_id);
-    if (r->swap_in_pending) {
-      CK(cudaStreamWaitEvent(c->compute, r->swap_in_event, 0));
-      r->swap_in_pending = false;
+    if (r->swap_in_seq) {
+      if (!ring_wait(c, c->copy_ring, c->compute, r->swap_in_seq)) return S2L_E_CUDA;
+      r->swap_in_seq = 0;
     }
   }
   const int32_t G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
@@ -823,6 +872,9 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
     CK(cudaEventRecord(tp.second, c->compute));
     c->attn_ev.push_back(tp);
   }
+  uint64_t useq = 0;
+  if (!ring_record(c, c->compute_ring, c->compute, &useq)) return S2L_E_CUDA;
+  for (int32_t i = 0; i < n_items; ++i) find(c, items[i].req_id)->use_seq = useq;
   if (!staging_release(c, s)) return S2L_E_CUDA;
   return S2L_OK;
 }

@@ -1,0 +1,314 @@
+"""C4 memory-pressure mix (BJ:L10): a deterministic round-robin driver
+that streams append-mode and update-mode requests through one libs2l context whose GPU pool
+is smaller than the working set, swapping requests out to pinned host memory and back in
+("Transfer all blocks ... from GPU to CPU memory ... swap blocks back to GPU with
+symmetric cost") to make room for each step.
+
+This is a harness driver, not the paper's scheduler (two-phase scheduling and the
+recompute-vs-swap policy are P:L134-L237): requests are stepped in
+round-robin order under a token budget (2048-8192 tokens per batch), and the victims
+of a swap-out are the least recently stepped GPU-resident requests.  All state it plans with
+comes from the library's own queries (`query`, `free_blocks`), so the same driver runs on a
+device context (bench) and on a host-only context (CPU tests, where `tests/` replays its op
+log through the oracle).
+
+Overlap (SURVEY NEXT-2, P:L184 resume): the swaps that prepare step s+1 are issued on the copy
+stream right after step s's compute has been enqueued, so they run while step s computes;
+the library orders them only against the kernels they actually conflict with.
+
+Workload recipe: request r is append-mode if r is even, update-mode if odd.
+  * append: total T ~ LogNormal(ln 5800, 0.976) (crawler trace, Tab. 2 median 5.8K)
+    truncated to [lo, hi]; U{6..10} chunks of near-equal size, tokens arrive with
+    each chunk;
+  * update: T ~ LogNormal(ln 10000, 0.688) (ANNS trace) truncated to [lo, hi]; the
+    input arrives whole and is prefilled as two chunks, then U{1, 2} update rounds, each an
+    LCP p ~ U[ceil(0.2 T), floor(0.8 T)] (reading Z14) with new length T, recomputing T - p
+    tokens (split into budget-sized pieces, budget-clamped partial chunks).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+TIER_GPU, TIER_CPU = 0, 1
+
+
+@dataclass
+class Work:
+    """One step's work for one request: optional update (new input -> invalidate_lcp first),
+    optional appended tokens, then K/V + attention for the next n_kv pending positions."""
+    n_kv: int
+    append_tokens: np.ndarray | None = None
+    new_input: np.ndarray | None = None
+
+
+@dataclass
+class Plan:
+    rid: int
+    mode: str
+    total: int
+    initial_tokens: np.ndarray
+    work: list = field(default_factory=list)
+
+
+def _lognormal_len(rng, median, sigma, lo, hi):
+    return int(min(hi, max(lo, round(math.exp(math.log(median) + sigma * rng.standard_normal())))))
+
+
+def c4_plans(seed: int, n_requests: int, lo: int = 1024, hi: int = 16384, budget: int = 8192,
+             rids=None) -> list:
+    """Per-request work lists (token ids from synth; lengths / chunking / LCP draws here)."""
+    from synth import workloads as W
+    rng = np.random.default_rng(seed)
+    plans = []
+    for r in range(n_requests):
+        mode = "append" if r % 2 == 0 else "update"
+        if mode == "append":
+            T = _lognormal_len(rng, 5800, 0.976, lo, hi)
+            n_chunks = int(rng.integers(6, 11))
+        else:
+            T = _lognormal_len(rng, 10000, 0.688, lo, hi)
+            rounds = int(rng.integers(1, 3))
+            ps = [int(rng.integers(-(-2 * T // 10), (8 * T) // 10 + 1)) for _ in range(rounds)]
+        if rids is not None and r not in rids:
+            continue
+        toks = W.request_tokens(seed, r, T)
+        if mode == "append":
+            bounds = [T * i // n_chunks for i in range(n_chunks + 1)]
+            work = [Work(n_kv=b - a, append_tokens=toks[a:b]) for a, b in zip(bounds, bounds[1:])]
+            plans.append(Plan(r, mode, T, toks[:0], work))
+        else:
+            work = [Work(n_kv=T // 2), Work(n_kv=T - T // 2)]
+            cur = toks
+            for i, p in enumerate(ps):
+                new = W.updated_tokens(seed, r, cur, p, T, i)
+                n = T - p
+                first = True
+                while n > 0:
+                    m = min(n, budget)
+                    work.append(Work(n_kv=m, new_input=new if first else None))
+                    first = False
+                    n -= m
+                cur = new
+            plans.append(Plan(r, mode, T, toks, work))
+    return plans
+
+
+def working_set_blocks(plans, k: int) -> int:
+    return sum(-(-p.total // k) for p in plans)
+
+
+class PressureDriver:
+    """Round-robin stepping + LRU swap residency over one context (`ctx`: s2l.Context).
+
+    Loop (see `run`): sel = plan(); prepare(sel); while sel: items(sel) -> caller enqueues
+    append + attention; finish(sel); nxt = plan(); prepare(nxt, protect=sel); sel = nxt.
+    Every library call is appended to `log` as (op, args, result) for the oracle replay.
+    """
+
+    def __init__(self, ctx, plans, k: int, budget: int):
+        self.ctx, self.k, self.budget = ctx, k, budget
+        self.plans = {p.rid: p for p in plans}
+        self.next_work = {p.rid: 0 for p in plans}
+        self.last_step = {p.rid: -1 for p in plans}
+        self.order = sorted(self.plans)
+        self.cursor = 0
+        self.step = 0
+        self.log = []
+        self.swapped_out_bytes = 0
+        self.swapped_in_bytes = 0
+        self.swap_out_calls = 0
+        self.swap_in_calls = 0
+        self.tokens = 0
+        self.deferred = []
+        for p in plans:
+            ctx.new_request(p.rid, p.initial_tokens)
+            self.log.append(("new", (p.rid, p.initial_tokens), 0))
+
+    # ---- planning ------------------------------------------------------------------------
+    def live(self):
+        return [r for r in self.order if r in self.plans and self.next_work[r] < len(self.plans[r].work)]
+
+    def plan(self):
+        """Next step's requests: round-robin from the cursor, one work item each, until the
+        token budget is reached (the first request is always taken)."""
+        live = self.live()
+        if not live:
+            return []
+        start = 0
+        while start < len(live) and live[start] < self.cursor:
+            start += 1
+        rot = live[start:] + live[:start]
+        sel, used = [], 0
+        for r in rot:
+            n = self.plans[r].work[self.next_work[r]].n_kv
+            if sel and used + n > self.budget:
+                break
+            sel.append(r)
+            used += n
+        self.cursor = sel[-1] + 1
+        return sel
+
+    def _blocks(self, n):
+        return -(-n // self.k)
+
+    def prepare(self, sel, protect=()):
+        """Updates first (LCP invalidation on either tier), then make room: swap
+        out least recently stepped GPU requests outside sel (and, if possible, outside
+        `protect` = the step still computing), swap in the members of sel on the CPU tier."""
+        for r in sel:
+            w = self.plans[r].work[self.next_work[r]]
+            if w.new_input is not None:
+                res = self.ctx.invalidate_lcp(r, w.new_input)
+                self.log.append(("invalidate", (r, w.new_input), res))
+        info = {r: self.ctx.query(r) for r in sel}
+        need = 0
+        to_in = []
+        for r in sel:
+            q = info[r]
+            w = self.plans[r].work[self.next_work[r]]
+            need += self._blocks(q["num_computed"] + w.n_kv) - q["num_blocks"]
+            if q["tier"] == TIER_CPU:
+                need += q["num_blocks"]
+                to_in.append(r)
+        free_gpu, _ = self.ctx.free_blocks()
+        victims = []
+        if free_gpu < need:
+            sel_set, prot = set(sel), set(protect)
+            cands = []
+            for r in self.order:
+                if r in sel_set or r not in self.plans:
+                    continue
+                q = self.ctx.query(r)
+                if q["tier"] == TIER_GPU and q["num_blocks"] > 0:
+                    cands.append((r in prot, self.last_step[r], r, q["num_blocks"]))
+            cands.sort()
+            for _, _, r, nb in cands:
+                if free_gpu >= need:
+                    break
+                victims.append(r)
+                free_gpu += nb
+            if free_gpu < need:
+                raise RuntimeError(f"step {self.step}: cannot make room ({free_gpu} < {need})")
+        if victims:
+            b = self.ctx.swap_out(victims)
+            self.log.append(("swap_out", tuple(victims), b))
+            self.swapped_out_bytes += b
+            self.swap_out_calls += 1
+        if to_in:
+            b = self.ctx.swap_in(to_in)
+            self.log.append(("swap_in", tuple(to_in), b))
+            self.swapped_in_bytes += b
+            self.swap_in_calls += 1
+
+    def items(self, sel):
+        """(append items, prefill items, n rows): rows of the step are packed in sel order."""
+        app, pre, row = [], [], 0
+        for r in sel:
+            w = self.plans[r].work[self.next_work[r]]
+            nc = self.ctx.query(r)["num_computed"]
+            app.append((r, w.append_tokens, w.n_kv, row))
+            pre.append((r, nc, w.n_kv, row))
+            row += w.n_kv
+        self.log.append(("append", tuple((r, t, n) for r, t, n, _ in app), 0))
+        self.log.append(("prefill", tuple((r, p, n) for r, p, n, _ in pre), 0))
+        self.tokens += row
+        return app, pre, row
+
+    def finish(self, sel):
+        """Advance each request; a request with no work left is finished.  Its release is
+        deferred by one step: its blocks are still read by this step's attention, so a swap-in
+        preparing the next step must not land in them (the library would order that H2D after
+        this step's compute and the swap would no longer overlap it)."""
+        self._release_deferred()
+        for r in sel:
+            self.next_work[r] += 1
+            self.last_step[r] = self.step
+            if self.next_work[r] == len(self.plans[r].work):
+                self.deferred.append(r)
+                del self.plans[r]
+        self.step += 1
+
+    def _release_deferred(self):
+        for r in self.deferred:
+            self.ctx.release(r)
+            self.log.append(("release", (r,), 0))
+        self.deferred = []
+
+    def run(self, execute):
+        """Drives the whole stream; execute(sel, app_items, prefill_items, rows) enqueues the
+        step's append + attention.  Returns the number of steps."""
+        sel = self.plan()
+        self.prepare(sel)
+        while sel:
+            app, pre, rows = self.items(sel)
+            execute(sel, app, pre, rows)
+            self.finish(sel)
+            nxt = self.plan()
+            if nxt:
+                self.prepare(nxt, protect=sel)
+            sel = nxt
+        self._release_deferred()
+        return self.step
+
+
+class SwapTimer:
+    """Context wrapper around the swap calls.  `serial=True` drains both streams before and
+    after every swap (the no-overlap baseline); `copy_stream` (the context's copy stream)
+    enables per-call CUDA events, read back with `copy_ms()` after synchronisation."""
+
+    def __init__(self, ctx, serial: bool = False, copy_stream=None):
+        self.ctx, self.serial, self.cs = ctx, serial, copy_stream
+        self.events = []
+
+    def __getattr__(self, name):
+        return getattr(self.ctx, name)
+
+    def _swap(self, fn, rids, kind):
+        if self.serial:
+            self.ctx.sync()
+        ev = None
+        if self.cs is not None:
+            import torch
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record(self.cs)
+        b = fn(rids)
+        if ev is not None:
+            ev[1].record(self.cs)
+            self.events.append((kind, b, ev))
+        if self.serial:
+            self.ctx.sync()
+        return b
+
+    def swap_out(self, rids):
+        return self._swap(self.ctx.swap_out, rids, "out")
+
+    def swap_in(self, rids):
+        return self._swap(self.ctx.swap_in, rids, "in")
+
+    def copy_ms(self):
+        """{kind: (bytes, ms)} summed over calls (each interval spans the copy-stream time
+        from the call's start to its end, including waits for the compute work it depends on)."""
+        out = {}
+        for kind, b, (e0, e1) in self.events:
+            tb, tm = out.get(kind, (0, 0.0))
+            out[kind] = (tb + b, tm + e0.elapsed_time(e1))
+        return out
+
+
+def device_executor(ctx, src_q, src_k, src_v, out, layers: int, on_step=None):
+    """execute() for PressureDriver.run on a device context: one append_chunk of the step's
+    K/V rows (taken from the source buffers at the step's packed rows) and one prefill_batch
+    per layer.  `on_step(sel, app, pre, rows)` runs after the launches (e.g. snapshots)."""
+    kv_rows = src_k.shape[1]
+
+    def execute(sel, app, pre, rows):
+        ctx.append_chunk(app, src_k, src_v, kv_rows=kv_rows)
+        for layer in range(layers):
+            ctx.prefill_batch(layer, pre, src_q, out)
+        if on_step is not None:
+            on_step(sel, app, pre, rows)
+
+    return execute

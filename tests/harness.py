@@ -161,3 +161,76 @@ class Pair:
             for rid, r in self.ora.reqs.items():
                 if r.tier == O.CPU and r.blocks:
                     assert np.array_equal(c[r.blocks], self.ora.pool[O.CPU][r.blocks]), rid
+
+
+class Twin:
+    """Context interface for drivers (paper_2604_16395_b200.pressure) that applies every call
+    to a libs2l context AND to a bookkeeping-only OracleKV (tiny geometry: block ids, counts,
+    LCP and statuses do not depend on L / heads / d), asserting identical results; swap
+    byte counts are compared in blocks (bytes / M_block of each side)."""
+
+    def __init__(self, lib, k, ng, nc, max_requests, max_blocks):
+        self.lib = lib
+        self.ora = OracleKV(1, 1, 1, 8, k, ng, nc, max_requests=max_requests,
+                            max_blocks_per_request=max_blocks, mirror_pools=False)
+        self.m_lib = s2l.block_bytes(lib.cfg)
+        self.ops = 0
+
+    def _same_state(self, rids):
+        for r in rids:
+            assert self.lib.query(r) == self.ora.info(r), r
+            assert self.lib.block_table(r) == self.ora.block_table(r), r
+        assert self.lib.free_blocks() == self.ora.free_counts()
+
+    def new_request(self, rid, toks=()):
+        self.lib.new_request(rid, toks)
+        assert self.ora.new_request(rid, toks) == O.OK
+        self.ops += 1
+
+    def release(self, rid):
+        self.lib.release(rid)
+        assert self.ora.release(rid) == O.OK
+        self._same_state([])
+
+    def invalidate_lcp(self, rid, new):
+        a = self.lib.invalidate_lcp(rid, new)
+        st, p, inv = self.ora.invalidate_lcp(rid, new)
+        assert st == O.OK and a == (p, inv), (a, p, inv)
+        self._same_state([rid])
+        return a
+
+    def _swap(self, fn_lib, fn_ora, rids):
+        b = fn_lib(rids)
+        st, bo = fn_ora(rids)
+        assert st == O.OK and b // self.m_lib == bo // self.ora.m_block and b % self.m_lib == 0
+        self._same_state(rids)
+        return b
+
+    def swap_out(self, rids):
+        return self._swap(self.lib.swap_out, self.ora.swap_out, rids)
+
+    def swap_in(self, rids):
+        return self._swap(self.lib.swap_in, self.ora.swap_in, rids)
+
+    def append_chunk(self, items, k=None, v=None, kv_rows=None):
+        rows = kv_rows if kv_rows is not None else (0 if k is None else k.shape[1])
+        self.lib.append_chunk(items, k, v, kv_rows=rows)
+        z = np.zeros((1, max(1, rows), 1, 8), np.uint16)
+        assert self.ora.append(items, z, z) == O.OK
+        self._same_state([it[0] for it in items])
+
+    def query(self, rid):
+        a = self.lib.query(rid)
+        assert a == self.ora.info(rid)
+        return a
+
+    def free_blocks(self):
+        a = self.lib.free_blocks()
+        assert a == self.ora.free_counts()
+        return a
+
+    def prefill_batch(self, *a, **kw):
+        return self.lib.prefill_batch(*a, **kw)
+
+    def sync(self):
+        return self.lib.sync()

@@ -440,3 +440,178 @@ def test_c4_mixed_stream_under_memory_pressure(seed):
     P.check_state()
     P.check_pool_valid_slots()
     P.check_pools_whole()
+
+
+def _sample_rows_small(rng, n, k=6):
+    return sorted(set([0, n - 1] + rng.choice(n, size=k, replace=False).tolist()))
+
+
+def test_stream_hazards_without_host_syncs():
+    """Swaps on the copy stream overlap compute that does not touch their blocks; the library
+    orders only real conflicts (DESIGN.md §5 stream hazards).  With no host synchronisation
+    between calls, three races are provoked and their results checked afterwards:
+      1. swap_out(A) then an append of B that reuses A's freed ids (append waits for the D2H);
+      2. attention of A in flight, swap_out(A), swap_in(C) into A's freed ids (the H2D waits
+         for A's attention, not only for A's appends);
+      3. attention of A in flight, invalidate_lcp(A) frees A's tail, swap_in(D) lands in it."""
+    from oracle.attention import attention_rows
+    from oracle.kvcache import OracleKV
+    geo = W.Geometry(L=2, h_q=64, h_kv=8, d=128, k=16)
+    seed = 777
+    rid = {"A": 0, "B": 1, "C": 2, "D": 3}
+    n = {"A": 4096, "B": 2048, "C": 2048, "D": 1024}
+    ng, nc = 528, 512
+    cfg = s2l.make_config(2, 64, 8, 128, 16, ng, nc, max_requests=8, max_blocks_per_request=512)
+    mb = s2l.block_bytes(cfg)
+    gpool = torch.empty(ng * mb // 2, dtype=torch.bfloat16, device="cuda")
+    cpool = torch.empty(nc * mb // 2, dtype=torch.bfloat16).pin_memory()
+    lib = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), None)
+    ora = OracleKV(2, 64, 8, 128, 16, ng, nc, max_requests=8, max_blocks_per_request=512, mirror_pools=False)
+    toks = {r: W.request_tokens(seed, rid[r], n[r]) for r in rid}
+    data = {r: _stream_qkv(seed, toks[r], geo) for r in rid}
+    dev = {r: (to_dev(data[r][0]), to_dev(data[r][1]), to_dev(data[r][2])) for r in rid}
+    rng = np.random.default_rng(5)
+
+    def append(r):
+        lib.append_chunk([(rid[r], None, n[r], 0)], dev[r][1], dev[r][2])
+        assert ora.append([(rid[r], None, n[r], 0)], data[r][1], data[r][2]) == 0
+
+    def swap(r, out):
+        a = (lib.swap_out if out else lib.swap_in)([rid[r]])
+        assert a == (ora.swap_out if out else ora.swap_in)([rid[r]])[1]
+
+    for r in rid:
+        lib.new_request(rid[r], toks[r]); ora.new_request(rid[r], toks[r])
+    for r in ("C", "D"):          # C and D start on the CPU tier
+        append(r)
+        swap(r, True)
+    append("A")
+    torch.cuda.synchronize()
+    lib.sync()
+    # race 1: swap_out(A) then an append of B into A's freed (quarantined) ids
+    swap("A", True)
+    append("B")
+    assert lib.block_table(rid["B"]) == list(range(128))
+    # race 2: attention of A in flight, swap A out, swap C in (C lands in A's ids)
+    swap("A", False)
+    qA = dev["A"][0]
+    oA = [torch.empty_like(qA) for _ in range(2)]
+    for layer in range(2):
+        lib.prefill_batch(layer, [(rid["A"], 0, n["A"], 0)], qA, oA[layer])
+    a_ids = set(lib.block_table(rid["A"]))
+    swap("A", True)
+    swap("C", False)
+    assert set(lib.block_table(rid["C"])) <= a_ids
+    oC = torch.empty_like(dev["C"][0])
+    lib.prefill_batch(1, [(rid["C"], 0, n["C"], 0)], dev["C"][0], oC)
+    # race 3: attention of A in flight, invalidate frees A's tail, D is swapped into it
+    swap("A", False)
+    oA3 = torch.empty_like(qA)
+    lib.prefill_batch(0, [(rid["A"], 0, n["A"], 0)], qA, oA3)
+    tail = set(lib.block_table(rid["A"])[63:])
+    newA = W.updated_tokens(seed, 9, toks["A"], 1000, n["A"], 0)
+    assert lib.invalidate_lcp(rid["A"], newA) == ora.invalidate_lcp(rid["A"], newA)[1:]
+    swap("D", False)
+    assert set(lib.block_table(rid["D"])) <= tail
+    oD = torch.empty_like(dev["D"][0])
+    lib.prefill_batch(0, [(rid["D"], 0, n["D"], 0)], dev["D"][0], oD)
+    lib.sync()
+    torch.cuda.synchronize()
+    # ---- checks
+    for r in rid:
+        assert lib.query(rid[r]) == ora.info(rid[r])
+        assert lib.block_table(rid[r]) == ora.block_table(rid[r])
+    assert lib.free_blocks() == ora.free_counts()
+    g = gpool.view(torch.int16).cpu().numpy().view(np.uint16).reshape(ng, 2, 2, 8, 16, 128)
+    for r in ("B", "C", "D"):
+        ids = np.array(lib.block_table(rid[r]))
+        pos = np.arange(n[r])
+        for kv in (0, 1):
+            got = g[ids[pos // 16], :, kv, :, pos % 16, :]
+            assert np.array_equal(got, np.transpose(data[r][1 + kv], (1, 0, 2, 3))), (r, kv)
+    outs = [(oA[0], 0, "A"), (oA[1], 1, "A"), (oA3, 0, "A"), (oC, 1, "C"), (oD, 0, "D")]
+    for o, layer, r in outs:
+        rows = _sample_rows_small(rng, n[r])
+        o_ref, _ = attention_rows(data[r][0], data[r][1][layer], data[r][2][layer], 0, rows)
+        err = normwise_err(bf16_dev_to_f64(o)[rows], o_ref)
+        assert err.max() <= 2e-2, (r, layer, float(err.max()))
+
+
+@pytest.mark.parametrize("serial", [False, True])
+def test_c4_pressure_driver_on_device(serial):
+    """The C4 driver (paper_2604_16395_b200.pressure) at reduced size on the device: 16
+    append / update requests, GPU pool 50% of the working set, swaps overlapping compute (or
+    serialised), no host synchronisation inside the stream.  Bookkeeping is mirrored into the
+    oracle call by call (Twin); every step's output is checked on sampled rows of its first
+    item against the oracle over that request's K/V history (all layers' attention runs; the
+    last layer's output is checked), and the pool bytes of the request are checked whole at
+    every 8th step."""
+    from oracle.attention import attention_rows
+    from paper_2604_16395_b200 import pressure
+    from tests.harness import Twin
+    L, K, budget = 2, 16, 2048
+    plans = pressure.c4_plans(31, 16, lo=256, hi=2048, budget=budget)
+    ws = pressure.working_set_blocks(plans, K)
+    ng, ncpu = ws // 2, ws
+    cfg = s2l.make_config(L, 32, 8, 128, K, ng, ncpu, max_requests=16, max_blocks_per_request=2048 // K)
+    mb = s2l.block_bytes(cfg)
+    gpool = torch.empty(ng * mb // 2, dtype=torch.bfloat16, device="cuda")
+    cpool = torch.empty(ncpu * mb // 2, dtype=torch.bfloat16).pin_memory()
+    cs = torch.cuda.Stream()
+    lib = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), cs)
+    tw = Twin(lib, K, ng, ncpu, 16, 2048 // K)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    src_k = torch.randn(L, budget, 8, 128, generator=g, device="cuda").to(torch.bfloat16)
+    src_v = torch.randn(L, budget, 8, 128, generator=g, device="cuda").to(torch.bfloat16)
+    src_q = torch.randn(budget, 32, 128, generator=g, device="cuda").to(torch.bfloat16)
+    kh = src_k.view(torch.int16).cpu().numpy().view(np.uint16)
+    vh = src_v.view(torch.int16).cpu().numpy().view(np.uint16)
+    qh = src_q.view(torch.int16).cpu().numpy().view(np.uint16)
+    segs, checks, byte_checks = {}, [], []
+    rng = np.random.default_rng(0)
+    drv = pressure.PressureDriver(pressure.SwapTimer(tw, serial=serial), plans, K, budget)
+    out_holder = {}
+
+    def on_step(sel, app, pre, rows):
+        for (r, _, n, row), (_, q_pos, _, _) in zip(app, pre):
+            kept, acc = [], 0
+            for a, m in segs.get(r, []):
+                if acc >= q_pos:
+                    break
+                kept.append((a, min(m, q_pos - acc)))
+                acc += kept[-1][1]
+            kept.append((row, n))
+            segs[r] = kept
+        r, q_pos, n, row = pre[0]
+        rows_s = sorted(set([0, n - 1] + rng.integers(0, n, 4).tolist()))
+        idx = torch.tensor([row + t for t in rows_s], device="cuda")
+        checks.append((r, list(segs[r]), q_pos, row, rows_s, out_holder["o"].index_select(0, idx)))
+        if drv.step % 8 == 0:
+            ids = lib.block_table(r)
+            nc_r = q_pos + n
+            blk = torch.tensor([ids[p // K] for p in range(nc_r)], device="cuda")
+            slot = torch.tensor([p % K for p in range(nc_r)], device="cuda")
+            view = gpool.view(ng, L, 2, 8, K, 128)
+            byte_checks.append((list(segs[r]), view[blk, :, :, :, slot, :].clone()))
+
+    out = torch.empty_like(src_q)
+    out_holder["o"] = out
+    ex = pressure.device_executor(drv.ctx, src_q, src_k, src_v, out, L, on_step)
+    drv.run(ex)
+    lib.sync()
+    torch.cuda.synchronize()
+    assert drv.swap_out_calls > 0 and drv.swap_in_calls > 0
+    assert lib.free_blocks() == (ng, ncpu)
+    for r, seg, q_pos, row, rows_s, o in checks:
+        kk = np.concatenate([kh[L - 1, a:a + m] for a, m in seg])
+        vv = np.concatenate([vh[L - 1, a:a + m] for a, m in seg])
+        n = seg[-1][1]
+        o_ref, _ = attention_rows(qh[row:row + n], kk, vv, q_pos, rows_s)
+        err = normwise_err(bf16_dev_to_f64(o), o_ref)
+        assert err.max() <= 2e-2, (r, q_pos, float(err.max()))
+    for seg, got in byte_checks:
+        got = got.view(torch.int16).cpu().numpy().view(np.uint16)      # [nc][L][2][h_kv][d]
+        want_k = np.concatenate([kh[:, a:a + m] for a, m in seg], axis=1)  # [L][nc][h_kv][d]
+        want_v = np.concatenate([vh[:, a:a + m] for a, m in seg], axis=1)
+        assert np.array_equal(got[:, :, 0], np.transpose(want_k, (1, 0, 2, 3)))
+        assert np.array_equal(got[:, :, 1], np.transpose(want_v, (1, 0, 2, 3)))

@@ -9,7 +9,7 @@
   C4 (BJ:L10) swap microbench: B in {1, 8, 64, 512} blocks x M_block in {64 KiB, 512 KiB,
               2 MiB}, scattered (interleaved requests) ids, out and in, vs the measured link.
 
-    python tools/bench_workloads.py [c3] [c5] [c4]   -> one JSON line per workload
+    python tools/bench_workloads.py [c3] [c5] [c4] [c4mix]   -> one JSON line per workload
 """
 import json
 import os
@@ -158,6 +158,141 @@ def c4():
                                  "in_gbs": best["in"], "out_frac": best["out"] / link["d2h"], "in_frac": best["in"] / link["h2d"]})
             ctx.close()
     return out
+
+
+def c4mix(n_req=128, budget=8192, L=None, check=True):
+    """C4 memory-pressure mix (BJ:L10): 128 append / update requests (paper_2604_16395_b200.
+    pressure recipe) through one context whose GPU pool holds 50% of the working set; the
+    round-robin driver swaps least recently stepped requests out to pinned host memory and
+    back in.  Each step = one append of all layers' K/V + one attention launch per layer.
+    Runs the stream twice on fresh contexts: `serial` (host waits for every swap: no
+    overlap) and `overlap` (swaps for step s+1 on the copy stream while step s computes).
+    Sampled rows of every 16th step's last-layer output are checked against the oracle."""
+    from oracle.attention import attention_rows
+    from paper_2604_16395_b200 import pressure
+    geo_hq, geo_hkv, D, K = 32, 8, 128, 16
+    seed = W.seed_of(4)
+    plans = pressure.c4_plans(seed, n_req, budget=budget)
+    ws = pressure.working_set_blocks(plans, K)
+    if L is None:
+        # SURVEY d.2 C4 allows L = 8 (M_block 512 KiB) when the L = 32 host pool (~150 GB
+        # pinned, zero-filled by every s2l_create) is impractical; L = 32 via c4mix32.
+        L = 8
+    ng, ncpu = ws // 2, ws
+    cfg = s2l.make_config(L, geo_hq, geo_hkv, D, K, ng, ncpu, max_requests=n_req,
+                          max_blocks_per_request=16384 // K)
+    mb = s2l.block_bytes(cfg)
+    gpool = torch.empty(ng * mb // 2, dtype=torch.bfloat16, device="cuda")
+    cpool = torch.empty(ncpu * mb // 2, dtype=torch.bfloat16, pin_memory=True)
+    R = budget
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    src_k = torch.randn(L, R, geo_hkv, D, generator=g, device="cuda").to(torch.bfloat16)
+    src_v = torch.randn(L, R, geo_hkv, D, generator=g, device="cuda").to(torch.bfloat16)
+    src_q = torch.randn(R, geo_hq, D, generator=g, device="cuda").to(torch.bfloat16)
+    out = torch.empty_like(src_q)
+    cs = torch.cuda.Stream()
+    res = {"workload": "C4 memory-pressure mix (BJ:L10)", "requests": n_req, "L": L, "m_block": mb,
+           "working_set_blocks": ws, "gpu_pool_blocks": ng, "cpu_pool_blocks": ncpu, "budget": budget}
+    flops_total = 0.0
+    big = None
+    for mode in ("warm", "compute_only", "serial", "overlap"):
+        if mode == "compute_only":     # same stream with the whole working set resident
+            cfg_big = s2l.make_config(L, geo_hq, geo_hkv, D, K, ws, 0, max_requests=n_req,
+                                      max_blocks_per_request=16384 // K)
+            big = torch.empty(ws * mb // 2, dtype=torch.bfloat16, device="cuda")
+            ctx = s2l.Context(cfg_big, big, None, torch.cuda.current_stream(), cs)
+        else:
+            ctx = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), cs)
+        wrap = pressure.SwapTimer(ctx, serial=(mode == "serial"), copy_stream=cs)
+        drv = pressure.PressureDriver(wrap, plans, K, budget)
+        step_ev = []
+        segs, snaps, flops = {}, [], [0.0]
+
+        def on_step(sel, app, pre, rows, segs=segs, snaps=snaps, flops=flops, drv=drv):
+            for (r, _, n, row), (_, q_pos, _, _) in zip(app, pre):
+                kept, acc = [], 0
+                for a, m in segs.get(r, []):
+                    if acc >= q_pos:
+                        break
+                    take = min(m, q_pos - acc)
+                    kept.append((a, take))
+                    acc += take
+                kept.append((row, n))
+                segs[r] = kept
+                flops[0] += L * attn_flops(n, q_pos)
+            if check and mode == "overlap" and drv.step % 16 == 0:
+                r, q_pos, n, row = pre[0]
+                rows_s = sorted(set([0, n - 1] + [int(x) for x in np.random.default_rng(drv.step).integers(0, n, 6)]))
+                idx = torch.tensor([row + t for t in rows_s], device="cuda")
+                snaps.append((list(segs[r]), q_pos, row, rows_s, out.index_select(0, idx)))
+
+        ex0 = pressure.device_executor(wrap, src_q, src_k, src_v, out, L, on_step)
+
+        def ex(sel, app, pre, rows, ex0=ex0, step_ev=step_ev):
+            e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            e[0].record()
+            ex0(sel, app, pre, rows)
+            e[1].record()
+            step_ev.append(e)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        steps = drv.run(ex)
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        torch.cuda.current_stream().wait_event(ev)
+        e1.record()
+        torch.cuda.synchronize()
+        host_s = time.perf_counter() - t0
+        ms = e0.elapsed_time(e1)
+        flops_total = flops[0]
+        busy = sum(a.elapsed_time(b) for a, b in step_ev)
+        gaps = sum(step_ev[i][1].elapsed_time(step_ev[i + 1][0]) for i in range(len(step_ev) - 1))
+        cm = wrap.copy_ms()
+        if mode != "warm":
+            res[mode] = {"ms": ms, "host_s": host_s, "steps": steps, "tflops": flops[0] / (ms * 1e-3) / 1e12,
+                         "compute_busy_ms": busy, "compute_gap_ms": gaps,
+                         "copy_out": {"bytes": cm.get("out", (0, 0))[0], "ms": cm.get("out", (0, 0))[1]},
+                         "copy_in": {"bytes": cm.get("in", (0, 0))[0], "ms": cm.get("in", (0, 0))[1]},
+                         "tokens": drv.tokens, "tokens_per_s": drv.tokens / (ms * 1e-3),
+                         "swap_out_bytes": drv.swapped_out_bytes, "swap_in_bytes": drv.swapped_in_bytes,
+                         "swap_out_calls": drv.swap_out_calls, "swap_in_calls": drv.swap_in_calls}
+        if snaps:
+            kh = src_k[L - 1].view(torch.int16).cpu().numpy().view(np.uint16)
+            vh = src_v[L - 1].view(torch.int16).cpu().numpy().view(np.uint16)
+            qh = src_q.view(torch.int16).cpu().numpy().view(np.uint16)
+            worst = 0.0
+            for seg, q_pos, row, rows_s, o in snaps:
+                kk = np.concatenate([kh[a:a + m] for a, m in seg])
+                vv = np.concatenate([vh[a:a + m] for a, m in seg])
+                n = seg[-1][1]
+                o_ref, _ = attention_rows(qh[row:row + n], kk, vv, q_pos, rows_s)
+                og = o.float().cpu().numpy().astype(np.float64)
+                num = np.abs(og - o_ref).max(axis=-1)
+                den = np.maximum(np.abs(o_ref).max(axis=-1), 1e-6)
+                worst = max(worst, float((num / den).max()))
+            res["parity"] = {"sampled_steps": len(snaps), "max_normwise_err": worst, "tol": 2e-2,
+                             "pass": worst <= 2e-2}
+        ctx.close()
+        if big is not None:
+            del big
+            big = None
+            torch.cuda.empty_cache()
+    res["attn_flops"] = flops_total
+    s, o, c0 = res["serial"]["ms"], res["overlap"]["ms"], res["compute_only"]["ms"]
+    res["overlap_vs_compute_only"] = o / c0
+    link = measure_link("cuda")
+    copy_ms = (res["overlap"]["swap_out_bytes"] / link["d2h"] + res["overlap"]["swap_in_bytes"] / link["h2d"]) / 1e6
+    res["link_gbs"] = link
+    res["copy_ms_at_link"] = copy_ms
+    res["overlap_gain_ms"] = s - o
+    res["hidden_copy_frac"] = (s - o) / copy_ms if copy_ms else None
+    return res
+
+
+def c4mix32():
+    return c4mix(L=32)
 
 
 if __name__ == "__main__":

@@ -19,7 +19,7 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
                      __int_as_float(__float_as_int(q.y) + (__float_as_int(y.y) << 23)));
 }
 
-template <int POLY>
+template <int POLY, int PACK>
 __global__ void k(const float* __restrict__ in, uint32_t* out, int iters, long long* cycles) {
   float s[128];
 #pragma unroll
@@ -38,7 +38,8 @@ __global__ void k(const float* __restrict__ in, uint32_t* out, int iters, long l
       float2 x = __ffma2_rn(make_float2(s[2 * c], s[2 * c + 1]), sc, nm);
       float2 p = ((c & 7) < POLY) ? exp2_poly2(x) : make_float2(fast_exp2(x.x), fast_exp2(x.y));
       acc = __fadd2_rn(acc, p);
-      sink ^= pack_bf16(p.x, p.y);
+      if (PACK == 0) sink ^= pack_bf16(p.x, p.y);
+      else { uint32_t r; asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(__float_as_uint(p.x)), "r"(__float_as_uint(p.y))); sink ^= r; }
     }
     l += acc.x + acc.y;
     s[it & 127] += 1e-3f;
@@ -48,22 +49,23 @@ __global__ void k(const float* __restrict__ in, uint32_t* out, int iters, long l
   if (threadIdx.x == 0 && blockIdx.x == 0) *cycles = (t1 - t0) / iters;
 }
 
-template <int POLY>
+template <int POLY, int PACK = 0>
 void run(int warps_per_smsp) {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   float* in; cudaMalloc(&in, 1024 * 4); cudaMemset(in, 0, 4096);
   uint32_t* out; cudaMalloc(&out, sms * 1024 * 4);
   long long* cyc; cudaMalloc(&cyc, 8);
   const int threads = 128 * warps_per_smsp;   // 4 SMSPs
-  k<POLY><<<sms, threads>>>(in, out, 200, cyc);
+  k<POLY, PACK><<<sms, threads>>>(in, out, 200, cyc);
   cudaDeviceSynchronize();
   long long h; cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
-  printf("poly %d/8, %d warp(s) per SMSP: %lld cycles per 128-column row-tile per warp\n", POLY, warps_per_smsp, h);
+  printf("pack %s poly %d/8, %d warp(s) per SMSP: %lld cycles per 128-column row-tile per warp\n", PACK ? "prmt" : "f2fp", POLY, warps_per_smsp, h);
   cudaFree(in); cudaFree(out); cudaFree(cyc);
 }
 
 int main() {
   run<0>(1); run<2>(1); run<4>(1); run<8>(1);
   run<0>(2); run<2>(2); run<4>(2);
+  run<0, 1>(1); run<2, 1>(1); run<0, 1>(2); run<2, 1>(2); run<3, 1>(2); run<4, 1>(2);
   return 0;
 }
