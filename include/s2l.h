@@ -141,7 +141,9 @@ s2l_status s2l_preempt_recompute(s2l_ctx* ctx, int64_t req_id);
  *   k, v: device, [num_layers][kv_rows][h_kv][d] bf16, item i's rows at
  *         [kv_row_i, kv_row_i + n_kv_i); kv_rows = token rows per layer.
  * Validation (first failing item in call order wins; capacity checked last):
- *   unknown id -> E_NO_REQUEST; id repeated in the call -> E_INVAL; CPU tier -> E_STATE;
+ *   unknown id -> E_NO_REQUEST; id repeated in the call -> E_INVAL; CPU tier with
+ *   n_kv != 0 -> E_STATE (a token-only item, n_kv = 0, is valid on either tier: input keeps
+ *   arriving while a request is swapped out, reading Z19);
  *   n_tokens/n_kv/kv_row < 0, kv_row+n_kv > kv_rows, n_kv > len(input)+n_tokens-nc, or
  *   ceil((nc+n_kv)/k) > max_blocks_per_request -> E_INVAL;
  *   total new blocks > free GPU blocks -> E_NO_GPU_BLOCKS.
@@ -175,11 +177,16 @@ s2l_status s2l_prefill_batch(s2l_ctx* ctx, int32_t layer, int32_t n_items,
 /* Swap-out (a5): all-or-nothing over the listed requests (all GPU tier, no
  * duplicates): allocate |blocks| CPU ids per request (lowest free), copy every block GPU ->
  * CPU in order on copy_stream (whole blocks, Z12), free the GPU ids, tier := CPU, nc kept.
+ * The copies wait only for the work they conflict with (the requests' appends / swap-ins, an
+ * H2D still reading the destination CPU blocks); later appends that reuse the freed GPU ids
+ * wait for them (DESIGN.md §5 stream hazards).
  * bytes_out = total blocks * M_block.  E_NO_CPU_BLOCKS if the CPU pool is short. */
 s2l_status s2l_swap_out(s2l_ctx* ctx, int32_t n_reqs, const int64_t* req_ids, int64_t* bytes_out);
 
 /* Swap-in (a6, "symmetric", P:L184 prefix only after an update): mirror of
- * s2l_swap_out CPU -> GPU.  E_NO_GPU_BLOCKS if the GPU pool is short. */
+ * s2l_swap_out CPU -> GPU, on the swap-in stream (s2l_set_swap_in_stream).  The H2D waits for
+ * the requests' swap-outs and for any kernel / D2H still using the destination GPU blocks;
+ * appends / attention of the requests wait for it.  E_NO_GPU_BLOCKS if the GPU pool is short. */
 s2l_status s2l_swap_in(s2l_ctx* ctx, int32_t n_reqs, const int64_t* req_ids, int64_t* bytes_out);
 
 s2l_status s2l_query(s2l_ctx* ctx, int64_t req_id, s2l_req_info* out);
@@ -192,7 +199,14 @@ s2l_status s2l_block_table(s2l_ctx* ctx, int64_t req_id, int32_t* ids_out, int64
 /* Free block counts of both tiers. */
 s2l_status s2l_free_blocks(s2l_ctx* ctx, int64_t* gpu_free, int64_t* cpu_free);
 
-/* Blocks until all work enqueued by this context on both streams has completed. */
+/* Swap-ins (H2D) run on a second copy stream so that they overlap swap-outs (D2H, on
+ * copy_stream) as well as compute; by default the library creates it.  This call replaces it
+ * with a caller-owned cudaStream_t (e.g. to record timing events on it); the previous stream
+ * is drained first.  Errors: S2L_E_INVAL (NULL), S2L_E_STATE (host-only context). */
+s2l_status s2l_set_swap_in_stream(s2l_ctx* ctx, void* stream);
+
+/* Blocks until all work enqueued by this context on its streams (compute, swap-out,
+ * swap-in) has completed. */
 s2l_status s2l_sync(s2l_ctx* ctx);
 
 /* Number of kernels this context has launched since creation (evidence counter). */

@@ -75,6 +75,7 @@ class OracleKV:
         self.max_requests, self.max_blocks = max_requests, max_blocks_per_request
         self.aligned = bool(lcp_block_aligned)
         self.free = {GPU: set(range(num_gpu_blocks)), CPU: set(range(num_cpu_blocks))}
+        self.cool = set()   # GPU ids released by the most recent swap-out (Z9), subset of free
         self.reqs: dict[int, Req] = {}
         self.mirror = mirror_pools
         shape = (L, 2, h_kv, k, d)
@@ -87,10 +88,15 @@ class OracleKV:
         return block_bytes(self.L, self.k, self.h_kv, self.d)
 
     def _take_lowest(self, tier, n):
-        """Z9: the n lowest free ids, ascending."""
-        ids = sorted(self.free[tier])[:n]
+        """Z9: the n lowest free ids, ascending -- except that GPU ids released by the most
+        recent swap-out ("cooling") come after every other free id (lowest first)."""
+        cool = self.cool if tier == GPU else set()
+        ids = sorted(self.free[tier] - cool)[:n]
+        if len(ids) < n:
+            ids += sorted(cool)[: n - len(ids)]
         for i in ids:
             self.free[tier].remove(i)
+            cool.discard(i)
         return ids
 
     def _give_back(self, tier, ids):
@@ -155,7 +161,7 @@ class OracleKV:
             if rid in seen:
                 return E_INVAL
             seen.add(rid)
-            if r.tier != GPU:
+            if r.tier != GPU and n_kv != 0:             # Z19: token-only append on either tier
                 return E_STATE
             n_tok = 0 if toks is None else len(toks)
             if n_kv < 0 or kv_row < 0:
@@ -233,6 +239,8 @@ class OracleKV:
             need += len(r.blocks)
         if need > len(self.free[dst]):
             return e_full, 0
+        if src == GPU and rids:
+            self.cool = set()                           # Z9: the previous swap-out's ids thaw
         for rid in rids:
             r = self.reqs[rid]
             new_ids = self._take_lowest(dst, len(r.blocks))
@@ -240,6 +248,8 @@ class OracleKV:
                 for s, t in zip(r.blocks, new_ids):
                     self.pool[dst][t] = self.pool[src][s]   # whole block (Z12)
             self._give_back(src, r.blocks)
+            if src == GPU:
+                self.cool.update(r.blocks)
             r.blocks, r.tier = new_ids, dst
         return OK, need * self.m_block
 

@@ -41,6 +41,9 @@
 #ifndef S2L_POLY_PAIRS
 #define S2L_POLY_PAIRS 2
 #endif
+#ifndef S2L_PQ
+#define S2L_PQ 0           // v2: 1 = P handed to the MMA warp in quarters (32 keys) instead of halves
+#endif
 #ifndef S2L_PACK_TRUNC
 #define S2L_PACK_TRUNC 0   // 1: P -> bf16 by truncation (PRMT) with a mean-bias correction of l
 #endif
@@ -710,7 +713,8 @@ constexpr uint32_t WOFF_BAR = WOFF_RING + WNST * kTileBytes;
 // P_full is split in two halves (keys 0-63 / 64-127) so the PV MMAs of the first half start
 // while the softmax still computes the second half.
 constexpr uint32_t WB_QF = 0, WB_RF = 1, WB_RE = 1 + WNST, WB_SF = 1 + 2 * WNST, WB_PF = WB_SF + 2,
-                   WB_PH = WB_PF + 2, WB_OF = WB_PH + 2, WB_QE = WB_OF + 2, WNBARS = WB_QE + 1;
+                   WB_PH = WB_PF + 2, WB_OF = WB_PH + 2, WB_QE = WB_OF + 2, WB_PQ = WB_QE + 1,
+                   WNBARS = WB_PQ + 8;
 constexpr uint32_t WOFF_TMEM = WOFF_BAR + WNBARS * 8;
 constexpr uint32_t SMEM = WOFF_TMEM + 16 + 1024;
 }  // namespace v2
@@ -810,6 +814,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       mbar_init(bar(WB_PH + i), 128);
       mbar_init(bar(WB_OF + i), 1);
     }
+    for (int q = 0; q < 8; ++q) mbar_init(bar(WB_PQ + q), 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
@@ -936,10 +941,24 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       auto issue_pv = [&](int i, uint32_t vslot, int32_t j) {
         const uint64_t vd = dv0 + ((vslot * kTileBytes) >> 4);
         if (lane == 0) TRACE(10, i, j);
-        mbar_wait(bar(WB_PF + i), j & 1);               // P keys 0-63 in TMEM
+        mbar_wait(bar(S2L_PQ ? WB_PQ + i * 4 : WB_PF + i), j & 1);   // first P part in TMEM
         tc_fence_after();
         if (lane == 0) TRACE(11, i, j);
 #ifndef S2L_EXP_NO_PV
+#if S2L_PQ
+        // P in quarters (32 keys each); quarter 0 was waited for above
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (q > 0) {
+            mbar_wait(bar(WB_PQ + i * 4 + q), j & 1);
+            tc_fence_after();
+          }
+#pragma unroll
+          for (int kk = 2 * q; kk < 2 * q + 2; ++kk)
+            mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8,
+                         vd + ((kk * 16 * 128) >> 4), idesc_o, (j > 0 || kk > 0));
+        }
+#else
 #pragma unroll
         for (int kk = 0; kk < kBN / 32; ++kk)
           mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
@@ -951,6 +970,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         for (int kk = kBN / 32; kk < kBN / 16; ++kk)
           mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
                        idesc_o, 1);
+#endif
 #endif
       };
       mbar_wait(bar(WB_QF), 0);
@@ -1004,6 +1024,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       tc_fence_before();
       mbar_arrive(bar(WB_PF + i));
       mbar_arrive(bar(WB_PH + i));
+      for (int q = 0; q < 4; ++q) mbar_arrive(bar(WB_PQ + i * 4 + q));
       continue;
 #endif
 #ifdef S2L_EXP_TMEM_ONLY  // timing experiment only: the softmax's TMEM traffic without its math
@@ -1020,6 +1041,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         tc_fence_before();
         mbar_arrive(bar(WB_PF + i));
         mbar_arrive(bar(WB_PH + i));
+        for (int q = 0; q < 4; ++q) mbar_arrive(bar(WB_PQ + i * 4 + q));
         continue;
       }
 #endif
@@ -1078,12 +1100,19 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         acc = masked_tile ? chunk_p<true, 0>(v32, acc, vis, 32 * cc, sc2, nm2, pk)
                           : chunk_p<false, kPolyPairsPer8>(v32, acc, vis, 32 * cc, sc2, nm2, pk);
         tmem_st16(tS + 16 * cc, pk);
+#if S2L_PQ
+        tmem_wait_st();                // keys 32cc .. 32cc+31 of P are in TMEM
+        tc_fence_before();
+        mbar_arrive(bar(WB_PQ + i * 4 + cc));
+        if (tr && (cc & 1)) TRACE(cc == 1 ? 23 : 24, i, j);
+#else
         if (cc == 1 || cc == 3) {      // keys 0-63 / 64-127 of P are in TMEM
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(bar((cc == 1 ? WB_PF : WB_PH) + i));
           if (tr) TRACE(cc == 1 ? 23 : 24, i, j);
         }
+#endif
       }
       l_run += acc.x + acc.y;
     }

@@ -73,11 +73,53 @@ class Allocator {
     }
     free_ += n;
   }
+  void clear() {
+    std::fill(bits_.begin(), bits_.end(), 0ull);
+    free_ = 0;
+    hint_ = 0;
+  }
+  // Moves every id of this set into `dst` and empties this set.
+  void drain_into(Allocator& dst) {
+    std::vector<int32_t> ids;
+    take_lowest(free_, ids);
+    dst.give_back(ids.data(), (int64_t)ids.size());
+  }
 
  private:
   std::vector<uint64_t> bits_;
   int64_t n_ = 0, free_ = 0;
   size_t hint_ = 0;
+};
+
+// A tier's free ids (reading Z9): the lowest free id first, except that the GPU ids released
+// by the most recent swap-out ("cooling": their D2H may still be reading them) are handed out
+// only after every other free id (lowest first among them).  Deterministic, so the oracle
+// reproduces it; all free ids count for capacity.  It keeps appends and swap-ins from
+// landing in blocks a D2H is still reading when other blocks are free.
+class TierPool {
+ public:
+  void init(int64_t n) {
+    main_.init(n);
+    cool_.init(n);
+    cool_.clear();
+  }
+  int64_t free_count() const { return main_.free_count() + cool_.free_count(); }
+  void take_lowest(int64_t n, std::vector<int32_t>& out) {
+    const int64_t a = std::min(n, main_.free_count());
+    main_.take_lowest(a, out);
+    cool_.take_lowest(n - a, out);
+  }
+  void give_back(const int32_t* ids, int64_t n) { main_.give_back(ids, n); }
+  // Starts a new cooling set (the previous one becomes ordinary free ids) with `ids`.
+  void give_back_cooling(const int32_t* ids, int64_t n) {
+    cool_.drain_into(main_);
+    cool_.give_back(ids, n);
+  }
+  // Adds ids to the current cooling set.
+  void give_back_cooling_append(const int32_t* ids, int64_t n) { cool_.give_back(ids, n); }
+
+ private:
+  Allocator main_, cool_;
 };
 
 struct Request {
@@ -88,7 +130,8 @@ struct Request {
   std::vector<int32_t> blocks;
   int64_t tti = 0;
   int32_t slot = -1;
-  uint64_t swap_in_seq = 0;   // copy-ring record after the H2D that filled its blocks (0: none)
+  uint64_t swap_in_seq = 0;   // in-ring record after the H2D that filled its GPU blocks (0: none)
+  uint64_t swap_out_seq = 0;  // out-ring record after the D2H that filled its CPU blocks
   uint64_t write_seq = 0;     // compute-ring record after the last append that wrote its blocks
   uint64_t use_seq = 0;       // compute-ring record after the last append / attention using them
 };
@@ -101,6 +144,7 @@ struct EventRing {
   static constexpr int kN = 64;
   cudaEvent_t ev[kN] = {};
   uint64_t seq = 0;
+  uint64_t done = 0;   // every record <= done is known to have completed
 };
 
 // Pinned-host + device staging ring.  Slot s is reused only after its event (recorded after
@@ -124,13 +168,14 @@ struct s2l_ctx {
   void* gpu_pool = nullptr;
   void* cpu_pool = nullptr;
   cudaStream_t compute = nullptr;
-  cudaStream_t copy = nullptr;
-  bool own_copy_stream = false;
+  cudaStream_t copy = nullptr;        // swap-out (D2H)
+  cudaStream_t copy_in = nullptr;     // swap-in (H2D): a second stream so both directions overlap
+  bool own_copy_stream = false, own_copy_in = false;
   int32_t* d_table = nullptr;          // [max_requests][max_blocks] int32
   std::vector<int32_t> h_table;        // host mirror
   std::vector<int32_t> dirty;          // table entries whose host value must reach the device
   std::vector<uint8_t> dirty_flag;
-  Allocator alloc[2];
+  TierPool alloc[2];
   std::vector<Request> slots;
   std::vector<int32_t> free_slots;     // stack; lowest slot on top
   std::unordered_map<int64_t, int32_t> by_id;
@@ -139,17 +184,17 @@ struct s2l_ctx {
   int64_t launches = 0;
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> attn_ev, append_ev, ev_pool;
-  // Stream hazards (DESIGN.md §5 "Stream hazards"), tracked per request and per GPU block so
-  // that swaps on the copy stream overlap the compute work they do not conflict with:
-  //  * compute_ring: one record after every append / attention launch; Request::write_seq
-  //    (a swap-out's D2H waits for it) and Request::use_seq;
-  //  * copy_ring: one record after every swap call; Request::swap_in_seq (compute waits for
-  //    it before touching the request);
-  //  * per free GPU block: freed_use = the previous owner's use_seq (an H2D that reuses the
-  //    block waits for it) and quar = the copy-ring record of a D2H / H2D still touching it
-  //    (an append that reuses the block waits for it).  Both are cleared on allocation.
-  EventRing compute_ring, copy_ring;
-  std::vector<uint64_t> freed_use, quar;
+  // Stream hazards (DESIGN.md §5 "Stream hazards"), tracked per request and per block so
+  // that swaps overlap the compute work (and the other copy direction) they do not conflict
+  // with.  Rings: compute_ring (one record per append / attention launch), out_ring (one per
+  // swap-out, on `copy`), in_ring (one per swap-in, on `copy_in`).
+  //  * Request: write_seq / use_seq (compute), swap_in_seq (in), swap_out_seq (out);
+  //  * free GPU block: freed_use (compute: previous owner's last use), quar_out (a D2H still
+  //    reading it), quar_in (an H2D of a since-freed request still writing it);
+  //  * free CPU block: cpu_quar_in (an H2D still reading it).
+  // All per-block marks are cleared when the block is allocated again.
+  EventRing compute_ring, out_ring, in_ring;
+  std::vector<uint64_t> freed_use, quar_out, quar_in, cpu_quar_in;
   unsigned char tmap_kv[384] __attribute__((aligned(64)));
   int32_t num_sms = 148;
   float* split_ws = nullptr;          // tail-wave split partials (num_sms pieces)
@@ -184,9 +229,21 @@ bool ring_record(s2l_ctx* c, EventRing& R, cudaStream_t st, uint64_t* seq) {
   *seq = n;
   return true;
 }
+// Orders `st` after record `seq` of ring R.  Records known to be complete cost nothing; a
+// record whose slot has been reused is represented by the oldest record still held (later on
+// the same in-order stream, so waiting for it is sufficient, and it is usually complete too).
 bool ring_wait(s2l_ctx* c, EventRing& R, cudaStream_t st, uint64_t seq) {
-  if (seq == 0) return true;
-  return cuda_ok(c, cudaStreamWaitEvent(st, R.ev[seq % EventRing::kN], 0), "event ring wait");
+  if (seq == 0 || seq <= R.done) return true;
+  const uint64_t oldest = R.seq >= (uint64_t)EventRing::kN ? R.seq - EventRing::kN + 1 : 1;
+  const uint64_t use = std::max(seq, oldest);
+  cudaEvent_t ev = R.ev[use % EventRing::kN];
+  const cudaError_t q = cudaEventQuery(ev);
+  if (q == cudaSuccess) {
+    R.done = std::max(R.done, use);
+    return true;
+  }
+  if (q != cudaErrorNotReady) return cuda_ok(c, q, "event ring query");
+  return cuda_ok(c, cudaStreamWaitEvent(st, ev, 0), "event ring wait");
 }
 
 s2l_status check_config(const s2l_config* cfg) {
@@ -243,7 +300,7 @@ void free_tail(s2l_ctx* c, Request* r, size_t keep) {
   if (r->tier == S2L_TIER_GPU && r->swap_in_seq && !c->host_only) {
     // blocks possibly still being filled by a swap-in: an append reusing them waits for it
     for (size_t j = keep; j < r->blocks.size(); ++j)
-      c->quar[(size_t)r->blocks[j]] = std::max(c->quar[(size_t)r->blocks[j]], r->swap_in_seq);
+      c->quar_in[(size_t)r->blocks[j]] = std::max(c->quar_in[(size_t)r->blocks[j]], r->swap_in_seq);
     if (keep == 0) r->swap_in_seq = 0;
   }
   c->alloc[r->tier].give_back(r->blocks.data() + keep, (int64_t)(r->blocks.size() - keep));
@@ -371,7 +428,12 @@ s2l_status swap_impl(s2l_ctx* c, int32_t n_reqs, const int64_t* ids, int64_t* by
     for (size_t j = 0; j < nid.size(); ++j) moves.emplace_back(r->blocks[j], nid[j]);
     if (src == S2L_TIER_GPU && !c->host_only)
       for (int32_t b : r->blocks) c->freed_use[(size_t)b] = r->use_seq;
-    c->alloc[src].give_back(r->blocks.data(), (int64_t)r->blocks.size());
+    if (src == S2L_TIER_GPU) {   // Z9: this call's GPU ids cool until the next swap-out
+      if (i == 0) c->alloc[src].give_back_cooling(nullptr, 0);
+      c->alloc[src].give_back_cooling_append(r->blocks.data(), (int64_t)r->blocks.size());
+    } else {
+      c->alloc[src].give_back(r->blocks.data(), (int64_t)r->blocks.size());
+    }
     for (size_t j = 0; j < nid.size(); ++j)
       set_table(c, r->slot, (int64_t)j, dst == S2L_TIER_GPU ? nid[j] : -1);
     r->blocks.swap(nid);
@@ -382,21 +444,34 @@ s2l_status swap_impl(s2l_ctx* c, int32_t n_reqs, const int64_t* ids, int64_t* by
   if (c->host_only || need == 0) return S2L_OK;
 
   // ---- copies on the copy stream: order only against the compute work they conflict with --
-  uint64_t w = 0;
+  cudaStream_t st = (src == S2L_TIER_GPU) ? c->copy : c->copy_in;
+  uint64_t wc = 0, wo = 0, wi = 0;   // waits on the compute / out / in rings
   if (src == S2L_TIER_GPU) {
-    // D2H reads blocks written by earlier appends of these requests (wait for the newest one;
-    // the compute ring is in order).  Blocks filled by an earlier swap-in: same copy stream.
-    for (Request* r : touched) w = std::max(w, r->write_seq);
-  } else {
-    // H2D overwrites free GPU blocks that kernels of their previous owner may still use
-    // (freed_use); blocks freed by a swap-out are read by a D2H earlier on this stream.
+    // D2H reads GPU blocks written by the requests' appends (compute) or swap-ins (in), and
+    // writes CPU blocks an earlier H2D may still be reading (cpu_quar_in).
+    for (Request* r : touched) {
+      wc = std::max(wc, r->write_seq);
+      wi = std::max(wi, r->swap_in_seq);
+    }
     for (const auto& m : moves) {
-      w = std::max(w, c->freed_use[(size_t)m.second]);
-      c->freed_use[(size_t)m.second] = 0;
-      c->quar[(size_t)m.second] = 0;
+      wi = std::max(wi, c->cpu_quar_in[(size_t)m.second]);
+      c->cpu_quar_in[(size_t)m.second] = 0;
+    }
+  } else {
+    // H2D reads CPU blocks written by the requests' swap-outs (out) and overwrites free GPU
+    // blocks that kernels of their previous owner (freed_use), a D2H (quar_out) or an
+    // earlier H2D on this stream (quar_in, ordered) may still touch.
+    for (Request* r : touched) wo = std::max(wo, r->swap_out_seq);
+    for (const auto& m : moves) {
+      const size_t b = (size_t)m.second;
+      wc = std::max(wc, c->freed_use[b]);
+      wo = std::max(wo, c->quar_out[b]);
+      c->freed_use[b] = c->quar_out[b] = c->quar_in[b] = 0;
     }
   }
-  if (!ring_wait(c, c->compute_ring, c->copy, w)) return S2L_E_CUDA;
+  if (!ring_wait(c, c->compute_ring, st, wc) || !ring_wait(c, c->out_ring, st, wo) ||
+      !ring_wait(c, c->in_ring, st, wi))
+    return S2L_E_CUDA;
   // Coalesce runs where both source and destination ids are consecutive (Z9 makes these long).
   char* gbase = (char*)c->gpu_pool;
   char* hbase = (char*)c->cpu_pool;
@@ -417,27 +492,30 @@ s2l_status swap_impl(s2l_ctx* c, int32_t n_reqs, const int64_t* ids, int64_t* by
   }
   if (sizes.size() == 1) {
     CK(cudaMemcpyAsync(dsts[0], srcs[0], sizes[0],
-                       dst == S2L_TIER_GPU ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, c->copy));
+                       dst == S2L_TIER_GPU ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st));
   } else {
     cudaMemcpyAttributes attr{};
     attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
     attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
     size_t attr_idx = 0, fail_idx = 0;
     cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(),
-                                         &attr, &attr_idx, 1, &fail_idx, c->copy);
+                                         &attr, &attr_idx, 1, &fail_idx, st);
     if (e != cudaSuccess) {
       cudaGetLastError();
       for (size_t i = 0; i < sizes.size(); ++i)
         CK(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i],
                            dst == S2L_TIER_GPU ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
-                           c->copy));
+                           st));
     }
   }
   uint64_t seq = 0;
-  if (!ring_record(c, c->copy_ring, c->copy, &seq)) return S2L_E_CUDA;
   if (src == S2L_TIER_GPU) {
-    for (const auto& m : moves) c->quar[(size_t)m.first] = seq;   // freed GPU ids: quarantined
+    if (!ring_record(c, c->out_ring, st, &seq)) return S2L_E_CUDA;
+    for (const auto& m : moves) c->quar_out[(size_t)m.first] = seq;   // freed GPU ids
+    for (Request* r : touched) r->swap_out_seq = seq;
   } else {
+    if (!ring_record(c, c->in_ring, st, &seq)) return S2L_E_CUDA;
+    for (const auto& m : moves) c->cpu_quar_in[(size_t)m.first] = seq;   // freed CPU ids
     for (Request* r : touched) r->swap_in_seq = seq;
   }
   return S2L_OK;
@@ -488,6 +566,8 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
     CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
     c->own_copy_stream = true;
   }
+  CK(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
+  c->own_copy_in = true;
   CK(cudaMalloc(&c->d_table, c->h_table.size() * sizeof(int32_t)));
   CK(cudaMemsetAsync(c->d_table, 0xFF, c->h_table.size() * sizeof(int32_t), c->compute));
   size_t gbytes = (size_t)cfg->num_gpu_blocks * (size_t)c->m_block;
@@ -496,10 +576,12 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
   if (hbytes) memset(cpu_pool_pinned, 0, hbytes);
   for (int s = 0; s < StagingRing::kSlots; ++s)
     CK(cudaEventCreateWithFlags(&c->ring.ev[s], cudaEventDisableTiming));
-  for (EventRing* R : {&c->compute_ring, &c->copy_ring})
+  for (EventRing* R : {&c->compute_ring, &c->out_ring, &c->in_ring})
     for (int i = 0; i < EventRing::kN; ++i) CK(cudaEventCreateWithFlags(&R->ev[i], cudaEventDisableTiming));
-  c->quar.assign((size_t)cfg->num_gpu_blocks, 0);
   c->freed_use.assign((size_t)cfg->num_gpu_blocks, 0);
+  c->quar_out.assign((size_t)cfg->num_gpu_blocks, 0);
+  c->quar_in.assign((size_t)cfg->num_gpu_blocks, 0);
+  c->cpu_quar_in.assign((size_t)cfg->num_cpu_blocks, 0);
   c->tc_ok = s2l::attn_tc_supported(c->geo);
   if (c->tc_ok && cfg->num_gpu_blocks > 0) {
     const char* err = nullptr;
@@ -542,12 +624,13 @@ void s2l_destroy(s2l_ctx* c) {
   if (!c->host_only) {
     cudaStreamSynchronize(c->compute);
     cudaStreamSynchronize(c->copy);
+    if (c->copy_in) cudaStreamSynchronize(c->copy_in);
     for (int s = 0; s < StagingRing::kSlots; ++s) {
       if (c->ring.host[s]) cudaFreeHost(c->ring.host[s]);
       if (c->ring.dev[s]) cudaFree(c->ring.dev[s]);
       if (c->ring.ev[s]) cudaEventDestroy(c->ring.ev[s]);
     }
-    for (EventRing* R : {&c->compute_ring, &c->copy_ring})
+    for (EventRing* R : {&c->compute_ring, &c->out_ring, &c->in_ring})
       for (int i = 0; i < EventRing::kN; ++i)
         if (R->ev[i]) cudaEventDestroy(R->ev[i]);
     for (auto* v : {&c->attn_ev, &c->append_ev, &c->ev_pool})
@@ -569,6 +652,7 @@ void s2l_destroy(s2l_ctx* c) {
     if (c->split_cnt) cudaFree(c->split_cnt);
     if (c->d_table) cudaFree(c->d_table);
     if (c->own_copy_stream) cudaStreamDestroy(c->copy);
+    if (c->own_copy_in && c->copy_in) cudaStreamDestroy(c->copy_in);
   }
   delete c;
 }
@@ -624,7 +708,9 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
     if (!r) return fail(S2L_E_NO_REQUEST, "item %d: unknown request %lld", i, (long long)it.req_id);
     if (!seen.insert(it.req_id).second)
       return fail(S2L_E_INVAL, "item %d: request %lld repeated", i, (long long)it.req_id);
-    if (r->tier != S2L_TIER_GPU)
+    // reading Z19: tokens may arrive while a request is swapped out (a preempted
+    // request keeps receiving input); writing K/V needs the GPU tier
+    if (r->tier != S2L_TIER_GPU && it.n_kv != 0)
       return fail(S2L_E_STATE, "item %d: request %lld is swapped out", i, (long long)it.req_id);
     if (it.n_tokens < 0 || it.n_kv < 0 || it.kv_row < 0 || (it.n_tokens > 0 && !it.tokens))
       return fail(S2L_E_INVAL, "item %d: negative sizes or NULL tokens", i);
@@ -651,7 +737,7 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
   std::vector<s2l::AppendItemDev> dev_items;
   std::vector<int32_t> ids;
   std::vector<Request*> wait_in, written;
-  uint64_t quar_wait = 0;   // newest swap-out D2H still reading a block reallocated here
+  uint64_t quar_wait = 0, quar_wait_in = 0;   // newest D2H / H2D still touching a block reallocated here
   dev_items.reserve(n_items);
   ids.reserve((size_t)total_ids);
   int64_t row_begin = 0;
@@ -665,10 +751,10 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
     for (size_t j = held; j < r->blocks.size(); ++j) set_table(c, r->slot, (int64_t)j, r->blocks[j]);
     if (!c->host_only)
       for (size_t j = held; j < r->blocks.size(); ++j) {
-        uint64_t& q = c->quar[(size_t)r->blocks[j]];
-        quar_wait = std::max(quar_wait, q);
-        q = 0;
-        c->freed_use[(size_t)r->blocks[j]] = 0;
+        const size_t b = (size_t)r->blocks[j];
+        quar_wait = std::max(quar_wait, c->quar_out[b]);
+        quar_wait_in = std::max(quar_wait_in, c->quar_in[b]);
+        c->quar_out[b] = c->quar_in[b] = c->freed_use[b] = 0;
       }
     if (it.n_kv) {
       s2l::AppendItemDev d{};
@@ -687,7 +773,8 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
   }
   if (c->host_only) return S2L_OK;
   if (total_rows == 0) {
-    if (!ring_wait(c, c->copy_ring, c->compute, quar_wait)) return S2L_E_CUDA;
+    if (!ring_wait(c, c->out_ring, c->compute, quar_wait) || !ring_wait(c, c->in_ring, c->compute, quar_wait_in))
+      return S2L_E_CUDA;
     return flush_patches(c);
   }
 
@@ -701,10 +788,10 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
   memcpy(h + off_ids, ids.data(), ids.size() * sizeof(int32_t));
   int32_t n_patch = take_patches(c, (s2l::TablePatch*)(h + off_patch));
   if (!staging_upload_and_mark(c, s, bytes)) return S2L_E_CUDA;
-  if (!ring_wait(c, c->copy_ring, c->compute, quar_wait)) return S2L_E_CUDA;
+  if (!ring_wait(c, c->out_ring, c->compute, quar_wait) || !ring_wait(c, c->in_ring, c->compute, quar_wait_in))
+    return S2L_E_CUDA;
   for (Request* r : wait_in) {
-    if (!ring_wait(c, c->copy_ring, c->compute, r->swap_in_seq)) return S2L_E_CUDA;
-    r->swap_in_seq = 0;
+    if (!ring_wait(c, c->in_ring, c->compute, r->swap_in_seq)) return S2L_E_CUDA;
   }
   char* dv = (char*)c->ring.dev[s];
   std::pair<cudaEvent_t, cudaEvent_t> tp{};
@@ -782,8 +869,7 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
   for (int32_t i = 0; i < n_items; ++i) {
     Request* r = find(c, items[i].req_id);
     if (r->swap_in_seq) {
-      if (!ring_wait(c, c->copy_ring, c->compute, r->swap_in_seq)) return S2L_E_CUDA;
-      r->swap_in_seq = 0;
+      if (!ring_wait(c, c->in_ring, c->compute, r->swap_in_seq)) return S2L_E_CUDA;
     }
   }
   const int32_t G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
@@ -918,11 +1004,23 @@ s2l_status s2l_free_blocks(s2l_ctx* c, int64_t* gpu_free, int64_t* cpu_free) {
   return S2L_OK;
 }
 
+s2l_status s2l_set_swap_in_stream(s2l_ctx* c, void* stream) {
+  if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
+  if (c->host_only) return fail(S2L_E_STATE, "host-only context has no device");
+  if (!stream) return fail(S2L_E_INVAL, "stream is NULL");
+  CK(cudaStreamSynchronize(c->copy_in));
+  if (c->own_copy_in) cudaStreamDestroy(c->copy_in);
+  c->copy_in = (cudaStream_t)stream;
+  c->own_copy_in = false;
+  return S2L_OK;
+}
+
 s2l_status s2l_sync(s2l_ctx* c) {
   if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
   if (c->host_only) return S2L_OK;
   CK(cudaStreamSynchronize(c->compute));
   CK(cudaStreamSynchronize(c->copy));
+  CK(cudaStreamSynchronize(c->copy_in));
   return c->sticky;
 }
 

@@ -7,7 +7,7 @@ symmetric cost") to make room for each step.
 This is a harness driver, not the paper's scheduler (two-phase scheduling and the
 recompute-vs-swap policy are P:L134-L237): requests are stepped in
 round-robin order under a token budget (2048-8192 tokens per batch), and the victims
-of a swap-out are the least recently stepped GPU-resident requests.  All state it plans with
+of a swap-out are the GPU-resident requests whose next round-robin turn is furthest away.  All state it plans with
 comes from the library's own queries (`query`, `free_blocks`), so the same driver runs on a
 device context (bench) and on a host-only context (CPU tests, where `tests/` replays its op
 log through the oracle).
@@ -101,15 +101,16 @@ def working_set_blocks(plans, k: int) -> int:
 
 
 class PressureDriver:
-    """Round-robin stepping + LRU swap residency over one context (`ctx`: s2l.Context).
+    """Round-robin stepping + furthest-next-use swap residency over one context.
 
     Loop (see `run`): sel = plan(); prepare(sel); while sel: items(sel) -> caller enqueues
     append + attention; finish(sel); nxt = plan(); prepare(nxt, protect=sel); sel = nxt.
     Every library call is appended to `log` as (op, args, result) for the oracle replay.
     """
 
-    def __init__(self, ctx, plans, k: int, budget: int):
+    def __init__(self, ctx, plans, k: int, budget: int, evict_ahead: bool = True):
         self.ctx, self.k, self.budget = ctx, k, budget
+        self.evict_ahead = evict_ahead
         self.plans = {p.rid: p for p in plans}
         self.next_work = {p.rid: 0 for p in plans}
         self.last_step = {p.rid: -1 for p in plans}
@@ -131,9 +132,9 @@ class PressureDriver:
     def live(self):
         return [r for r in self.order if r in self.plans and self.next_work[r] < len(self.plans[r].work)]
 
-    def plan(self):
+    def plan(self, peek: bool = False):
         """Next step's requests: round-robin from the cursor, one work item each, until the
-        token budget is reached (the first request is always taken)."""
+        token budget is reached (the first request is always taken).  peek: do not advance."""
         live = self.live()
         if not live:
             return []
@@ -148,50 +149,81 @@ class PressureDriver:
                 break
             sel.append(r)
             used += n
-        self.cursor = sel[-1] + 1
+        if not peek:
+            self.cursor = sel[-1] + 1
         return sel
 
     def _blocks(self, n):
         return -(-n // self.k)
 
+    def _need(self, sel, info):
+        """GPU blocks the step's requests still need: swap-ins + blocks their appends take."""
+        need = 0
+        for r in sel:
+            q = info[r]
+            w = self.plans[r].work[self.next_work[r]]
+            need += max(0, self._blocks(q["num_computed"] + w.n_kv) - q["num_blocks"])
+            if q["tier"] == TIER_CPU:
+                need += q["num_blocks"]
+        return need
+
+    def _pick(self, need, free_gpu, keep, avoid):
+        """GPU requests outside `keep` (preferring those outside `avoid`) to swap out so that
+        free_gpu >= need, those whose next round-robin turn is furthest away first (Belady's
+        choice: the round-robin order is the future access order; LRU would evict exactly the
+        requests due next).  Returns (victims, free_gpu after them); None if impossible."""
+        if free_gpu >= need:
+            return [], free_gpu
+        live = self.live()
+        pos = {r: i for i, r in enumerate(live)}
+        start = 0
+        while start < len(live) and live[start] < self.cursor:
+            start += 1
+        cands = []
+        for r in self.order:
+            if r in keep or r not in self.plans:
+                continue
+            q = self.ctx.query(r)
+            if q["tier"] == TIER_GPU and q["num_blocks"] > 0:
+                dist = (pos[r] - start) % len(live) if r in pos else len(live)
+                cands.append((r in avoid, -dist, r, q["num_blocks"]))
+        cands.sort()
+        victims = []
+        for _, _, r, nb in cands:
+            if free_gpu >= need:
+                break
+            victims.append(r)
+            free_gpu += nb
+        return (victims, free_gpu) if free_gpu >= need else None
+
     def prepare(self, sel, protect=()):
         """Updates first (LCP invalidation on either tier), then make room: swap
-        out least recently stepped GPU requests outside sel (and, if possible, outside
-        `protect` = the step still computing), swap in the members of sel on the CPU tier."""
+        out GPU requests outside sel (and, if possible, outside `protect` = the step still
+        computing) and swap in the members of sel on the CPU tier.  With evict_ahead the same
+        swap-out call also makes room for the step after sel: its D2H then runs while this
+        step and the next compute, and (reading Z9) the ids it releases are allocated only
+        after every other free id, so the next step's appends and swap-ins avoid them."""
         for r in sel:
             w = self.plans[r].work[self.next_work[r]]
             if w.new_input is not None:
                 res = self.ctx.invalidate_lcp(r, w.new_input)
                 self.log.append(("invalidate", (r, w.new_input), res))
         info = {r: self.ctx.query(r) for r in sel}
-        need = 0
-        to_in = []
-        for r in sel:
-            q = info[r]
-            w = self.plans[r].work[self.next_work[r]]
-            need += self._blocks(q["num_computed"] + w.n_kv) - q["num_blocks"]
-            if q["tier"] == TIER_CPU:
-                need += q["num_blocks"]
-                to_in.append(r)
+        need = self._need(sel, info)
+        to_in = [r for r in sel if info[r]["tier"] == TIER_CPU]
         free_gpu, _ = self.ctx.free_blocks()
-        victims = []
-        if free_gpu < need:
-            sel_set, prot = set(sel), set(protect)
-            cands = []
-            for r in self.order:
-                if r in sel_set or r not in self.plans:
-                    continue
-                q = self.ctx.query(r)
-                if q["tier"] == TIER_GPU and q["num_blocks"] > 0:
-                    cands.append((r in prot, self.last_step[r], r, q["num_blocks"]))
-            cands.sort()
-            for _, _, r, nb in cands:
-                if free_gpu >= need:
-                    break
-                victims.append(r)
-                free_gpu += nb
-            if free_gpu < need:
-                raise RuntimeError(f"step {self.step}: cannot make room ({free_gpu} < {need})")
+        got = self._pick(need, free_gpu, set(sel), set(protect))
+        if got is None:
+            raise RuntimeError(f"step {self.step}: cannot make room for {need} blocks")
+        victims, free_after = got
+        if self.evict_ahead:
+            nxt = [r for r in self.plan(peek=True) if r not in sel]
+            if nxt:
+                info2 = {r: self.ctx.query(r) for r in nxt}
+                more = self._pick(need + self._need(nxt, info2), free_after,
+                                  set(sel) | set(nxt) | set(victims), set(protect))
+                if more is not None:                   # best effort
+                    victims += more[0]
         if victims:
             b = self.ctx.swap_out(victims)
             self.log.append(("swap_out", tuple(victims), b))
@@ -255,12 +287,14 @@ class PressureDriver:
 
 
 class SwapTimer:
-    """Context wrapper around the swap calls.  `serial=True` drains both streams before and
-    after every swap (the no-overlap baseline); `copy_stream` (the context's copy stream)
-    enables per-call CUDA events, read back with `copy_ms()` after synchronisation."""
+    """Context wrapper around the swap calls.  `serial=True` drains all streams before and
+    after every swap (the no-overlap baseline); `copy_stream` / `swap_in_stream` (the
+    context's swap-out / swap-in streams) enable per-call CUDA events, read back with
+    `copy_ms()` after synchronisation."""
 
-    def __init__(self, ctx, serial: bool = False, copy_stream=None):
-        self.ctx, self.serial, self.cs = ctx, serial, copy_stream
+    def __init__(self, ctx, serial: bool = False, copy_stream=None, swap_in_stream=None):
+        self.ctx, self.serial = ctx, serial
+        self.streams = {"out": copy_stream, "in": swap_in_stream}
         self.events = []
 
     def __getattr__(self, name):
@@ -269,14 +303,14 @@ class SwapTimer:
     def _swap(self, fn, rids, kind):
         if self.serial:
             self.ctx.sync()
-        ev = None
-        if self.cs is not None:
+        ev, cs = None, self.streams[kind]
+        if cs is not None:
             import torch
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            ev[0].record(self.cs)
+            ev[0].record(cs)
         b = fn(rids)
         if ev is not None:
-            ev[1].record(self.cs)
+            ev[1].record(cs)
             self.events.append((kind, b, ev))
         if self.serial:
             self.ctx.sync()

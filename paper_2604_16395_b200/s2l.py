@@ -51,7 +51,7 @@ class ReqInfo(C.Structure):
 EXPORTS = ["s2l_block_bytes", "s2l_create", "s2l_create_host_only", "s2l_destroy", "s2l_new_request",
            "s2l_release_request", "s2l_preempt_recompute", "s2l_append_chunk", "s2l_invalidate_lcp",
            "s2l_prefill_batch", "s2l_swap_out", "s2l_swap_in", "s2l_query", "s2l_block_table",
-           "s2l_free_blocks", "s2l_sync", "s2l_kernel_launches", "s2l_set_timing", "s2l_timing_read",
+           "s2l_free_blocks", "s2l_sync", "s2l_set_swap_in_stream", "s2l_kernel_launches", "s2l_set_timing", "s2l_timing_read",
            "s2l_last_error", "s2l_version"]
 
 _libs: dict = {}
@@ -84,6 +84,7 @@ def lib(path: str | None = None) -> C.CDLL:
         "s2l_block_table": (I32, [VP, I64, P(I32), I64, P(I64)]),
         "s2l_free_blocks": (I32, [VP, P(I64), P(I64)]),
         "s2l_sync": (I32, [VP]),
+        "s2l_set_swap_in_stream": (I32, [VP, VP]),
         "s2l_kernel_launches": (I64, [VP]),
         "s2l_set_timing": (I32, [VP, I32]),
         "s2l_timing_read": (I32, [VP, P(C.c_double), P(I64), P(C.c_double), P(I64)]),
@@ -128,7 +129,7 @@ class Context:
     """One libs2l context (one device).  Methods raise S2LError on a non-OK status."""
 
     def __init__(self, cfg: Config, gpu_pool=None, cpu_pool=None, compute_stream=None,
-                 copy_stream=None, host_only=False, lib_path=None):
+                 copy_stream=None, host_only=False, lib_path=None, swap_in_stream=None):
         self._L = lib(lib_path)
         self.cfg = cfg
         self.host_only = host_only
@@ -140,7 +141,9 @@ class Context:
                                     _stream(compute_stream), _stream(copy_stream), C.byref(h))
         self._check(st)
         self._h = h
-        self._keep = (gpu_pool, cpu_pool, compute_stream, copy_stream)
+        self._keep = (gpu_pool, cpu_pool, compute_stream, copy_stream, swap_in_stream)
+        if swap_in_stream is not None:
+            self._check(self._L.s2l_set_swap_in_stream(h, _stream(swap_in_stream)))
 
     def _check(self, st):
         if st != OK:

@@ -192,6 +192,11 @@ class Twin:
         assert self.ora.release(rid) == O.OK
         self._same_state([])
 
+    def preempt_recompute(self, rid):
+        self.lib.preempt_recompute(rid)
+        assert self.ora.preempt_recompute(rid) == O.OK
+        self._same_state([rid])
+
     def invalidate_lcp(self, rid, new):
         a = self.lib.invalidate_lcp(rid, new)
         st, p, inv = self.ora.invalidate_lcp(rid, new)

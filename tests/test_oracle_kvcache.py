@@ -229,7 +229,8 @@ def test_invalidate_while_swapped_then_resume():
     assert kv.block_table(0) == [0, 1, 2] and kv.info(0)["tier"] == O.CPU
     assert kv.free_counts() == (16, 13)
     assert kv.swap_in([0])[0] == O.OK
-    assert kv.info(0)["num_computed"] == 9 and kv.block_table(0) == [0, 1, 2]
+    # Z9: ids 0-4 were released by the swap-out (cooling), so free ids 5.. go first
+    assert kv.info(0)["num_computed"] == 9 and kv.block_table(0) == [5, 6, 7]
     # fully invalidated while swapped -> fresh GPU request with no blocks
     kv.swap_out([0])
     st, p, inval = kv.invalidate_lcp(0, [5])

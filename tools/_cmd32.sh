@@ -1,0 +1,3 @@
+python -m paper_2604_16395_b200.build --force > /dev/null
+C4_TIMELINE=1 timeout -s KILL 900 python tools/bench_workloads.py c4mix > gpurun_out/c4mix.jsonl 2> gpurun_out/c4mix.err; cat gpurun_out/c4mix.jsonl; tail -40 gpurun_out/c4mix.err
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -q -x -k "c4_pressure or hazards" 2>&1 | tail -2

@@ -163,7 +163,7 @@ def c4():
 def c4mix(n_req=128, budget=8192, L=None, check=True):
     """C4 memory-pressure mix (BJ:L10): 128 append / update requests (paper_2604_16395_b200.
     pressure recipe) through one context whose GPU pool holds 50% of the working set; the
-    round-robin driver swaps least recently stepped requests out to pinned host memory and
+    round-robin driver swaps the requests due furthest in the future out to pinned host memory and
     back in.  Each step = one append of all layers' K/V + one attention launch per layer.
     Runs the stream twice on fresh contexts: `serial` (host waits for every swap: no
     overlap) and `overlap` (swaps for step s+1 on the copy stream while step s computes).
@@ -190,7 +190,7 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
     src_v = torch.randn(L, R, geo_hkv, D, generator=g, device="cuda").to(torch.bfloat16)
     src_q = torch.randn(R, geo_hq, D, generator=g, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(src_q)
-    cs = torch.cuda.Stream()
+    cs, cs_in = torch.cuda.Stream(), torch.cuda.Stream()
     res = {"workload": "C4 memory-pressure mix (BJ:L10)", "requests": n_req, "L": L, "m_block": mb,
            "working_set_blocks": ws, "gpu_pool_blocks": ng, "cpu_pool_blocks": ncpu, "budget": budget}
     flops_total = 0.0
@@ -200,10 +200,10 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
             cfg_big = s2l.make_config(L, geo_hq, geo_hkv, D, K, ws, 0, max_requests=n_req,
                                       max_blocks_per_request=16384 // K)
             big = torch.empty(ws * mb // 2, dtype=torch.bfloat16, device="cuda")
-            ctx = s2l.Context(cfg_big, big, None, torch.cuda.current_stream(), cs)
+            ctx = s2l.Context(cfg_big, big, None, torch.cuda.current_stream(), cs, swap_in_stream=cs_in)
         else:
-            ctx = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), cs)
-        wrap = pressure.SwapTimer(ctx, serial=(mode == "serial"), copy_stream=cs)
+            ctx = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), cs, swap_in_stream=cs_in)
+        wrap = pressure.SwapTimer(ctx, serial=(mode == "serial"), copy_stream=cs, swap_in_stream=cs_in)
         drv = pressure.PressureDriver(wrap, plans, K, budget)
         step_ev = []
         segs, snaps, flops = {}, [], [0.0]
@@ -239,14 +239,28 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
         t0 = time.perf_counter()
         e0.record()
         steps = drv.run(ex)
-        ev = torch.cuda.Event()
-        ev.record(cs)
-        torch.cuda.current_stream().wait_event(ev)
+        for st in (cs, cs_in):
+            ev = torch.cuda.Event()
+            ev.record(st)
+            torch.cuda.current_stream().wait_event(ev)
         e1.record()
         torch.cuda.synchronize()
         host_s = time.perf_counter() - t0
         ms = e0.elapsed_time(e1)
         flops_total = flops[0]
+        if mode == "overlap" and os.environ.get("C4_TIMELINE"):
+            # timeline of steps 100..111 relative to the run start (stderr)
+            lo, hi = 100, 112
+            sys.stderr.write("step  compute[start,end]  (ms from run start)\n")
+            for i in range(lo, min(hi, len(step_ev))):
+                a0, a1 = step_ev[i]
+                sys.stderr.write(f"  {i:4d} {e0.elapsed_time(a0):9.2f} {e0.elapsed_time(a1):9.2f}\n")
+            t_lo = e0.elapsed_time(step_ev[lo][0]) if len(step_ev) > lo else 0
+            t_hi = e0.elapsed_time(step_ev[min(hi, len(step_ev)) - 1][1]) if len(step_ev) > lo else 0
+            for kind, b_, (c0, c1) in wrap.events:
+                t0c, t1c = e0.elapsed_time(c0), e0.elapsed_time(c1)
+                if t1c >= t_lo and t0c <= t_hi:
+                    sys.stderr.write(f"  copy {kind:3s} {t0c:9.2f} {t1c:9.2f}  {b_ / 1e6:8.1f} MB\n")
         busy = sum(a.elapsed_time(b) for a, b in step_ev)
         gaps = sum(step_ev[i][1].elapsed_time(step_ev[i + 1][0]) for i in range(len(step_ev) - 1))
         cm = wrap.copy_ms()
