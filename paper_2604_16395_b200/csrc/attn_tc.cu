@@ -41,6 +41,10 @@
 #ifndef S2L_POLY_PAIRS
 #define S2L_POLY_PAIRS 2
 #endif
+#ifndef S2L_SPLIT_S
+#define S2L_SPLIT_S 1      // v2: 1 = S(j+1) in two N=64 halves, keys 64-127 issued as soon as the
+                           // softmax has read S(j)'s upper half (overlaps the softmax)
+#endif
 #ifndef S2L_PQ
 #define S2L_PQ 0           // v2: 1 = P handed to the MMA warp in quarters (32 keys) instead of halves
 #endif
@@ -714,7 +718,7 @@ constexpr uint32_t WOFF_BAR = WOFF_RING + WNST * kTileBytes;
 // while the softmax still computes the second half.
 constexpr uint32_t WB_QF = 0, WB_RF = 1, WB_RE = 1 + WNST, WB_SF = 1 + 2 * WNST, WB_PF = WB_SF + 2,
                    WB_PH = WB_PF + 2, WB_OF = WB_PH + 2, WB_QE = WB_OF + 2, WB_PQ = WB_QE + 1,
-                   WNBARS = WB_PQ + 8;
+                   WB_SR = WB_PQ + 8, WB_SH = WB_SR + 2, WNBARS = WB_SH + 2;
 constexpr uint32_t WOFF_TMEM = WOFF_BAR + WNBARS * 8;
 constexpr uint32_t SMEM = WOFF_TMEM + 16 + 1024;
 }  // namespace v2
@@ -815,6 +819,10 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       mbar_init(bar(WB_OF + i), 1);
     }
     for (int q = 0; q < 8; ++q) mbar_init(bar(WB_PQ + q), 128);
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(bar(WB_SR + q), 128);   // split S: softmax q has read S keys 64-127
+      mbar_init(bar(WB_SH + q), 1);     // split S: S(j+1) keys 64-127 computed
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
@@ -979,6 +987,50 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       issue_s(0, kslot);
       issue_s(1, kslot);
       mma_commit_elect(bar(WB_RE + kslot));
+#if S2L_SPLIT_S
+      // S_i(j+1) = Q_i K_{j+1}^T in two N = 64 halves.  Keys 64-127 land in S columns 64-127,
+      // which P_i(j) (bf16, columns 0-63) does not use: they are issued as soon as softmax i
+      // has read S_i(j)'s upper half, i.e. while it still works; keys 0-63 overwrite P_i(j)'s
+      // columns and follow PV_i(j) on the in-order tensor pipe.
+      constexpr uint32_t idesc_h = idesc_bf16(kBM, 64, 0, 0);
+      auto issue_s_half = [&](int i, uint32_t ks, int h, uint32_t done) {
+        const uint64_t kd = dk0 + ((ks * kTileBytes + h * 64 * 128) >> 4);   // key row 64h
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const uint32_t off = ((kk >> 2) * kAtom + (kk & 3) * 32) >> 4;
+          mma_ss_elect(tmem + i * 128 + h * 64, dq[i] + off, kd + off, idesc_h, kk > 0);
+        }
+        mma_commit_elect(done);
+      };
+      for (int32_t j = 0; j < nT; ++j) {
+        const uint32_t vslot = next_full();
+        const bool more = j + 1 < nT;
+        uint32_t knext = 0;
+        if (more) {
+          knext = next_full();
+          mbar_wait(bar(WB_SR + 0), j & 1);
+          tc_fence_after();
+          issue_s_half(0, knext, 1, bar(WB_SH + 0));
+        }
+        issue_pv(0, vslot, j);
+        if (more) issue_s_half(0, knext, 0, bar(WB_SF + 0));
+        else mma_commit_elect(bar(WB_OF + 0));
+        if (more) {
+          mbar_wait(bar(WB_SR + 1), j & 1);
+          tc_fence_after();
+          issue_s_half(1, knext, 1, bar(WB_SH + 1));
+        }
+        issue_pv(1, vslot, j);
+        mma_commit_elect(bar(WB_RE + vslot));
+        if (more) {
+          issue_s_half(1, knext, 0, bar(WB_SF + 1));
+          mma_commit_elect(bar(WB_RE + knext));
+        } else {
+          mma_commit_elect(bar(WB_OF + 1));
+        }
+      }
+      if (false)
+#endif
       for (int32_t j = 0; j < nT; ++j) {
         const uint32_t vslot = next_full();
         issue_pv(0, vslot, j);
@@ -1017,7 +1069,11 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     for (int32_t j = 0; j < nT; ++j) {
       const bool tr = (warp & 3) == 0 && lane == 0;
       if (tr) TRACE(20, i, j);
+#if S2L_SPLIT_S
+      mbar_wait(j == 0 ? bar(WB_SF + i) : bar(WB_SH + i), j == 0 ? 0 : ((j - 1) & 1));
+#else
       mbar_wait(bar(WB_SF + i), j & 1);
+#endif
       tc_fence_after();
       if (tr) TRACE(21, i, j);
 #ifdef S2L_EXP_MMA_ONLY   // timing experiment only: tensor-core / TMA pipeline without softmax
@@ -1053,6 +1109,25 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       float mt[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) mt[q] = -INFINITY;
+#if S2L_SPLIT_S
+      // upper half first: once it is in registers the MMA warp may compute S(j+1)'s upper half
+      tmem_ld32(tS + 64, sv + 64);
+      tmem_ld32(tS + 96, sv + 96);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(bar(WB_SR + i));
+      if (masked_tile) { max32<true>(sv + 64, vis, 64, mt); max32<true>(sv + 96, vis, 96, mt); }
+      else { max32<false>(sv + 64, vis, 64, mt); max32<false>(sv + 96, vis, 96, mt); }
+      if (j > 0) {
+        mbar_wait(bar(WB_SF + i), j & 1);              // lower half of S(j)
+        tc_fence_after();
+      }
+      tmem_ld32(tS, sv);
+      tmem_ld32(tS + 32, sv + 32);
+      tmem_wait_ld();
+      if (masked_tile) { max32<true>(sv, vis, 0, mt); max32<true>(sv + 32, vis, 32, mt); }
+      else { max32<false>(sv, vis, 0, mt); max32<false>(sv + 32, vis, 32, mt); }
+#else
       tmem_ld32(tS, sv);
       tmem_ld32(tS + 32, sv + 32);
       tmem_wait_ld();
@@ -1063,6 +1138,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       tmem_wait_ld();
       if (masked_tile) { max32<true>(sv + 64, vis, 64, mt); max32<true>(sv + 96, vis, 96, mt); }
       else { max32<false>(sv + 64, vis, 64, mt); max32<false>(sv + 96, vis, 96, mt); }
+#endif
       float mx = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])), fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7])));
       mx *= sl2;
       if (tr) TRACE(22, i, j);
