@@ -268,8 +268,8 @@ def measure_swap(dev_index, link):
     mb = s2l.block_bytes(cfg)
     gpool = torch.empty((nblk + 64) * mb // 2, dtype=torch.bfloat16, device=f"cuda:{dev_index}")
     cpool = torch.empty((nblk + 64) * mb // 2, dtype=torch.bfloat16).pin_memory()
-    copy_s = torch.cuda.Stream()
-    ctx = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), copy_s)
+    copy_s, in_s = torch.cuda.Stream(), torch.cuda.Stream()   # swap-out / swap-in streams
+    ctx = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), copy_s, swap_in_stream=in_s)
     # four requests of 128 blocks (2048 tokens) each, interleaved so ids are scattered
     rids = [0, 1, 2, 3]
     kv = torch.zeros(L, 4 * 512, H_KV, D, dtype=torch.bfloat16, device=f"cuda:{dev_index}")
@@ -280,17 +280,18 @@ def measure_swap(dev_index, link):
     ctx.sync()
     res = {"m_block_bytes": mb, "blocks": nblk}
     for _ in range(2):  # warm-up + measure
-        t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
-        t2 = torch.cuda.Event(enable_timing=True)
+        t0, t1, t2, t3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
         torch.cuda.synchronize()
         t0.record(copy_s)
         b_out = ctx.swap_out(rids)
         t1.record(copy_s)
+        ctx.sync()
+        t2.record(in_s)
         b_in = ctx.swap_in(rids)
-        t2.record(copy_s)
+        t3.record(in_s)
         ctx.sync()
         torch.cuda.synchronize()
-    out_ms, in_ms = t0.elapsed_time(t1), t1.elapsed_time(t2)
+    out_ms, in_ms = t0.elapsed_time(t1), t2.elapsed_time(t3)
     res.update(out_gbs=b_out / out_ms / 1e6, in_gbs=b_in / in_ms / 1e6, bytes_each_way=b_out)
     res["out_frac_link"] = res["out_gbs"] / link["d2h"]
     res["in_frac_link"] = res["in_gbs"] / link["h2d"]
@@ -517,6 +518,15 @@ def main():
                      "append_ms_per_step": tinfo["append_ms"] / args.steps},
         "clocks": clocks,
     }
+    # a3 append kernel against the HBM roofline: K and V rows read once and written once
+    # (8 KiB per token per layer at Llama-3-8B: 2 x 2 x h_kv x d x 2 B)
+    app_bytes = 2 * 2 * NREQ * TOTAL * H_KV * D * 2          # per step (all chunks)
+    app_ms = tinfo["append_ms"] / args.steps
+    if app_ms > 0:
+        line["append"] = {"bound": "hbm", "achieved": app_bytes / (app_ms * 1e-3) / 1e9, "unit": "GB/s",
+                          "peak": pk.get("hbm"), "frac": (app_bytes / (app_ms * 1e-3) / 1e9) / pk["hbm"]
+                          if pk.get("hbm") else None, "bytes_per_step": app_bytes,
+                          "launches": tinfo.get("append_launches")}
     # parity gather (NCCL) after timing
     line["parity"] = parity_check(S, data, rank, world, dist)
 

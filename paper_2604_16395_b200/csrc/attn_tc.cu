@@ -39,11 +39,14 @@
 #define S2L_EXP_MODE 0   // 0: f32 MUFU.EX2 + FMA-pipe polynomial share; 1: MUFU.EX2 f16x2
 #endif
 #ifndef S2L_POLY_PAIRS
-#define S2L_POLY_PAIRS 2
+#define S2L_POLY_PAIRS 1
 #endif
 #ifndef S2L_SPLIT_S
 #define S2L_SPLIT_S 1      // v2: 1 = S(j+1) in two N=64 halves, keys 64-127 issued as soon as the
                            // softmax has read S(j)'s upper half (overlaps the softmax)
+#endif
+#ifndef S2L_SM64
+#define S2L_SM64 1         // v2: exponentials in 64-column chunks, polynomial pairs spread evenly
 #endif
 #ifndef S2L_PQ
 #define S2L_PQ 0           // v2: 1 = P handed to the MMA warp in quarters (32 keys) instead of halves
@@ -590,6 +593,38 @@ __device__ __forceinline__ float2 chunk_p(const uint32_t (&v)[32], float2 acc, i
   float2 a[4] = {acc, make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
+    a[c & 3] = __fadd2_rn(a[c & 3], x[c]);
+    pk[c] = pack_p(x[c].x, x[c].y);
+  }
+  return __fadd2_rn(__fadd2_rn(a[0], a[1]), __fadd2_rn(a[2], a[3]));
+}
+// 64-column variant (32 pairs per phase, the FMA-pipe polynomial spread over every 8/kPolyPer8-th
+// pair): more independent work per phase for the single softmax warp of an SMSP
+// (tools/micro/softmax_bench2.cu: ~10 % fewer cycles per tile than 32-column phases).
+template <bool kMasked, int kPolyPer8>
+__device__ __forceinline__ float2 chunk_p64(const uint32_t* v, float2 acc, int vis, int base,
+                                            float2 sc2, float2 nm2, uint32_t (&pk)[32]) {
+  float2 x[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    float s0 = __uint_as_float(v[2 * c]), s1 = __uint_as_float(v[2 * c + 1]);
+    if (kMasked) {
+      if (base + 2 * c > vis) s0 = -INFINITY;
+      if (base + 2 * c + 1 > vis) s1 = -INFINITY;
+    }
+    x[c] = __ffma2_rn(make_float2(s0, s1), sc2, nm2);
+  }
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const bool poly = !kMasked && kPolyPer8 > 0 &&
+                      ((kPolyPer8 == 1 || kPolyPer8 == 2 || kPolyPer8 == 4) ? (c % (8 / (kPolyPer8 ? kPolyPer8 : 1))) == 0
+                                                                             : (c & 7) < kPolyPer8);
+    if (poly) x[c] = exp2_poly2(x[c]);
+    else x[c] = make_float2(fast_exp2(x[c].x), fast_exp2(x[c].y));
+  }
+  float2 a[4] = {acc, make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
     a[c & 3] = __fadd2_rn(a[c & 3], x[c]);
     pk[c] = pack_p(x[c].x, x[c].y);
   }
@@ -1169,6 +1204,21 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
       const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_use, -m_use);
       float2 acc = make_float2(0.f, 0.f);
+#if S2L_SM64
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t pk[32];
+        acc = masked_tile ? chunk_p64<true, 0>(sv + 64 * hh, acc, vis, 64 * hh, sc2, nm2, pk)
+                          : chunk_p64<false, kPolyPairsPer8>(sv + 64 * hh, acc, vis, 64 * hh, sc2, nm2, pk);
+        tmem_st16(tS + 32 * hh, pk);
+        tmem_st16(tS + 32 * hh + 16, pk + 16);
+        tmem_wait_st();                // keys 64hh .. 64hh+63 of P are in TMEM
+        tc_fence_before();
+        mbar_arrive(bar((hh == 0 ? WB_PF : WB_PH) + i));
+        if (tr) TRACE(hh == 0 ? 23 : 24, i, j);
+      }
+      if (false)
+#endif
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
         uint32_t pk[16];

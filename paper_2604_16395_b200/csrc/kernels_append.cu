@@ -38,10 +38,14 @@ __device__ __forceinline__ int32_t find_item(const AppendItemDev* items, int32_t
 // of the row ([h_kv][d] contiguous, so the warp reads the row coalesced) and stores them to
 // (block, slot) of every kv head (each head's d*2 bytes contiguous in the pool).  All loads of
 // a warp are issued before its stores.  blockIdx.y = layer * 2 + (0: K, 1: V).
-constexpr int kRowsPerWarp = 2;
+#ifndef S2L_APPEND_ROWS
+#define S2L_APPEND_ROWS 4
+#endif
+constexpr int kRowsPerWarp = S2L_APPEND_ROWS;
 
 // kMaxVecPerLane >= vectors per lane per row (vpt/32: 4 at Llama-3 h_kv 8, d 128).
-template <int kMaxVecPerLane>
+// kVpr = d/8 vectors per head row when known at compile time (16 at d = 128), else 0.
+template <int kMaxVecPerLane, int kVpr>
 __global__ void __launch_bounds__(256) append_kernel(
     const AppendItemDev* __restrict__ items_g, int32_t n_items, int64_t total_rows,
     const int32_t* __restrict__ ids_g, int32_t n_ids, const TablePatch* __restrict__ patches,
@@ -99,8 +103,9 @@ __global__ void __launch_bounds__(256) append_kernel(
       for (int u = 0; u < kMaxVecPerLane; ++u) {
         const int32_t gi = lane + 32 * u;
         if (gi < vpt) {
-          const int32_t head = gi / vec_per_row, vec = gi - head * vec_per_row;
-          pool[dst_row[rr] + (int64_t)head * kb * vec_per_row + vec] = val[rr][u];
+          const int32_t vpr = kVpr ? kVpr : vec_per_row;
+          const int32_t head = gi / vpr, vec = gi - head * vpr;
+          pool[dst_row[rr] + (int64_t)head * kb * vpr + vec] = val[rr][u];
         }
       }
     }
@@ -132,15 +137,17 @@ cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t
   if (blocks < 1) blocks = 1;
   if (blocks > 65535) blocks = 65535;
   dim3 grid((unsigned)blocks, g.L * 2);
-#define S2L_APPEND(MAXV)                                                                       \
-  append_kernel<MAXV><<<grid, 256, 0, st>>>(items, n_items, total_rows, ids, n_ids, patches,  \
+#define S2L_APPEND(MAXV, VPR)                                                                  \
+  append_kernel<MAXV, VPR><<<grid, 256, 0, st>>>(items, n_items, total_rows, ids, n_ids, patches, \
                                             n_patches, table, (const uint4*)k, (const uint4*)v, \
                                             kv_rows, (uint4*)pool, g.L, g.h_kv, vec_per_row,    \
                                             kb_log2)
-  if (vpt <= 32) S2L_APPEND(1);
-  else if (vpt <= 128) S2L_APPEND(4);
-  else if (vpt <= 512) S2L_APPEND(16);
-  else if (vpt <= 2048) S2L_APPEND(64);
+  if (vec_per_row == 16 && vpt <= 128) S2L_APPEND(4, 16);          // d = 128, h_kv <= 8
+  else if (vec_per_row == 16 && vpt <= 512) S2L_APPEND(16, 16);
+  else if (vpt <= 32) S2L_APPEND(1, 0);
+  else if (vpt <= 128) S2L_APPEND(4, 0);
+  else if (vpt <= 512) S2L_APPEND(16, 0);
+  else if (vpt <= 2048) S2L_APPEND(64, 0);
   else return cudaErrorInvalidValue;
 #undef S2L_APPEND
   return cudaGetLastError();

@@ -132,8 +132,8 @@ def c4():
                 continue
             gp = torch.empty((2 * B + 8) * mb // 2, dtype=torch.bfloat16, device="cuda")
             cp = torch.empty((2 * B + 8) * mb // 2, dtype=torch.bfloat16).pin_memory()
-            cs = torch.cuda.Stream()
-            ctx = s2l.Context(cfg, gp, cp, torch.cuda.current_stream(), cs)
+            cs, cs_in = torch.cuda.Stream(), torch.cuda.Stream()     # swap-out / swap-in streams
+            ctx = s2l.Context(cfg, gp, cp, torch.cuda.current_stream(), cs, swap_in_stream=cs_in)
             # two interleaved requests -> scattered ids for request 0 (B blocks)
             kv = torch.zeros(L, 32, 8, 128, dtype=torch.bfloat16, device="cuda")
             ctx.new_request(0, np.zeros(B * 16, np.int32))
@@ -145,14 +145,16 @@ def c4():
             nblk = ctx.query(0)["num_blocks"]
             best = {}
             for _ in range(3):
-                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
                 e0.record(cs)
                 b_out = ctx.swap_out([0])
                 e1.record(cs)
-                ctx.swap_in([0])
-                e2.record(cs)
                 ctx.sync()
-                for key, ms in (("out", e0.elapsed_time(e1)), ("in", e1.elapsed_time(e2))):
+                e2.record(cs_in)
+                ctx.swap_in([0])
+                e3.record(cs_in)
+                ctx.sync()
+                for key, ms in (("out", e0.elapsed_time(e1)), ("in", e2.elapsed_time(e3))):
                     best[key] = max(best.get(key, 0), b_out / (ms * 1e-3) / 1e9)
             out["cells"].append({"L": L, "m_block": mb, "blocks": nblk, "bytes": b_out, "out_gbs": best["out"],
                                  "in_gbs": best["in"], "out_frac": best["out"] / link["d2h"], "in_frac": best["in"] / link["h2d"]})
