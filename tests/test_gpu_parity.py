@@ -631,3 +631,91 @@ def test_c4_pressure_driver_on_device(serial):
         want_v = np.concatenate([vh[:, a:a + m] for a, m in seg], axis=1)
         assert np.array_equal(got[:, :, 0], np.transpose(want_k, (1, 0, 2, 3)))
         assert np.array_equal(got[:, :, 1], np.transpose(want_v, (1, 0, 2, 3)))
+
+
+@pytest.mark.parametrize("policy,preemption", [("FCFS", "cost"), ("LCAS", "swap"), ("MCPS", "recompute")])
+def test_streaming_scheduler_on_device(policy, preemption):
+    """NEXT-3 at the parity bar: the two-phase scheduler (paper_2604_16395_b200.scheduler)
+    drives a device context through a short synthetic crawler / ANNS mix under a GPU pool small
+    enough to force preemption; every library call is mirrored into the oracle (Twin), and each
+    step's attention output is checked on sampled rows of its first item against the oracle over
+    that request's K/V history (tracked through appends, LCP invalidations and recompute)."""
+    from oracle.attention import attention_rows
+    from paper_2604_16395_b200 import costmodel, scheduler as S
+    from synth import traces
+    from tests.harness import Twin
+    L, K, budget = 2, 16, 1024
+    tr = traces.crawler_trace(41, 6, qps=50.0, lo=256, hi=1536, delay_scale=0.01) + \
+        [(e[0], e[1] + 100, *e[2:]) for e in traces.anns_trace(42, 6, qps=50.0, lo=256, hi=1536, delay_scale=0.1)]
+    tr.sort(key=lambda e: (e[0], e[1]))
+    ng, ncpu = 160, 640
+    cfg = s2l.make_config(L, 32, 8, 128, K, ng, ncpu, max_requests=16, max_blocks_per_request=1536 // K)
+    mb = s2l.block_bytes(cfg)
+    gpool = torch.empty(ng * mb // 2, dtype=torch.bfloat16, device="cuda")
+    cpool = torch.empty(ncpu * mb // 2, dtype=torch.bfloat16).pin_memory()
+    lib = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), torch.cuda.Stream())
+    tw = Twin(lib, K, ng, ncpu, 16, 1536 // K)
+    cm = costmodel.analytic(K, mb, 50e9, 2e-6)
+    sch = S.StreamingScheduler(tw, policy, K, budget, ng, cost_model=cm, preemption=preemption)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    src_k = torch.randn(L, budget, 8, 128, generator=g, device="cuda").to(torch.bfloat16)
+    src_v = torch.randn(L, budget, 8, 128, generator=g, device="cuda").to(torch.bfloat16)
+    src_q = torch.randn(budget, 32, 128, generator=g, device="cuda").to(torch.bfloat16)
+    kh = src_k.view(torch.int16).cpu().numpy().view(np.uint16)
+    vh = src_v.view(torch.int16).cpu().numpy().view(np.uint16)
+    qh = src_q.view(torch.int16).cpu().numpy().view(np.uint16)
+    segs, checks = {}, []
+    rng = np.random.default_rng(1)
+    t, i = 0.0, 0
+    while True:
+        while i < len(tr) and tr[i][0] <= t:
+            tc, rid, n, tok, new, mode = tr[i]
+            sch.on_chunk(tc, rid, n, tokens=tok, new_input=new, mode=mode)
+            i += 1
+        items = sch.step(t)
+        if not items:
+            if i >= len(tr):
+                break
+            t = tr[i][0]
+            continue
+        rows, app, pre = 0, [], []
+        for r, q_pos, n in items:
+            app.append((r, None, n, rows))
+            pre.append((r, q_pos, n, rows))
+            kept, acc = [], 0
+            for a, m in segs.get(r, []):          # K/V history: positions < q_pos survive
+                if acc >= q_pos:
+                    break
+                kept.append((a, min(m, q_pos - acc)))
+                acc += kept[-1][1]
+            assert acc == q_pos
+            segs[r] = kept + [(rows, n)]
+            rows += n
+        tw.append_chunk(app, src_k, src_v, kv_rows=budget)
+        out = torch.empty_like(src_q)
+        for layer in range(L):
+            lib.prefill_batch(layer, pre, src_q, out)
+        r, q_pos, n, row = pre[0]
+        rs = sorted(set([0, n - 1] + rng.integers(0, n, 3).tolist()))
+        checks.append((list(segs[r]), q_pos, row, rs, out.index_select(0, torch.tensor([row + x for x in rs], device="cuda"))))
+        t += 1e-3
+        sch.finish_step(t, items)
+        for r in list(segs):
+            if r not in lib_reqs(tw):
+                segs.pop(r)                        # released (finished)
+    lib.sync()
+    torch.cuda.synchronize()
+    assert len(sch.ttfts()) == 12
+    ev = [e[1] for e in sch.events]
+    assert ev.count("PREEMPTED_SWAP") + ev.count("PREEMPTED_RECOMPUTE") > 0
+    for seg, q_pos, row, rs, o in checks:
+        kk = np.concatenate([kh[L - 1, a:a + m] for a, m in seg])
+        vv = np.concatenate([vh[L - 1, a:a + m] for a, m in seg])
+        n = seg[-1][1]
+        o_ref, _ = attention_rows(qh[row:row + n], kk, vv, q_pos, rs)
+        err = normwise_err(bf16_dev_to_f64(o), o_ref)
+        assert err.max() <= 2e-2, (q_pos, float(err.max()))
+
+
+def lib_reqs(tw):
+    return set(tw.ora.reqs)
