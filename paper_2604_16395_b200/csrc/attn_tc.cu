@@ -48,6 +48,10 @@
 #ifndef S2L_SM64
 #define S2L_SM64 1         // v2: exponentials in 64-column chunks, polynomial pairs spread evenly
 #endif
+#ifndef S2L_HSPLIT
+#define S2L_HSPLIT 0       // v2 (needs SPLIT_S, SM64, !PQ): both softmax warpgroups work on every
+                           // tile, split by S columns (two warps per SMSP per tile)
+#endif
 #ifndef S2L_PQ
 #define S2L_PQ 0           // v2: 1 = P handed to the MMA warp in quarters (32 keys) instead of halves
 #endif
@@ -95,7 +99,12 @@ struct TcParams {
   float* ws_ml;    // [pieces][2][128][2] running max (log2 units) and row sum
   int32_t* ws_cnt;
   uint32_t* trace;   // S2L_TRACE builds only: per-event SM clock stamps of CTA 0
+  int32_t n_inl;     // > 0: the items are inl[0 .. n_inl) (by value), not *items
+  AttnItemDev inl[kInlineAttnItems];
 };
+__device__ __forceinline__ AttnItemDev item_at(const TcParams& p, int32_t i) {
+  return p.n_inl ? p.inl[i] : p.items[i];
+}
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -307,7 +316,7 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 // ---------------------------------------------------------------- the kernel
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                   const __grid_constant__ CUtensorMap tmap_kv, const TcParams p) {
+                   const __grid_constant__ CUtensorMap tmap_kv, const __grid_constant__ TcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sb = smem_u32(smem);
@@ -321,9 +330,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   int32_t lo = 0, hi = p.n_items - 1;
   while (lo < hi) {
     const int32_t mid = (lo + hi + 1) >> 1;
-    if (p.items[mid].unit_begin <= unit) lo = mid; else hi = mid - 1;
+    if (item_at(p, mid).unit_begin <= unit) lo = mid; else hi = mid - 1;
   }
-  const AttnItemDev it = p.items[lo];
+  const AttnItemDev it = item_at(p, lo);
   const int32_t local = unit - it.unit_begin;
   const int32_t tile = it.tiles - 1 - local / p.h_kv;
   const int32_t kvh = local % p.h_kv;
@@ -755,7 +764,12 @@ constexpr uint32_t WB_QF = 0, WB_RF = 1, WB_RE = 1 + WNST, WB_SF = 1 + 2 * WNST,
                    WB_PH = WB_PF + 2, WB_OF = WB_PH + 2, WB_QE = WB_OF + 2, WB_PQ = WB_QE + 1,
                    WB_SR = WB_PQ + 8, WB_SH = WB_SR + 2, WNBARS = WB_SH + 2;
 constexpr uint32_t WOFF_TMEM = WOFF_BAR + WNBARS * 8;
+#if S2L_HSPLIT
+constexpr uint32_t WOFF_XCH = WOFF_TMEM + 16;          // [2][128] floats: row-max / row-sum exchange
+constexpr uint32_t SMEM = WOFF_XCH + 1024 + 1024;
+#else
 constexpr uint32_t SMEM = WOFF_TMEM + 16 + 1024;
+#endif
 }  // namespace v2
 
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
@@ -799,7 +813,7 @@ __device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
 __global__ void __launch_bounds__(v2::kThreads, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_kv,
-                    const __grid_constant__ CUtensorMap tmap_kv4, const TcParams p) {
+                    const __grid_constant__ CUtensorMap tmap_kv4, const __grid_constant__ TcParams p) {
   using namespace v2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -823,9 +837,9 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
   int32_t lo = 0, hi = p.n_items - 1;
   while (lo < hi) {
     const int32_t mid = (lo + hi + 1) >> 1;
-    if (p.items[mid].unit_begin <= unit) lo = mid; else hi = mid - 1;
+    if (item_at(p, mid).unit_begin <= unit) lo = mid; else hi = mid - 1;
   }
-  const AttnItemDev it = p.items[lo];
+  const AttnItemDev it = item_at(p, lo);
   const int32_t local = unit - it.unit_begin;
   const int32_t pairs = (it.tiles + 1) >> 1;
   const int32_t pair = pairs - 1 - local / p.h_kv;
@@ -1087,6 +1101,233 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       }
       __syncwarp();
     }
+#if S2L_HSPLIT
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
+    // ============ softmax / correction / epilogue, S columns split over the two warpgroups ============
+    // Warpgroup hf handles keys [64 hf, 64 hf + 64) of BOTH Q tiles (tile 0 then tile 1 each KV
+    // step): every tile's softmax runs on two warps per SMSP (one per warpgroup, same TMEM
+    // lanes = rows), which halves its latency on the ping-pong's critical chain.  The two warps
+    // of a row agree on the row max through shared memory (named barrier of 64 threads); the
+    // exponentials, P (warpgroup 0 writes P keys 0-63 = TMEM columns 0-31 and arrives P_full,
+    // warpgroup 1 keys 64-127 = columns 32-63 and arrives P_half), the O rescale and the
+    // epilogue are split by columns.  Warpgroup 1 reads S's upper half, which exists first
+    // (split S), and signals S_read; warpgroup 0 waits for S's lower half, whose completion
+    // also implies the previous PV -- the pair barrier hands that ordering to warpgroup 1.
+    const int hf = (warp - 4) >> 2;
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const int base = 64 * hf;
+    const uint32_t pair_bar = 2u + (uint32_t)(warp & 3);
+    float* xch = (float*)(smem + WOFF_XCH);            // [2 halves][128 rows]
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
+    const float sl2 = p.scale_log2;
+    const int32_t hq = kvh * G + r % G;
+    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
+    int32_t tokv[2];
+    bool validv[2];
+    int64_t limitv[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      tokv[i] = tok0 + i * toks + r / G;
+      validv[i] = tokv[i] < it.n_q;
+      limitv[i] = it.q_pos + (validv[i] ? tokv[i] : tok_last);
+    }
+    for (int32_t j = 0; j < nT; ++j) {
+#pragma unroll 1
+      for (int i = 0; i < 2; ++i) {
+        const uint32_t tS = tmem + lane_off + i * 128;
+        const uint32_t tO = tmem + lane_off + TMEM_O + i * 128;
+        const bool tr = (warp & 3) == 0 && lane == 0;
+        if (tr) TRACE(20, i, j);
+        if (hf == 1 && j > 0) mbar_wait(bar(WB_SH + i), (j - 1) & 1);
+        else mbar_wait(bar(WB_SF + i), j & 1);
+        tc_fence_after();
+        if (tr) TRACE(21, i, j);
+        const int64_t key0 = (int64_t)(jb + j) * kBN;
+        const int64_t vis64 = limitv[i] - key0;
+        const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBN ? kBN : vis64));
+        const bool masked = __any_sync(0xffffffffu, vis < base + 63);
+        uint32_t sv[64];
+        tmem_ld32(tS + base, sv);
+        tmem_ld32(tS + base + 32, sv + 32);
+        tmem_wait_ld();
+        if (hf == 1) {
+          tc_fence_before();
+          mbar_arrive(bar(WB_SR + i));                  // S(j) keys 64-127 are in registers
+        }
+        float mt[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mt[q] = -INFINITY;
+        if (masked) { max32<true>(sv, vis, base, mt); max32<true>(sv + 32, vis, base + 32, mt); }
+        else { max32<false>(sv, vis, base, mt); max32<false>(sv + 32, vis, base + 32, mt); }
+        const float mh = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])),
+                               fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7])));
+        xch[hf * 128 + r] = mh;
+        pair_sync();                                     // both halves loaded + maxes written
+        const float mx = fmaxf(mh, xch[(hf ^ 1) * 128 + r]) * sl2;
+        pair_sync();                                     // exchange slots free again
+        tc_fence_after();
+        if (tr) TRACE(22, i, j);
+        const float m_new = (mx > m_run[i] + kRescaleThresh) ? mx : m_run[i];
+        if (j > 0 && __any_sync(0xffffffffu, m_new != m_run[i])) {
+          // PV(j-1) is complete (warpgroup 0 waited for S's lower half before the barrier)
+          const float alpha = (m_new != m_run[i]) ? fast_exp2(m_run[i] - m_new) : 1.f;
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t ov[16];
+            tmem_ld16(tO + base + c * 16, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              float2 x = __fmul2_rn(make_float2(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])),
+                                    make_float2(alpha, alpha));
+              ov[e] = __float_as_uint(x.x);
+              ov[e + 1] = __float_as_uint(x.y);
+            }
+            tmem_st16(tO + base + c * 16, ov);
+          }
+          l_run[i] *= alpha;
+        }
+        m_run[i] = m_new;
+        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
+        const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_use, -m_use);
+        uint32_t pk[32];
+        const float2 acc = masked ? chunk_p64<true, 0>(sv, make_float2(0.f, 0.f), vis, base, sc2, nm2, pk)
+                                  : chunk_p64<false, kPolyPairsPer8>(sv, make_float2(0.f, 0.f), vis, base, sc2, nm2, pk);
+        tmem_st16(tS + 32 * hf, pk);
+        tmem_st16(tS + 32 * hf + 16, pk + 16);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(bar((hf == 0 ? WB_PF : WB_PH) + i));
+        if (tr) TRACE(hf == 0 ? 23 : 24, i, j);
+        l_run[i] += acc.x + acc.y;
+      }
+    }
+    // ---- epilogue: combine the halves' row sums, then each half writes its 64 columns
+    float l_tot[2];
+#pragma unroll 1
+    for (int i = 0; i < 2; ++i) {
+      xch[hf * 128 + r] = l_run[i];
+      pair_sync();
+      l_tot[i] = l_run[i] + xch[(hf ^ 1) * 128 + r];
+      pair_sync();
+    }
+#pragma unroll 1
+    for (int i = 0; i < 2; ++i) {
+      mbar_wait(bar(WB_OF + i), 0);
+      tc_fence_after();
+      const uint32_t tO = tmem + lane_off + TMEM_O + i * 128;
+      __nv_bfloat16* orow = p.o + ((it.q_row + tokv[i]) * p.h_q + hq) * (int64_t)kD;
+      if (npieces == 1) {
+        const float inv = kPNorm / l_tot[i];
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t ov[16];
+          tmem_ld16(tO + base + c * 16, ov);
+          tmem_wait_ld();
+          if (validv[i]) {
+            uint32_t w[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              w[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
+            uint4* dst = reinterpret_cast<uint4*>(orow + base + c * 16);
+            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          }
+        }
+        if (hf == 0 && validv[i] && p.lse)
+          p.lse[(it.q_row + tokv[i]) * p.h_q + hq] = (m_run[i] + __log2f(l_tot[i])) * 0.69314718055994531f;
+      } else {
+        const int32_t su = unit - p.split_begin;
+        const int64_t prow = (((int64_t)su * npieces + piece) * 2 + i) * 128 + r;
+        float* wo = p.ws + prow * kD + base;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t ov[16];
+          tmem_ld16(tO + base + c * 16, ov);
+          tmem_wait_ld();
+          float4* dst = reinterpret_cast<float4*>(wo + c * 16);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
+                                 __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
+        }
+        if (hf == 0) {
+          p.ws_ml[prow * 2] = m_run[i];
+          p.ws_ml[prow * 2 + 1] = l_tot[i];
+        }
+      }
+    }
+    if (npieces > 1) {
+      __threadfence();
+      asm volatile("bar.sync 1, 256;" ::: "memory");       // both softmax warpgroups wrote
+      uint32_t* flag = (uint32_t*)(smem + WOFF_TMEM + 8);
+      const int32_t su = unit - p.split_begin;
+      if (threadIdx.x == 128) {
+        const int32_t old = atomicAdd(p.ws_cnt + su, 1);
+        const uint32_t last = (old == npieces - 1) ? 1u : 0u;
+        if (last) p.ws_cnt[su] = 0;                          // ready for the next launch
+        *flag = last;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (*flag) {
+        __threadfence();
+#pragma unroll 1
+        for (int i = 0; i < 2; ++i) {
+          float M = -INFINITY;
+          for (int k = 0; k < npieces; ++k) {
+            const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
+            M = fmaxf(M, __ldcg(p.ws_ml + pr * 2));
+          }
+          constexpr int kMaxPieces = 8;
+          float wk[kMaxPieces];
+          float Lsum = 0.f;
+#pragma unroll
+          for (int k = 0; k < kMaxPieces; ++k) {
+            wk[k] = 0.f;
+            if (k < npieces) {
+              const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
+              wk[k] = fast_exp2(__ldcg(p.ws_ml + pr * 2) - M);
+              Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
+            }
+          }
+          const float inv = kPNorm / Lsum;
+          __nv_bfloat16* orow = p.o + ((it.q_row + tokv[i]) * p.h_q + hq) * (int64_t)kD;
+#pragma unroll 1
+          for (int c0 = base; c0 < base + 64; c0 += 32) {
+            float acc[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+#pragma unroll
+            for (int k = 0; k < kMaxPieces; ++k) {
+              if (k < npieces) {
+                const float* po = p.ws + ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * kD + c0;
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                  const float2 x = __ldcg(reinterpret_cast<const float2*>(po + c));
+                  acc[c] += wk[k] * x.x;
+                  acc[c + 1] += wk[k] * x.y;
+                }
+              }
+            }
+            if (validv[i]) {
+#pragma unroll
+              for (int c = 0; c < 32; c += 8) {
+                uint4 v4 = make_uint4(pack_bf16(acc[c] * inv, acc[c + 1] * inv), pack_bf16(acc[c + 2] * inv, acc[c + 3] * inv),
+                                      pack_bf16(acc[c + 4] * inv, acc[c + 5] * inv), pack_bf16(acc[c + 6] * inv, acc[c + 7] * inv));
+                *reinterpret_cast<uint4*>(orow + c0 + c) = v4;
+              }
+            }
+          }
+          if (hf == 0 && validv[i] && p.lse)
+            p.lse[(it.q_row + tokv[i]) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
+        }
+      }
+    }
+    tc_fence_before();
+  }
+#else
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
     // ================= softmax / correction / epilogue of Q tile i =================
@@ -1346,6 +1587,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     }
     tc_fence_before();
   }
+#endif  // S2L_HSPLIT
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -1379,7 +1621,7 @@ constexpr int kPolyPairsPer8 = v2::kPolyPairsPer8;
 __global__ void __launch_bounds__(v4::kThreads, 1)
     attn_tc4_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_kv,
-                    const __grid_constant__ CUtensorMap tmap_kv4, const TcParams p) {
+                    const __grid_constant__ CUtensorMap tmap_kv4, const __grid_constant__ TcParams p) {
   using namespace v4;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -1403,9 +1645,9 @@ __global__ void __launch_bounds__(v4::kThreads, 1)
   int32_t lo = 0, hi = p.n_items - 1;
   while (lo < hi) {
     const int32_t mid = (lo + hi + 1) >> 1;
-    if (p.items[mid].unit_begin <= unit) lo = mid; else hi = mid - 1;
+    if (item_at(p, mid).unit_begin <= unit) lo = mid; else hi = mid - 1;
   }
-  const AttnItemDev it = p.items[lo];
+  const AttnItemDev it = item_at(p, lo);
   const int32_t local = unit - it.unit_begin;
   const int32_t pairs = (it.tiles + 1) >> 1;
   const int32_t pair = pairs - 1 - local / p.h_kv;
@@ -1843,7 +2085,7 @@ constexpr int kPolyPairsPer8 = v2::kPolyPairsPer8;
 __global__ void __launch_bounds__(v5::kThreads, 1)
     attn_tc5_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_kv,
-                    const __grid_constant__ CUtensorMap tmap_kv64, const TcParams p) {
+                    const __grid_constant__ CUtensorMap tmap_kv64, const __grid_constant__ TcParams p) {
   using namespace v5;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -1867,9 +2109,9 @@ __global__ void __launch_bounds__(v5::kThreads, 1)
   int32_t lo = 0, hi = p.n_items - 1;
   while (lo < hi) {
     const int32_t mid = (lo + hi + 1) >> 1;
-    if (p.items[mid].unit_begin <= unit) lo = mid; else hi = mid - 1;
+    if (item_at(p, mid).unit_begin <= unit) lo = mid; else hi = mid - 1;
   }
-  const AttnItemDev it = p.items[lo];
+  const AttnItemDev it = item_at(p, lo);
   const int32_t local = unit - it.unit_begin;
   const int32_t pairs = (it.tiles + 1) >> 1;
   const int32_t pair = pairs - 1 - local / p.h_kv;
@@ -2262,9 +2504,9 @@ __device__ __forceinline__ WorkInfo decode_work(const TcParams& p, int32_t w) {
   int32_t lo = 0, hi = p.n_items - 1;
   while (lo < hi) {
     const int32_t mid = (lo + hi + 1) >> 1;
-    if (p.items[mid].unit_begin <= wk.unit) lo = mid; else hi = mid - 1;
+    if (item_at(p, mid).unit_begin <= wk.unit) lo = mid; else hi = mid - 1;
   }
-  wk.it = p.items[lo];
+  wk.it = item_at(p, lo);
   const int32_t local = wk.unit - wk.it.unit_begin;
   const int32_t pairs = (wk.it.tiles + 1) >> 1;
   const int32_t pair = pairs - 1 - local / p.h_kv;
@@ -2282,7 +2524,7 @@ __device__ __forceinline__ WorkInfo decode_work(const TcParams& p, int32_t w) {
 __global__ void __launch_bounds__(v2::kThreads, 1)
     attn_tc3_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_kv,
-                    const __grid_constant__ CUtensorMap tmap_kv4, const TcParams p) {
+                    const __grid_constant__ CUtensorMap tmap_kv4, const __grid_constant__ TcParams p) {
   using namespace v2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -2772,7 +3014,8 @@ int attn_tc_tiles_per_cta() {
   return v;
 }
 
-cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t n_items,
+cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const AttnItemDev* items_host,
+                           int32_t n_items,
                            int32_t total_units, int32_t split_begin, int32_t split_s,
                            float* ws, int32_t max_pieces, int32_t* ws_cnt,
                            const int32_t* table, int32_t layer, const void* tmap_q,
@@ -2799,6 +3042,11 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t 
   if (total_units <= 0) return cudaSuccess;
   TcParams p{};
   p.items = items;
+  p.n_inl = 0;
+  if (items_host && n_items <= kInlineAttnItems) {
+    memcpy(p.inl, items_host, (size_t)n_items * sizeof(AttnItemDev));
+    p.n_inl = n_items;
+  }
   p.table = table;
   p.o = (__nv_bfloat16*)o;
   p.lse = lse;

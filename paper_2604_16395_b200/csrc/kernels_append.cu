@@ -12,6 +12,8 @@
 
 #include <cuda_bf16.h>
 
+#include <cstring>
+
 namespace s2l {
 namespace {
 
@@ -19,6 +21,10 @@ __global__ void table_patch_kernel(const TablePatch* __restrict__ patches, int32
                                    int32_t* __restrict__ table) {
   for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     table[patches[i].idx] = patches[i].value;
+}
+__global__ void table_patch_inline_kernel(const __grid_constant__ InlinePatches ps, int32_t n,
+                                          int32_t* __restrict__ table) {
+  for (int32_t i = threadIdx.x; i < n; i += blockDim.x) table[ps.p[i].idx] = ps.p[i].value;
 }
 
 constexpr int kSmemItems = 256;    // items / ids staged in shared memory when they fit (38 KB)
@@ -45,13 +51,19 @@ constexpr int kRowsPerWarp = S2L_APPEND_ROWS;
 
 // kMaxVecPerLane >= vectors per lane per row (vpt/32: 4 at Llama-3 h_kv 8, d 128).
 // kVpr = d/8 vectors per head row when known at compile time (16 at d = 128), else 0.
+// Descriptors either through device pointers (staging ring) or, when blob_mode != 0, from
+// the kernel's by-value parameter blob (items at 0, ids at off_ids, patches at off_patch).
 template <int kMaxVecPerLane, int kVpr>
 __global__ void __launch_bounds__(256) append_kernel(
-    const AppendItemDev* __restrict__ items_g, int32_t n_items, int64_t total_rows,
-    const int32_t* __restrict__ ids_g, int32_t n_ids, const TablePatch* __restrict__ patches,
+    const AppendItemDev* __restrict__ items_p, int32_t n_items, int64_t total_rows,
+    const int32_t* __restrict__ ids_p, int32_t n_ids, const TablePatch* __restrict__ patches_p,
     int32_t n_patches, int32_t* __restrict__ table, const uint4* __restrict__ k,
     const uint4* __restrict__ v, int64_t kv_rows, uint4* __restrict__ pool, int32_t L,
-    int32_t h_kv, int32_t vec_per_row, int32_t kb_log2) {
+    int32_t h_kv, int32_t vec_per_row, int32_t kb_log2, const __grid_constant__ InlineBlob blob,
+    int32_t blob_mode, int32_t off_ids, int32_t off_patch) {
+  const AppendItemDev* items_g = blob_mode ? reinterpret_cast<const AppendItemDev*>(blob.b) : items_p;
+  const int32_t* ids_g = blob_mode ? reinterpret_cast<const int32_t*>(blob.b + off_ids) : ids_p;
+  const TablePatch* patches = blob_mode ? reinterpret_cast<const TablePatch*>(blob.b + off_patch) : patches_p;
   __shared__ AppendItemDev s_items[kSmemItems];
   __shared__ int32_t s_ids[kSmemIds];
   const bool staged = n_items <= kSmemItems && n_ids <= kSmemIds;
@@ -114,6 +126,16 @@ __global__ void __launch_bounds__(256) append_kernel(
 
 }  // namespace
 
+cudaError_t launch_table_patch_inline(const TablePatch* host_patches, int32_t n, int32_t* table,
+                                      cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (n > kInlinePatches) return cudaErrorInvalidValue;
+  InlinePatches ps;
+  memcpy(ps.p, host_patches, (size_t)n * sizeof(TablePatch));
+  table_patch_inline_kernel<<<1, 256, 0, st>>>(ps, n, table);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_table_patch(const TablePatch* patches, int32_t n, int32_t* table,
                                cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
@@ -123,11 +145,13 @@ cudaError_t launch_table_patch(const TablePatch* patches, int32_t n, int32_t* ta
   return cudaGetLastError();
 }
 
-cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t n_items,
-                          int64_t total_rows, const int32_t* ids, int32_t n_ids,
-                          const TablePatch* patches,
-                          int32_t n_patches, int32_t* table, const void* k, const void* v,
-                          int64_t kv_rows, void* pool, cudaStream_t st) {
+namespace {
+cudaError_t launch_append_impl(const Geometry& g, const AppendItemDev* items, int32_t n_items,
+                               int64_t total_rows, const int32_t* ids, int32_t n_ids,
+                               const TablePatch* patches, int32_t n_patches, int32_t* table,
+                               const void* k, const void* v, int64_t kv_rows, void* pool,
+                               const InlineBlob& blob, int32_t blob_mode, int32_t off_ids,
+                               int32_t off_patch, cudaStream_t st) {
   const int32_t vec_per_row = g.d / 8;
   const int64_t vpt = (int64_t)g.h_kv * vec_per_row;
   int kb_log2 = 0;
@@ -137,11 +161,11 @@ cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t
   if (blocks < 1) blocks = 1;
   if (blocks > 65535) blocks = 65535;
   dim3 grid((unsigned)blocks, g.L * 2);
-#define S2L_APPEND(MAXV, VPR)                                                                  \
+#define S2L_APPEND(MAXV, VPR)                                                                   \
   append_kernel<MAXV, VPR><<<grid, 256, 0, st>>>(items, n_items, total_rows, ids, n_ids, patches, \
-                                            n_patches, table, (const uint4*)k, (const uint4*)v, \
-                                            kv_rows, (uint4*)pool, g.L, g.h_kv, vec_per_row,    \
-                                            kb_log2)
+                                                 n_patches, table, (const uint4*)k, (const uint4*)v, \
+                                                 kv_rows, (uint4*)pool, g.L, g.h_kv, vec_per_row,    \
+                                                 kb_log2, blob, blob_mode, off_ids, off_patch)
   if (vec_per_row == 16 && vpt <= 128) S2L_APPEND(4, 16);          // d = 128, h_kv <= 8
   else if (vec_per_row == 16 && vpt <= 512) S2L_APPEND(16, 16);
   else if (vpt <= 32) S2L_APPEND(1, 0);
@@ -151,6 +175,26 @@ cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t
   else return cudaErrorInvalidValue;
 #undef S2L_APPEND
   return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t n_items,
+                          int64_t total_rows, const int32_t* ids, int32_t n_ids,
+                          const TablePatch* patches,
+                          int32_t n_patches, int32_t* table, const void* k, const void* v,
+                          int64_t kv_rows, void* pool, cudaStream_t st) {
+  static InlineBlob empty;   // unused in pointer mode (still copied as a parameter)
+  return launch_append_impl(g, items, n_items, total_rows, ids, n_ids, patches, n_patches, table,
+                            k, v, kv_rows, pool, empty, 0, 0, 0, st);
+}
+
+cudaError_t launch_append_inline(const Geometry& g, const InlineBlob& blob, int32_t n_items,
+                                 int64_t total_rows, int32_t off_ids, int32_t n_ids,
+                                 int32_t off_patch, int32_t n_patches, int32_t* table,
+                                 const void* k, const void* v, int64_t kv_rows, void* pool,
+                                 cudaStream_t st) {
+  return launch_append_impl(g, nullptr, n_items, total_rows, nullptr, n_ids, nullptr, n_patches,
+                            table, k, v, kv_rows, pool, blob, 1, off_ids, off_patch, st);
 }
 
 }  // namespace s2l

@@ -385,6 +385,13 @@ std::pair<cudaEvent_t, cudaEvent_t> timing_pair(s2l_ctx* c) {
 // append kernel carried them).
 s2l_status flush_patches(s2l_ctx* c) {
   if (c->dirty.empty()) return S2L_OK;
+  if ((int64_t)c->dirty.size() <= s2l::kInlinePatches) {   // by value: no copy-engine upload
+    std::vector<s2l::TablePatch> ps(c->dirty.size());
+    int32_t n = take_patches(c, ps.data());
+    CK(s2l::launch_table_patch_inline(ps.data(), n, c->d_table, c->compute));
+    c->launches++;
+    return S2L_OK;
+  }
   size_t bytes = c->dirty.size() * sizeof(s2l::TablePatch);
   int s = staging_acquire(c, bytes);
   if (s < 0) return S2L_E_CUDA;
@@ -781,28 +788,45 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
   size_t off_ids = align16(dev_items.size() * sizeof(s2l::AppendItemDev));
   size_t off_patch = align16(off_ids + ids.size() * sizeof(int32_t));
   size_t bytes = off_patch + c->dirty.size() * sizeof(s2l::TablePatch);
-  int s = staging_acquire(c, bytes);
-  if (s < 0) return S2L_E_CUDA;
-  char* h = (char*)c->ring.host[s];
+  // Small calls pass their descriptors by value in the kernel parameters; a staged upload
+  // would queue on the copy engine behind bulk H2D traffic and stall the compute stream.
+  const bool inl = bytes <= (size_t)s2l::kInlineBytes;
+  int s = -1;
+  char* h = nullptr;
+  std::unique_ptr<s2l::InlineBlob> blob;
+  if (inl) {
+    blob.reset(new s2l::InlineBlob());
+    h = (char*)blob->b;
+  } else {
+    s = staging_acquire(c, bytes);
+    if (s < 0) return S2L_E_CUDA;
+    h = (char*)c->ring.host[s];
+  }
   memcpy(h, dev_items.data(), dev_items.size() * sizeof(s2l::AppendItemDev));
   memcpy(h + off_ids, ids.data(), ids.size() * sizeof(int32_t));
   int32_t n_patch = take_patches(c, (s2l::TablePatch*)(h + off_patch));
-  if (!staging_upload_and_mark(c, s, bytes)) return S2L_E_CUDA;
+  if (!inl && !staging_upload_and_mark(c, s, bytes)) return S2L_E_CUDA;
   if (!ring_wait(c, c->out_ring, c->compute, quar_wait) || !ring_wait(c, c->in_ring, c->compute, quar_wait_in))
     return S2L_E_CUDA;
   for (Request* r : wait_in) {
     if (!ring_wait(c, c->in_ring, c->compute, r->swap_in_seq)) return S2L_E_CUDA;
   }
-  char* dv = (char*)c->ring.dev[s];
   std::pair<cudaEvent_t, cudaEvent_t> tp{};
   if (c->timing) {
     tp = timing_pair(c);
     CK(cudaEventRecord(tp.first, c->compute));
   }
-  CK(s2l::launch_append(c->geo, (const s2l::AppendItemDev*)dv, (int32_t)dev_items.size(),
-                        total_rows, (const int32_t*)(dv + off_ids), (int32_t)ids.size(),
-                        (const s2l::TablePatch*)(dv + off_patch), n_patch, c->d_table, k, v,
-                        kv_rows, c->gpu_pool, c->compute));
+  if (inl) {
+    CK(s2l::launch_append_inline(c->geo, *blob, (int32_t)dev_items.size(), total_rows,
+                                 (int32_t)off_ids, (int32_t)ids.size(), (int32_t)off_patch, n_patch,
+                                 c->d_table, k, v, kv_rows, c->gpu_pool, c->compute));
+  } else {
+    char* dv = (char*)c->ring.dev[s];
+    CK(s2l::launch_append(c->geo, (const s2l::AppendItemDev*)dv, (int32_t)dev_items.size(),
+                          total_rows, (const int32_t*)(dv + off_ids), (int32_t)ids.size(),
+                          (const s2l::TablePatch*)(dv + off_patch), n_patch, c->d_table, k, v,
+                          kv_rows, c->gpu_pool, c->compute));
+  }
   c->launches++;
   if (c->timing) {
     CK(cudaEventRecord(tp.second, c->compute));
@@ -811,7 +835,7 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
   uint64_t wseq = 0;
   if (!ring_record(c, c->compute_ring, c->compute, &wseq)) return S2L_E_CUDA;
   for (Request* r : written) r->write_seq = r->use_seq = wseq;
-  if (!staging_release(c, s)) return S2L_E_CUDA;
+  if (!inl && !staging_release(c, s)) return S2L_E_CUDA;
   return S2L_OK;
 }
 
@@ -898,11 +922,17 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
   }
   if (units >= (1ll << 31)) return fail(S2L_E_INVAL, "batch too large");
   size_t bytes = dev.size() * sizeof(s2l::AttnItemDev);
-  int s = staging_acquire(c, bytes);
-  if (s < 0) return S2L_E_CUDA;
-  memcpy(c->ring.host[s], dev.data(), bytes);
-  if (!staging_upload_and_mark(c, s, bytes)) return S2L_E_CUDA;
-  const s2l::AttnItemDev* dv = (const s2l::AttnItemDev*)c->ring.dev[s];
+  // tensor-core kernel: up to kInlineAttnItems items travel in the kernel parameters
+  const bool inl = c->tc_ok && n_items <= s2l::kInlineAttnItems;
+  int s = -1;
+  const s2l::AttnItemDev* dv = nullptr;
+  if (!inl) {
+    s = staging_acquire(c, bytes);
+    if (s < 0) return S2L_E_CUDA;
+    memcpy(c->ring.host[s], dev.data(), bytes);
+    if (!staging_upload_and_mark(c, s, bytes)) return S2L_E_CUDA;
+    dv = (const s2l::AttnItemDev*)c->ring.dev[s];
+  }
   std::pair<cudaEvent_t, cudaEvent_t> tp{};
   if (c->timing) {
     tp = timing_pair(c);
@@ -942,7 +972,8 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
       }
     }
     s2l::set_attn_trace(c->attn_launch_no++ == c->trace_launch ? c->trace_buf : nullptr);
-    CK(s2l::launch_attn_tc(c->geo, dv, n_items, (int32_t)units, split_begin, split_s,
+    CK(s2l::launch_attn_tc(c->geo, dv, inl ? dev.data() : nullptr, n_items, (int32_t)units,
+                           split_begin, split_s,
                            c->split_ws, c->num_sms, c->split_cnt, c->d_table, layer, tq,
                            c->tmap_kv, o, lse, c->num_sms,
                            (c->persistent ? s2l::kAttnPersistent : 0) |
@@ -961,7 +992,7 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
   uint64_t useq = 0;
   if (!ring_record(c, c->compute_ring, c->compute, &useq)) return S2L_E_CUDA;
   for (int32_t i = 0; i < n_items; ++i) find(c, items[i].req_id)->use_seq = useq;
-  if (!staging_release(c, s)) return S2L_E_CUDA;
+  if (!inl && !staging_release(c, s)) return S2L_E_CUDA;
   return S2L_OK;
 }
 

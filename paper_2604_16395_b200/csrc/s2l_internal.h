@@ -36,6 +36,20 @@ struct AttnItemDev {
   int32_t unit_begin;  // prefix sum of tiles * h_kv over items
 };
 
+// Descriptors of small calls travel inside the kernel's parameter block (read through the
+// constant bank) instead of the staging ring: a staged upload is a cudaMemcpyAsync that queues
+// on the copy engine behind bulk H2D traffic (inputs, swap-ins) and would stall the compute
+// stream behind it.  Larger calls fall back to the staging ring.
+constexpr int kInlineBytes = 6144;      // append: items + block ids + table patches
+struct InlineBlob {
+  alignas(16) uint8_t b[kInlineBytes];
+};
+constexpr int kInlineAttnItems = 64;    // attention: items inline up to this many
+constexpr int kInlinePatches = 512;     // table-patch kernel
+struct InlinePatches {
+  TablePatch p[kInlinePatches];
+};
+
 struct Geometry {
   int32_t L, h_q, h_kv, d, k;
   int32_t max_blocks;  // columns of the device block table
@@ -45,6 +59,9 @@ struct Geometry {
 
 cudaError_t launch_table_patch(const TablePatch* patches, int32_t n, int32_t* table,
                                cudaStream_t st);
+// Same with the patches (n <= kInlinePatches) passed by value from host memory.
+cudaError_t launch_table_patch_inline(const TablePatch* host_patches, int32_t n, int32_t* table,
+                                      cudaStream_t st);
 
 // Writes K/V rows into the pool and applies the table patches (fused).
 cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t n_items,
@@ -52,6 +69,13 @@ cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t
                           const TablePatch* patches,
                           int32_t n_patches, int32_t* table, const void* k, const void* v,
                           int64_t kv_rows, void* pool, cudaStream_t st);
+// Same with items / ids / patches laid out in a host blob (items at 0, ids at off_ids,
+// patches at off_patch; total <= kInlineBytes) passed by value.
+cudaError_t launch_append_inline(const Geometry& g, const InlineBlob& blob, int32_t n_items,
+                                 int64_t total_rows, int32_t off_ids, int32_t n_ids,
+                                 int32_t off_patch, int32_t n_patches, int32_t* table,
+                                 const void* k, const void* v, int64_t kv_rows, void* pool,
+                                 cudaStream_t st);
 
 // CUDA-core attention for any geometry (one warp per (query row, q head)).
 cudaError_t launch_attn_generic(const Geometry& g, const AttnItemDev* items, int32_t n_items,
@@ -67,7 +91,10 @@ int attn_tc_tiles_per_cta();
 // Grid = split_begin + (total_units - split_begin) * split_s CTAs: units below split_begin
 // run whole, the remaining (tail-wave) units run as split_s KV-range pieces whose partials
 // (ws: O partials of max_pieces pieces, then their (m, l)) are merged by the last piece (ws_cnt).
-cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, int32_t n_items,
+// items: device pointer, or (n_items <= kInlineAttnItems and items_host != nullptr) the host
+// array is copied into the kernel's parameters instead.
+cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const AttnItemDev* items_host,
+                           int32_t n_items,
                            int32_t total_units, int32_t split_begin, int32_t split_s,
                            float* ws, int32_t max_pieces, int32_t* ws_cnt,
                            const int32_t* table, int32_t layer, const void* tmap_q,
