@@ -156,8 +156,10 @@ s2l_status s2l_append_chunk(s2l_ctx* ctx, int32_t n_items, const s2l_append_item
  * return the rest to the pool of the tier holding them (GPU, or CPU when swapped);
  * nc := b; input := new_tokens; invalidated = nc_old - b is added to
  * total_tokens_invalidated.  A swapped request left with no blocks becomes a
- * GPU-tier request.  Host-only: the device block-table tail reset is applied by the
- * next kernel launch on compute_stream.  lcp_out / tokens_invalidated_out may be NULL. */
+ * GPU-tier request.  Host-only: the freed entries of the block table are reset on the
+ * host mirror; the device copy of an entry is only read below a request's valid block count, so
+ * it is updated when the entry receives a block id again (patch on the next kernel launch).
+ * lcp_out / tokens_invalidated_out may be NULL. */
 s2l_status s2l_invalidate_lcp(s2l_ctx* ctx, int64_t req_id, const int32_t* new_tokens,
                               int64_t new_len, int64_t* lcp_out, int64_t* tokens_invalidated_out);
 

@@ -285,10 +285,15 @@ Request* find(s2l_ctx* c, int64_t id) {
   return it == c->by_id.end() ? nullptr : &c->slots[it->second];
 }
 
+// Host mirror of the block table; entries that receive a block id are queued as device
+// patches.  Freed entries (-1) are updated on the host only: the kernels read a request's
+// entries only below its valid block count (attention: nblk_valid = ceil(kv_len / k); append:
+// the staged id list), so the device copy of a freed entry is never read, and resetting it
+// would make a release / swap-out of a long request a large patch upload.
 void set_table(s2l_ctx* c, int32_t slot, int64_t col, int32_t value) {
   size_t idx = (size_t)slot * c->cfg.max_blocks_per_request + (size_t)col;
   c->h_table[idx] = value;
-  if (!c->dirty_flag[idx]) {
+  if (value >= 0 && !c->dirty_flag[idx]) {
     c->dirty_flag[idx] = 1;
     c->dirty.push_back((int32_t)idx);
   }

@@ -38,7 +38,7 @@ def main():
     comp = torch.cuda.current_stream()
     h2d, d2h = streams
     qd, kd, vd, od = dev_bufs
-    T = {k: [] for k in ("h0", "h1", "c0", "c1", "d0", "d1")}
+    T = {k: [] for k in ("h0", "h1", "c0", "ca", "c1", "d0", "d1")}
     for r, t in zip(S_host.rids, S_host.toks):
         ctx.new_request(r, t)
     ev_loaded = [torch.cuda.Event() for _ in range(nb)]
@@ -61,6 +61,7 @@ def main():
         comp.wait_event(ev_loaded[b])
         x = ev(); x.record(comp); T["c0"].append(x)
         ctx.append_chunk(S_host.items_a[j], kd[b], vd[b])
+        x = ev(); x.record(comp); T["ca"].append(x)
         ctx.prefill_batch(0, S_host.items_p[j], qd[b], od[b])
         x = ev(); x.record(comp); T["c1"].append(x)
         ev_done[b].record(comp)
@@ -76,10 +77,10 @@ def main():
     torch.cuda.synchronize()
     for r in S_host.rids:
         ctx.release(r)
-    print("chunk  h2d[start,end]   compute[start,end]   d2h[start,end]  (ms)")
+    print("chunk  h2d[start,end]   compute[start,append end,end]   d2h[start,end]  (ms)")
     for j in list(range(0, 8)) + list(range(28, 32)):
         f = lambda k: t0.elapsed_time(T[k][j])
-        print(f"{j:3d}  {f('h0'):7.2f} {f('h1'):7.2f}   {f('c0'):7.2f} {f('c1'):7.2f}   {f('d0'):7.2f} {f('d1'):7.2f}")
+        print(f"{j:3d}  {f('h0'):7.2f} {f('h1'):7.2f}   {f('c0'):7.2f} {f('ca'):7.2f} {f('c1'):7.2f}   {f('d0'):7.2f} {f('d1'):7.2f}")
     h2d, d2h = streams
     qd, kd, vd, od = dev_bufs
     for name, do_h2d, do_d2h in (("h2d only", True, False), ("d2h only", False, True), ("both", True, True)):
