@@ -174,3 +174,51 @@ def test_fuzz_10000_steps_bit_exact(aligned):
         b = _apply(ora, op, args)
         assert a == b, (step, op, args, a, b)
         _same_state(lib, ora)
+
+
+def test_z9_ids_released_by_the_last_swap_out_are_allocated_last():
+    """Reading Z9: lowest free id first, except that the GPU ids released by the most recent
+    swap-out come after every other free id; they become ordinary free ids at the next
+    swap-out.  Library and oracle agree on every table."""
+    lib, ora = _pair(ng=12, nc=12, max_blocks=12)
+    z = np.zeros((1, 64, 1, 16), np.uint16)
+    for x in (lib, ora):
+        x.new_request(1, list(range(16)))
+        x.new_request(2, list(range(32)))
+    lib.append_chunk([(1, None, 16, 0)], kv_rows=64)            # ids 0-3
+    ora.append([(1, None, 16, 0)], z, z)
+    assert lib.swap_out([1]) == ora.swap_out([1])[1]             # 0-3 cooling
+    lib.append_chunk([(2, None, 32, 0)], kv_rows=64)            # 8 blocks: 4-11 first, then none cooling
+    ora.append([(2, None, 32, 0)], z, z)
+    assert lib.block_table(2) == ora.block_table(2) == list(range(4, 12))
+    assert lib.swap_in([1]) == ora.swap_in([1])[1]               # only cooling ids left: 0-3
+    assert lib.block_table(1) == ora.block_table(1) == [0, 1, 2, 3]
+    # next swap-out thaws the previous cooling set: request 2's ids cool, request 1 comes back
+    # into the lowest ordinary free ids
+    assert lib.swap_out([2]) == ora.swap_out([2])[1]
+    assert lib.swap_out([1]) == ora.swap_out([1])[1]             # 2's ids thaw, 1's ids cool
+    assert lib.swap_in([2]) == ora.swap_in([2])[1]
+    assert lib.block_table(2) == ora.block_table(2) == list(range(4, 12))
+    assert lib.free_blocks() == ora.free_counts()
+
+
+def test_z19_token_only_append_on_the_cpu_tier():
+    """Reading Z19: input keeps arriving while a request is swapped out; a
+    token-only append (n_kv = 0) is valid on either tier, K/V writes need the GPU tier."""
+    lib, ora = _pair(ng=8, nc=8, max_blocks=8)
+    z = np.zeros((1, 16, 1, 16), np.uint16)
+    for x in (lib, ora):
+        x.new_request(3, [1, 2, 3, 4, 5, 6, 7, 8])
+    lib.append_chunk([(3, None, 8, 0)], kv_rows=16)
+    ora.append([(3, None, 8, 0)], z, z)
+    assert lib.swap_out([3]) == ora.swap_out([3])[1]
+    assert s2l.status_of(lib.append_chunk, [(3, [9, 10, 11], 0, 0)], kv_rows=16) == s2l.OK
+    assert ora.append([(3, [9, 10, 11], 0, 0)], z, z) == O.OK
+    assert lib.query(3) == ora.info(3) and lib.query(3)["num_tokens"] == 11
+    assert s2l.status_of(lib.append_chunk, [(3, None, 3, 0)], kv_rows=16) == s2l.E_STATE
+    assert ora.append([(3, None, 3, 0)], z, z) == O.E_STATE
+    assert lib.swap_in([3]) == ora.swap_in([3])[1]
+    lib.append_chunk([(3, None, 3, 0)], kv_rows=16)
+    ora.append([(3, None, 3, 0)], z, z)
+    assert lib.query(3) == ora.info(3) and lib.query(3)["num_computed"] == 11
+    assert lib.block_table(3) == ora.block_table(3)
