@@ -842,8 +842,15 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
   const AttnItemDev it = item_at(p, lo);
   const int32_t local = unit - it.unit_begin;
   const int32_t pairs = (it.tiles + 1) >> 1;
+#if S2L_HEAD_MAJOR
+  // the pairs of one (item, kv head) are adjacent units: they stream the same K/V tiles at
+  // about the same time, so L2 serves the repeats
+  const int32_t pair = pairs - 1 - local % pairs;
+  const int32_t kvh = local / pairs;
+#else
   const int32_t pair = pairs - 1 - local / p.h_kv;
   const int32_t kvh = local % p.h_kv;
+#endif
   const int32_t G = p.group;
   const int32_t toks = kBM / G;
   const int32_t tok0 = pair * 2 * toks;               // first token of tile 0; tile 1 at +toks

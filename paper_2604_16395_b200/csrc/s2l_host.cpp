@@ -964,7 +964,8 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
         if (u1 <= first) break;
         for (int64_t pr = 0; pr < pairs; ++pr) {       // pair index; its units are >= first?
           const int64_t local0 = (pairs - 1 - pr) * c->cfg.num_kv_heads;
-          if (u0 + local0 + c->cfg.num_kv_heads <= first) continue;
+          // head-major order: a pair's units are spread over the item; count every pair
+          if (!S2L_HEAD_MAJOR && u0 + local0 + c->cfg.num_kv_heads <= first) continue;
           const int64_t toks = 128 / G;
           const int64_t tok_last = std::min<int64_t>((pr * 2 + 2) * toks, d.n_q) - 1;
           const int64_t nT = (d.q_pos + tok_last) / 128 + 1;

@@ -5,6 +5,10 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifndef S2L_HEAD_MAJOR
+#define S2L_HEAD_MAJOR 1   // v2 unit order inside an item: 0 = pair-major, 1 = kv-head-major
+#endif
+
 namespace s2l {
 
 // ---- device-side descriptors written into the staging ring by the host -------------------
