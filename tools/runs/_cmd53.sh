@@ -1,0 +1,4 @@
+python -m paper_2604_16395_b200.build --force > /dev/null
+echo "== gpu tests"; timeout -s KILL 900 python -m pytest tests -m gpu -q 2>&1 | tail -2
+bash tools/round_evidence.sh r01f
+timeout -s KILL 900 python tools/bench_workloads.py c4mix > gpurun_out/c4mix_r01f.jsonl 2> gpurun_out/c4mix_r01f.err; tail -c 200 gpurun_out/c4mix_r01f.jsonl
