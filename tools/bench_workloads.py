@@ -304,6 +304,8 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
     res["copy_ms_at_link"] = copy_ms
     res["overlap_gain_ms"] = s - o
     res["hidden_copy_frac"] = (s - o) / copy_ms if copy_ms else None
+    # overlap = (compute + copy - wall) / copy, copy at the measured link rate
+    res["overlap_frac"] = (c0 + copy_ms - o) / copy_ms if copy_ms else None
     return res
 
 
