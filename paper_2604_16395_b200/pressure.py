@@ -108,7 +108,7 @@ class PressureDriver:
     Every library call is appended to `log` as (op, args, result) for the oracle replay.
     """
 
-    def __init__(self, ctx, plans, k: int, budget: int, evict_ahead: bool = True):
+    def __init__(self, ctx, plans, k: int, budget: int, evict_ahead: int = 2):
         self.ctx, self.k, self.budget = ctx, k, budget
         self.evict_ahead = evict_ahead
         self.plans = {p.rid: p for p in plans}
@@ -217,13 +217,22 @@ class PressureDriver:
             raise RuntimeError(f"step {self.step}: cannot make room for {need} blocks")
         victims, free_after = got
         if self.evict_ahead:
-            nxt = [r for r in self.plan(peek=True) if r not in sel]
-            if nxt:
+            # room for the next `evict_ahead` steps too (best effort), so that a large D2H starts
+            # while earlier steps compute instead of right before the step that needs the room
+            keep, want = set(sel) | set(victims), need
+            saved = self.cursor
+            for _ in range(int(self.evict_ahead)):
+                nxt = [r for r in self.plan(peek=True) if r not in keep]
+                if not nxt:
+                    break
+                self.cursor = nxt[-1] + 1                  # peek one step further
                 info2 = {r: self.ctx.query(r) for r in nxt}
-                more = self._pick(need + self._need(nxt, info2), free_after,
-                                  set(sel) | set(nxt) | set(victims), set(protect))
-                if more is not None:                   # best effort
-                    victims += more[0]
+                want += self._need(nxt, info2)
+                keep |= set(nxt)
+            self.cursor = saved
+            more = self._pick(want, free_after, keep, set(protect))
+            if more is not None:
+                victims += more[0]
         if victims:
             b = self.ctx.swap_out(victims)
             self.log.append(("swap_out", tuple(victims), b))

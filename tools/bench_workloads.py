@@ -206,7 +206,7 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
         else:
             ctx = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), cs, swap_in_stream=cs_in)
         wrap = pressure.SwapTimer(ctx, serial=(mode == "serial"), copy_stream=cs, swap_in_stream=cs_in)
-        drv = pressure.PressureDriver(wrap, plans, K, budget)
+        drv = pressure.PressureDriver(wrap, plans, K, budget, evict_ahead=int(os.environ.get("C4_AHEAD", "2")))
         step_ev = []
         segs, snaps, flops = {}, [], [0.0]
 
