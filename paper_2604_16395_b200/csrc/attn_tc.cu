@@ -48,16 +48,6 @@
 #ifndef S2L_SM64
 #define S2L_SM64 1         // v2: exponentials in 64-column chunks, polynomial pairs spread evenly
 #endif
-#ifndef S2L_HSPLIT
-#define S2L_HSPLIT 0       // v2 (needs SPLIT_S, SM64, !PQ): both softmax warpgroups work on every
-                           // tile, split by S columns (two warps per SMSP per tile)
-#endif
-#ifndef S2L_PQ
-#define S2L_PQ 0           // v2: 1 = P handed to the MMA warp in quarters (32 keys) instead of halves
-#endif
-#ifndef S2L_PACK_TRUNC
-#define S2L_PACK_TRUNC 0   // 1: P -> bf16 by truncation (PRMT) with a mean-bias correction of l
-#endif
 
 namespace s2l {
 namespace {
@@ -288,24 +278,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
-// P -> bf16x2 for the PV MMA.  S2L_PACK_TRUNC=1 keeps the high halves (PRMT, off the
-// F2FP pipe the softmax's FMNMX/FFMA2 also use); truncation lowers each p by 2^-8 * E[1/(1+m)]
-// on average (m = mantissa fraction, log-uniform for 2^x: E = 1/(2 ln 2)), and the epilogues
-// divide by l * (1 - that mean) instead of l (kPNorm), leaving a zero-mean rounding error.
-__device__ __forceinline__ uint32_t pack_p(float lo, float hi) {
-#if S2L_PACK_TRUNC
-  uint32_t r;
-  asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(__float_as_uint(lo)), "r"(__float_as_uint(hi)));
-  return r;
-#else
-  return pack_bf16(lo, hi);
-#endif
-}
-#if S2L_PACK_TRUNC
-constexpr float kPNorm = 1.f / (1.f - 0.0028177f);
-#else
-constexpr float kPNorm = 1.f;
-#endif
+// P -> bf16x2 (round to nearest even) for the PV MMA.
+__device__ __forceinline__ uint32_t pack_p(float lo, float hi) { return pack_bf16(lo, hi); }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                              uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
@@ -533,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // epilogue
     mbar_wait(bar(B_OD), (nT - 1) & 1);
     tc_fence_after();
-    const float inv = kPNorm / l_run;
+    const float inv = 1.f / l_run;
     __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -761,15 +735,10 @@ constexpr uint32_t WOFF_BAR = WOFF_RING + WNST * kTileBytes;
 // P_full is split in two halves (keys 0-63 / 64-127) so the PV MMAs of the first half start
 // while the softmax still computes the second half.
 constexpr uint32_t WB_QF = 0, WB_RF = 1, WB_RE = 1 + WNST, WB_SF = 1 + 2 * WNST, WB_PF = WB_SF + 2,
-                   WB_PH = WB_PF + 2, WB_OF = WB_PH + 2, WB_QE = WB_OF + 2, WB_PQ = WB_QE + 1,
-                   WB_SR = WB_PQ + 8, WB_SH = WB_SR + 2, WNBARS = WB_SH + 2;
+                   WB_PH = WB_PF + 2, WB_OF = WB_PH + 2, WB_QE = WB_OF + 2, WB_SR = WB_QE + 1,
+                   WB_SH = WB_SR + 2, WNBARS = WB_SH + 2;
 constexpr uint32_t WOFF_TMEM = WOFF_BAR + WNBARS * 8;
-#if S2L_HSPLIT
-constexpr uint32_t WOFF_XCH = WOFF_TMEM + 16;          // [2][128] floats: row-max / row-sum exchange
-constexpr uint32_t SMEM = WOFF_XCH + 1024 + 1024;
-#else
 constexpr uint32_t SMEM = WOFF_TMEM + 16 + 1024;
-#endif
 }  // namespace v2
 
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
@@ -874,7 +843,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       mbar_init(bar(WB_PH + i), 128);
       mbar_init(bar(WB_OF + i), 1);
     }
-    for (int q = 0; q < 8; ++q) mbar_init(bar(WB_PQ + q), 128);
     for (int q = 0; q < 2; ++q) {
       mbar_init(bar(WB_SR + q), 128);   // split S: softmax q has read S keys 64-127
       mbar_init(bar(WB_SH + q), 1);     // split S: S(j+1) keys 64-127 computed
@@ -1005,24 +973,10 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       auto issue_pv = [&](int i, uint32_t vslot, int32_t j) {
         const uint64_t vd = dv0 + ((vslot * kTileBytes) >> 4);
         if (lane == 0) TRACE(10, i, j);
-        mbar_wait(bar(S2L_PQ ? WB_PQ + i * 4 : WB_PF + i), j & 1);   // first P part in TMEM
+        mbar_wait(bar(WB_PF + i), j & 1);               // P keys 0-63 in TMEM
         tc_fence_after();
         if (lane == 0) TRACE(11, i, j);
 #ifndef S2L_EXP_NO_PV
-#if S2L_PQ
-        // P in quarters (32 keys each); quarter 0 was waited for above
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (q > 0) {
-            mbar_wait(bar(WB_PQ + i * 4 + q), j & 1);
-            tc_fence_after();
-          }
-#pragma unroll
-          for (int kk = 2 * q; kk < 2 * q + 2; ++kk)
-            mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8,
-                         vd + ((kk * 16 * 128) >> 4), idesc_o, (j > 0 || kk > 0));
-        }
-#else
 #pragma unroll
         for (int kk = 0; kk < kBN / 32; ++kk)
           mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
@@ -1034,7 +988,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         for (int kk = kBN / 32; kk < kBN / 16; ++kk)
           mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
                        idesc_o, 1);
-#endif
 #endif
       };
       mbar_wait(bar(WB_QF), 0);
@@ -1108,233 +1061,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       }
       __syncwarp();
     }
-#if S2L_HSPLIT
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
-    // ============ softmax / correction / epilogue, S columns split over the two warpgroups ============
-    // Warpgroup hf handles keys [64 hf, 64 hf + 64) of BOTH Q tiles (tile 0 then tile 1 each KV
-    // step): every tile's softmax runs on two warps per SMSP (one per warpgroup, same TMEM
-    // lanes = rows), which halves its latency on the ping-pong's critical chain.  The two warps
-    // of a row agree on the row max through shared memory (named barrier of 64 threads); the
-    // exponentials, P (warpgroup 0 writes P keys 0-63 = TMEM columns 0-31 and arrives P_full,
-    // warpgroup 1 keys 64-127 = columns 32-63 and arrives P_half), the O rescale and the
-    // epilogue are split by columns.  Warpgroup 1 reads S's upper half, which exists first
-    // (split S), and signals S_read; warpgroup 0 waits for S's lower half, whose completion
-    // also implies the previous PV -- the pair barrier hands that ordering to warpgroup 1.
-    const int hf = (warp - 4) >> 2;
-    const int r = (warp & 3) * 32 + lane;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const int base = 64 * hf;
-    const uint32_t pair_bar = 2u + (uint32_t)(warp & 3);
-    float* xch = (float*)(smem + WOFF_XCH);            // [2 halves][128 rows]
-    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
-    const float sl2 = p.scale_log2;
-    const int32_t hq = kvh * G + r % G;
-    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
-    int32_t tokv[2];
-    bool validv[2];
-    int64_t limitv[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      tokv[i] = tok0 + i * toks + r / G;
-      validv[i] = tokv[i] < it.n_q;
-      limitv[i] = it.q_pos + (validv[i] ? tokv[i] : tok_last);
-    }
-    for (int32_t j = 0; j < nT; ++j) {
-#pragma unroll 1
-      for (int i = 0; i < 2; ++i) {
-        const uint32_t tS = tmem + lane_off + i * 128;
-        const uint32_t tO = tmem + lane_off + TMEM_O + i * 128;
-        const bool tr = (warp & 3) == 0 && lane == 0;
-        if (tr) TRACE(20, i, j);
-        if (hf == 1 && j > 0) mbar_wait(bar(WB_SH + i), (j - 1) & 1);
-        else mbar_wait(bar(WB_SF + i), j & 1);
-        tc_fence_after();
-        if (tr) TRACE(21, i, j);
-        const int64_t key0 = (int64_t)(jb + j) * kBN;
-        const int64_t vis64 = limitv[i] - key0;
-        const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBN ? kBN : vis64));
-        const bool masked = __any_sync(0xffffffffu, vis < base + 63);
-        uint32_t sv[64];
-        tmem_ld32(tS + base, sv);
-        tmem_ld32(tS + base + 32, sv + 32);
-        tmem_wait_ld();
-        if (hf == 1) {
-          tc_fence_before();
-          mbar_arrive(bar(WB_SR + i));                  // S(j) keys 64-127 are in registers
-        }
-        float mt[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) mt[q] = -INFINITY;
-        if (masked) { max32<true>(sv, vis, base, mt); max32<true>(sv + 32, vis, base + 32, mt); }
-        else { max32<false>(sv, vis, base, mt); max32<false>(sv + 32, vis, base + 32, mt); }
-        const float mh = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])),
-                               fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7])));
-        xch[hf * 128 + r] = mh;
-        pair_sync();                                     // both halves loaded + maxes written
-        const float mx = fmaxf(mh, xch[(hf ^ 1) * 128 + r]) * sl2;
-        pair_sync();                                     // exchange slots free again
-        tc_fence_after();
-        if (tr) TRACE(22, i, j);
-        const float m_new = (mx > m_run[i] + kRescaleThresh) ? mx : m_run[i];
-        if (j > 0 && __any_sync(0xffffffffu, m_new != m_run[i])) {
-          // PV(j-1) is complete (warpgroup 0 waited for S's lower half before the barrier)
-          const float alpha = (m_new != m_run[i]) ? fast_exp2(m_run[i] - m_new) : 1.f;
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            uint32_t ov[16];
-            tmem_ld16(tO + base + c * 16, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 16; e += 2) {
-              float2 x = __fmul2_rn(make_float2(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])),
-                                    make_float2(alpha, alpha));
-              ov[e] = __float_as_uint(x.x);
-              ov[e + 1] = __float_as_uint(x.y);
-            }
-            tmem_st16(tO + base + c * 16, ov);
-          }
-          l_run[i] *= alpha;
-        }
-        m_run[i] = m_new;
-        const float m_use = (m_new == -INFINITY) ? 0.f : m_new;
-        const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_use, -m_use);
-        uint32_t pk[32];
-        const float2 acc = masked ? chunk_p64<true, 0>(sv, make_float2(0.f, 0.f), vis, base, sc2, nm2, pk)
-                                  : chunk_p64<false, kPolyPairsPer8>(sv, make_float2(0.f, 0.f), vis, base, sc2, nm2, pk);
-        tmem_st16(tS + 32 * hf, pk);
-        tmem_st16(tS + 32 * hf + 16, pk + 16);
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(bar((hf == 0 ? WB_PF : WB_PH) + i));
-        if (tr) TRACE(hf == 0 ? 23 : 24, i, j);
-        l_run[i] += acc.x + acc.y;
-      }
-    }
-    // ---- epilogue: combine the halves' row sums, then each half writes its 64 columns
-    float l_tot[2];
-#pragma unroll 1
-    for (int i = 0; i < 2; ++i) {
-      xch[hf * 128 + r] = l_run[i];
-      pair_sync();
-      l_tot[i] = l_run[i] + xch[(hf ^ 1) * 128 + r];
-      pair_sync();
-    }
-#pragma unroll 1
-    for (int i = 0; i < 2; ++i) {
-      mbar_wait(bar(WB_OF + i), 0);
-      tc_fence_after();
-      const uint32_t tO = tmem + lane_off + TMEM_O + i * 128;
-      __nv_bfloat16* orow = p.o + ((it.q_row + tokv[i]) * p.h_q + hq) * (int64_t)kD;
-      if (npieces == 1) {
-        const float inv = kPNorm / l_tot[i];
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t ov[16];
-          tmem_ld16(tO + base + c * 16, ov);
-          tmem_wait_ld();
-          if (validv[i]) {
-            uint32_t w[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              w[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
-            uint4* dst = reinterpret_cast<uint4*>(orow + base + c * 16);
-            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-          }
-        }
-        if (hf == 0 && validv[i] && p.lse)
-          p.lse[(it.q_row + tokv[i]) * p.h_q + hq] = (m_run[i] + __log2f(l_tot[i])) * 0.69314718055994531f;
-      } else {
-        const int32_t su = unit - p.split_begin;
-        const int64_t prow = (((int64_t)su * npieces + piece) * 2 + i) * 128 + r;
-        float* wo = p.ws + prow * kD + base;
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t ov[16];
-          tmem_ld16(tO + base + c * 16, ov);
-          tmem_wait_ld();
-          float4* dst = reinterpret_cast<float4*>(wo + c * 16);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
-                                 __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
-        }
-        if (hf == 0) {
-          p.ws_ml[prow * 2] = m_run[i];
-          p.ws_ml[prow * 2 + 1] = l_tot[i];
-        }
-      }
-    }
-    if (npieces > 1) {
-      __threadfence();
-      asm volatile("bar.sync 1, 256;" ::: "memory");       // both softmax warpgroups wrote
-      uint32_t* flag = (uint32_t*)(smem + WOFF_TMEM + 8);
-      const int32_t su = unit - p.split_begin;
-      if (threadIdx.x == 128) {
-        const int32_t old = atomicAdd(p.ws_cnt + su, 1);
-        const uint32_t last = (old == npieces - 1) ? 1u : 0u;
-        if (last) p.ws_cnt[su] = 0;                          // ready for the next launch
-        *flag = last;
-      }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      if (*flag) {
-        __threadfence();
-#pragma unroll 1
-        for (int i = 0; i < 2; ++i) {
-          float M = -INFINITY;
-          for (int k = 0; k < npieces; ++k) {
-            const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
-            M = fmaxf(M, __ldcg(p.ws_ml + pr * 2));
-          }
-          constexpr int kMaxPieces = 8;
-          float wk[kMaxPieces];
-          float Lsum = 0.f;
-#pragma unroll
-          for (int k = 0; k < kMaxPieces; ++k) {
-            wk[k] = 0.f;
-            if (k < npieces) {
-              const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
-              wk[k] = fast_exp2(__ldcg(p.ws_ml + pr * 2) - M);
-              Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
-            }
-          }
-          const float inv = kPNorm / Lsum;
-          __nv_bfloat16* orow = p.o + ((it.q_row + tokv[i]) * p.h_q + hq) * (int64_t)kD;
-#pragma unroll 1
-          for (int c0 = base; c0 < base + 64; c0 += 32) {
-            float acc[32];
-#pragma unroll
-            for (int c = 0; c < 32; ++c) acc[c] = 0.f;
-#pragma unroll
-            for (int k = 0; k < kMaxPieces; ++k) {
-              if (k < npieces) {
-                const float* po = p.ws + ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * kD + c0;
-#pragma unroll
-                for (int c = 0; c < 32; c += 2) {
-                  const float2 x = __ldcg(reinterpret_cast<const float2*>(po + c));
-                  acc[c] += wk[k] * x.x;
-                  acc[c + 1] += wk[k] * x.y;
-                }
-              }
-            }
-            if (validv[i]) {
-#pragma unroll
-              for (int c = 0; c < 32; c += 8) {
-                uint4 v4 = make_uint4(pack_bf16(acc[c] * inv, acc[c + 1] * inv), pack_bf16(acc[c + 2] * inv, acc[c + 3] * inv),
-                                      pack_bf16(acc[c + 4] * inv, acc[c + 5] * inv), pack_bf16(acc[c + 6] * inv, acc[c + 7] * inv));
-                *reinterpret_cast<uint4*>(orow + c0 + c) = v4;
-              }
-            }
-          }
-          if (hf == 0 && validv[i] && p.lse)
-            p.lse[(it.q_row + tokv[i]) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
-        }
-      }
-    }
-    tc_fence_before();
-  }
-#else
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
     // ================= softmax / correction / epilogue of Q tile i =================
@@ -1363,7 +1089,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       tc_fence_before();
       mbar_arrive(bar(WB_PF + i));
       mbar_arrive(bar(WB_PH + i));
-      for (int q = 0; q < 4; ++q) mbar_arrive(bar(WB_PQ + i * 4 + q));
       continue;
 #endif
 #ifdef S2L_EXP_TMEM_ONLY  // timing experiment only: the softmax's TMEM traffic without its math
@@ -1380,8 +1105,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         tc_fence_before();
         mbar_arrive(bar(WB_PF + i));
         mbar_arrive(bar(WB_PH + i));
-        for (int q = 0; q < 4; ++q) mbar_arrive(bar(WB_PQ + i * 4 + q));
-        continue;
+          continue;
       }
 #endif
       const int64_t key0 = (int64_t)(jb + j) * kBN;
@@ -1474,19 +1198,12 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         acc = masked_tile ? chunk_p<true, 0>(v32, acc, vis, 32 * cc, sc2, nm2, pk)
                           : chunk_p<false, kPolyPairsPer8>(v32, acc, vis, 32 * cc, sc2, nm2, pk);
         tmem_st16(tS + 16 * cc, pk);
-#if S2L_PQ
-        tmem_wait_st();                // keys 32cc .. 32cc+31 of P are in TMEM
-        tc_fence_before();
-        mbar_arrive(bar(WB_PQ + i * 4 + cc));
-        if (tr && (cc & 1)) TRACE(cc == 1 ? 23 : 24, i, j);
-#else
         if (cc == 1 || cc == 3) {      // keys 0-63 / 64-127 of P are in TMEM
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(bar((cc == 1 ? WB_PF : WB_PH) + i));
           if (tr) TRACE(cc == 1 ? 23 : 24, i, j);
         }
-#endif
       }
       l_run += acc.x + acc.y;
     }
@@ -1495,7 +1212,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     tc_fence_after();
     __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
     if (npieces == 1) {
-      const float inv = kPNorm / l_run;
+      const float inv = 1.f / l_run;
 #pragma unroll 1
       for (int c = 0; c < 8; ++c) {
         uint32_t ov[16];
@@ -1560,7 +1277,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
             Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
           }
         }
-        const float inv = kPNorm / Lsum;
+        const float inv = 1.f / Lsum;
 #pragma unroll 1
         for (int c0 = 0; c0 < kD; c0 += 32) {
           float acc[32];
@@ -1594,7 +1311,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     }
     tc_fence_before();
   }
-#endif  // S2L_HSPLIT
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -1952,7 +1668,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1)
     const float l_tot = lsl[0] + lsl[1];
     __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD + 64 * h;
     if (npieces == 1) {
-      const float inv = kPNorm / l_tot;
+      const float inv = 1.f / l_tot;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t ov[16];
@@ -2018,7 +1734,7 @@ __global__ void __launch_bounds__(v4::kThreads, 1)
             Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
           }
         }
-        const float inv = kPNorm / Lsum;
+        const float inv = 1.f / Lsum;
 #pragma unroll 1
         for (int c0 = 0; c0 < 64; c0 += 32) {
           float acc[32];
@@ -2379,7 +2095,7 @@ __global__ void __launch_bounds__(v5::kThreads, 1)
     tc_fence_after();
     __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
     if (npieces == 1) {
-      const float inv = kPNorm / l_run;
+      const float inv = 1.f / l_run;
 #pragma unroll 1
       for (int c = 0; c < 8; ++c) {
         uint32_t ov[16];
@@ -2443,7 +2159,7 @@ __global__ void __launch_bounds__(v5::kThreads, 1)
             Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
           }
         }
-        const float inv = kPNorm / Lsum;
+        const float inv = 1.f / Lsum;
 #pragma unroll 1
         for (int c0 = 0; c0 < kD; c0 += 32) {
           float acc[32];
@@ -2800,7 +2516,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       tc_fence_after();
       __nv_bfloat16* orow = p.o + ((wk.it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
       if (wk.npieces == 1) {
-        const float inv = kPNorm / l_run;
+        const float inv = 1.f / l_run;
 #pragma unroll 1
         for (int c = 0; c < 8; ++c) {
           uint32_t ov[16];
@@ -2867,7 +2583,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
               Lsum += wk8[k] * __ldcg(p.ws_ml + pr * 2 + 1);
             }
           }
-          const float inv = kPNorm / Lsum;
+          const float inv = 1.f / Lsum;
 #pragma unroll 1
           for (int c0 = 0; c0 < kD; c0 += 32) {
             float acc[32];
