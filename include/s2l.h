@@ -110,7 +110,9 @@ int64_t s2l_block_bytes(const s2l_config* cfg);
  * Both pools are zero-filled (device: cudaMemsetAsync on compute_stream; host: memset) so
  * never-written slots are finite.  The library allocates its own device block table and a
  * small pinned + device staging ring.  Ownership of the pools stays with the caller and
- * they must outlive the context.  Errors: S2L_E_INVAL (geometry), S2L_E_CUDA. */
+ * they must outlive the context.  The library orders its own kernels and copies (stream
+ * hazards); swaps run on their own streams, so a caller that reads or writes
+ * pool memory directly must call s2l_sync first.  Errors: S2L_E_INVAL (geometry), S2L_E_CUDA. */
 s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinned,
                       void* compute_stream, void* copy_stream, s2l_ctx** out);
 

@@ -719,3 +719,42 @@ def test_streaming_scheduler_on_device(policy, preemption):
 
 def lib_reqs(tw):
     return set(tw.ora.reqs)
+
+
+def test_swap_round_trip_full_size_c4_blocks():
+    """a5/a6 at the C4 / bench size: 512 blocks of M_block = 2 MiB (L = 32, Llama-3-8B KV)
+    of four interleaved requests (scattered ids) swapped out and back in, twice (the second
+    round reuses CPU ids freed by the first and GPU ids released under the Z9 cooling rule);
+    every request's blocks must come back bit-identical (whole blocks, Z12)."""
+    L, nblk = 32, 512
+    cfg = s2l.make_config(L, 32, 8, 128, 16, nblk + 64, nblk + 64, max_requests=8, max_blocks_per_request=nblk)
+    mb = s2l.block_bytes(cfg)
+    assert mb == 2 * 1024 * 1024
+    gpool = torch.empty((nblk + 64) * mb // 2, dtype=torch.bfloat16, device="cuda")
+    cpool = torch.empty((nblk + 64) * mb // 2, dtype=torch.bfloat16).pin_memory()
+    lib = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), torch.cuda.Stream(),
+                      swap_in_stream=torch.cuda.Stream())
+    rids = [0, 1, 2, 3]
+    g = torch.Generator(device="cuda").manual_seed(3)
+    kv = torch.randn(L, 4 * 512, 8, 128, generator=g, device="cuda").to(torch.bfloat16)
+    for r in rids:
+        lib.new_request(r, np.zeros(2048, np.int32))
+    for a in range(0, 2048, 512):
+        lib.append_chunk([(r, None, 512, i * 512) for i, r in enumerate(rids)], kv, kv)
+    lib.sync()
+    view = gpool.view(nblk + 64, mb // 2)
+    before = {r: view[torch.tensor(lib.block_table(r), device="cuda")].clone() for r in rids}
+    for _ in range(2):
+        assert lib.swap_out(rids) == nblk * mb
+        cview = cpool.view(nblk + 64, mb // 2)
+        lib.sync()
+        for r in rids:                                     # host copy == device blocks before
+            got = cview[torch.tensor(lib.block_table(r))].cuda()
+            assert torch.equal(got.view(torch.int16), before[r].view(torch.int16)), r
+        view.fill_(0)                                      # freed GPU blocks: clobber them
+        torch.cuda.synchronize()                           # (caller-side write: finish it first)
+        assert lib.swap_in(rids) == nblk * mb
+        lib.sync()
+        for r in rids:
+            got = view[torch.tensor(lib.block_table(r), device="cuda")]
+            assert torch.equal(got.view(torch.int16), before[r].view(torch.int16)), r
