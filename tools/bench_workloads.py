@@ -76,7 +76,21 @@ def c3():
     torch.cuda.synchronize()
     ti = ctx.timing_read()
     ms = s0.elapsed_time(s1)
-    return {"workload": "C3 update round (BJ:L9)", "requests": R, "tokens_recomputed": int(sum(rows)),
+    # sampled-row parity at full size: rows {0, 1, n-2, n-1} + 4 random of 4
+    # requests, all heads, vs the fp64 oracle over the request's new input
+    from oracle.attention import attention_rows
+    og = oo.float().cpu().numpy().astype(np.float64)
+    rng = np.random.default_rng(3)
+    worst = 0.0
+    for r in (0, 7, 19, 31):
+        n, p0 = rows[r], int(ps[r])
+        rs = sorted(set([0, 1, n - 2, n - 1] + rng.integers(0, n, 4).tolist()))
+        o_ref, _ = attention_rows(data[r][0][p0:], data[r][1][0], data[r][2][0], p0, rs)
+        got = og[int(off[r]):int(off[r]) + n][rs]
+        err = np.abs(got - o_ref).max(-1) / np.maximum(np.abs(o_ref).max(-1), 1e-6)
+        worst = max(worst, float(err.max()))
+    parity = {"requests_checked": 4, "max_normwise_err": worst, "tol": 2e-2, "pass": worst <= 2e-2}
+    return {"workload": "C3 update round (BJ:L9)", "requests": R, "tokens_recomputed": int(sum(rows)), "parity": parity,
             "attn_flops": flops, "round_ms": ms, "round_tflops": flops / (ms * 1e-3) / 1e12,
             "attn_kernel_tflops": flops / (ti["attn_ms"] * 1e-3) / 1e12, "append_ms": ti["append_ms"],
             "invalidate_us_per_request": inval_us}
@@ -115,7 +129,20 @@ def c5():
     torch.cuda.synchronize()
     ti = ctx.timing_read()
     ms = s0.elapsed_time(s1) / 3
-    return {"workload": "C5 single 128K request, 2K chunks, 64q/8kv (BJ:L11), 1 GPU all heads", "stream_ms": ms,
+    # sampled-row parity of the last stream replay at full size: chunks 0, 31, 63, rows
+    # {0, n-1} + 2 random, all 64 heads, vs the fp64 oracle
+    from oracle.attention import attention_rows
+    rng = np.random.default_rng(5)
+    worst = 0.0
+    for j in (0, 31, 63):
+        a = j * chunk
+        rs = sorted(set([0, chunk - 1] + rng.integers(0, chunk, 2).tolist()))
+        o_ref, _ = attention_rows(q[a:a + chunk], k[0], v[0], a, rs)
+        got = O[j].float().cpu().numpy().astype(np.float64)[rs]
+        err = np.abs(got - o_ref).max(-1) / np.maximum(np.abs(o_ref).max(-1), 1e-6)
+        worst = max(worst, float(err.max()))
+    parity = {"chunks_checked": [0, 31, 63], "max_normwise_err": worst, "tol": 2e-2, "pass": worst <= 2e-2}
+    return {"workload": "C5 single 128K request, 2K chunks, 64q/8kv (BJ:L11), 1 GPU all heads", "parity": parity, "stream_ms": ms,
             "attn_flops": flops, "tflops": flops / (ms * 1e-3) / 1e12,
             "attn_kernel_tflops": 3 * flops / (ti["attn_ms"] * 1e-3) / 1e12,
             "prefill_tokens_per_s": T / (ms * 1e-3)}
