@@ -108,10 +108,18 @@ class PressureDriver:
     Every library call is appended to `log` as (op, args, result) for the oracle replay.
     """
 
-    def __init__(self, ctx, plans, k: int, budget: int, evict_ahead: int = 2):
+    def __init__(self, ctx, plans, k: int, budget: int, evict_ahead: int = 2, cost=None):
+        """cost: None -> every victim is swapped (the C4 definition, BJ:L10); else a callable
+        cost(num_computed, num_blocks) -> "recompute" | "swap" (the paper's cost-based
+        preemption, P:L79 / §4.3): a recompute victim drops its blocks (no D2H) and later
+        re-prefills its computed prefix."""
         self.ctx, self.k, self.budget = ctx, k, budget
         self.evict_ahead = evict_ahead
+        self.cost = cost
+        self.recompute_preemptions = 0
+        self.recomputed_tokens = 0
         self.plans = {p.rid: p for p in plans}
+        self.work = {p.rid: list(p.work) for p in plans}      # own copy: recompute inserts items
         self.next_work = {p.rid: 0 for p in plans}
         self.last_step = {p.rid: -1 for p in plans}
         self.order = sorted(self.plans)
@@ -130,7 +138,7 @@ class PressureDriver:
 
     # ---- planning ------------------------------------------------------------------------
     def live(self):
-        return [r for r in self.order if r in self.plans and self.next_work[r] < len(self.plans[r].work)]
+        return [r for r in self.order if r in self.plans and self.next_work[r] < len(self.work[r])]
 
     def plan(self, peek: bool = False):
         """Next step's requests: round-robin from the cursor, one work item each, until the
@@ -144,7 +152,7 @@ class PressureDriver:
         rot = live[start:] + live[:start]
         sel, used = [], 0
         for r in rot:
-            n = self.plans[r].work[self.next_work[r]].n_kv
+            n = self.work[r][self.next_work[r]].n_kv
             if sel and used + n > self.budget:
                 break
             sel.append(r)
@@ -161,7 +169,7 @@ class PressureDriver:
         need = 0
         for r in sel:
             q = info[r]
-            w = self.plans[r].work[self.next_work[r]]
+            w = self.work[r][self.next_work[r]]
             need += max(0, self._blocks(q["num_computed"] + w.n_kv) - q["num_blocks"])
             if q["tier"] == TIER_CPU:
                 need += q["num_blocks"]
@@ -204,7 +212,7 @@ class PressureDriver:
         step and the next compute, and (reading Z9) the ids it releases are allocated only
         after every other free id, so the next step's appends and swap-ins avoid them."""
         for r in sel:
-            w = self.plans[r].work[self.next_work[r]]
+            w = self.work[r][self.next_work[r]]
             if w.new_input is not None:
                 res = self.ctx.invalidate_lcp(r, w.new_input)
                 self.log.append(("invalidate", (r, w.new_input), res))
@@ -233,6 +241,15 @@ class PressureDriver:
             more = self._pick(want, free_after, keep, set(protect))
             if more is not None:
                 victims += more[0]
+        if victims and self.cost is not None:
+            swap_v = []
+            for r in victims:
+                q = self.ctx.query(r)
+                if self.cost(q["num_computed"], q["num_blocks"]) == "recompute":
+                    self._preempt_recompute(r, q["num_computed"])
+                else:
+                    swap_v.append(r)
+            victims = swap_v
         if victims:
             b = self.ctx.swap_out(victims)
             self.log.append(("swap_out", tuple(victims), b))
@@ -244,11 +261,26 @@ class PressureDriver:
             self.swapped_in_bytes += b
             self.swap_in_calls += 1
 
+    def _preempt_recompute(self, r, nc):
+        """Recompute preemption: free the blocks now; the computed prefix [0, nc) of
+        the current input is prefilled again, in budget-sized pieces, before its next work."""
+        self.ctx.preempt_recompute(r)
+        self.log.append(("preempt", (r,), 0))
+        self.recompute_preemptions += 1
+        self.recomputed_tokens += nc
+        pieces, left = [], nc
+        while left > 0:
+            m = min(left, self.budget)
+            pieces.append(Work(n_kv=m))
+            left -= m
+        i = self.next_work[r]
+        self.work[r][i:i] = pieces
+
     def items(self, sel):
         """(append items, prefill items, n rows): rows of the step are packed in sel order."""
         app, pre, row = [], [], 0
         for r in sel:
-            w = self.plans[r].work[self.next_work[r]]
+            w = self.work[r][self.next_work[r]]
             nc = self.ctx.query(r)["num_computed"]
             app.append((r, w.append_tokens, w.n_kv, row))
             pre.append((r, nc, w.n_kv, row))
@@ -267,7 +299,7 @@ class PressureDriver:
         for r in sel:
             self.next_work[r] += 1
             self.last_step[r] = self.step
-            if self.next_work[r] == len(self.plans[r].work):
+            if self.next_work[r] == len(self.work[r]):
                 self.deferred.append(r)
                 del self.plans[r]
         self.step += 1

@@ -10,7 +10,7 @@ from synth import workloads as W
 from tests.harness import Twin
 
 
-def _run_host(seed, n_req, lo, hi, budget, frac=0.5, k=16):
+def _run_host(seed, n_req, lo, hi, budget, frac=0.5, k=16, cost=None):
     plans = pressure.c4_plans(seed, n_req, lo=lo, hi=hi, budget=budget)
     ws = pressure.working_set_blocks(plans, k)
     biggest = max(-(-p.total // k) for p in plans)
@@ -19,7 +19,7 @@ def _run_host(seed, n_req, lo, hi, budget, frac=0.5, k=16):
     cfg = s2l.make_config(1, 1, 1, 8, k, ng, nc, max_requests=n_req, max_blocks_per_request=biggest + 1)
     lib = s2l.Context(cfg, host_only=True)
     tw = Twin(lib, k, ng, nc, n_req, biggest + 1)
-    drv = pressure.PressureDriver(tw, plans, k, budget)
+    drv = pressure.PressureDriver(tw, plans, k, budget, cost=cost)
 
     def execute(sel, app, pre, rows):
         tw.append_chunk(app, None, None, kv_rows=rows)
@@ -105,3 +105,16 @@ def test_c4_recipe():
     a = np.median([p.total for p in plans if p.mode == "append"])
     u = np.median([p.total for p in plans if p.mode == "update"])
     assert 3500 < a < 9000 and 7000 < u < 13000
+
+
+def test_cost_based_preemption_recomputes_small_victims():
+    """With a cost rule (P:L79 / §4.3) small victims are dropped and re-prefilled instead of
+    swapped; bookkeeping still mirrors the oracle call by call, every request finishes, and the
+    recomputed tokens are exactly the dropped prefixes."""
+    rule = lambda nc, nb: "recompute" if nc < 400 else "swap"
+    plans, drv, steps, ng, ws = _run_host(13, 24, 64, 1024, 512, cost=rule)
+    assert drv.recompute_preemptions > 0 and drv.swap_out_calls > 0
+    assert not drv.live() and not drv.plans
+    want = sum(w.n_kv for p in plans for w in p.work) + drv.recomputed_tokens
+    assert drv.tokens == want
+    assert drv.ctx.lib.free_blocks() == (ng, drv.ctx.ora.num_cpu_blocks)

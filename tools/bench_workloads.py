@@ -224,7 +224,14 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
            "working_set_blocks": ws, "gpu_pool_blocks": ng, "cpu_pool_blocks": ncpu, "budget": budget}
     flops_total = 0.0
     big = None
-    for mode in ("warm", "compute_only", "serial", "overlap"):
+    # the paper's rule: recompute a victim if C_recomp(l) <= 2 C_swap(ceil(l/k)); here
+    # C_recomp = L layers of causal attention at ~1 PFLOP/s, C_swap = blocks x M_block / 55 GB/s
+    def cost_rule(nc, nb):
+        rec = L * 4.0 * D * geo_hq * nc * nc / 2 / 1.0e15
+        swp = nb * mb / 55e9
+        return "recompute" if rec <= 2 * swp else "swap"
+
+    for mode in ("warm", "compute_only", "serial", "overlap", "overlap_cost"):
         if mode == "compute_only":     # same stream with the whole working set resident
             cfg_big = s2l.make_config(L, geo_hq, geo_hkv, D, K, ws, 0, max_requests=n_req,
                                       max_blocks_per_request=16384 // K)
@@ -233,7 +240,8 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
         else:
             ctx = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), cs, swap_in_stream=cs_in)
         wrap = pressure.SwapTimer(ctx, serial=(mode == "serial"), copy_stream=cs, swap_in_stream=cs_in)
-        drv = pressure.PressureDriver(wrap, plans, K, budget, evict_ahead=int(os.environ.get("C4_AHEAD", "2")))
+        drv = pressure.PressureDriver(wrap, plans, K, budget, evict_ahead=int(os.environ.get("C4_AHEAD", "2")),
+                                      cost=cost_rule if mode == "overlap_cost" else None)
         step_ev = []
         segs, snaps, flops = {}, [], [0.0]
 
@@ -300,7 +308,9 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
                          "copy_in": {"bytes": cm.get("in", (0, 0))[0], "ms": cm.get("in", (0, 0))[1]},
                          "tokens": drv.tokens, "tokens_per_s": drv.tokens / (ms * 1e-3),
                          "swap_out_bytes": drv.swapped_out_bytes, "swap_in_bytes": drv.swapped_in_bytes,
-                         "swap_out_calls": drv.swap_out_calls, "swap_in_calls": drv.swap_in_calls}
+                         "swap_out_calls": drv.swap_out_calls, "swap_in_calls": drv.swap_in_calls,
+                         "recompute_preemptions": drv.recompute_preemptions,
+                         "recomputed_tokens": drv.recomputed_tokens}
         if snaps:
             kh = src_k[L - 1].view(torch.int16).cpu().numpy().view(np.uint16)
             vh = src_v[L - 1].view(torch.int16).cpu().numpy().view(np.uint16)
