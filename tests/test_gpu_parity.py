@@ -553,8 +553,8 @@ def test_stream_hazards_without_host_syncs():
         assert err.max() <= 2e-2, (r, layer, float(err.max()))
 
 
-@pytest.mark.parametrize("serial", [False, True])
-def test_c4_pressure_driver_on_device(serial):
+@pytest.mark.parametrize("serial,cost", [(False, False), (True, False), (False, True)])
+def test_c4_pressure_driver_on_device(serial, cost):
     """The C4 driver (paper_2604_16395_b200.pressure) at reduced size on the device: 16
     append / update requests, GPU pool 50% of the working set, swaps overlapping compute (or
     serialised), no host synchronisation inside the stream.  Bookkeeping is mirrored into the
@@ -585,7 +585,8 @@ def test_c4_pressure_driver_on_device(serial):
     qh = src_q.view(torch.int16).cpu().numpy().view(np.uint16)
     segs, checks, byte_checks = {}, [], []
     rng = np.random.default_rng(0)
-    drv = pressure.PressureDriver(pressure.SwapTimer(tw, serial=serial), plans, K, budget)
+    rule = (lambda nc, nb: "recompute" if nc < 700 else "swap") if cost else None
+    drv = pressure.PressureDriver(pressure.SwapTimer(tw, serial=serial), plans, K, budget, cost=rule)
     out_holder = {}
 
     def on_step(sel, app, pre, rows):
@@ -617,6 +618,8 @@ def test_c4_pressure_driver_on_device(serial):
     lib.sync()
     torch.cuda.synchronize()
     assert drv.swap_out_calls > 0 and drv.swap_in_calls > 0
+    if cost:
+        assert drv.recompute_preemptions > 0
     assert lib.free_blocks() == (ng, ncpu)
     for r, seg, q_pos, row, rows_s, o in checks:
         kk = np.concatenate([kh[L - 1, a:a + m] for a, m in seg])
