@@ -14,16 +14,20 @@
  *   - a device block table [max_requests][max_blocks_per_request] int32 (library-owned)
  *     read by the kernels; block j of a request holds positions [j*k, j*k+k).
  *
- * Allocation (Z9): every allocation takes the LOWEST free ids of the tier, ascending;
+ * Allocation (Z9): every allocation takes the LOWEST free ids of the tier, ascending, except
+ * that the GPU ids released by the most recent swap-out come after every other free GPU id;
  * requests/items of one call are served in call order.  Every call that can fail is
  * all-or-nothing: arguments and capacity are validated before any state changes.
  *
- * Streams: `compute_stream` runs append/patch/attention kernels; `copy_stream` runs swap
- * copies (cudaStream_t handles passed as void*; NULL = legacy default stream).  The library
- * inserts the event waits that make reuse of swapped / freed blocks safe.
- * Pointer arguments to device/pinned buffers must stay valid until the work enqueued by the
- * call has completed on its stream (stream-ordered semantics).  Host token arrays and item
- * arrays are copied before the call returns.
+ * Streams: `compute_stream` runs append/patch/attention kernels; `copy_stream` runs swap-out
+ * copies and a second stream (library-created, or s2l_set_swap_in_stream) runs swap-in copies
+ * (cudaStream_t handles passed as void*; NULL = legacy default stream).  The library inserts
+ * only the event waits real conflicts need (per request and per block, DESIGN.md §5 stream
+ * hazards), so swaps overlap unrelated compute.  Per-call descriptors of small calls travel in
+ * the kernel parameters, larger ones through a pinned staging ring.  Pointer arguments to
+ * device/pinned buffers must stay valid until the work enqueued by the call has completed on
+ * its stream (stream-ordered semantics).  Host token arrays and item arrays are copied before
+ * the call returns.
  *
  * Errors: every function returns an s2l_status.  State/argument errors are detected before
  * any mutation.  A CUDA error is reported as S2L_E_CUDA and is sticky for the context.
