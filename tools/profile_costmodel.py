@@ -8,7 +8,11 @@
   swap_latency(C): s2l_swap_out then s2l_swap_in of C blocks of M_block = 2 MiB (L = 32,
       P:L188 "2 MB"), per direction, on the copy stream.
 
-    python tools/profile_costmodel.py [out.json]
+  --gemm: the recompute curve also runs the Llama-3-8B dense layers of the same tokens as
+      cuBLAS bf16 GEMMs with random weights (QKV, O, gate/up, down per layer), i.e. the whole
+      C_prefill of the paper -- library GEMMs, not this repo's kernels.
+
+    python tools/profile_costmodel.py [out.json] [--gemm]
 """
 import json
 import os
@@ -31,7 +35,27 @@ def dev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).view(torch.bfloat16).cuda()
 
 
-def recompute_point(T, q, k, v):
+HIDDEN, INTER = 4096, 14336
+
+
+class Dense:
+    """Per-layer dense work of Llama-3-8B for n tokens (cuBLAS bf16, random weights)."""
+
+    def __init__(self, nmax):
+        g = torch.Generator(device="cuda").manual_seed(1)
+        mk = lambda a, b: (torch.randn(a, b, generator=g, device="cuda") * 0.02).to(torch.bfloat16)
+        self.w = [mk(HIDDEN, (H_Q + 2 * H_KV) * D), mk(H_Q * D, HIDDEN), mk(HIDDEN, 2 * INTER), mk(INTER, HIDDEN)]
+        self.x = mk(nmax, HIDDEN)
+        self.h = mk(nmax, INTER)
+
+    def layer(self, n):
+        torch.matmul(self.x[:n], self.w[0])
+        torch.matmul(self.x[:n], self.w[1])
+        torch.matmul(self.x[:n], self.w[2])
+        torch.matmul(self.h[:n], self.w[3])
+
+
+def recompute_point(T, q, k, v, dense=None):
     cfg = s2l.make_config(1, H_Q, H_KV, D, K, T // K + 8, 0, max_requests=1, max_blocks_per_request=T // K + 8)
     pool = torch.empty(cfg.num_gpu_blocks * s2l.block_bytes(cfg) // 2, dtype=torch.bfloat16, device="cuda")
     ctx = s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None)
@@ -46,6 +70,8 @@ def recompute_point(T, q, k, v):
         for (a, n), qq, kk, vv, oo in zip(chunks, Q, Kd, Vd, O):
             ctx.append_chunk([(0, None, n, 0)], kk, vv)
             ctx.prefill_batch(0, [(0, a, n, 0)], qq, oo)
+            if dense is not None:
+                dense.layer(n)
         ctx.release(0)
 
     for _ in range(2):
@@ -68,8 +94,8 @@ def swap_points(counts):
     mb = s2l.block_bytes(cfg)
     gp = torch.empty((nmax + 8) * mb // 2, dtype=torch.bfloat16, device="cuda")
     cp = torch.empty((nmax + 8) * mb // 2, dtype=torch.bfloat16).pin_memory()
-    cs = torch.cuda.Stream()
-    ctx = s2l.Context(cfg, gp, cp, torch.cuda.current_stream(), cs)
+    cs, cs_in = torch.cuda.Stream(), torch.cuda.Stream()      # swap-out / swap-in streams
+    ctx = s2l.Context(cfg, gp, cp, torch.cuda.current_stream(), cs, swap_in_stream=cs_in)
     kv = torch.zeros(L_MODEL, 1024, H_KV, D, dtype=torch.bfloat16, device="cuda")
     out = {}
     for c in counts:
@@ -82,15 +108,17 @@ def swap_points(counts):
         ctx.sync()
         best_o = best_i = 1e9
         for _ in range(3):
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
             e0.record(cs)
             ctx.swap_out([1])
             e1.record(cs)
+            ctx.sync()
+            e2.record(cs_in)
             ctx.swap_in([1])
-            e2.record(cs)
+            e3.record(cs_in)
             ctx.sync()
             best_o = min(best_o, e0.elapsed_time(e1) * 1e-3)
-            best_i = min(best_i, e1.elapsed_time(e2) * 1e-3)
+            best_i = min(best_i, e2.elapsed_time(e3) * 1e-3)
         out[c] = (best_o, best_i)
         ctx.release(1)
     ctx.close()
@@ -98,18 +126,23 @@ def swap_points(counts):
 
 
 def main():
-    path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "costmodel_b200.json")
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    gemm = "--gemm" in sys.argv
+    path = args[0] if args else os.path.join(ROOT, "gpurun_out", "costmodel_b200%s.json" % ("_full" if gemm else ""))
     torch.cuda.set_device(0)
     Ts = [1024 * 2 ** i for i in range(8)]                # 1K .. 128K
     toks = W.request_tokens(W.seed_of(4), 0, Ts[-1])
     q, k, v = W.request_qkv(W.seed_of(4), toks, W.LLAMA3_8B)
-    rec = [recompute_point(T, q[:T], k[:, :T], v[:, :T]) * L_MODEL for T in Ts]
+    dense = Dense(CHUNK) if gemm else None
+    rec = [recompute_point(T, q[:T], k[:, :T], v[:, :T], dense) * L_MODEL for T in Ts]
     counts = [1, 8, 64, 256, 512, 1024]
     sw, mb = swap_points(counts)
     swap_s = [0.5 * (sw[c][0] + sw[c][1]) for c in counts]
     cm = CostModel(K, PiecewiseLinear(Ts, rec), PiecewiseLinear(counts, swap_s),
                    {"gpu": torch.cuda.get_device_name(0), "m_block_bytes": mb, "layers": L_MODEL,
-                    "recompute": "append + chunked-prefill attention only (no model GEMMs), 8192-token chunks",
+                    "recompute": ("append + chunked-prefill attention + cuBLAS dense layers (random weights)"
+                                  if gemm else "append + chunked-prefill attention only (no model GEMMs)")
+                                 + ", 8192-token chunks",
                     "swap_out_s": {c: sw[c][0] for c in counts}, "swap_in_s": {c: sw[c][1] for c in counts}})
     cm.save(path)
     print(json.dumps({"recompute_s": dict(zip(Ts, rec)), "swap_s_per_direction": dict(zip(counts, swap_s)),

@@ -133,7 +133,9 @@ def main():
     seed = 2026
     tr = (traces.crawler_trace if args.workload == "crawler" else traces.anns_trace)(
         seed, args.n, args.qps, delay_scale=args.delay_scale)
-    cmp = os.path.join(ROOT, "profiles", "r01", "costmodel_b200.json")
+    # cost model matching the simulated prefill: with --gemm the full-prefill profile (attention +
+    # append + dense layers), else attention + append only
+    cmp = os.path.join(ROOT, "profiles", "r01", "costmodel_b200_full.json" if args.gemm else "costmodel_b200.json")
     cm = costmodel.CostModel.load(cmp) if os.path.exists(cmp) else None
     mb = 2 * args.layers * K * H_KV * D * 2
     gpool = torch.empty(args.gpu_blocks * mb // 2, dtype=torch.bfloat16, device="cuda")
@@ -141,7 +143,7 @@ def main():
     out = {"workload": f"TTFT {args.workload} trace (synthetic, synth/traces.py)", "qps": args.qps,
            "queries": args.n, "layers": args.layers, "gemm": args.gemm, "budget": args.budget,
            "gpu_blocks": args.gpu_blocks, "cpu_blocks": args.cpu_blocks, "delay_scale": args.delay_scale,
-           "cost_model": "profiles/r01/costmodel_b200.json" if cm else None, "runs": []}
+           "cost_model": os.path.relpath(cmp, ROOT) if cm else None, "runs": []}
     for p in args.policies.split(","):
         res = run(tr, "DEFAULT" if p == "NS" else p, p != "NS", args, cm, (gpool, cpool))
         out["runs"].append(res)
