@@ -175,6 +175,18 @@ def run_step(ctx, S: "Stream", q=None, k=None, v=None, o=None):
         ctx.release(r)
 
 
+def run_step_fused(ctx, S: "Stream"):
+    """The C2 step through the fused path (NEXT-2): reserve the chunk's blocks, then one
+    append + attention launch per chunk (s2l_prefill_append)."""
+    for r, t in zip(S.rids, S.toks):
+        ctx.new_request(r, t)
+    for j in range(S.steps):
+        ctx.append_chunk(S.items_a[j], None, None, kv_rows=S.k[j].shape[1])
+        ctx.prefill_append(0, S.items_p[j], S.q[j], S.k[j][0], S.v[j][0], S.o[j])
+    for r in S.rids:
+        ctx.release(r)
+
+
 def timed(fn, steps, warmup, dist=None):
     """W untimed warm-ups, then K steps bracketed by barrier + synchronize; max over ranks."""
     import torch
@@ -531,6 +543,17 @@ def main():
     line["parity"] = parity_check(S, data, rank, world, dist)
 
     if not args.no_side and rank == 0:
+        # NEXT-2: the same step through the fused append + attention path (s2l_prefill_append),
+        # timed alternately with the plain step so clock drift affects both alike
+        ffn = lambda: run_step_fused(ctx, S)
+        fms, pms = [], []
+        for _ in range(3):
+            fms.append(timed(ffn, max(2, args.steps // 2), 1, None) / max(2, args.steps // 2))
+            pms.append(timed(fn, max(2, args.steps // 2), 1, None) / max(2, args.steps // 2))
+        fms, pms = sorted(fms)[1], sorted(pms)[1]
+        line["next2_fused"] = {"value": flops_rank / (fms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": fms,
+                               "plain_ms_per_step_same_window": pms,
+                               "path": "s2l_append_chunk (reserve) + s2l_prefill_append: one launch per chunk"}
         # e2e through the C ABI with host buffers
         S_host = Stream(rids, toks, data, dev, pinned=True)
         dev_bufs = tuple([torch.empty_like(S.q[0] if i in (0, 3) else S.k[0]) for _ in range(E2E_BUFS)]

@@ -153,6 +153,9 @@ s2l_status s2l_preempt_recompute(s2l_ctx* ctx, int64_t req_id);
  *   n_tokens/n_kv/kv_row < 0, kv_row+n_kv > kv_rows, n_kv > len(input)+n_tokens-nc, or
  *   ceil((nc+n_kv)/k) > max_blocks_per_request -> E_INVAL;
  *   total new blocks > free GPU blocks -> E_NO_GPU_BLOCKS.
+ * Reserve (NEXT-2): k = v = NULL on a device context does all of the above except the data
+ * write; the K/V of each layer are then written by s2l_prefill_append (until then the rows are
+ * undefined).  Exactly one of k / v NULL -> E_INVAL.
  * On any error nothing changes (all-or-nothing). */
 s2l_status s2l_append_chunk(s2l_ctx* ctx, int32_t n_items, const s2l_append_item* items,
                             const void* k, const void* v, int64_t kv_rows);
@@ -181,6 +184,20 @@ s2l_status s2l_invalidate_lcp(s2l_ctx* ctx, int64_t req_id, const int32_t* new_t
 s2l_status s2l_prefill_batch(s2l_ctx* ctx, int32_t layer, int32_t n_items,
                              const s2l_prefill_item* items, const void* q, void* o, float* lse,
                              int64_t q_rows);
+
+/* Fused append + attention for one layer (a3 + a4, P:L59 / P:L67 / P:L69): for
+ * each item, first the K/V rows of positions [q_pos, q_pos+n_q) of layer `layer` are taken from
+ * k / v rows [q_row, q_row+n_q) and stored in the pool (as s2l_append_chunk stores them), then
+ * the attention of s2l_prefill_batch is computed over the prefix plus those rows.  The blocks
+ * must already be held (s2l_append_chunk, normally in reserve mode with k = v = NULL).
+ *   k, v: device [q_rows][h_kv][d] bf16 of this layer (same row indexing as q).
+ * When every q_pos is a multiple of k (and the tensor-core kernel runs) one kernel does both:
+ * it reads the chunk's K/V tiles from k / v and each work unit writes the blocks starting in its
+ * own token range to the pool; otherwise a one-layer append launch precedes the attention.
+ * Errors: those of s2l_prefill_batch; k or v NULL, or a request repeated in the call -> E_INVAL. */
+s2l_status s2l_prefill_append(s2l_ctx* ctx, int32_t layer, int32_t n_items,
+                              const s2l_prefill_item* items, const void* q, const void* k,
+                              const void* v, void* o, float* lse, int64_t q_rows);
 
 /* Swap-out (a5): all-or-nothing over the listed requests (all GPU tier, no
  * duplicates): allocate |blocks| CPU ids per request (lowest free), copy every block GPU ->

@@ -89,6 +89,14 @@ struct TcParams {
   float* ws_ml;    // [pieces][2][128][2] running max (log2 units) and row sum
   int32_t* ws_cnt;
   uint32_t* trace;   // S2L_TRACE builds only: per-event SM clock stamps of CTA 0
+  // fused append (NEXT-2, v2 only): the chunk's K/V (positions >= q_pos, block-aligned) are
+  // read from the caller's rows of this layer (tmap_kin / tmap_vin: [rows][h_kv][d], row
+  // q_row + t) instead of the pool, and each unit writes the blocks that start inside its own
+  // token range to the pool (TMA store; a partial last block by plain stores into pool).
+  int32_t fuse;
+  __nv_bfloat16* pool;
+  CUtensorMap tmap_kin, tmap_vin;     // box {64, 1, k}: one block of one kv head
+  CUtensorMap tmap_kin_t, tmap_vin_t; // box {64, 1, 128}: a whole 128-key tile
   int32_t n_inl;     // > 0: the items are inl[0 .. n_inl) (by value), not *items
   AttnItemDev inl[kInlineAttnItems];
 };
@@ -154,6 +162,19 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const void* tmap, uint
       "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(w), "r"(bar)
       : "memory");
 }
+// TMA store smem -> global (bulk async-group of the issuing thread).
+__device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(tmap),
+               "r"(x), "r"(y), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the smem sources of this thread's committed stores may be overwritten
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// this thread's committed stores are complete (visible in global memory)
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -779,6 +800,8 @@ __device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
       : "memory");
 }
+// kFuse: the fused-append instantiation (NEXT-2); the plain one compiles without that code.
+template <bool kFuse>
 __global__ void __launch_bounds__(v2::kThreads, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_kv,
@@ -887,19 +910,32 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       };
       int32_t next_id = (lane < nb_tile) ? load_id(0) : 0;
       uint32_t rp = 0;
+      // fused append: blocks starting at or after q_pos come from the caller's rows; this unit
+      // writes the blocks whose first position lies in its token range [wr_lo, wr_hi)
+      const bool fuse = kFuse && p.fuse != 0;
+      const int64_t wr_lo = it.q_pos + tok0, wr_hi = it.q_pos + min(tok0 + 2 * toks, it.n_q);
+      bool st_pending = false;                          // lane 0 has TMA stores in flight
       for (int32_t j = 0; j < nT; ++j) {
         const int32_t cur_id = next_id;
         if (j + 1 < nT && lane < nb_tile) next_id = load_id(j + 1);   // prefetch the next ids
         int32_t ids[8];
 #pragma unroll
         for (int b = 0; b < 8; ++b) ids[b] = __shfl_sync(0xffffffffu, cur_id, b);
-        bool run = (jb + j + 1) * nb_tile <= nblk_valid;   // whole tile inside the table
+        const int64_t tpos = (int64_t)(jb + j) * kBN;     // first key position of the tile
+        const bool fresh = fuse && tpos + kBN > it.q_pos; // tile holds chunk blocks
+        bool run = !fresh && (jb + j + 1) * nb_tile <= nblk_valid;   // whole tile inside the table
 #pragma unroll
         for (int b = 1; b < 8; ++b)
           if (b < nb_tile) run = run && (ids[b] == ids[0] + b);
+        uint32_t slot[2];
 #pragma unroll
         for (int kind = 0; kind < 2; ++kind, ++rp) {
           const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
+          slot[kind] = s;
+          if (st_pending) {                             // the stores still read a ring slot
+            if (lane == 0) bulk_wait_read();
+            st_pending = false;
+          }
           mbar_wait(bar(WB_RE + s), ph ^ 1);
           if (lane == 0 && run) {
             // consecutive block ids: two 4-D boxes (d halves) cover the whole 128-key tile
@@ -907,39 +943,83 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
             const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
             tma_load_4d(dst, &tmap_kv4, bar(WB_RF + s), 0, 0, lkh[kind], ids[0]);
             tma_load_4d(dst + kAtom, &tmap_kv4, bar(WB_RF + s), 64, 0, lkh[kind], ids[0]);
+          } else if (lane == 0 && fresh && tpos >= it.q_pos) {
+            // tile wholly inside the chunk: two boxes {64, 1, 128} of the caller's rows
+            mbar_expect_tx(bar(WB_RF + s), kTileBytes);
+            const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
+            const CUtensorMap* tin = kind ? &p.tmap_vin_t : &p.tmap_kin_t;
+            const int32_t z = (int32_t)(it.q_row + (tpos - it.q_pos));
+            tma_load_3d(dst, tin, bar(WB_RF + s), 0, kvh, z);
+            tma_load_3d(dst + kAtom, tin, bar(WB_RF + s), 64, kvh, z);
           } else if (lane == 0) {
             // one lane issues the whole tile: 2 boxes {64, k} (d halves) per block
-#ifdef S2L_EXP_HALF_LOAD   // timing experiment only: load one d-half of each K/V tile
-            mbar_expect_tx(bar(WB_RF + s), kTileBytes / 2);
-#else
             mbar_expect_tx(bar(WB_RF + s), kTileBytes);
-#endif
             const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
-#ifdef S2L_EXP_BOX32   // timing experiment only: boxes of 2 blocks (wrong rows, same bytes)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              if (b < nb_tile / 2) {
-                const int32_t y = ids[2 * b] * rows_per_block + row_kv[kind];
-                tma_load_2d(dst + b * 2 * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
-                tma_load_2d(dst + kAtom + b * 2 * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
-              }
-            }
-            if (false)
-#endif
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
               if (b < nb_tile) {
-                const int32_t y = ids[b] * rows_per_block + row_kv[kind];
-                tma_load_2d(dst + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
-#ifndef S2L_EXP_HALF_LOAD
-                tma_load_2d(dst + kAtom + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
+                const int64_t pos0 = tpos + b * p.kb;
+#ifdef S2L_EXP_FUSE_POOLREAD   // timing experiment only: chunk tiles from the pool (stale data)
+                if (false) {
+#else
+                if (fresh && pos0 >= it.q_pos) {
 #endif
+                  // chunk block: rows q_row + (pos0 - q_pos) .. of this layer's K or V input
+                  const CUtensorMap* tin = kind ? &p.tmap_vin : &p.tmap_kin;
+                  const int32_t z = (int32_t)(it.q_row + (pos0 - it.q_pos));
+                  tma_load_3d(dst + b * p.kb * 128, tin, bar(WB_RF + s), 0, kvh, z);
+                  tma_load_3d(dst + kAtom + b * p.kb * 128, tin, bar(WB_RF + s), 64, kvh, z);
+                } else {
+                  const int32_t y = ids[b] * rows_per_block + row_kv[kind];
+                  tma_load_2d(dst + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
+                  tma_load_2d(dst + kAtom + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
+                }
+              }
+            }
+          }
+          __syncwarp();
+        }
+#ifdef S2L_EXP_FUSE_NOWRITE    // timing experiment only: no pool writes
+        if (false) {
+#else
+        if (fresh && tpos + kBN > wr_lo && tpos < wr_hi) {
+#endif
+          // write this unit's chunk blocks of the tile (K and V) from the ring to the pool
+#pragma unroll
+          for (int kind = 0; kind < 2; ++kind) {
+            const uint32_t s = slot[kind], ph = ((rp - 2 + kind) / WNST) & 1;
+            mbar_wait(bar(WB_RF + s), ph);
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+              const int64_t pos0 = tpos + b * p.kb;
+              if (b >= nb_tile || pos0 < wr_lo || pos0 >= wr_hi) continue;
+              const uint32_t src = sb + WOFF_RING + s * kTileBytes + b * p.kb * 128;
+              const int32_t y = ids[b] * rows_per_block + row_kv[kind];
+              const int64_t valid = min((int64_t)p.kb, it.q_pos + it.n_q - pos0);
+              if (valid == p.kb) {
+                if (lane == 0) {
+                  tma_store_2d(&tmap_kv, src, 0, y);
+                  tma_store_2d(&tmap_kv, src + kAtom, 64, y);
+                  bulk_commit();
+                }
+                st_pending = true;
+              } else {
+                // partial last block: the valid rows by plain 16-byte copies (SW128 un-swizzle)
+                for (int32_t e = lane; e < (int32_t)valid * 16; e += 32) {
+                  const int32_t r = e >> 4, h = (e >> 3) & 1, c = e & 7;
+                  uint4 val;
+                  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                               : "=r"(val.x), "=r"(val.y), "=r"(val.z), "=r"(val.w)
+                               : "r"(src + h * kAtom + r * 128 + ((c ^ (r & 7)) << 4)));
+                  *reinterpret_cast<uint4*>(p.pool + ((int64_t)y + r) * kD + h * 64 + c * 8) = val;
+                }
               }
             }
           }
           __syncwarp();
         }
       }
+      if (kFuse && lane == 0) bulk_wait_all();
     } else if (warp == 1) {
       // ================= MMA issuer (whole warp, one elected lane issues) =================
       constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);
@@ -2707,6 +2787,30 @@ bool make_tmap_kv(void* out, const void* pool, int64_t num_blocks, int32_t L, in
   return true;
 }
 
+bool make_tmap_in(void* out, const void* k, const void* v, int64_t rows, int32_t h_kv, int32_t d,
+                  int32_t kb, const char** err) {
+  auto fn = encode_fn(err);
+  if (!fn) return false;
+  // one layer's K (out[0,128), out[256,384)) and V (out[128,256), out[384,512)) rows
+  // [rows][h_kv][d]; box {64, 1, kb} lands in shared memory exactly like the pool's per-block
+  // box {64, kb}, box {64, 1, 128} like a whole-tile block run
+  for (int i = 0; i < 4; ++i) {
+    cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)h_kv, (cuuint64_t)rows};
+    cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)h_kv * d * 2};
+    cuuint32_t box[3] = {64, 1, (cuuint32_t)(i < 2 ? kb : kBN)};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn((CUtensorMap*)((char*)out + 128 * i), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                    (void*)((i & 1) ? v : k), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      *err = "cuTensorMapEncodeTiled(k/v input) failed";
+      return false;
+    }
+  }
+  return true;
+}
+
 bool make_tmap_q(void* out, const void* q, int64_t q_rows, int32_t h_q, int32_t d, int32_t group,
                  const char** err) {
   auto fn = encode_fn(err);
@@ -2743,15 +2847,23 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
                            float* ws, int32_t max_pieces, int32_t* ws_cnt,
                            const int32_t* table, int32_t layer, const void* tmap_q,
                            const void* tmap_kv, void* o, float* lse, int32_t num_sms,
-                           int32_t flags, cudaStream_t st) {
+                           int32_t flags, cudaStream_t st, const void* tmap_in, void* pool) {
   const int variant = attn_tc_tiles_per_cta();
+  const bool fuse = (flags & kAttnFuseAppend) != 0;
+  if (fuse && (variant != 2 || (flags & (kAttnPersistent | kAttnSplitSoftmax | kAttnKV64)) ||
+               !tmap_in || !pool))
+    return cudaErrorInvalidValue;   // the fused append exists in attn_tc2_kernel only
   const bool persistent = (flags & kAttnPersistent) != 0;
   static bool attr_set[3] = {false, false, false};
   if (!attr_set[variant]) {
     cudaError_t e = variant == 2
-        ? cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM)
+        ? cudaFuncSetAttribute(attn_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM)
         : cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
+    if (variant == 2) {
+      e = cudaFuncSetAttribute(attn_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM);
+      if (e != cudaSuccess) return e;
+    }
     if (variant == 2) {
       e = cudaFuncSetAttribute(attn_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM);
       if (e != cudaSuccess) return e;
@@ -2795,6 +2907,14 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
     grid = split_begin + (total_units - split_begin) * split_s;
   }
   p.trace = g_trace;
+  p.fuse = fuse ? 1 : 0;
+  p.pool = (__nv_bfloat16*)pool;
+  if (fuse) {
+    memcpy(&p.tmap_kin, tmap_in, sizeof(CUtensorMap));
+    memcpy(&p.tmap_vin, (const char*)tmap_in + 128, sizeof(CUtensorMap));
+    memcpy(&p.tmap_kin_t, (const char*)tmap_in + 256, sizeof(CUtensorMap));
+    memcpy(&p.tmap_vin_t, (const char*)tmap_in + 384, sizeof(CUtensorMap));
+  }
   p.ws = ws;
   p.ws_ml = ws ? ws + (int64_t)max_pieces * 2 * 128 * kD : nullptr;
   p.ws_cnt = ws_cnt;
@@ -2809,7 +2929,7 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
     const int32_t g = grid < num_sms ? grid : num_sms;
     attn_tc3_kernel<<<g, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, p);
   } else if (variant == 2)
-    attn_tc2_kernel<<<grid, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, p);
+    (fuse ? attn_tc2_kernel<true> : attn_tc2_kernel<false>)<<<grid, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, p);
   else
     attn_tc_kernel<<<total_units, kThreads, SMEM_BYTES, st>>>(tq, tkv, p);
   return cudaGetLastError();

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(256) append_kernel(
     int32_t n_patches, int32_t* __restrict__ table, const uint4* __restrict__ k,
     const uint4* __restrict__ v, int64_t kv_rows, uint4* __restrict__ pool, int32_t L,
     int32_t h_kv, int32_t vec_per_row, int32_t kb_log2, const __grid_constant__ InlineBlob blob,
-    int32_t blob_mode, int32_t off_ids, int32_t off_patch) {
+    int32_t blob_mode, int32_t off_ids, int32_t off_patch, int32_t layer0) {
   const AppendItemDev* items_g = blob_mode ? reinterpret_cast<const AppendItemDev*>(blob.b) : items_p;
   const int32_t* ids_g = blob_mode ? reinterpret_cast<const int32_t*>(blob.b + off_ids) : ids_p;
   const TablePatch* patches = blob_mode ? reinterpret_cast<const TablePatch*>(blob.b + off_patch) : patches_p;
@@ -75,12 +75,13 @@ __global__ void __launch_bounds__(256) append_kernel(
   const AppendItemDev* items = staged ? s_items : items_g;
   const int32_t* ids = staged ? s_ids : ids_g;
   const int32_t lk = blockIdx.y;
-  const int32_t layer = lk >> 1, kind = lk & 1;
+  const int32_t layer = layer0 + (lk >> 1), kind = lk & 1;   // k/v hold layers layer0 ..
+
   if (lk == 0 && blockIdx.x == 0) {
     for (int32_t i = threadIdx.x; i < n_patches; i += blockDim.x) table[patches[i].idx] = patches[i].value;
   }
   const int32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint4* src = (kind ? v : k) + (int64_t)layer * kv_rows * h_kv * vec_per_row;
+  const uint4* src = (kind ? v : k) + (int64_t)(lk >> 1) * kv_rows * h_kv * vec_per_row;
   const int32_t vpt = h_kv * vec_per_row;                 // vectors per token row
   const int32_t kb = 1 << kb_log2;
   const int64_t row0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * kRowsPerWarp;
@@ -151,7 +152,7 @@ cudaError_t launch_append_impl(const Geometry& g, const AppendItemDev* items, in
                                const TablePatch* patches, int32_t n_patches, int32_t* table,
                                const void* k, const void* v, int64_t kv_rows, void* pool,
                                const InlineBlob& blob, int32_t blob_mode, int32_t off_ids,
-                               int32_t off_patch, cudaStream_t st) {
+                               int32_t off_patch, cudaStream_t st, int32_t layer0, int32_t nl) {
   const int32_t vec_per_row = g.d / 8;
   const int64_t vpt = (int64_t)g.h_kv * vec_per_row;
   int kb_log2 = 0;
@@ -160,12 +161,13 @@ cudaError_t launch_append_impl(const Geometry& g, const AppendItemDev* items, in
   int64_t blocks = (warps + 7) / 8;                  // 8 warps per CTA
   if (blocks < 1) blocks = 1;
   if (blocks > 65535) blocks = 65535;
-  dim3 grid((unsigned)blocks, g.L * 2);
+  if (nl <= 0) nl = g.L;
+  dim3 grid((unsigned)blocks, nl * 2);
 #define S2L_APPEND(MAXV, VPR)                                                                   \
   append_kernel<MAXV, VPR><<<grid, 256, 0, st>>>(items, n_items, total_rows, ids, n_ids, patches, \
                                                  n_patches, table, (const uint4*)k, (const uint4*)v, \
                                                  kv_rows, (uint4*)pool, g.L, g.h_kv, vec_per_row,    \
-                                                 kb_log2, blob, blob_mode, off_ids, off_patch)
+                                                 kb_log2, blob, blob_mode, off_ids, off_patch, layer0)
   if (vec_per_row == 16 && vpt <= 128) S2L_APPEND(4, 16);          // d = 128, h_kv <= 8
   else if (vec_per_row == 16 && vpt <= 512) S2L_APPEND(16, 16);
   else if (vpt <= 32) S2L_APPEND(1, 0);
@@ -182,19 +184,19 @@ cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t
                           int64_t total_rows, const int32_t* ids, int32_t n_ids,
                           const TablePatch* patches,
                           int32_t n_patches, int32_t* table, const void* k, const void* v,
-                          int64_t kv_rows, void* pool, cudaStream_t st) {
+                          int64_t kv_rows, void* pool, cudaStream_t st, int32_t layer0, int32_t nl) {
   static InlineBlob empty;   // unused in pointer mode (still copied as a parameter)
   return launch_append_impl(g, items, n_items, total_rows, ids, n_ids, patches, n_patches, table,
-                            k, v, kv_rows, pool, empty, 0, 0, 0, st);
+                            k, v, kv_rows, pool, empty, 0, 0, 0, st, layer0, nl);
 }
 
 cudaError_t launch_append_inline(const Geometry& g, const InlineBlob& blob, int32_t n_items,
                                  int64_t total_rows, int32_t off_ids, int32_t n_ids,
                                  int32_t off_patch, int32_t n_patches, int32_t* table,
                                  const void* k, const void* v, int64_t kv_rows, void* pool,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, int32_t layer0, int32_t nl) {
   return launch_append_impl(g, nullptr, n_items, total_rows, nullptr, n_ids, nullptr, n_patches,
-                            table, k, v, kv_rows, pool, blob, 1, off_ids, off_patch, st);
+                            table, k, v, kv_rows, pool, blob, 1, off_ids, off_patch, st, layer0, nl);
 }
 
 }  // namespace s2l

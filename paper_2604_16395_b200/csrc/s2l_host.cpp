@@ -741,7 +741,10 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
   if (need > c->alloc[S2L_TIER_GPU].free_count())
     return fail(S2L_E_NO_GPU_BLOCKS, "append needs %lld blocks, %lld free", (long long)need,
                 (long long)c->alloc[S2L_TIER_GPU].free_count());
-  if (!c->host_only && total_rows > 0 && (!k || !v)) return fail(S2L_E_INVAL, "k/v is NULL");
+  // k = v = NULL on a device context: reserve (NEXT-2) -- allocate and advance nc, the K/V of
+  // each layer is written later by s2l_prefill_append
+  if (!c->host_only && (!k) != (!v)) return fail(S2L_E_INVAL, "exactly one of k/v is NULL");
+  const bool reserve = !k;
   if (c->host_only && (k || v)) return fail(S2L_E_STATE, "host-only context cannot write K/V");
   if (c->sticky) return fail(c->sticky, "context has a sticky CUDA error");
 
@@ -784,7 +787,7 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
     r->nc += it.n_kv;
   }
   if (c->host_only) return S2L_OK;
-  if (total_rows == 0) {
+  if (total_rows == 0 || reserve) {
     if (!ring_wait(c, c->out_ring, c->compute, quar_wait) || !ring_wait(c, c->in_ring, c->compute, quar_wait_in))
       return S2L_E_CUDA;
     return flush_patches(c);
@@ -872,9 +875,60 @@ s2l_status s2l_invalidate_lcp(s2l_ctx* c, int64_t id, const int32_t* new_tokens,
   return S2L_OK;
 }
 
-s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
-                             const s2l_prefill_item* items, const void* q, void* o, float* lse,
-                             int64_t q_rows) {
+// One layer's append of the chunk rows [q_pos, q_pos+n_q) of each item from k/v rows
+// [q_row, q_row+n_q) ([q_rows][h_kv][d]) by the append kernel (fallback of the fused path).
+static s2l_status layer_append(s2l_ctx* c, int32_t layer, int32_t n_items,
+                               const s2l_prefill_item* items, const void* k, const void* v,
+                               int64_t q_rows) {
+  const int64_t kb = c->cfg.block_size;
+  std::vector<s2l::AppendItemDev> dev_items;
+  std::vector<int32_t> ids;
+  int64_t row_begin = 0;
+  for (int32_t i = 0; i < n_items; ++i) {
+    const s2l_prefill_item& it = items[i];
+    Request* r = find(c, it.req_id);
+    s2l::AppendItemDev d{};
+    d.nc = it.q_pos;
+    d.n_kv = it.n_q;
+    d.kv_row = it.q_row;
+    d.row_begin = row_begin;
+    d.id_off = (int32_t)ids.size();
+    for (int64_t b = it.q_pos / kb; b < ceil_div(it.q_pos + it.n_q, kb); ++b) ids.push_back(r->blocks[(size_t)b]);
+    dev_items.push_back(d);
+    row_begin += it.n_q;
+  }
+  size_t off_ids = align16(dev_items.size() * sizeof(s2l::AppendItemDev));
+  size_t bytes = align16(off_ids + ids.size() * sizeof(int32_t));
+  if (bytes <= (size_t)s2l::kInlineBytes) {
+    std::unique_ptr<s2l::InlineBlob> blob(new s2l::InlineBlob());
+    memcpy(blob->b, dev_items.data(), dev_items.size() * sizeof(s2l::AppendItemDev));
+    memcpy(blob->b + off_ids, ids.data(), ids.size() * sizeof(int32_t));
+    CK(s2l::launch_append_inline(c->geo, *blob, n_items, row_begin, (int32_t)off_ids,
+                                 (int32_t)ids.size(), (int32_t)bytes, 0, c->d_table, k, v, q_rows,
+                                 c->gpu_pool, c->compute, layer, 1));
+  } else {
+    int s = staging_acquire(c, bytes);
+    if (s < 0) return S2L_E_CUDA;
+    char* h = (char*)c->ring.host[s];
+    memcpy(h, dev_items.data(), dev_items.size() * sizeof(s2l::AppendItemDev));
+    memcpy(h + off_ids, ids.data(), ids.size() * sizeof(int32_t));
+    if (!staging_upload_and_mark(c, s, bytes)) return S2L_E_CUDA;
+    char* dv = (char*)c->ring.dev[s];
+    CK(s2l::launch_append(c->geo, (const s2l::AppendItemDev*)dv, n_items, row_begin,
+                          (const int32_t*)(dv + off_ids), (int32_t)ids.size(), nullptr, 0,
+                          c->d_table, k, v, q_rows, c->gpu_pool, c->compute, layer, 1));
+    if (!staging_release(c, s)) return S2L_E_CUDA;
+  }
+  c->launches++;
+  return S2L_OK;
+}
+
+// s2l_prefill_batch, and with k/v != NULL s2l_prefill_append (NEXT-2: the chunk's K/V of this
+// layer are written to the pool by the attention kernel itself when every q_pos is
+// block-aligned, else by a one-layer append launch before it).
+static s2l_status prefill_impl(s2l_ctx* c, int32_t layer, int32_t n_items,
+                               const s2l_prefill_item* items, const void* q, const void* k,
+                               const void* v, void* o, float* lse, int64_t q_rows) {
   if (!c) return fail(S2L_E_INVAL, "ctx is NULL");
   if (c->host_only) return fail(S2L_E_STATE, "host-only context has no device");
   if (n_items < 0 || (n_items > 0 && !items)) return fail(S2L_E_INVAL, "bad item array");
@@ -891,6 +945,18 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
                   (long long)it.q_pos, (long long)it.n_q, (long long)r->nc);
   }
   if (n_items > 0 && (!q || !o)) return fail(S2L_E_INVAL, "q/o is NULL");
+  const bool append = k != nullptr;
+  bool fused = false;
+  if (append) {
+    if (!v) return fail(S2L_E_INVAL, "k/v is NULL");
+    std::unordered_set<int64_t> seen;
+    fused = c->tc_ok && s2l::attn_tc_tiles_per_cta() == 2 && !c->persistent && !c->split_softmax && !c->kv64;
+    for (int32_t i = 0; i < n_items; ++i) {
+      if (!seen.insert(items[i].req_id).second)
+        return fail(S2L_E_INVAL, "item %d: request %lld repeated", i, (long long)items[i].req_id);
+      if (items[i].q_pos % c->cfg.block_size) fused = false;
+    }
+  }
   if (c->sticky) return fail(c->sticky, "context has a sticky CUDA error");
   if (n_items == 0) return S2L_OK;
   s2l_status st = flush_patches(c);
@@ -900,6 +966,10 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
     if (r->swap_in_seq) {
       if (!ring_wait(c, c->in_ring, c->compute, r->swap_in_seq)) return S2L_E_CUDA;
     }
+  }
+  if (append && !fused) {
+    st = layer_append(c, layer, n_items, items, k, v, q_rows);
+    if (st) return st;
   }
   const int32_t G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
   // Items ordered by descending KV length (q_pos + n_q) so that the longest Q tiles start
@@ -977,6 +1047,10 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
         split_s = (int32_t)s_want;
       }
     }
+    alignas(64) unsigned char tin[512];
+    if (fused && !s2l::make_tmap_in(tin, k, v, q_rows, c->cfg.num_kv_heads, c->cfg.head_dim,
+                                    (int32_t)c->cfg.block_size, &err))
+      return fail(S2L_E_CUDA, "tensor map (k/v input): %s", err ? err : "?");
     s2l::set_attn_trace(c->attn_launch_no++ == c->trace_launch ? c->trace_buf : nullptr);
     CK(s2l::launch_attn_tc(c->geo, dv, inl ? dev.data() : nullptr, n_items, (int32_t)units,
                            split_begin, split_s,
@@ -984,8 +1058,9 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
                            c->tmap_kv, o, lse, c->num_sms,
                            (c->persistent ? s2l::kAttnPersistent : 0) |
                                (c->split_softmax ? s2l::kAttnSplitSoftmax : 0) |
-                               (c->kv64 ? s2l::kAttnKV64 : 0),
-                           c->compute));
+                               (c->kv64 ? s2l::kAttnKV64 : 0) |
+                               (fused ? s2l::kAttnFuseAppend : 0),
+                           c->compute, fused ? tin : nullptr, c->gpu_pool));
   } else {
     CK(s2l::launch_attn_generic(c->geo, dv, n_items, total_q, c->d_table, layer, q, o, lse,
                                 c->gpu_pool, c->compute));
@@ -997,9 +1072,26 @@ s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
   }
   uint64_t useq = 0;
   if (!ring_record(c, c->compute_ring, c->compute, &useq)) return S2L_E_CUDA;
-  for (int32_t i = 0; i < n_items; ++i) find(c, items[i].req_id)->use_seq = useq;
+  for (int32_t i = 0; i < n_items; ++i) {
+    Request* r = find(c, items[i].req_id);
+    r->use_seq = useq;
+    if (append) r->write_seq = useq;
+  }
   if (!inl && !staging_release(c, s)) return S2L_E_CUDA;
   return S2L_OK;
+}
+
+s2l_status s2l_prefill_batch(s2l_ctx* c, int32_t layer, int32_t n_items,
+                             const s2l_prefill_item* items, const void* q, void* o, float* lse,
+                             int64_t q_rows) {
+  return prefill_impl(c, layer, n_items, items, q, nullptr, nullptr, o, lse, q_rows);
+}
+
+s2l_status s2l_prefill_append(s2l_ctx* c, int32_t layer, int32_t n_items,
+                              const s2l_prefill_item* items, const void* q, const void* k,
+                              const void* v, void* o, float* lse, int64_t q_rows) {
+  if (c && (!k || !v) && n_items > 0) return fail(S2L_E_INVAL, "k/v is NULL");
+  return prefill_impl(c, layer, n_items, items, q, k ? k : v, v, o, lse, q_rows);
 }
 
 s2l_status s2l_swap_out(s2l_ctx* c, int32_t n, const int64_t* ids, int64_t* bytes_out) {

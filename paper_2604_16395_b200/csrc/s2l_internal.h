@@ -67,19 +67,21 @@ cudaError_t launch_table_patch(const TablePatch* patches, int32_t n, int32_t* ta
 cudaError_t launch_table_patch_inline(const TablePatch* host_patches, int32_t n, int32_t* table,
                                       cudaStream_t st);
 
-// Writes K/V rows into the pool and applies the table patches (fused).
+// Writes K/V rows into the pool and applies the table patches (fused).  k / v hold layers
+// layer0 .. layer0+nl-1 ([nl][kv_rows][h_kv][d]); nl = 0 means all L layers from layer 0.
 cudaError_t launch_append(const Geometry& g, const AppendItemDev* items, int32_t n_items,
                           int64_t total_rows, const int32_t* ids, int32_t n_ids,
                           const TablePatch* patches,
                           int32_t n_patches, int32_t* table, const void* k, const void* v,
-                          int64_t kv_rows, void* pool, cudaStream_t st);
+                          int64_t kv_rows, void* pool, cudaStream_t st, int32_t layer0 = 0,
+                          int32_t nl = 0);
 // Same with items / ids / patches laid out in a host blob (items at 0, ids at off_ids,
 // patches at off_patch; total <= kInlineBytes) passed by value.
 cudaError_t launch_append_inline(const Geometry& g, const InlineBlob& blob, int32_t n_items,
                                  int64_t total_rows, int32_t off_ids, int32_t n_ids,
                                  int32_t off_patch, int32_t n_patches, int32_t* table,
                                  const void* k, const void* v, int64_t kv_rows, void* pool,
-                                 cudaStream_t st);
+                                 cudaStream_t st, int32_t layer0 = 0, int32_t nl = 0);
 
 // CUDA-core attention for any geometry (one warp per (query row, q head)).
 cudaError_t launch_attn_generic(const Geometry& g, const AttnItemDev* items, int32_t n_items,
@@ -103,11 +105,16 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
                            float* ws, int32_t max_pieces, int32_t* ws_cnt,
                            const int32_t* table, int32_t layer, const void* tmap_q,
                            const void* tmap_kv, void* o, float* lse, int32_t num_sms,
-                           int32_t flags, cudaStream_t st);
+                           int32_t flags, cudaStream_t st, const void* tmap_in = nullptr,
+                           void* pool = nullptr);
 // flags of launch_attn_tc
 constexpr int32_t kAttnPersistent = 1;   // v2 only: grid = min(work items, SMs), CTAs loop
 constexpr int32_t kAttnSplitSoftmax = 2; // v4: each tile's softmax split over two warps per SMSP
 constexpr int32_t kAttnKV64 = 4;         // v5: 64-key steps, double-buffered S per tile
+// v2 only: fused append (NEXT-2).  Every item's q_pos is a multiple of the block size; the
+// chunk rows [q_pos, q_pos+n_q) of this layer are read from tmap_in (make_tmap_in) and written
+// to the pool by the kernel.  No two items may share a request.
+constexpr int32_t kAttnFuseAppend = 8;
 // Experiments: device buffer receiving kernel timeline stamps (S2L_TRACE builds); nullptr = off.
 void set_attn_trace(uint32_t* buf);   // v2 only: grid = min(work items, SMs), CTAs loop
 constexpr int64_t kSplitPieceFloats = 2 * 128 * 130;   // O [2][128][128] + (m, l) [2][128][2]
@@ -116,6 +123,10 @@ bool make_tmap_q(void* out128, const void* q, int64_t q_rows, int32_t h_q, int32
                  int32_t group, const char** err);
 // Maps of the pool into out384: [0,128) per-block boxes, [128,256) 128-key block runs,
 // [256,384) 64-key block runs (k <= 64).
+// One layer's K and V input rows ([rows][h_kv][d] bf16) into out512: per-block boxes (K at 0,
+// V at 128) and whole-tile boxes (K at 256, V at 384).
+bool make_tmap_in(void* out512, const void* k, const void* v, int64_t rows, int32_t h_kv,
+                  int32_t d, int32_t kb, const char** err);
 bool make_tmap_kv(void* out384, const void* pool, int64_t num_blocks, int32_t L, int32_t h_kv,
                   int32_t d, int32_t k, const char** err);
 

@@ -50,7 +50,7 @@ class ReqInfo(C.Structure):
 
 EXPORTS = ["s2l_block_bytes", "s2l_create", "s2l_create_host_only", "s2l_destroy", "s2l_new_request",
            "s2l_release_request", "s2l_preempt_recompute", "s2l_append_chunk", "s2l_invalidate_lcp",
-           "s2l_prefill_batch", "s2l_swap_out", "s2l_swap_in", "s2l_query", "s2l_block_table",
+           "s2l_prefill_batch", "s2l_prefill_append", "s2l_swap_out", "s2l_swap_in", "s2l_query", "s2l_block_table",
            "s2l_free_blocks", "s2l_sync", "s2l_set_swap_in_stream", "s2l_kernel_launches", "s2l_set_timing", "s2l_timing_read",
            "s2l_last_error", "s2l_version"]
 
@@ -78,6 +78,7 @@ def lib(path: str | None = None) -> C.CDLL:
         "s2l_append_chunk": (I32, [VP, I32, P(AppendItem), VP, VP, I64]),
         "s2l_invalidate_lcp": (I32, [VP, I64, P(I32), I64, P(I64), P(I64)]),
         "s2l_prefill_batch": (I32, [VP, I32, I32, P(PrefillItem), VP, VP, VP, I64]),
+        "s2l_prefill_append": (I32, [VP, I32, I32, P(PrefillItem), VP, VP, VP, VP, VP, I64]),
         "s2l_swap_out": (I32, [VP, I32, P(I64), P(I64)]),
         "s2l_swap_in": (I32, [VP, I32, P(I64), P(I64)]),
         "s2l_query": (I32, [VP, I64, P(ReqInfo)]),
@@ -92,6 +93,8 @@ def lib(path: str | None = None) -> C.CDLL:
         "s2l_version": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():
+        if path != LIB_PATH and not hasattr(L, name):
+            continue            # an older build loaded for an A/B comparison
         f = getattr(L, name)
         f.restype, f.argtypes = res, args
     _libs[path] = L
@@ -198,6 +201,15 @@ class Context:
         arr = (PrefillItem * max(1, len(items)))(*[PrefillItem(*it) for it in items])
         return self._check(self._L.s2l_prefill_batch(self._h, layer, len(items), arr, _ptr(q), _ptr(o),
                                                      _ptr(lse), q.shape[0] if q is not None else 0))
+
+    def prefill_append(self, layer: int, items, q, k, v, o, lse=None):
+        """Fused append + attention of one layer (NEXT-2).  items: [(rid, q_pos, n_q, q_row)];
+        q, o: [rows][h_q][d]; k, v: [rows][h_kv][d] bf16 of this layer; the blocks are held
+        (append_chunk with k = v = None reserves them)."""
+        arr = (PrefillItem * max(1, len(items)))(*[PrefillItem(*it) for it in items])
+        return self._check(self._L.s2l_prefill_append(self._h, layer, len(items), arr, _ptr(q), _ptr(k),
+                                                      _ptr(v), _ptr(o), _ptr(lse),
+                                                      q.shape[0] if q is not None else 0))
 
     def swap_out(self, rids):
         ids = (C.c_int64 * max(1, len(rids)))(*rids)

@@ -69,6 +69,30 @@ class Pair:
         self._keep = (kd, vd)
         return a
 
+    def append_reserve(self, items, k_bits, v_bits):
+        """Library: append_chunk in reserve mode (k = v = NULL, NEXT-2); oracle: the full append
+        (its bytes are what the per-layer prefill_append calls must leave in the pool)."""
+        a = s2l.status_of(self.lib.append_chunk, items, None, None, kv_rows=k_bits.shape[1])
+        b = self.ora.append(items, k_bits, v_bits)
+        assert a == b, (a, b)
+        return a
+
+    def prefill_append(self, items, q_bits, k_bits_l, v_bits_l, layer=0, check=True):
+        """Fused append + attention of one layer (library) vs the oracle's attention over the
+        pool its append wrote."""
+        qd, kd, vd = to_dev(q_bits), to_dev(k_bits_l), to_dev(v_bits_l)
+        od = torch.zeros_like(qd)
+        ld = torch.zeros(q_bits.shape[0], self.h_q, dtype=torch.float32, device="cuda")
+        self.lib.prefill_append(layer, items, qd, kd, vd, od, ld)
+        torch.cuda.synchronize()
+        st, o_ref, l_ref = self.ora.prefill(items, q_bits, layer)
+        assert st == O.OK
+        o_gpu = bf16_dev_to_f64(od)
+        l_gpu = ld.cpu().numpy().astype(np.float64)
+        if check:
+            self.check_attention(items, o_gpu, o_ref, l_gpu, l_ref)
+        return o_gpu, o_ref
+
     def invalidate(self, rid, new):
         a = self.lib.invalidate_lcp(rid, new)
         st, p, inv = self.ora.invalidate_lcp(rid, new)

@@ -761,3 +761,97 @@ def test_swap_round_trip_full_size_c4_blocks():
         for r in rids:
             got = view[torch.tensor(lib.block_table(r), device="cuda")]
             assert torch.equal(got.view(torch.int16), before[r].view(torch.int16)), r
+
+
+# ----------------------------------------------------------------------------- NEXT-2 fused append
+def _fused_rounds(P, seed, geo, chunks, check_every=True):
+    """Each round: append_chunk in reserve mode, then one fused append + attention call per
+    layer (library) vs the oracle's append + per-layer attention."""
+    lengths = [sum(c) for c in chunks]
+    toks = {r: W.request_tokens(seed, r, n) for r, n in enumerate(lengths)}
+    data = {r: _stream_qkv(seed, toks[r], geo) for r in toks}
+    for r in toks:
+        P.new(r, toks[r])
+    pos = {r: 0 for r in toks}
+    for j in range(max(len(c) for c in chunks)):
+        items_a, items_p, ks, vs, qs, row = [], [], [], [], [], 0
+        for r in toks:
+            if j >= len(chunks[r]):
+                continue
+            n, a = chunks[r][j], pos[r]
+            items_a.append((r, None, n, row))
+            items_p.append((r, a, n, row))
+            ks.append(data[r][1][:, a:a + n]); vs.append(data[r][2][:, a:a + n]); qs.append(data[r][0][a:a + n])
+            row += n
+            pos[r] += n
+        kk, vv, qq = np.concatenate(ks, axis=1), np.concatenate(vs, axis=1), np.concatenate(qs)
+        P.append_reserve(items_a, kk, vv)
+        for layer in range(geo.L):
+            P.prefill_append(items_p, qq, kk[layer], vv[layer], layer=layer, check=check_every)
+        P.check_state()
+        P.check_pool_valid_slots()
+    P.check_pools_whole()
+
+
+@pytest.mark.parametrize("h_q,h_kv,k,L", [(8, 2, 16, 2), (32, 8, 16, 1), (4, 4, 64, 2), (16, 2, 128, 1), (8, 8, 32, 1)])
+def test_fused_append_prefill_aligned(h_q, h_kv, k, L):
+    """Every q_pos block-aligned: the attention kernel reads the chunk's K/V from the caller's
+    rows and writes the pool itself (full blocks by TMA store, the partial last block by plain
+    stores); pool bytes bit-exact, attention within tolerance, every layer."""
+    geo = W.Geometry(L=L, h_q=h_q, h_kv=h_kv, d=128, k=k)
+    P = Pair(L, h_q, h_kv, 128, k, 256, 8, max_blocks=128)
+    b = k
+    _fused_rounds(P, W.seed_of(21), geo, [[4 * b, 8 * b, 37], [b, 300], [200], [2 * b, 2 * b, 2 * b, 5]])
+
+
+def test_fused_append_prefill_unaligned_falls_back():
+    """A q_pos inside a block (token-granular appends / invalidation): the same call runs a
+    one-layer append launch before the attention; results and bytes identical to the oracle."""
+    geo = W.Geometry(L=2, h_q=8, h_kv=2, d=128, k=16)
+    P = Pair(2, 8, 2, 128, 16, 128, 8, max_blocks=64)
+    _fused_rounds(P, W.seed_of(22), geo, [[10, 50, 130], [16, 7, 200]])
+
+
+def test_fused_append_prefill_after_update_and_errors():
+    """Update mode then the fused path from the LCP; error cases."""
+    geo = W.Geometry(L=1, h_q=8, h_kv=2, d=128, k=16)
+    P = Pair(1, 8, 2, 128, 16, 64, 8, max_blocks=64)
+    seed = W.seed_of(23)
+    toks = W.request_tokens(seed, 0, 256)
+    q, k, v = _stream_qkv(seed, toks, geo)
+    P.new(0, toks)
+    P.append_reserve([(0, None, 256, 0)], k, v)
+    P.prefill_append([(0, 0, 256, 0)], q, k[0], v[0])
+    new = W.updated_tokens(seed, 0, toks, 100, 300, 0)
+    p, inval = P.invalidate(0, new)
+    q2, k2, v2 = _stream_qkv(seed, new, geo)
+    c = P.lib.query(0)["num_computed"]
+    P.append_reserve([(0, None, 300 - c, 0)], k2[:, c:], v2[:, c:])
+    P.prefill_append([(0, c, 300 - c, 0)], q2[c:], k2[0, c:], v2[0, c:])
+    P.check_pool_valid_slots()
+    qd, kd = to_dev(q2[c:]), to_dev(k2[0, c:])
+    od = torch.zeros_like(qd)
+    with pytest.raises(s2l.S2LError) as e:
+        P.lib.prefill_append(0, [(0, c, 300 - c, 0)], qd, kd, None, od)
+    assert e.value.status == s2l.E_INVAL
+    with pytest.raises(s2l.S2LError) as e:
+        P.lib.prefill_append(0, [(0, c, 10, 0), (0, c + 10, 10, 10)], qd, kd, kd, od)
+    assert e.value.status == s2l.E_INVAL
+
+
+def test_fused_append_prefill_c2_shape_sampled():
+    """C2 geometry (Llama-3-8B attention: 32 q / 8 kv heads, k = 16), 4 requests x 512-token
+    chunks to 4K through the fused path; full pool bytes and sampled attention rows vs the
+    oracle at the last round."""
+    geo = W.Geometry(L=1, h_q=32, h_kv=8, d=128, k=16)
+    P = Pair(1, 32, 8, 128, 16, 4 * 256 + 8, 8, max_blocks=256)
+    _fused_rounds(P, W.seed_of(24), geo, [[512] * 8] * 4, check_every=False)
+    # last round's attention vs the oracle (the rounds above ran unchecked for speed)
+    seed = W.seed_of(24)
+    items, qs = [], []
+    for r in range(4):
+        toks = W.request_tokens(seed, r, 4096)
+        q, k, v = _stream_qkv(seed, toks, geo)
+        items.append((r, 3584, 512, 512 * r))
+        qs.append(q[3584:])
+    P.prefill(items, np.concatenate(qs))

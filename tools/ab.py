@@ -44,13 +44,16 @@ def main():
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
+    # "FUSED=1" in a spec's env list: time bench.run_step_fused (NEXT-2) for that context
+    step_fn = [bench.run_step_fused if "FUSED=1" in spec else bench.run_step for spec in libs]
     flops = bench.step_flops()
     res = {p: [] for p in libs}
-    for path, (ctx, _) in zip(libs, ctxs):       # warm every context (clocks, caches)
-        bench.timed(lambda: bench.run_step(ctx, S), 1, 4)
+    assert len(set(libs)) == len(libs), "specs must differ"
+    for fn, (ctx, _) in zip(step_fn, ctxs):      # warm every context (clocks, caches)
+        bench.timed(lambda: fn(ctx, S), 1, 4)
     for r in range(rounds):
-        for path, (ctx, _) in zip(libs, ctxs):
-            ms = bench.timed(lambda: bench.run_step(ctx, S), 3, 1)
+        for path, fn, (ctx, _) in zip(libs, step_fn, ctxs):
+            ms = bench.timed(lambda: fn(ctx, S), 3, 1)
             res[path].append(flops * 3 / (ms * 1e-3) / 1e12)
     for path in libs:
         v = res[path]
