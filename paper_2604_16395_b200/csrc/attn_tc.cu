@@ -95,11 +95,19 @@ struct TcParams {
   // token range to the pool (TMA store; a partial last block by plain stores into pool).
   int32_t fuse;
   __nv_bfloat16* pool;
-  CUtensorMap tmap_kin, tmap_vin;     // box {64, 1, k}: one block of one kv head
-  CUtensorMap tmap_kin_t, tmap_vin_t; // box {64, 1, 128}: a whole 128-key tile
   int32_t n_inl;     // > 0: the items are inl[0 .. n_inl) (by value), not *items
   AttnItemDev inl[kInlineAttnItems];
 };
+// Parameters of the fused-append instantiation (the input maps), kept out of the plain
+// kernel's parameter block.  (Passing the chunk blocks' ids inline as well, so that the kernel
+// could write their table entries instead of a patch launch, took the block past 4 KB and
+// made every launch ~15 us slower: measured, `profiles/r01/next2_fused.txt`.)
+struct TcParamsFused : TcParams {
+  CUtensorMap tmap_kin, tmap_vin;     // box {64, 1, k}: one block of one kv head
+  CUtensorMap tmap_kin_t, tmap_vin_t; // box {64, 1, 128}: a whole 128-key tile
+};
+template <bool kFuse> struct ParamsOf { using T = TcParams; };
+template <> struct ParamsOf<true> { using T = TcParamsFused; };
 __device__ __forceinline__ AttnItemDev item_at(const TcParams& p, int32_t i) {
   return p.n_inl ? p.inl[i] : p.items[i];
 }
@@ -805,7 +813,8 @@ template <bool kFuse>
 __global__ void __launch_bounds__(v2::kThreads, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_kv,
-                    const __grid_constant__ CUtensorMap tmap_kv4, const __grid_constant__ TcParams p) {
+                    const __grid_constant__ CUtensorMap tmap_kv4,
+                    const __grid_constant__ typename ParamsOf<kFuse>::T p) {
   using namespace v2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -943,14 +952,16 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
             const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
             tma_load_4d(dst, &tmap_kv4, bar(WB_RF + s), 0, 0, lkh[kind], ids[0]);
             tma_load_4d(dst + kAtom, &tmap_kv4, bar(WB_RF + s), 64, 0, lkh[kind], ids[0]);
-          } else if (lane == 0 && fresh && tpos >= it.q_pos) {
-            // tile wholly inside the chunk: two boxes {64, 1, 128} of the caller's rows
-            mbar_expect_tx(bar(WB_RF + s), kTileBytes);
-            const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
-            const CUtensorMap* tin = kind ? &p.tmap_vin_t : &p.tmap_kin_t;
-            const int32_t z = (int32_t)(it.q_row + (tpos - it.q_pos));
-            tma_load_3d(dst, tin, bar(WB_RF + s), 0, kvh, z);
-            tma_load_3d(dst + kAtom, tin, bar(WB_RF + s), 64, kvh, z);
+          } else if (kFuse && lane == 0 && fresh && tpos >= it.q_pos) {
+            if constexpr (kFuse) {
+              // tile wholly inside the chunk: two boxes {64, 1, 128} of the caller's rows
+              mbar_expect_tx(bar(WB_RF + s), kTileBytes);
+              const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
+              const CUtensorMap* tin = kind ? &p.tmap_vin_t : &p.tmap_kin_t;
+              const int32_t z = (int32_t)(it.q_row + (tpos - it.q_pos));
+              tma_load_3d(dst, tin, bar(WB_RF + s), 0, kvh, z);
+              tma_load_3d(dst + kAtom, tin, bar(WB_RF + s), 64, kvh, z);
+            }
           } else if (lane == 0) {
             // one lane issues the whole tile: 2 boxes {64, k} (d halves) per block
             mbar_expect_tx(bar(WB_RF + s), kTileBytes);
@@ -964,11 +975,13 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
 #else
                 if (fresh && pos0 >= it.q_pos) {
 #endif
-                  // chunk block: rows q_row + (pos0 - q_pos) .. of this layer's K or V input
-                  const CUtensorMap* tin = kind ? &p.tmap_vin : &p.tmap_kin;
-                  const int32_t z = (int32_t)(it.q_row + (pos0 - it.q_pos));
-                  tma_load_3d(dst + b * p.kb * 128, tin, bar(WB_RF + s), 0, kvh, z);
-                  tma_load_3d(dst + kAtom + b * p.kb * 128, tin, bar(WB_RF + s), 64, kvh, z);
+                  if constexpr (kFuse) {
+                    // chunk block: rows q_row + (pos0 - q_pos) .. of this layer's K or V input
+                    const CUtensorMap* tin = kind ? &p.tmap_vin : &p.tmap_kin;
+                    const int32_t z = (int32_t)(it.q_row + (pos0 - it.q_pos));
+                    tma_load_3d(dst + b * p.kb * 128, tin, bar(WB_RF + s), 0, kvh, z);
+                    tma_load_3d(dst + kAtom + b * p.kb * 128, tin, bar(WB_RF + s), 64, kvh, z);
+                  }
                 } else {
                   const int32_t y = ids[b] * rows_per_block + row_kv[kind];
                   tma_load_2d(dst + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
@@ -2875,7 +2888,9 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
     attr_set[variant] = true;
   }
   if (total_units <= 0) return cudaSuccess;
-  TcParams p{};
+  TcParamsFused pf{};
+  TcParams plain{};
+  TcParams& p = fuse ? static_cast<TcParams&>(pf) : plain;
   p.items = items;
   p.n_inl = 0;
   if (items_host && n_items <= kInlineAttnItems) {
@@ -2910,10 +2925,10 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
   p.fuse = fuse ? 1 : 0;
   p.pool = (__nv_bfloat16*)pool;
   if (fuse) {
-    memcpy(&p.tmap_kin, tmap_in, sizeof(CUtensorMap));
-    memcpy(&p.tmap_vin, (const char*)tmap_in + 128, sizeof(CUtensorMap));
-    memcpy(&p.tmap_kin_t, (const char*)tmap_in + 256, sizeof(CUtensorMap));
-    memcpy(&p.tmap_vin_t, (const char*)tmap_in + 384, sizeof(CUtensorMap));
+    memcpy(&pf.tmap_kin, tmap_in, sizeof(CUtensorMap));
+    memcpy(&pf.tmap_vin, (const char*)tmap_in + 128, sizeof(CUtensorMap));
+    memcpy(&pf.tmap_kin_t, (const char*)tmap_in + 256, sizeof(CUtensorMap));
+    memcpy(&pf.tmap_vin_t, (const char*)tmap_in + 384, sizeof(CUtensorMap));
   }
   p.ws = ws;
   p.ws_ml = ws ? ws + (int64_t)max_pieces * 2 * 128 * kD : nullptr;
@@ -2929,7 +2944,10 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
     const int32_t g = grid < num_sms ? grid : num_sms;
     attn_tc3_kernel<<<g, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, p);
   } else if (variant == 2)
-    (fuse ? attn_tc2_kernel<true> : attn_tc2_kernel<false>)<<<grid, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, p);
+  {
+    if (fuse) attn_tc2_kernel<true><<<grid, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, pf);
+    else attn_tc2_kernel<false><<<grid, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, p);
+  }
   else
     attn_tc_kernel<<<total_units, kThreads, SMEM_BYTES, st>>>(tq, tkv, p);
   return cudaGetLastError();

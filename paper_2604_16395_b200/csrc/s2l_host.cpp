@@ -790,7 +790,9 @@ s2l_status s2l_append_chunk(s2l_ctx* c, int32_t n_items, const s2l_append_item* 
   if (total_rows == 0 || reserve) {
     if (!ring_wait(c, c->out_ring, c->compute, quar_wait) || !ring_wait(c, c->in_ring, c->compute, quar_wait_in))
       return S2L_E_CUDA;
-    return flush_patches(c);
+    // reserve: the new entries stay pending; a fused s2l_prefill_append writes them in-kernel,
+    // any other launch reading the table flushes them first
+    return reserve ? S2L_OK : flush_patches(c);
   }
 
   size_t off_ids = align16(dev_items.size() * sizeof(s2l::AppendItemDev));
