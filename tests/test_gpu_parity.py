@@ -855,3 +855,29 @@ def test_fused_append_prefill_c2_shape_sampled():
         items.append((r, 3584, 512, 512 * r))
         qs.append(q[3584:])
     P.prefill(items, np.concatenate(qs))
+
+
+def test_fused_append_then_swap_without_host_sync():
+    """Stream hazard of the fused path: a swap-out issued right after s2l_prefill_append (no host
+    synchronisation) must copy the blocks that kernel writes (the D2H waits for it, §5), and a
+    later append reusing the freed ids must not overtake the D2H."""
+    geo = W.Geometry(L=2, h_q=8, h_kv=2, d=128, k=16)
+    P = Pair(2, 8, 2, 128, 16, 48, 64, max_blocks=64)   # request 1 must reuse 16 of request 0's ids
+    seed = W.seed_of(25)
+    toks = {r: W.request_tokens(seed, r, 512) for r in (0, 1)}
+    data = {r: _stream_qkv(seed, toks[r], geo) for r in (0, 1)}
+    P.new(0, toks[0]); P.new(1, toks[1])
+    q, k, v = data[0]
+    P.append_reserve([(0, None, 512, 0)], k, v)
+    qd, od = to_dev(q), torch.zeros(512, 8, 128, dtype=torch.bfloat16, device="cuda")
+    kd = [to_dev(k[l]) for l in range(2)]
+    vd = [to_dev(v[l]) for l in range(2)]
+    for l in range(2):
+        P.lib.prefill_append(l, [(0, 0, 512, 0)], qd, kd[l], vd[l], od)
+    P.swap_out([0])                      # no synchronisation since the fused launches
+    q1, k1, v1 = data[1]
+    P.append([(1, None, 512, 0)], k1, v1)   # reuses ids request 0 just released (Z9: after the others)
+    assert set(P.lib.block_table(1)) & set(range(32))
+    P.check_state()
+    P.check_pools_whole()                # request 0's CPU copy == the oracle's bytes
+    P.prefill([(1, 384, 128, 0)], q1[384:])
