@@ -108,13 +108,18 @@ class PressureDriver:
     Every library call is appended to `log` as (op, args, result) for the oracle replay.
     """
 
-    def __init__(self, ctx, plans, k: int, budget: int, evict_ahead: int = 2, cost=None):
+    def __init__(self, ctx, plans, k: int, budget: int, evict_ahead: int = 2, cost=None,
+                 prefetch_ahead: int = 0):
         """cost: None -> every victim is swapped (the C4 definition, BJ:L10); else a callable
         cost(num_computed, num_blocks) -> "recompute" | "swap" (the paper's cost-based
         preemption, P:L79 / §4.3): a recompute victim drops its blocks (no D2H) and later
         re-prefills its computed prefix."""
         self.ctx, self.k, self.budget = ctx, k, budget
         self.evict_ahead = evict_ahead
+        # prefetch_ahead: also swap in the CPU-tier requests of the next `prefetch_ahead` steps
+        # after sel when the room is already there, so their H2D gets several steps of compute
+        self.prefetch_ahead = prefetch_ahead
+        self.prefetched = 0
         self.cost = cost
         self.recompute_preemptions = 0
         self.recomputed_tokens = 0
@@ -255,6 +260,24 @@ class PressureDriver:
             self.log.append(("swap_out", tuple(victims), b))
             self.swapped_out_bytes += b
             self.swap_out_calls += 1
+        if self.prefetch_ahead and victims is not None:
+            free_now, _ = self.ctx.free_blocks()
+            spare = free_now - need                      # sel's swap-ins and appends come first
+            seen, saved = set(sel), self.cursor
+            for _ in range(int(self.prefetch_ahead)):
+                nxt = [r for r in self.plan(peek=True) if r not in seen]
+                if not nxt:
+                    break
+                self.cursor = nxt[-1] + 1
+                for r in nxt:
+                    q = self.ctx.query(r)
+                    upd = self.work[r][self.next_work[r]].new_input is not None   # would drop blocks
+                    if q["tier"] == TIER_CPU and not upd and 0 < q["num_blocks"] <= spare:
+                        to_in.append(r)
+                        spare -= q["num_blocks"]
+                        self.prefetched += 1
+                seen |= set(nxt)
+            self.cursor = saved
         if to_in:
             b = self.ctx.swap_in(to_in)
             self.log.append(("swap_in", tuple(to_in), b))

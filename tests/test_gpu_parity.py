@@ -553,8 +553,8 @@ def test_stream_hazards_without_host_syncs():
         assert err.max() <= 2e-2, (r, layer, float(err.max()))
 
 
-@pytest.mark.parametrize("serial,cost", [(False, False), (True, False), (False, True)])
-def test_c4_pressure_driver_on_device(serial, cost):
+@pytest.mark.parametrize("serial,cost,prefetch", [(False, False, 0), (True, False, 0), (False, True, 0), (False, False, 2)])
+def test_c4_pressure_driver_on_device(serial, cost, prefetch):
     """The C4 driver (paper_2604_16395_b200.pressure) at reduced size on the device: 16
     append / update requests, GPU pool 50% of the working set, swaps overlapping compute (or
     serialised), no host synchronisation inside the stream.  Bookkeeping is mirrored into the
@@ -586,7 +586,8 @@ def test_c4_pressure_driver_on_device(serial, cost):
     segs, checks, byte_checks = {}, [], []
     rng = np.random.default_rng(0)
     rule = (lambda nc, nb: "recompute" if nc < 700 else "swap") if cost else None
-    drv = pressure.PressureDriver(pressure.SwapTimer(tw, serial=serial), plans, K, budget, cost=rule)
+    drv = pressure.PressureDriver(pressure.SwapTimer(tw, serial=serial), plans, K, budget, cost=rule,
+                                  prefetch_ahead=prefetch)
     out_holder = {}
 
     def on_step(sel, app, pre, rows):

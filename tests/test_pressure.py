@@ -10,7 +10,7 @@ from synth import workloads as W
 from tests.harness import Twin
 
 
-def _run_host(seed, n_req, lo, hi, budget, frac=0.5, k=16, cost=None):
+def _run_host(seed, n_req, lo, hi, budget, frac=0.5, k=16, cost=None, prefetch=0):
     plans = pressure.c4_plans(seed, n_req, lo=lo, hi=hi, budget=budget)
     ws = pressure.working_set_blocks(plans, k)
     biggest = max(-(-p.total // k) for p in plans)
@@ -19,7 +19,7 @@ def _run_host(seed, n_req, lo, hi, budget, frac=0.5, k=16, cost=None):
     cfg = s2l.make_config(1, 1, 1, 8, k, ng, nc, max_requests=n_req, max_blocks_per_request=biggest + 1)
     lib = s2l.Context(cfg, host_only=True)
     tw = Twin(lib, k, ng, nc, n_req, biggest + 1)
-    drv = pressure.PressureDriver(tw, plans, k, budget, cost=cost)
+    drv = pressure.PressureDriver(tw, plans, k, budget, cost=cost, prefetch_ahead=prefetch)
 
     def execute(sel, app, pre, rows):
         tw.append_chunk(app, None, None, kv_rows=rows)
@@ -28,9 +28,11 @@ def _run_host(seed, n_req, lo, hi, budget, frac=0.5, k=16, cost=None):
     return plans, drv, steps, ng, ws
 
 
-@pytest.mark.parametrize("seed", [11, 12])
-def test_driver_bookkeeping_matches_oracle_under_pressure(seed):
-    plans, drv, steps, ng, ws = _run_host(seed, 24, 64, 1024, 512)
+@pytest.mark.parametrize("seed,prefetch", [(11, 0), (12, 0), (11, 2), (12, 1)])
+def test_driver_bookkeeping_matches_oracle_under_pressure(seed, prefetch):
+    plans, drv, steps, ng, ws = _run_host(seed, 24, 64, 1024, 512, prefetch=prefetch)
+    if prefetch:
+        assert drv.prefetched > 0
     assert ng < ws                                   # the pool really is under pressure
     assert drv.swap_out_calls > 0 and drv.swap_in_calls > 0
     assert not drv.live() and not drv.plans          # every request finished and was released

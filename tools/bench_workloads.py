@@ -221,6 +221,7 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
     out = torch.empty_like(src_q)
     cs, cs_in = torch.cuda.Stream(), torch.cuda.Stream()
     res = {"workload": "C4 memory-pressure mix (BJ:L10)", "requests": n_req, "L": L, "m_block": mb,
+           "evict_ahead": int(os.environ.get("C4_AHEAD", "2")), "prefetch_ahead": int(os.environ.get("C4_PREFETCH", "0")),
            "working_set_blocks": ws, "gpu_pool_blocks": ng, "cpu_pool_blocks": ncpu, "budget": budget}
     flops_total = 0.0
     big = None
@@ -241,7 +242,8 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
             ctx = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), cs, swap_in_stream=cs_in)
         wrap = pressure.SwapTimer(ctx, serial=(mode == "serial"), copy_stream=cs, swap_in_stream=cs_in)
         drv = pressure.PressureDriver(wrap, plans, K, budget, evict_ahead=int(os.environ.get("C4_AHEAD", "2")),
-                                      cost=cost_rule if mode == "overlap_cost" else None)
+                                      cost=cost_rule if mode == "overlap_cost" else None,
+                                      prefetch_ahead=int(os.environ.get("C4_PREFETCH", "0")))
         step_ev = []
         segs, snaps, flops = {}, [], [0.0]
 
@@ -309,6 +311,7 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
                          "tokens": drv.tokens, "tokens_per_s": drv.tokens / (ms * 1e-3),
                          "swap_out_bytes": drv.swapped_out_bytes, "swap_in_bytes": drv.swapped_in_bytes,
                          "swap_out_calls": drv.swap_out_calls, "swap_in_calls": drv.swap_in_calls,
+                         "prefetched_swap_ins": drv.prefetched,
                          "recompute_preemptions": drv.recompute_preemptions,
                          "recomputed_tokens": drv.recomputed_tokens}
         if snaps:
