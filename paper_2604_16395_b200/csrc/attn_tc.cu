@@ -894,6 +894,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  pdl_prologue();   // the item descriptors above come from the parameters or the staging ring
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtrl));
@@ -2945,8 +2946,8 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
     attn_tc3_kernel<<<g, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, p);
   } else if (variant == 2)
   {
-    if (fuse) attn_tc2_kernel<true><<<grid, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, pf);
-    else attn_tc2_kernel<false><<<grid, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, p);
+    if (fuse) return launch_k(attn_tc2_kernel<true>, dim3(grid), dim3(v2::kThreads), v2::SMEM, st, tq, tkv, tkv4, pf);
+    return launch_k(attn_tc2_kernel<false>, dim3(grid), dim3(v2::kThreads), v2::SMEM, st, tq, tkv, tkv4, p);
   }
   else
     attn_tc_kernel<<<total_units, kThreads, SMEM_BYTES, st>>>(tq, tkv, p);

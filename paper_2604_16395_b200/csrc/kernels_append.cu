@@ -19,11 +19,13 @@ namespace {
 
 __global__ void table_patch_kernel(const TablePatch* __restrict__ patches, int32_t n,
                                    int32_t* __restrict__ table) {
+  pdl_prologue();
   for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     table[patches[i].idx] = patches[i].value;
 }
 __global__ void table_patch_inline_kernel(const __grid_constant__ InlinePatches ps, int32_t n,
                                           int32_t* __restrict__ table) {
+  pdl_prologue();
   for (int32_t i = threadIdx.x; i < n; i += blockDim.x) table[ps.p[i].idx] = ps.p[i].value;
 }
 
@@ -61,6 +63,7 @@ __global__ void __launch_bounds__(256) append_kernel(
     const uint4* __restrict__ v, int64_t kv_rows, uint4* __restrict__ pool, int32_t L,
     int32_t h_kv, int32_t vec_per_row, int32_t kb_log2, const __grid_constant__ InlineBlob blob,
     int32_t blob_mode, int32_t off_ids, int32_t off_patch, int32_t layer0) {
+  pdl_prologue();
   const AppendItemDev* items_g = blob_mode ? reinterpret_cast<const AppendItemDev*>(blob.b) : items_p;
   const int32_t* ids_g = blob_mode ? reinterpret_cast<const int32_t*>(blob.b + off_ids) : ids_p;
   const TablePatch* patches = blob_mode ? reinterpret_cast<const TablePatch*>(blob.b + off_patch) : patches_p;
@@ -133,8 +136,7 @@ cudaError_t launch_table_patch_inline(const TablePatch* host_patches, int32_t n,
   if (n > kInlinePatches) return cudaErrorInvalidValue;
   InlinePatches ps;
   memcpy(ps.p, host_patches, (size_t)n * sizeof(TablePatch));
-  table_patch_inline_kernel<<<1, 256, 0, st>>>(ps, n, table);
-  return cudaGetLastError();
+  return launch_k(table_patch_inline_kernel, dim3(1), dim3(256), 0, st, ps, n, table);
 }
 
 cudaError_t launch_table_patch(const TablePatch* patches, int32_t n, int32_t* table,
@@ -142,8 +144,7 @@ cudaError_t launch_table_patch(const TablePatch* patches, int32_t n, int32_t* ta
   if (n <= 0) return cudaSuccess;
   int blocks = (n + 255) / 256;
   if (blocks > 1024) blocks = 1024;
-  table_patch_kernel<<<blocks, 256, 0, st>>>(patches, n, table);
-  return cudaGetLastError();
+  return launch_k(table_patch_kernel, dim3(blocks), dim3(256), 0, st, patches, n, table);
 }
 
 namespace {
@@ -163,11 +164,12 @@ cudaError_t launch_append_impl(const Geometry& g, const AppendItemDev* items, in
   if (blocks > 65535) blocks = 65535;
   if (nl <= 0) nl = g.L;
   dim3 grid((unsigned)blocks, nl * 2);
-#define S2L_APPEND(MAXV, VPR)                                                                   \
-  append_kernel<MAXV, VPR><<<grid, 256, 0, st>>>(items, n_items, total_rows, ids, n_ids, patches, \
-                                                 n_patches, table, (const uint4*)k, (const uint4*)v, \
-                                                 kv_rows, (uint4*)pool, g.L, g.h_kv, vec_per_row,    \
-                                                 kb_log2, blob, blob_mode, off_ids, off_patch, layer0)
+#define S2L_APPEND(MAXV, VPR)                                                                     \
+  e = launch_k(append_kernel<MAXV, VPR>, grid, dim3(256), 0, st, items, n_items, total_rows, ids,   \
+               n_ids, patches, n_patches, table, (const uint4*)k, (const uint4*)v, kv_rows,         \
+               (uint4*)pool, g.L, g.h_kv, vec_per_row, kb_log2, blob, blob_mode, off_ids, off_patch, \
+               layer0)
+  cudaError_t e = cudaSuccess;
   if (vec_per_row == 16 && vpt <= 128) S2L_APPEND(4, 16);          // d = 128, h_kv <= 8
   else if (vec_per_row == 16 && vpt <= 512) S2L_APPEND(16, 16);
   else if (vpt <= 32) S2L_APPEND(1, 0);
@@ -176,7 +178,7 @@ cudaError_t launch_append_impl(const Geometry& g, const AppendItemDev* items, in
   else if (vpt <= 2048) S2L_APPEND(64, 0);
   else return cudaErrorInvalidValue;
 #undef S2L_APPEND
-  return cudaGetLastError();
+  return e;
 }
 }  // namespace
 

@@ -8,8 +8,45 @@
 #ifndef S2L_HEAD_MAJOR
 #define S2L_HEAD_MAJOR 1   // v2 unit order inside an item: 0 = pair-major, 1 = kv-head-major
 #endif
+// Programmatic dependent launch between the library's consecutive kernels on the compute
+// stream (append -> attention -> append ...): a kernel launched with it may be scheduled while
+// its predecessor drains; it executes griddepcontrol.wait (predecessor complete, its writes
+// visible) before touching global memory, so only the launch latency overlaps.  Off: measured
+// 0.5-1.7 % slower on the C2 step (profiles/r01/pdl_ab.txt), the gaps it hides are ~3 us.
+#ifndef S2L_PDL
+#define S2L_PDL 0
+#endif
+
+#include <utility>
 
 namespace s2l {
+
+#ifdef __CUDACC__
+// Kernel prologue of a PDL-launched kernel: wait for the predecessor grid, then allow the
+// successor grid to be scheduled (it waits for this one in turn).
+__device__ __forceinline__ void pdl_prologue() {
+#if S2L_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+// Launch with the programmatic-stream-serialization attribute (S2L_PDL) or plainly.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = S2L_PDL ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+#endif
 
 // ---- device-side descriptors written into the staging ring by the host -------------------
 
