@@ -106,8 +106,13 @@ def _i32p(arr):
 
 
 def _ptr(t):
-    """Device/host pointer of a torch tensor (or None -> NULL)."""
-    return None if t is None else C.c_void_p(t.data_ptr())
+    """Device/host pointer of a torch tensor (or None -> NULL).  The ABI takes dense row-major
+    arrays, so a strided view (e.g. a column slice of a fused QKV output) is refused."""
+    if t is None:
+        return None
+    if not t.is_contiguous():
+        raise ValueError("libs2l takes contiguous tensors (call .contiguous() on strided views)")
+    return C.c_void_p(t.data_ptr())
 
 
 def _stream(s):

@@ -882,3 +882,73 @@ def test_fused_append_then_swap_without_host_sync():
     P.check_state()
     P.check_pools_whole()                # request 0's CPU copy == the oracle's bytes
     P.prefill([(1, 384, 128, 0)], q1[384:])
+
+
+# ----------------------------------------------------------------------------- NEXT-4 per-layer API in a forward pass
+def test_streaming_decoder_chunked_equals_one_shot_and_oracle():
+    """A 2-layer random-weight decoder (paper_2604_16395_b200.model) prefilled chunk by chunk
+    through s2l_prefill_append (reserve once per chunk, one fused launch per layer) gives the
+    same last-layer hidden states as one-shot prefill of the whole input (chunked prefill
+    reuses the cache of earlier chunks); every layer's attention output of the chunked run equals
+    the fp64 oracle on the layer's own Q/K/V at sampled rows."""
+    from oracle.attention import attention_rows
+    from paper_2604_16395_b200 import model as M
+    shape = M.Shape(layers=2, hidden=1024, h_q=8, h_kv=2, d=128, inter=2048)
+    lens = {0: 300, 1: 200}
+    chunks = {0: [128, 128, 44], 1: [64, 64, 72]}
+    gtok = torch.Generator().manual_seed(5)
+    toks = {r: torch.randint(0, 32768, (n,), generator=gtok) for r, n in lens.items()}
+
+    def make(ng):
+        cfg = s2l.make_config(shape.layers, shape.h_q, shape.h_kv, shape.d, 16, ng, 0, max_requests=4,
+                              max_blocks_per_request=64)
+        pool = torch.empty(ng * s2l.block_bytes(cfg) // 2, dtype=torch.bfloat16, device="cuda")
+        ctx = s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None)
+        for r in lens:
+            ctx.new_request(r, toks[r].tolist())
+        return ctx, pool
+
+    ca, pa = make(64)
+    A = M.StreamingDecoder(shape, ca, seed=3)
+    pos = {r: 0 for r in lens}
+    last = {}
+    traces = []
+    for j in range(3):
+        items, tt, row = [], [], 0
+        for r in lens:
+            n = chunks[r][j]
+            items.append((r, pos[r], n, row))
+            tt.append(toks[r][pos[r]:pos[r] + n])
+            row += n
+        tr = []
+        x = A.chunk(items, torch.cat(tt).cuda(), trace=tr)
+        traces.append((items, tr))
+        for r, p, n, rw in items:
+            last[r] = (p, x[rw:rw + n].float().cpu())
+            pos[r] += n
+    cb, pb = make(64)
+    B = M.StreamingDecoder(shape, cb, seed=3)
+    items = [(0, 0, 300, 0), (1, 0, 200, 300)]
+    xb = B.chunk(items, torch.cat([toks[0], toks[1]]).cuda()).float().cpu()
+    for r, p, n, rw in items:
+        pl, xl = last[r]
+        ref = xb[rw + pl: rw + p + n]
+        err = ((xl - ref).abs().amax(-1) / ref.abs().amax(-1).clamp_min(1e-6)).max().item()
+        assert err <= 2e-2, (r, err)
+    # every layer's attention of the last chunk vs the oracle on that layer's own Q/K/V history
+    bits = lambda t: t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+    for layer in range(shape.layers):
+        for r in lens:
+            ks, vs = [], []
+            for items_j, tr in traces:
+                _, q, k, v, o = tr[layer]
+                for rr, p, n, rw in items_j:
+                    if rr == r:
+                        ks.append(bits(k[rw:rw + n])); vs.append(bits(v[rw:rw + n]))
+                        qr, orow, qp, nn = bits(q[rw:rw + n]), o[rw:rw + n], p, n
+            rows_s = [0, nn // 2, nn - 1]
+            o_ref, _ = attention_rows(qr, np.concatenate(ks), np.concatenate(vs), qp, rows_s)
+            og = orow[rows_s].float().cpu().numpy().astype(np.float64)
+            err = normwise_err(og, o_ref).max()
+            assert err <= 2e-2, (layer, r, err)
+    ca.close(); cb.close()
