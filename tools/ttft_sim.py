@@ -26,7 +26,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from paper_2604_16395_b200 import costmodel, s2l, scheduler as S  # noqa: E402
+from paper_2604_16395_b200 import costmodel, model as M, s2l, scheduler as S  # noqa: E402
 from synth import traces  # noqa: E402
 
 H_Q, H_KV, D, K = 32, 8, 128, 16
@@ -71,6 +71,25 @@ class Model:
                 torch.matmul(self.h[:rows], self.w[3])
 
 
+class DecoderModel:
+    """--model: the step is a real forward pass of a random-weight Llama-3-8B-shaped decoder
+    (paper_2604_16395_b200.model, NEXT-4): per layer the projections produce the chunk's Q/K/V
+    and one s2l_prefill_append stores K/V and computes the attention (token ids are synthetic:
+    the weights are random)."""
+
+    def __init__(self, ctx, layers):
+        shape = M.Shape(layers=layers, hidden=HIDDEN, h_q=H_Q, h_kv=H_KV, d=D, inter=INTER)
+        self.dec = M.StreamingDecoder(shape, ctx, seed=7)
+
+    def step(self, items):
+        its, toks, rows = [], [], 0
+        for r, q_pos, n in items:
+            its.append((r, q_pos, n, rows))
+            toks.append((torch.arange(q_pos, q_pos + n) * 7919 + r * 104729) % 32768)
+            rows += n
+        self.dec.chunk(its, torch.cat(toks).cuda())
+
+
 def run(trace, policy, streaming, args, cm, pools):
     gpool, cpool = pools
     cfg = s2l.make_config(args.layers, H_Q, H_KV, D, K, args.gpu_blocks, args.cpu_blocks,
@@ -79,7 +98,7 @@ def run(trace, policy, streaming, args, cm, pools):
     sch = S.StreamingScheduler(ctx, policy, K, args.budget, args.gpu_blocks, cost_model=cm,
                                preemption=args.preemption if cm is not None or args.preemption != "cost" else "recompute",
                                streaming=streaming)
-    model = Model(ctx, args.layers, args.budget, args.gemm)
+    model = DecoderModel(ctx, args.layers) if args.model else Model(ctx, args.layers, args.budget, args.gemm)
     t, i, steps, gpu_ms, host_s = 0.0, 0, 0, 0.0, 0.0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     while True:
@@ -126,6 +145,8 @@ def main():
     ap.add_argument("--cpu-blocks", type=int, default=8192)
     ap.add_argument("--delay-scale", type=float, default=1.0)
     ap.add_argument("--gemm", action="store_true")
+    ap.add_argument("--model", action="store_true",
+                    help="real decoder forward (random weights) through the per-layer fused API")
     ap.add_argument("--preemption", default="cost", choices=["cost", "recompute", "swap"])
     ap.add_argument("--policies", default="NS,DEFAULT,FCFS,MCPS,LCAS")
     args = ap.parse_args()
@@ -135,13 +156,14 @@ def main():
         seed, args.n, args.qps, delay_scale=args.delay_scale)
     # cost model matching the simulated prefill: with --gemm the full-prefill profile (attention +
     # append + dense layers), else attention + append only
-    cmp = os.path.join(ROOT, "profiles", "r01", "costmodel_b200_full.json" if args.gemm else "costmodel_b200.json")
+    cmp = os.path.join(ROOT, "profiles", "r01",
+                       "costmodel_b200_full.json" if (args.gemm or args.model) else "costmodel_b200.json")
     cm = costmodel.CostModel.load(cmp) if os.path.exists(cmp) else None
     mb = 2 * args.layers * K * H_KV * D * 2
     gpool = torch.empty(args.gpu_blocks * mb // 2, dtype=torch.bfloat16, device="cuda")
     cpool = torch.empty(args.cpu_blocks * mb // 2, dtype=torch.bfloat16, pin_memory=True)
     out = {"workload": f"TTFT {args.workload} trace (synthetic, synth/traces.py)", "qps": args.qps,
-           "queries": args.n, "layers": args.layers, "gemm": args.gemm, "budget": args.budget,
+           "queries": args.n, "layers": args.layers, "gemm": args.gemm, "model": args.model, "budget": args.budget,
            "gpu_blocks": args.gpu_blocks, "cpu_blocks": args.cpu_blocks, "delay_scale": args.delay_scale,
            "cost_model": os.path.relpath(cmp, ROOT) if cm else None, "runs": []}
     for p in args.policies.split(","):
