@@ -222,3 +222,16 @@ def test_z19_token_only_append_on_the_cpu_tier():
     ora.append([(3, None, 3, 0)], z, z)
     assert lib.query(3) == ora.info(3) and lib.query(3)["num_computed"] == 11
     assert lib.block_table(3) == ora.block_table(3)
+
+
+def test_binding_refuses_strided_tensors():
+    """The ABI takes dense row-major arrays: a strided view (e.g. the V columns of a fused QKV
+    projection output) must be refused by the binding instead of being read as dense rows."""
+    import torch
+    qkv = torch.zeros(4, 3 * 8, dtype=torch.bfloat16)
+    v = qkv[:, 16:].view(4, 1, 8)
+    assert not v.is_contiguous()
+    with pytest.raises(ValueError):
+        s2l._ptr(v)
+    assert s2l._ptr(v.contiguous()) is not None
+    assert s2l._ptr(None) is None
