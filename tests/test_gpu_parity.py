@@ -952,3 +952,31 @@ def test_streaming_decoder_chunked_equals_one_shot_and_oracle():
             err = normwise_err(og, o_ref).max()
             assert err <= 2e-2, (layer, r, err)
     ca.close(); cb.close()
+
+
+def test_fused_append_then_invalidate_and_swap_in_without_host_sync():
+    """Stream hazard of the fused path (WAW across streams): the fused kernel writes request A's
+    blocks; without a host sync A is invalidated to 0 and request B is swapped in, receiving
+    those ids (Z9: B's own released ids come last).  The H2D must wait for the fused kernel,
+    else the kernel's late writes would corrupt B's restored blocks."""
+    geo = W.Geometry(L=1, h_q=8, h_kv=2, d=128, k=16)
+    P = Pair(1, 8, 2, 128, 16, 48, 64, max_blocks=64)
+    seed = W.seed_of(26)
+    toks = {r: W.request_tokens(seed, r, 512) for r in (0, 1)}
+    data = {r: _stream_qkv(seed, toks[r], geo) for r in (0, 1)}
+    P.new(0, toks[0]); P.new(1, toks[1])
+    qb, kb_, vb = data[1]
+    P.append_reserve([(1, None, 256, 0)], kb_[:, :256], vb[:, :256])
+    P.prefill_append([(1, 0, 256, 0)], qb[:256], kb_[0, :256], vb[0, :256])
+    assert P.swap_out([1])[0] == s2l.OK                  # B on the CPU tier, ids 0..15 released
+    qa, ka, va = data[0]
+    P.append_reserve([(0, None, 512, 0)], ka, va)        # A takes 16..47
+    qd, kd, vd = to_dev(qa), to_dev(ka[0]), to_dev(va[0])
+    od = torch.zeros_like(qd)
+    P.lib.prefill_append(0, [(0, 0, 512, 0)], qd, kd, vd, od)   # no synchronisation after this
+    P.invalidate(0, [])                                   # frees all of A's blocks
+    assert P.swap_in([1])[0] == s2l.OK                    # B lands in ids A's kernel writes
+    assert set(P.lib.block_table(1)) & set(range(16, 48))
+    P.check_state()
+    P.check_pools_whole()
+    P.prefill([(1, 128, 128, 0)], qb[128:256])
