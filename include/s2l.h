@@ -191,9 +191,10 @@ s2l_status s2l_prefill_batch(s2l_ctx* ctx, int32_t layer, int32_t n_items,
  * the attention of s2l_prefill_batch is computed over the prefix plus those rows.  The blocks
  * must already be held (s2l_append_chunk, normally in reserve mode with k = v = NULL).
  *   k, v: device [q_rows][h_kv][d] bf16 of this layer (same row indexing as q).
- * When every q_pos is a multiple of k (and the tensor-core kernel runs) one kernel does both:
- * it reads the chunk's K/V tiles from k / v and each work unit writes the blocks starting in its
- * own token range to the pool; otherwise a one-layer append launch precedes the attention.
+ For items whose q_pos is a multiple of k (tensor-core kernel) one kernel does both: it reads
+ * the chunk's K/V tiles from k / v and each work unit writes the blocks starting in its own token
+ * range to the pool; the other items (or all, when more than 64 items are passed and one is
+ * unaligned) are appended by a one-layer append launch before the attention.
  * Errors: those of s2l_prefill_batch; k or v NULL, or a request repeated in the call -> E_INVAL. */
 s2l_status s2l_prefill_append(s2l_ctx* ctx, int32_t layer, int32_t n_items,
                               const s2l_prefill_item* items, const void* q, const void* k,

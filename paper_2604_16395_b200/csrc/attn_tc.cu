@@ -105,6 +105,7 @@ struct TcParams {
 struct TcParamsFused : TcParams {
   CUtensorMap tmap_kin, tmap_vin;     // box {64, 1, k}: one block of one kv head
   CUtensorMap tmap_kin_t, tmap_vin_t; // box {64, 1, 128}: a whole 128-key tile
+  uint64_t fuse_mask;                 // bit i: item i's append is fused (others: from the pool)
 };
 template <bool kFuse> struct ParamsOf { using T = TcParams; };
 template <> struct ParamsOf<true> { using T = TcParamsFused; };
@@ -922,7 +923,8 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       uint32_t rp = 0;
       // fused append: blocks starting at or after q_pos come from the caller's rows; this unit
       // writes the blocks whose first position lies in its token range [wr_lo, wr_hi)
-      const bool fuse = kFuse && p.fuse != 0;
+      bool fuse = false;
+      if constexpr (kFuse) fuse = p.fuse != 0 && (lo >= 64 || ((p.fuse_mask >> lo) & 1ull));
       const int64_t wr_lo = it.q_pos + tok0, wr_hi = it.q_pos + min(tok0 + 2 * toks, it.n_q);
       bool st_pending = false;                          // lane 0 has TMA stores in flight
       for (int32_t j = 0; j < nT; ++j) {
@@ -2861,7 +2863,8 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
                            float* ws, int32_t max_pieces, int32_t* ws_cnt,
                            const int32_t* table, int32_t layer, const void* tmap_q,
                            const void* tmap_kv, void* o, float* lse, int32_t num_sms,
-                           int32_t flags, cudaStream_t st, const void* tmap_in, void* pool) {
+                           int32_t flags, cudaStream_t st, const void* tmap_in, void* pool,
+                           uint64_t fuse_mask) {
   const int variant = attn_tc_tiles_per_cta();
   const bool fuse = (flags & kAttnFuseAppend) != 0;
   if (fuse && (variant != 2 || (flags & (kAttnPersistent | kAttnSplitSoftmax | kAttnKV64)) ||
@@ -2930,6 +2933,7 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
     memcpy(&pf.tmap_vin, (const char*)tmap_in + 128, sizeof(CUtensorMap));
     memcpy(&pf.tmap_kin_t, (const char*)tmap_in + 256, sizeof(CUtensorMap));
     memcpy(&pf.tmap_vin_t, (const char*)tmap_in + 384, sizeof(CUtensorMap));
+    pf.fuse_mask = fuse_mask;
   }
   p.ws = ws;
   p.ws_ml = ws ? ws + (int64_t)max_pieces * 2 * 128 * kD : nullptr;

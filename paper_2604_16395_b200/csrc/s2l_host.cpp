@@ -948,15 +948,26 @@ static s2l_status prefill_impl(s2l_ctx* c, int32_t layer, int32_t n_items,
   }
   if (n_items > 0 && (!q || !o)) return fail(S2L_E_INVAL, "q/o is NULL");
   const bool append = k != nullptr;
-  bool fused = false;
+  bool fused = false;                    // the attention launch fuses (some of) the appends
+  std::vector<uint8_t> in_kernel(n_items > 0 ? n_items : 1, 0);   // item's append inside it
+  std::vector<s2l_prefill_item> separate;                         // items appended by a launch
   if (append) {
     if (!v) return fail(S2L_E_INVAL, "k/v is NULL");
     std::unordered_set<int64_t> seen;
-    fused = c->tc_ok && s2l::attn_tc_tiles_per_cta() == 2 && !c->persistent && !c->split_softmax && !c->kv64;
+    const bool kern = c->tc_ok && s2l::attn_tc_tiles_per_cta() == 2 && !c->persistent &&
+                      !c->split_softmax && !c->kv64;
+    int32_t aligned = 0;
     for (int32_t i = 0; i < n_items; ++i) {
       if (!seen.insert(items[i].req_id).second)
         return fail(S2L_E_INVAL, "item %d: request %lld repeated", i, (long long)items[i].req_id);
-      if (items[i].q_pos % c->cfg.block_size) fused = false;
+      aligned += items[i].q_pos % c->cfg.block_size == 0;
+    }
+    // per item when the items travel inline (the kernel gets a mask), else all or nothing
+    const bool per_item = n_items <= s2l::kInlineAttnItems;
+    fused = kern && aligned > 0 && (aligned == n_items || per_item);
+    for (int32_t i = 0; i < n_items; ++i) {
+      in_kernel[i] = fused && items[i].q_pos % c->cfg.block_size == 0;
+      if (!in_kernel[i]) separate.push_back(items[i]);
     }
   }
   if (c->sticky) return fail(c->sticky, "context has a sticky CUDA error");
@@ -969,8 +980,8 @@ static s2l_status prefill_impl(s2l_ctx* c, int32_t layer, int32_t n_items,
       if (!ring_wait(c, c->in_ring, c->compute, r->swap_in_seq)) return S2L_E_CUDA;
     }
   }
-  if (append && !fused) {
-    st = layer_append(c, layer, n_items, items, k, v, q_rows);
+  if (!separate.empty()) {
+    st = layer_append(c, layer, (int32_t)separate.size(), separate.data(), k, v, q_rows);
     if (st) return st;
   }
   const int32_t G = c->cfg.num_q_heads / c->cfg.num_kv_heads;
@@ -982,6 +993,12 @@ static s2l_status prefill_impl(s2l_ctx* c, int32_t layer, int32_t n_items,
     return items[x].q_pos + items[x].n_q > items[y].q_pos + items[y].n_q;
   });
   std::vector<s2l::AttnItemDev> dev(n_items);
+  uint64_t fuse_mask = ~0ull;            // bit i: item i (kernel order) appended in-kernel
+  if (fused && n_items <= s2l::kInlineAttnItems) {
+    fuse_mask = 0;
+    for (int32_t i = 0; i < n_items; ++i)
+      if (in_kernel[order[i]]) fuse_mask |= 1ull << i;
+  }
   const int64_t tiles_per_cta = c->tc_ok ? s2l::attn_tc_tiles_per_cta() : 1;
   int64_t units = 0, total_q = 0;
   for (int32_t i = 0; i < n_items; ++i) {
@@ -1062,7 +1079,7 @@ static s2l_status prefill_impl(s2l_ctx* c, int32_t layer, int32_t n_items,
                                (c->split_softmax ? s2l::kAttnSplitSoftmax : 0) |
                                (c->kv64 ? s2l::kAttnKV64 : 0) |
                                (fused ? s2l::kAttnFuseAppend : 0),
-                           c->compute, fused ? tin : nullptr, c->gpu_pool));
+                           c->compute, fused ? tin : nullptr, c->gpu_pool, fuse_mask));
   } else {
     CK(s2l::launch_attn_generic(c->geo, dv, n_items, total_q, c->d_table, layer, q, o, lse,
                                 c->gpu_pool, c->compute));

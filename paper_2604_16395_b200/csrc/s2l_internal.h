@@ -143,14 +143,16 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
                            const int32_t* table, int32_t layer, const void* tmap_q,
                            const void* tmap_kv, void* o, float* lse, int32_t num_sms,
                            int32_t flags, cudaStream_t st, const void* tmap_in = nullptr,
-                           void* pool = nullptr);
+                           void* pool = nullptr, uint64_t fuse_mask = ~0ull);
+// fuse_mask (kAttnFuseAppend, items inline): bit i set = item i (in the items array's order)
+// has its append fused; the others were appended before the launch and read from the pool.
 // flags of launch_attn_tc
 constexpr int32_t kAttnPersistent = 1;   // v2 only: grid = min(work items, SMs), CTAs loop
 constexpr int32_t kAttnSplitSoftmax = 2; // v4: each tile's softmax split over two warps per SMSP
 constexpr int32_t kAttnKV64 = 4;         // v5: 64-key steps, double-buffered S per tile
-// v2 only: fused append (NEXT-2).  Every item's q_pos is a multiple of the block size; the
-// chunk rows [q_pos, q_pos+n_q) of this layer are read from tmap_in (make_tmap_in) and written
-// to the pool by the kernel.  No two items may share a request.
+// v2 only: fused append (NEXT-2).  For every item selected by fuse_mask (q_pos a multiple of
+// the block size) the chunk rows [q_pos, q_pos+n_q) of this layer are read from tmap_in
+// (make_tmap_in) and written to the pool by the kernel.  No two items may share a request.
 constexpr int32_t kAttnFuseAppend = 8;
 // Experiments: device buffer receiving kernel timeline stamps (S2L_TRACE builds); nullptr = off.
 void set_attn_trace(uint32_t* buf);   // v2 only: grid = min(work items, SMs), CTAs loop
