@@ -554,6 +554,12 @@ def main():
         line["next2_fused"] = {"value": flops_rank / (fms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": fms,
                                "plain_ms_per_step_same_window": pms,
                                "path": "s2l_append_chunk (reserve) + s2l_prefill_append: one launch per chunk"}
+        # full-size parity of the fused path: the last chunk's attention reads the prefix the fused
+        # launches of this step wrote into the pool
+        S.o[-1].zero_()
+        ffn()
+        torch.cuda.synchronize()
+        line["next2_fused"]["parity"] = parity_check(S, data, 0, 1, None)
         # e2e through the C ABI with host buffers
         S_host = Stream(rids, toks, data, dev, pinned=True)
         dev_bufs = tuple([torch.empty_like(S.q[0] if i in (0, 3) else S.k[0]) for _ in range(E2E_BUFS)]
