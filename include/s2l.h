@@ -14,9 +14,12 @@
  *   - a device block table [max_requests][max_blocks_per_request] int32 (library-owned)
  *     read by the kernels; block j of a request holds positions [j*k, j*k+k).
  *
- * Allocation (Z9): every allocation takes the LOWEST free ids of the tier, ascending, except
- * that the GPU ids released by the most recent swap-out come after every other free GPU id;
- * requests/items of one call are served in call order.  Every call that can fail is
+ * Allocation (Z9; the paper only says "free block pool"): every allocation takes the
+ * LOWEST free ids of the tier, ascending, independent of the order in which ids were freed
+ * (SURVEY.md §8.2 c.4 Z9); requests/items of one call are served in call order.  Opt-in
+ * (s2l_config.alloc_cooling = 1, a performance choice, not the paper's): the GPU ids released
+ * by the most recent swap-out ("cooling": their D2H copy may still be reading them) come after
+ * every other free GPU id, so appends and swap-ins rarely wait for a D2H.  Every call that can fail is
  * all-or-nothing: arguments and capacity are validated before any state changes.
  *
  * Streams: `compute_stream` runs append/patch/attention kernels; `copy_stream` runs swap-out
@@ -75,6 +78,8 @@ typedef struct s2l_config {
   int32_t max_blocks_per_request; /* columns of the device block table                      */
   int32_t lcp_block_aligned;      /* 0 = token-granular LCP (default, Z4);
                                      1 = round the kept prefix down to a block     */
+  int32_t alloc_cooling;          /* 0 = plain lowest-free-id order (Z9, default);
+                                     1 = GPU ids freed by the latest swap-out go last       */
 } s2l_config;
 
 /* One request of an s2l_append_chunk call. */

@@ -22,7 +22,10 @@
 Readings: Z4 token-granular LCP by default (keep ⌈b/k⌉ blocks,
 the boundary block's stale tail is never read), `lcp_block_aligned` reproduces SPEC's
 block round-down; Z5 b = min(p, nc); Z9 lowest free id first on both tiers,
-items/requests served in call order; Z12 swap copies whole blocks.
+independent of free order (the paper only says "free block pool"),
+items/requests served in call order; `alloc_cooling` is an OPT-IN performance variant of
+Z9 (not the paper's) (GPU ids released by the most recent swap-out come after every other free id),
+mirrored here as an explicit parameter with its own golden; Z12 swap copies whole blocks.
 
 The oracle keeps its OWN model of everything:
   * per request: input tokens, nc, tier, ordered block ids, total_tokens_invalidated,
@@ -68,14 +71,15 @@ class Req:
 class OracleKV:
     def __init__(self, L, h_q, h_kv, d, k, num_gpu_blocks, num_cpu_blocks,
                  max_requests=1 << 30, max_blocks_per_request=1 << 30, lcp_block_aligned=False,
-                 mirror_pools=True):
+                 mirror_pools=True, alloc_cooling=False):
         assert h_q % h_kv == 0
         self.L, self.h_q, self.h_kv, self.d, self.k = L, h_q, h_kv, d, k
         self.num_gpu_blocks, self.num_cpu_blocks = num_gpu_blocks, num_cpu_blocks
         self.max_requests, self.max_blocks = max_requests, max_blocks_per_request
         self.aligned = bool(lcp_block_aligned)
         self.free = {GPU: set(range(num_gpu_blocks)), CPU: set(range(num_cpu_blocks))}
-        self.cool = set()   # GPU ids released by the most recent swap-out (Z9), subset of free
+        self.cooling = bool(alloc_cooling)
+        self.cool = set()   # alloc_cooling: GPU ids released by the latest swap-out, subset of free
         self.reqs: dict[int, Req] = {}
         self.mirror = mirror_pools
         shape = (L, 2, h_kv, k, d)
@@ -88,8 +92,8 @@ class OracleKV:
         return block_bytes(self.L, self.k, self.h_kv, self.d)
 
     def _take_lowest(self, tier, n):
-        """Z9: the n lowest free ids, ascending -- except that GPU ids released by the most
-        recent swap-out ("cooling") come after every other free id (lowest first)."""
+        """Z9: the n lowest free ids, ascending.  alloc_cooling variant: GPU ids released by
+        the most recent swap-out ("cooling") come after every other free id (lowest first)."""
         cool = self.cool if tier == GPU else set()
         ids = sorted(self.free[tier] - cool)[:n]
         if len(ids) < n:
@@ -239,8 +243,8 @@ class OracleKV:
             need += len(r.blocks)
         if need > len(self.free[dst]):
             return e_full, 0
-        if src == GPU and rids:
-            self.cool = set()                           # Z9: the previous swap-out's ids thaw
+        if src == GPU and rids and self.cooling:
+            self.cool = set()                           # the previous swap-out's ids thaw
         for rid in rids:
             r = self.reqs[rid]
             new_ids = self._take_lowest(dst, len(r.blocks))
@@ -248,7 +252,7 @@ class OracleKV:
                 for s, t in zip(r.blocks, new_ids):
                     self.pool[dst][t] = self.pool[src][s]   # whole block (Z12)
             self._give_back(src, r.blocks)
-            if src == GPU:
+            if src == GPU and self.cooling:
                 self.cool.update(r.blocks)
             r.blocks, r.tier = new_ids, dst
         return OK, need * self.m_block

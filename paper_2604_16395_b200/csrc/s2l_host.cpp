@@ -91,11 +91,11 @@ class Allocator {
   size_t hint_ = 0;
 };
 
-// A tier's free ids (reading Z9): the lowest free id first, except that the GPU ids released
-// by the most recent swap-out ("cooling": their D2H may still be reading them) are handed out
-// only after every other free id (lowest first among them).  Deterministic, so the oracle
-// reproduces it; all free ids count for capacity.  It keeps appends and swap-ins from
-// landing in blocks a D2H is still reading when other blocks are free.
+// A tier's free ids (reading Z9): the lowest free id first.  With s2l_config.alloc_cooling
+// (opt-in, a performance choice the paper does not make), the GPU ids released by the most
+// recent swap-out ("cooling": their D2H may still be reading them) are handed out only after
+// every other free id (lowest first among them); all free ids count for capacity.  It keeps
+// appends and swap-ins from landing in blocks a D2H is still reading when others are free.
 class TierPool {
  public:
   void init(int64_t n) {
@@ -262,6 +262,8 @@ s2l_status check_config(const s2l_config* cfg) {
     return fail(S2L_E_INVAL, "bad pool / table sizes");
   if (g.lcp_block_aligned != 0 && g.lcp_block_aligned != 1)
     return fail(S2L_E_INVAL, "lcp_block_aligned must be 0 or 1");
+  if (g.alloc_cooling != 0 && g.alloc_cooling != 1)
+    return fail(S2L_E_INVAL, "alloc_cooling must be 0 or 1");
   return S2L_OK;
 }
 
@@ -440,7 +442,7 @@ s2l_status swap_impl(s2l_ctx* c, int32_t n_reqs, const int64_t* ids, int64_t* by
     for (size_t j = 0; j < nid.size(); ++j) moves.emplace_back(r->blocks[j], nid[j]);
     if (src == S2L_TIER_GPU && !c->host_only)
       for (int32_t b : r->blocks) c->freed_use[(size_t)b] = r->use_seq;
-    if (src == S2L_TIER_GPU) {   // Z9: this call's GPU ids cool until the next swap-out
+    if (src == S2L_TIER_GPU && c->cfg.alloc_cooling) {   // opt-in: ids cool until the next swap-out
       if (i == 0) c->alloc[src].give_back_cooling(nullptr, 0);
       c->alloc[src].give_back_cooling_append(r->blocks.data(), (int64_t)r->blocks.size());
     } else {

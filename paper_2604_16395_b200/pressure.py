@@ -214,8 +214,9 @@ class PressureDriver:
         out GPU requests outside sel (and, if possible, outside `protect` = the step still
         computing) and swap in the members of sel on the CPU tier.  With evict_ahead the same
         swap-out call also makes room for the step after sel: its D2H then runs while this
-        step and the next compute, and (reading Z9) the ids it releases are allocated only
-        after every other free id, so the next step's appends and swap-ins avoid them."""
+        step and the next compute, and (with the opt-in s2l_config.alloc_cooling) the ids it
+        releases are allocated only after every other free id, so the next step's appends and
+        swap-ins avoid them."""
         for r in sel:
             w = self.work[r][self.next_work[r]]
             if w.new_input is not None:

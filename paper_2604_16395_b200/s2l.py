@@ -31,7 +31,8 @@ class Config(C.Structure):
     _fields_ = [("num_layers", C.c_int32), ("num_q_heads", C.c_int32), ("num_kv_heads", C.c_int32),
                 ("head_dim", C.c_int32), ("block_size", C.c_int32), ("num_gpu_blocks", C.c_int32),
                 ("num_cpu_blocks", C.c_int32), ("max_requests", C.c_int32),
-                ("max_blocks_per_request", C.c_int32), ("lcp_block_aligned", C.c_int32)]
+                ("max_blocks_per_request", C.c_int32), ("lcp_block_aligned", C.c_int32),
+                ("alloc_cooling", C.c_int32)]
 
 
 class AppendItem(C.Structure):
@@ -122,11 +123,13 @@ def _stream(s):
 
 
 def make_config(num_layers, num_q_heads, num_kv_heads, head_dim, block_size, num_gpu_blocks,
-                num_cpu_blocks, max_requests=256, max_blocks_per_request=None, lcp_block_aligned=0):
+                num_cpu_blocks, max_requests=256, max_blocks_per_request=None, lcp_block_aligned=0,
+                alloc_cooling=0):
     if max_blocks_per_request is None:
         max_blocks_per_request = max(1, num_gpu_blocks + num_cpu_blocks)
     return Config(num_layers, num_q_heads, num_kv_heads, head_dim, block_size, num_gpu_blocks,
-                  num_cpu_blocks, max_requests, max_blocks_per_request, int(lcp_block_aligned))
+                  num_cpu_blocks, max_requests, max_blocks_per_request, int(lcp_block_aligned),
+                  int(alloc_cooling))
 
 
 def block_bytes(cfg: Config) -> int:

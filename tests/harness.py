@@ -34,12 +34,12 @@ class Pair:
     """A libs2l device context and an OracleKV with identical geometry."""
 
     def __init__(self, L, h_q, h_kv, d, k, ng, nc, aligned=False, max_requests=64, max_blocks=None,
-                 mirror=True, stream=None):
+                 mirror=True, stream=None, cooling=False):
         self.geo = (L, h_q, h_kv, d, k)
         self.L, self.h_q, self.h_kv, self.d, self.k = L, h_q, h_kv, d, k
         cfg = s2l.make_config(L, h_q, h_kv, d, k, ng, nc, max_requests=max_requests,
                               max_blocks_per_request=max_blocks or max(ng, nc, 1),
-                              lcp_block_aligned=int(aligned))
+                              lcp_block_aligned=int(aligned), alloc_cooling=int(cooling))
         self.m_block = s2l.block_bytes(cfg)
         self.gpu_pool = torch.empty(max(1, ng) * self.m_block // 2, dtype=torch.bfloat16, device="cuda")
         self.cpu_pool = torch.empty(max(1, nc) * self.m_block // 2, dtype=torch.bfloat16).pin_memory()
@@ -50,7 +50,7 @@ class Pair:
         self.lib = s2l.Context(cfg, self.gpu_pool, self.cpu_pool if nc else None, self.stream, None)
         self.ora = OracleKV(L, h_q, h_kv, d, k, ng, nc, max_requests=max_requests,
                             max_blocks_per_request=max_blocks or max(ng, nc, 1), lcp_block_aligned=aligned,
-                            mirror_pools=mirror)
+                            mirror_pools=mirror, alloc_cooling=cooling)
         self.ng, self.nc = ng, nc
 
     # ---- ops on both sides -----------------------------------------------------------
@@ -196,7 +196,8 @@ class Twin:
     def __init__(self, lib, k, ng, nc, max_requests, max_blocks):
         self.lib = lib
         self.ora = OracleKV(1, 1, 1, 8, k, ng, nc, max_requests=max_requests,
-                            max_blocks_per_request=max_blocks, mirror_pools=False)
+                            max_blocks_per_request=max_blocks, mirror_pools=False,
+                            alloc_cooling=bool(lib.cfg.alloc_cooling))
         self.m_lib = s2l.block_bytes(lib.cfg)
         self.ops = 0
 

@@ -446,7 +446,8 @@ def _sample_rows_small(rng, n, k=6):
     return sorted(set([0, n - 1] + rng.choice(n, size=k, replace=False).tolist()))
 
 
-def test_stream_hazards_without_host_syncs():
+@pytest.mark.parametrize("cooling", [False, True])
+def test_stream_hazards_without_host_syncs(cooling):
     """Swaps run on their own streams and overlap compute that does not touch their blocks; the
     library orders only real conflicts (DESIGN.md §5 stream hazards).  With no host
     synchronisation inside each race, three races are provoked (the pool is sized so that the
@@ -462,12 +463,14 @@ def test_stream_hazards_without_host_syncs():
     rid = {"A": 0, "B": 1, "C": 2, "D": 3}
     n = {"A": 4096, "B": 2048, "C": 2048, "D": 1024}
     ng, nc = 300, 600
-    cfg = s2l.make_config(2, 64, 8, 128, 16, ng, nc, max_requests=8, max_blocks_per_request=512)
+    cfg = s2l.make_config(2, 64, 8, 128, 16, ng, nc, max_requests=8, max_blocks_per_request=512,
+                          alloc_cooling=int(cooling))
     mb = s2l.block_bytes(cfg)
     gpool = torch.empty(ng * mb // 2, dtype=torch.bfloat16, device="cuda")
     cpool = torch.empty(nc * mb // 2, dtype=torch.bfloat16).pin_memory()
     lib = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), None)
-    ora = OracleKV(2, 64, 8, 128, 16, ng, nc, max_requests=8, max_blocks_per_request=512, mirror_pools=False)
+    ora = OracleKV(2, 64, 8, 128, 16, ng, nc, max_requests=8, max_blocks_per_request=512, mirror_pools=False,
+                   alloc_cooling=cooling)
     toks = {r: W.request_tokens(seed, rid[r], n[r]) for r in rid}
     data = {r: _stream_qkv(seed, toks[r], geo) for r in rid}
     dev = {r: (to_dev(data[r][0]), to_dev(data[r][1]), to_dev(data[r][2])) for r in rid}
@@ -514,7 +517,7 @@ def test_stream_hazards_without_host_syncs():
         swap(r, True)
     append("A")
     lib.sync()
-    # race 1: swap_out(A) then an append of B that must reuse A's released (cooling) ids
+    # race 1: swap_out(A) then an append of B that must reuse A's released ids
     a_ids = set(lib.block_table(rid["A"]))
     swap("A", True)
     append("B")
@@ -553,8 +556,10 @@ def test_stream_hazards_without_host_syncs():
         assert err.max() <= 2e-2, (r, layer, float(err.max()))
 
 
-@pytest.mark.parametrize("serial,cost,prefetch", [(False, False, 0), (True, False, 0), (False, True, 0), (False, False, 2)])
-def test_c4_pressure_driver_on_device(serial, cost, prefetch):
+@pytest.mark.parametrize("serial,cost,prefetch,cooling", [(False, False, 0, False), (False, False, 0, True),
+                                                          (True, False, 0, False), (False, True, 0, False),
+                                                          (False, False, 2, True)])
+def test_c4_pressure_driver_on_device(serial, cost, prefetch, cooling):
     """The C4 driver (paper_2604_16395_b200.pressure) at reduced size on the device: 16
     append / update requests, GPU pool 50% of the working set, swaps overlapping compute (or
     serialised), no host synchronisation inside the stream.  Bookkeeping is mirrored into the
@@ -569,7 +574,8 @@ def test_c4_pressure_driver_on_device(serial, cost, prefetch):
     plans = pressure.c4_plans(31, 16, lo=256, hi=2048, budget=budget)
     ws = pressure.working_set_blocks(plans, K)
     ng, ncpu = ws // 2, ws
-    cfg = s2l.make_config(L, 32, 8, 128, K, ng, ncpu, max_requests=16, max_blocks_per_request=2048 // K)
+    cfg = s2l.make_config(L, 32, 8, 128, K, ng, ncpu, max_requests=16, max_blocks_per_request=2048 // K,
+                          alloc_cooling=int(cooling))
     mb = s2l.block_bytes(cfg)
     gpool = torch.empty(ng * mb // 2, dtype=torch.bfloat16, device="cuda")
     cpool = torch.empty(ncpu * mb // 2, dtype=torch.bfloat16).pin_memory()
@@ -728,7 +734,7 @@ def lib_reqs(tw):
 def test_swap_round_trip_full_size_c4_blocks():
     """a5/a6 at the C4 / bench size: 512 blocks of M_block = 2 MiB (L = 32, Llama-3-8B KV)
     of four interleaved requests (scattered ids) swapped out and back in, twice (the second
-    round reuses CPU ids freed by the first and GPU ids released under the Z9 cooling rule);
+    round reuses CPU ids freed by the first and GPU ids released by the swap-out);
     every request's blocks must come back bit-identical (whole blocks, Z12)."""
     L, nblk = 32, 512
     cfg = s2l.make_config(L, 32, 8, 128, 16, nblk + 64, nblk + 64, max_requests=8, max_blocks_per_request=nblk)
@@ -877,7 +883,7 @@ def test_fused_append_then_swap_without_host_sync():
         P.lib.prefill_append(l, [(0, 0, 512, 0)], qd, kd[l], vd[l], od)
     P.swap_out([0])                      # no synchronisation since the fused launches
     q1, k1, v1 = data[1]
-    P.append([(1, None, 512, 0)], k1, v1)   # reuses ids request 0 just released (Z9: after the others)
+    P.append([(1, None, 512, 0)], k1, v1)   # reuses ids request 0 just released
     assert set(P.lib.block_table(1)) & set(range(32))
     P.check_state()
     P.check_pools_whole()                # request 0's CPU copy == the oracle's bytes
@@ -957,8 +963,8 @@ def test_streaming_decoder_chunked_equals_one_shot_and_oracle():
 def test_fused_append_then_invalidate_and_swap_in_without_host_sync():
     """Stream hazard of the fused path (WAW across streams): the fused kernel writes request A's
     blocks; without a host sync A is invalidated to 0 and request B is swapped in, receiving
-    those ids (Z9: B's own released ids come last).  The H2D must wait for the fused kernel,
-    else the kernel's late writes would corrupt B's restored blocks."""
+    those ids.  The H2D must wait for the fused kernel, else the kernel's late writes would
+    corrupt B's restored blocks."""
     geo = W.Geometry(L=1, h_q=8, h_kv=2, d=128, k=16)
     P = Pair(1, 8, 2, 128, 16, 48, 64, max_blocks=64)
     seed = W.seed_of(26)
@@ -970,13 +976,14 @@ def test_fused_append_then_invalidate_and_swap_in_without_host_sync():
     P.prefill_append([(1, 0, 256, 0)], qb[:256], kb_[0, :256], vb[0, :256])
     assert P.swap_out([1])[0] == s2l.OK                  # B on the CPU tier, ids 0..15 released
     qa, ka, va = data[0]
-    P.append_reserve([(0, None, 512, 0)], ka, va)        # A takes 16..47
+    P.append_reserve([(0, None, 512, 0)], ka, va)        # A takes 32 of the 48 ids
+    a_ids = set(P.lib.block_table(0))
     qd, kd, vd = to_dev(qa), to_dev(ka[0]), to_dev(va[0])
     od = torch.zeros_like(qd)
     P.lib.prefill_append(0, [(0, 0, 512, 0)], qd, kd, vd, od)   # no synchronisation after this
     P.invalidate(0, [])                                   # frees all of A's blocks
     assert P.swap_in([1])[0] == s2l.OK                    # B lands in ids A's kernel writes
-    assert set(P.lib.block_table(1)) & set(range(16, 48))
+    assert set(P.lib.block_table(1)) & a_ids
     P.check_state()
     P.check_pools_whole()
     P.prefill([(1, 128, 128, 0)], qb[128:256])

@@ -2,6 +2,7 @@
 host-only context compared bit-exact with the oracle's state machine (block tables of both
 tiers, nc, LCP, invalidated counts, total_tokens_invalidated, free counts, status codes,
 swap bytes)."""
+import json
 import os
 import random
 import re
@@ -43,19 +44,22 @@ def test_config_validation():
     for bad in [s2l.make_config(1, 3, 2, 16, 4, 8, 8),        # h % h_kv
                 s2l.make_config(1, 2, 1, 12, 4, 8, 8),        # head_dim % 8
                 s2l.make_config(1, 2, 1, 16, 3, 8, 8),        # block not power of two
-                s2l.make_config(1, 2, 1, 16, 4, 8, 8, lcp_block_aligned=2)]:
+                s2l.make_config(1, 2, 1, 16, 4, 8, 8, lcp_block_aligned=2),
+                s2l.make_config(1, 2, 1, 16, 4, 8, 8, alloc_cooling=2)]:
         with pytest.raises(s2l.S2LError) as e:
             s2l.Context(bad, host_only=True)
         assert e.value.status == s2l.E_INVAL
 
 
-def _pair(L=1, h_q=2, h_kv=1, d=16, k=4, ng=8, nc=8, aligned=False, max_requests=64, max_blocks=None):
+def _pair(L=1, h_q=2, h_kv=1, d=16, k=4, ng=8, nc=8, aligned=False, max_requests=64, max_blocks=None,
+          cooling=False):
     cfg = s2l.make_config(L, h_q, h_kv, d, k, ng, nc, max_requests=max_requests,
-                          max_blocks_per_request=max_blocks or (ng + nc), lcp_block_aligned=int(aligned))
+                          max_blocks_per_request=max_blocks or (ng + nc), lcp_block_aligned=int(aligned),
+                          alloc_cooling=int(cooling))
     lib = s2l.Context(cfg, host_only=True)
     ora = OracleKV(L, h_q, h_kv, d, k, ng, nc, max_requests=max_requests,
                    max_blocks_per_request=max_blocks or (ng + nc), lcp_block_aligned=aligned,
-                   mirror_pools=False)
+                   mirror_pools=False, alloc_cooling=cooling)
     return lib, ora
 
 
@@ -66,9 +70,9 @@ def _same_state(lib, ora):
         assert lib.block_table(rid) == ora.block_table(rid), rid
 
 
-@pytest.mark.parametrize("aligned", [False, True])
-def test_c1_walk_matches_oracle(aligned):
-    lib, ora = _pair(aligned=aligned)
+@pytest.mark.parametrize("aligned,cooling", [(False, False), (True, False), (False, True)])
+def test_c1_walk_matches_oracle(aligned, cooling):
+    lib, ora = _pair(aligned=aligned, cooling=cooling)
     toks = list(range(100, 124))
     for x in (lib, ora):
         x.new_request(1, [])
@@ -89,6 +93,10 @@ def test_c1_walk_matches_oracle(aligned):
     _same_state(lib, ora)
     assert lib.swap_in([1]) == ora.swap_in([1])[1]
     _same_state(lib, ora)
+    # the hand-derived golden of each allocation order (tests/golden/c1_walk.json)
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "c1_walk.json")))
+    if not aligned:
+        assert lib.block_table(1) == gold["swap_in_alloc_cooling" if cooling else "swap_in"]["gpu_table"]
 
 
 def test_spec_invalidate_numbers_via_library():
@@ -141,12 +149,13 @@ def _apply(x, op, args):
     raise ValueError(op)
 
 
-@pytest.mark.parametrize("aligned", [False, True])
-def test_fuzz_10000_steps_bit_exact(aligned):
-    """Random interleavings of every bookkeeping call: library == oracle after every step."""
-    rng = random.Random(11 + aligned)
+@pytest.mark.parametrize("aligned,cooling", [(False, False), (True, False), (False, True)])
+def test_fuzz_10000_steps_bit_exact(aligned, cooling):
+    """Random interleavings of every bookkeeping call: library == oracle after every step,
+    under Z9's plain order and the opt-in alloc_cooling order."""
+    rng = random.Random(11 + aligned + 2 * cooling)
     lib, ora = _pair(L=1, h_q=2, h_kv=1, d=16, k=4, ng=24, nc=16, aligned=aligned, max_requests=5,
-                     max_blocks=12)
+                     max_blocks=12, cooling=cooling)
     for step in range(10000):
         op = rng.choice(["new", "append", "append", "append", "inval", "swap_out", "swap_in",
                          "release", "preempt"])
@@ -176,11 +185,34 @@ def test_fuzz_10000_steps_bit_exact(aligned):
         _same_state(lib, ora)
 
 
-def test_z9_ids_released_by_the_last_swap_out_are_allocated_last():
-    """Reading Z9: lowest free id first, except that the GPU ids released by the most recent
-    swap-out come after every other free id; they become ordinary free ids at the next
-    swap-out.  Library and oracle agree on every table."""
+def test_z9_plain_lowest_free_id_independent_of_free_order():
+    """Reading Z9 (default): the lowest free ids, ascending, whatever order they were freed
+    in -- ids released by a swap-out are reused at once.  Hand-derived tables."""
     lib, ora = _pair(ng=12, nc=12, max_blocks=12)
+    z = np.zeros((1, 64, 1, 16), np.uint16)
+    for x in (lib, ora):
+        x.new_request(1, list(range(16)))
+        x.new_request(2, list(range(32)))
+        x.new_request(3, list(range(8)))
+    lib.append_chunk([(3, None, 8, 0)], kv_rows=64)             # ids 0-1
+    ora.append([(3, None, 8, 0)], z, z)
+    lib.append_chunk([(1, None, 16, 0)], kv_rows=64)            # ids 2-5
+    ora.append([(1, None, 16, 0)], z, z)
+    assert lib.swap_out([1]) == ora.swap_out([1])[1]             # frees 2-5
+    lib.release(3); ora.release(3)                               # frees 0-1 (later)
+    lib.append_chunk([(2, None, 24, 0)], kv_rows=64)            # 6 blocks: 0-5, ascending
+    ora.append([(2, None, 24, 0)], z, z)
+    assert lib.block_table(2) == ora.block_table(2) == [0, 1, 2, 3, 4, 5]
+    assert lib.swap_in([1]) == ora.swap_in([1])[1]               # 6-9
+    assert lib.block_table(1) == ora.block_table(1) == [6, 7, 8, 9]
+    assert lib.free_blocks() == ora.free_counts() == (2, 12)
+
+
+def test_alloc_cooling_ids_released_by_the_last_swap_out_are_allocated_last():
+    """Opt-in alloc_cooling (a performance variant of Z9, not the paper's): the GPU ids
+    released by the most recent swap-out come after every other free id; they become
+    ordinary free ids at the next swap-out.  Library and oracle agree on every table."""
+    lib, ora = _pair(ng=12, nc=12, max_blocks=12, cooling=True)
     z = np.zeros((1, 64, 1, 16), np.uint16)
     for x in (lib, ora):
         x.new_request(1, list(range(16)))

@@ -22,16 +22,18 @@ def _rows(rng, L, n, h_kv, d):
     return rng.integers(0, 1 << 16, size=(L, n, h_kv, d), dtype=np.uint16)
 
 
-def _c1(aligned=False):
+def _c1(aligned=False, cooling=False):
     g = _gold("c1_walk.json")["geometry"]
     return OracleKV(g["L"], g["h_q"], g["h_kv"], g["d"], g["k"], g["num_gpu_blocks"],
-                    g["num_cpu_blocks"], lcp_block_aligned=aligned)
+                    g["num_cpu_blocks"], lcp_block_aligned=aligned, alloc_cooling=cooling)
 
 
-@pytest.mark.parametrize("variant", ["token", "aligned"])
-def test_c1_walk(variant):
+@pytest.mark.parametrize("variant,cooling", [("token", False), ("aligned", False), ("token", True)])
+def test_c1_walk(variant, cooling):
+    """Hand-derived C1 walk; Z9's plain lowest-free-id order by default, and the opt-in
+    alloc_cooling variant against its own golden swap-in table."""
     gold = _gold("c1_walk.json")
-    kv = _c1(aligned=(variant == "aligned"))
+    kv = _c1(aligned=(variant == "aligned"), cooling=cooling)
     rng = np.random.default_rng(0)
     toks = list(range(100, 124))
     assert kv.new_request(1, []) == O.OK
@@ -60,7 +62,7 @@ def test_c1_walk(variant):
         assert kv.swap_out([1]) == (O.OK, so["bytes"])
         assert kv.block_table(1) == so["cpu_table"]
         assert kv.free_counts() == (so["gpu_free"], so["cpu_free"])
-        si = gold["swap_in"]
+        si = gold["swap_in_alloc_cooling" if cooling else "swap_in"]
         assert kv.swap_in([1]) == (O.OK, si["bytes"])
         assert kv.block_table(1) == si["gpu_table"]
         assert kv.free_counts() == (si["gpu_free"], si["cpu_free"])
@@ -213,11 +215,12 @@ def test_swap_round_trip_identity_and_mirror():
     assert np.array_equal(kv.reqs[0].Kc, Kc)
 
 
-def test_invalidate_while_swapped_then_resume():
+@pytest.mark.parametrize("cooling", [False, True])
+def test_invalidate_while_swapped_then_resume(cooling):
     """invalidate on CPU, free CPU blocks beyond the LCP, swap in the prefix,
     recompute from the LCP."""
     rng = np.random.default_rng(9)
-    kv = OracleKV(1, 2, 1, 8, 4, 16, 16)
+    kv = OracleKV(1, 2, 1, 8, 4, 16, 16, alloc_cooling=cooling)
     toks = list(range(20))
     kv.new_request(0, toks)
     k, v = _rows(rng, 1, 20, 1, 8), _rows(rng, 1, 20, 1, 8)
@@ -229,8 +232,10 @@ def test_invalidate_while_swapped_then_resume():
     assert kv.block_table(0) == [0, 1, 2] and kv.info(0)["tier"] == O.CPU
     assert kv.free_counts() == (16, 13)
     assert kv.swap_in([0])[0] == O.OK
-    # Z9: ids 0-4 were released by the swap-out (cooling), so free ids 5.. go first
-    assert kv.info(0)["num_computed"] == 9 and kv.block_table(0) == [5, 6, 7]
+    # Z9: the lowest free ids 0-2; alloc_cooling: ids 0-4 were released by the swap-out, so
+    # the free ids 5.. go first
+    assert kv.info(0)["num_computed"] == 9
+    assert kv.block_table(0) == ([5, 6, 7] if cooling else [0, 1, 2])
     # fully invalidated while swapped -> fresh GPU request with no blocks
     kv.swap_out([0])
     st, p, inval = kv.invalidate_lcp(0, [5])

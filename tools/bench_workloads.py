@@ -209,7 +209,8 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
         L = 8
     ng, ncpu = ws // 2, ws
     cfg = s2l.make_config(L, geo_hq, geo_hkv, D, K, ng, ncpu, max_requests=n_req,
-                          max_blocks_per_request=16384 // K)
+                          max_blocks_per_request=16384 // K,
+                          alloc_cooling=int(os.environ.get("C4_COOLING", "1")))
     mb = s2l.block_bytes(cfg)
     gpool = torch.empty(ng * mb // 2, dtype=torch.bfloat16, device="cuda")
     cpool = torch.empty(ncpu * mb // 2, dtype=torch.bfloat16, pin_memory=True)
