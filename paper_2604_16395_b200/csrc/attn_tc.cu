@@ -33,20 +33,15 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 // Build-time variants (experiments; defaults are the measured best).
-#ifndef S2L_EXP_MODE
-#define S2L_EXP_MODE 0   // 0: f32 MUFU.EX2 + FMA-pipe polynomial share; 1: MUFU.EX2 f16x2
-#endif
 #ifndef S2L_POLY_PAIRS
 #define S2L_POLY_PAIRS 1
 #endif
 #ifndef S2L_SPLIT_S
 #define S2L_SPLIT_S 1      // v2: 1 = S(j+1) in two N=64 halves, keys 64-127 issued as soon as the
                            // softmax has read S(j)'s upper half (overlaps the softmax)
-#endif
-#ifndef S2L_SM64
-#define S2L_SM64 1         // v2: exponentials in 64-column chunks, polynomial pairs spread evenly
 #endif
 
 namespace s2l {
@@ -55,21 +50,9 @@ namespace {
 constexpr int kD = 128;
 constexpr int kBM = 128;
 constexpr int kBN = 128;
-constexpr int kThreads = 256;
 constexpr uint32_t kTileBytes = kBM * kD * 2;  // 32 KB: a 128 x 128 bf16 operand tile
 constexpr uint32_t kAtom = 16384;              // one [128 rows][64 cols] SW128 column of atoms
 
-constexpr uint32_t OFF_Q = 0;
-constexpr uint32_t OFF_K = OFF_Q + kTileBytes;
-constexpr uint32_t OFF_V = OFF_K + 2 * kTileBytes;
-constexpr uint32_t OFF_P = OFF_V + 2 * kTileBytes;
-constexpr uint32_t OFF_BAR = OFF_P + kTileBytes;
-enum : uint32_t {
-  B_Q = 0, B_KF = 1, B_KE = 3, B_VF = 5, B_VE = 7, B_SF = 9, B_SE = 11, B_PF = 13, B_OD = 14,
-  NUM_BARS = 15
-};
-constexpr uint32_t OFF_TMEM = OFF_BAR + NUM_BARS * 8;
-constexpr uint32_t SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + slack for 1024-B alignment
 constexpr uint32_t TMEM_COLS = 512;                    // S0 [0,128) S1 [128,256) O [256,384)
 constexpr uint32_t TMEM_O = 256;
 constexpr float kRescaleThresh = 8.0f;                 // log2 units: rescale when max grows 256x
@@ -84,7 +67,6 @@ struct TcParams {
   // tail-wave KV split (v2): CTAs >= split_begin are pieces of units split into split_s
   // contiguous KV ranges; partials go to ws, the last piece of a unit merges (ws_cnt).
   int32_t split_begin, split_s;
-  int32_t n_work;  // v3: work items = split_begin + (units - split_begin) * split_s
   float* ws;       // [pieces][2][128][128] partial O (unnormalised, fp32)
   float* ws_ml;    // [pieces][2][128][2] running max (log2 units) and row sum
   int32_t* ws_cnt;
@@ -291,18 +273,6 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
                      __int_as_float(__float_as_int(q.y) + (__float_as_int(y.y) << 23)));
 }
 
-// 2^x for a pair through MUFU.EX2 in packed f16x2 (two exponentials per MUFU slot).  x is
-// rounded to f16 first (|x| < 2^4 for every term that matters: relative error of the result
-// <= ~2^-7 only where 2^x < 2^-8 of the row max); results below 2^-24 flush to 0.
-__device__ __forceinline__ float2 exp2_f16x2(float2 x) {
-  uint32_t hx, he;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(hx) : "f"(x.y), "f"(x.x));
-  asm("ex2.approx.f16x2 %0, %1;" : "=r"(he) : "r"(hx));
-  float lo, hi;
-  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
-      : "=f"(lo), "=f"(hi) : "r"(he));
-  return make_float2(lo, hi);
-}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -317,302 +287,8 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
                : "memory");
 }
 
-// ---------------------------------------------------------------- the kernel
-__global__ void __launch_bounds__(kThreads, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                   const __grid_constant__ CUtensorMap tmap_kv, const __grid_constant__ TcParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t sb = smem_u32(smem);
-  const uint32_t sQ = sb + OFF_Q, sK = sb + OFF_K, sV = sb + OFF_V, sP = sb + OFF_P;
-  auto bar = [&](uint32_t i) { return sb + OFF_BAR + 8u * i; };
-  uint32_t* tmem_holder = (uint32_t*)(smem + OFF_TMEM);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // ---- work unit: (item, kv head, Q tile), items sorted longest-first, last tile first
-  const int32_t unit = blockIdx.x;
-  int32_t lo = 0, hi = p.n_items - 1;
-  while (lo < hi) {
-    const int32_t mid = (lo + hi + 1) >> 1;
-    if (item_at(p, mid).unit_begin <= unit) lo = mid; else hi = mid - 1;
-  }
-  const AttnItemDev it = item_at(p, lo);
-  const int32_t local = unit - it.unit_begin;
-  const int32_t tile = it.tiles - 1 - local / p.h_kv;
-  const int32_t kvh = local % p.h_kv;
-  const int32_t G = p.group;
-  const int32_t toks = kBM / G;
-  const int32_t tok0 = tile * toks;
-  const int32_t tok_last = min(tok0 + toks, it.n_q) - 1;
-  const int64_t key_last = it.q_pos + tok_last;
-  const int32_t nT = (int32_t)(key_last / kBN) + 1;
-  const int64_t kv_len = it.q_pos + it.n_q;
-  const int32_t nblk_valid = (int32_t)((kv_len + p.kb - 1) / p.kb);
-
-  if (threadIdx.x == 0) {
-    mbar_init(bar(B_Q), 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(bar(B_KF + s), 1);
-      mbar_init(bar(B_KE + s), 1);
-      mbar_init(bar(B_VF + s), 1);
-      mbar_init(bar(B_VE + s), 1);
-      mbar_init(bar(B_SF + s), 1);
-      mbar_init(bar(B_SE + s), 128);
-    }
-    mbar_init(bar(B_PF), 128);
-    mbar_init(bar(B_OD), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_holder;
-
-  if (warp == 0) {
-    // ================= TMA producer =================
-    if (lane == 0) {
-      mbar_expect_tx(bar(B_Q), kTileBytes);
-      const int32_t z = (int32_t)(it.q_row + tok0);
-      tma_load_3d(sQ, &tmap_q, bar(B_Q), 0, kvh * G, z);
-      tma_load_3d(sQ + kAtom, &tmap_q, bar(B_Q), 64, kvh * G, z);
-    }
-    const int32_t nb_tile = kBN / p.kb;
-    const int32_t* trow = p.table + (int64_t)it.slot * p.max_blocks;
-    const int32_t rows_per_block = p.L * 2 * p.h_kv * p.kb;
-    const int32_t row_k = ((p.layer * 2 + 0) * p.h_kv + kvh) * p.kb;
-    const int32_t row_v = ((p.layer * 2 + 1) * p.h_kv + kvh) * p.kb;
-    for (int32_t j = 0; j < nT; ++j) {
-      const int s = j & 1;
-      const uint32_t ph = (j >> 1) & 1;
-      int32_t bid = 0;
-      if (lane < nb_tile) {
-        const int32_t b = j * nb_tile + lane;
-        bid = __ldg(trow + (b < nblk_valid ? b : 0));
-      }
-      const int32_t id = __shfl_sync(0xffffffffu, bid, lane >> 1);
-      const int32_t blk_i = lane >> 1, half = lane & 1;
-      // K_j
-      mbar_wait(bar(B_KE + s), ph ^ 1);
-      if (lane == 0) mbar_expect_tx(bar(B_KF + s), kTileBytes);
-      __syncwarp();
-      if (lane < 2 * nb_tile)
-        tma_load_2d(sK + s * kTileBytes + half * kAtom + blk_i * p.kb * 128, &tmap_kv,
-                    bar(B_KF + s), half * 64, id * rows_per_block + row_k);
-      // V_j
-      mbar_wait(bar(B_VE + s), ph ^ 1);
-      if (lane == 0) mbar_expect_tx(bar(B_VF + s), kTileBytes);
-      __syncwarp();
-      if (lane < 2 * nb_tile)
-        tma_load_2d(sV + s * kTileBytes + half * kAtom + blk_i * p.kb * 128, &tmap_kv,
-                    bar(B_VF + s), half * 64, id * rows_per_block + row_v);
-    }
-  } else if (warp == 1) {
-    // ================= MMA issuer (one thread) =================
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);  // Q K-major, K K-major
-      constexpr uint32_t idesc_o = idesc_bf16(kBM, kD, 0, 1);   // P K-major, V MN-major
-      mbar_wait(bar(B_Q), 0);
-      auto issue_s = [&](int32_t i) {
-        const int s = i & 1;
-        const uint32_t ph = (i >> 1) & 1;
-        mbar_wait(bar(B_KF + s), ph);
-        mbar_wait(bar(B_SE + s), ph ^ 1);
-        tc_fence_after();
-        const uint32_t kbase = sK + s * kTileBytes;
-#pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
-          mma_bf16(tmem + s * 128, sdesc(sQ + off, 16, 1024), sdesc(kbase + off, 16, 1024),
-                   idesc_s, kk > 0);
-        }
-        mma_commit(bar(B_SF + s));
-        mma_commit(bar(B_KE + s));
-      };
-      issue_s(0);
-      for (int32_t j = 0; j < nT; ++j) {
-        if (j + 1 < nT) issue_s(j + 1);
-        const int s = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(bar(B_VF + s), ph);
-        mbar_wait(bar(B_PF), j & 1);
-        tc_fence_after();
-        const uint32_t vbase = sV + s * kTileBytes;
-#pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
-          const uint32_t aoff = (kk >> 2) * kAtom + (kk & 3) * 32;
-          mma_bf16(tmem + TMEM_O, sdesc(sP + aoff, 16, 1024),
-                   sdesc(vbase + kk * 16 * 128, kAtom, 1024), idesc_o, (j > 0 || kk > 0));
-        }
-        mma_commit(bar(B_VE + s));
-        mma_commit(bar(B_OD));
-      }
-    }
-    __syncwarp();
-  } else if (warp >= 4) {
-    // ================= softmax / correction / epilogue =================
-    const int r = threadIdx.x - 128;                 // tile row == TMEM lane
-    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
-    const int32_t tok = tok0 + r / G;
-    const int32_t hq = kvh * G + r % G;
-    const bool valid = tok < it.n_q;
-    const int64_t limit = it.q_pos + (valid ? tok : tok_last);
-    const float sl2 = p.scale_log2;
-    float m_run = -INFINITY, l_run = 0.f;
-    uint32_t sv[128];
-    for (int32_t j = 0; j < nT; ++j) {
-      const int s = j & 1;
-      mbar_wait(bar(B_SF + s), (j >> 1) & 1);
-      tc_fence_after();
-      {
-        const uint32_t ta = tmem + lane_off + s * 128;
-        tmem_ld32(ta, sv);
-        tmem_ld32(ta + 32, sv + 32);
-        tmem_ld32(ta + 64, sv + 64);
-        tmem_ld32(ta + 96, sv + 96);
-        tmem_wait_ld();
-      }
-      tc_fence_before();
-      mbar_arrive(bar(B_SE + s));
-      const int64_t key0 = (int64_t)j * kBN;
-      if (key0 + kBN - 1 > limit) {
-        const int32_t vis = (int32_t)(limit - key0);   // keys c <= vis are visible
-#pragma unroll
-        for (int c = 0; c < kBN; ++c)
-          if (c > vis) sv[c] = __float_as_uint(-INFINITY);
-      }
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < kBN; ++c) mx = fmaxf(mx, __uint_as_float(sv[c]));
-      mx *= sl2;
-      const float m_new = (mx > m_run + kRescaleThresh) ? mx : m_run;
-      if (j > 0) {
-        mbar_wait(bar(B_OD), (j - 1) & 1);  // PV_{j-1} done: P buffer free, O stable
-        tc_fence_after();
-        const bool resc = m_new != m_run;
-        if (__any_sync(0xffffffffu, resc)) {
-          const float alpha = resc ? fast_exp2(m_run - m_new) : 1.f;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t ov[32];
-            const uint32_t ta = tmem + lane_off + TMEM_O + c * 32;
-            tmem_ld32(ta, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            tmem_st32(ta, ov);
-          }
-          tmem_wait_st();
-          l_run *= alpha;
-        }
-      }
-      m_run = m_new;
-      float sum = 0.f;
-      const uint32_t prow = sP + r * 128;
-#pragma unroll
-      for (int chunk = 0; chunk < 16; ++chunk) {
-        uint32_t w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float p0 = fast_exp2(fmaf(__uint_as_float(sv[chunk * 8 + 2 * e]), sl2, -m_run));
-          const float p1 = fast_exp2(fmaf(__uint_as_float(sv[chunk * 8 + 2 * e + 1]), sl2, -m_run));
-          sum += p0 + p1;
-          w[e] = pack_p(p0, p1);
-        }
-        const uint32_t atom = chunk >> 3, cc = chunk & 7;
-        st_shared_v4(prow + atom * kAtom + ((cc ^ (r & 7)) << 4), w[0], w[1], w[2], w[3]);
-      }
-      l_run += sum;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tc_fence_before();
-      mbar_arrive(bar(B_PF));
-    }
-    // epilogue
-    mbar_wait(bar(B_OD), (nT - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l_run;
-    __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t ov[32];
-      tmem_ld32(tmem + lane_off + TMEM_O + c * 32, ov);
-      tmem_wait_ld();
-      if (valid) {
-        uint32_t w[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          w[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) dst[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
-      }
-    }
-    if (valid && p.lse)
-      p.lse[(it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
-    tc_fence_before();
-  }
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS));
-  }
-}
-
-
-// ---- softmax helpers for v2 (two passes over a 128-column S row in 32-column chunks) ----
-template <bool kMasked>
-__device__ __forceinline__ float chunk_max(const uint32_t (&v)[32], float mx, int vis, int base) {
-#pragma unroll
-  for (int c = 0; c < 32; ++c) {
-    float x = __uint_as_float(v[c]);
-    if (kMasked && base + c > vis) x = -INFINITY;
-    mx = fmaxf(mx, x);
-  }
-  return mx;
-}
-// p = 2^(s*scale - m) for 32 columns; returns the running pair sum, writes 16 packed bf16x2.
-template <bool kMasked, int kPolyPer8>
-__device__ __forceinline__ float2 chunk_p(const uint32_t (&v)[32], float2 acc, int vis, int base,
-                                          float2 sc2, float2 nm2, uint32_t (&pk)[16]) {
-  // Phase-ordered so a single warp has 16 independent pairs in flight per phase (the softmax
-  // of a tile runs one warp per SMSP, so latency is hidden only by this ILP).
-  float2 x[16];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    float s0 = __uint_as_float(v[2 * c]), s1 = __uint_as_float(v[2 * c + 1]);
-    if (kMasked) {
-      if (base + 2 * c > vis) s0 = -INFINITY;
-      if (base + 2 * c + 1 > vis) s1 = -INFINITY;
-    }
-    x[c] = __ffma2_rn(make_float2(s0, s1), sc2, nm2);
-  }
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-#if S2L_EXP_MODE == 1
-    x[c] = exp2_f16x2(x[c]);
-#else
-    if (!kMasked && (c & 7) < kPolyPer8) x[c] = exp2_poly2(x[c]);
-    else x[c] = make_float2(fast_exp2(x[c].x), fast_exp2(x[c].y));
-#endif
-  }
-  float2 a[4] = {acc, make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    a[c & 3] = __fadd2_rn(a[c & 3], x[c]);
-    pk[c] = pack_p(x[c].x, x[c].y);
-  }
-  return __fadd2_rn(__fadd2_rn(a[0], a[1]), __fadd2_rn(a[2], a[3]));
-}
-// 64-column variant (32 pairs per phase, the FMA-pipe polynomial spread over every 8/kPolyPer8-th
-// pair): more independent work per phase for the single softmax warp of an SMSP
+ // p = 2^(s*scale - m) for 64 columns (32 pairs per phase, the FMA-pipe polynomial spread
+// over every 8/kPolyPer8-th pair): more independent work per phase for the single softmax warp of an SMSP
 // (tools/micro/softmax_bench2.cu: ~10 % fewer cycles per tile than 32-column phases).
 template <bool kMasked, int kPolyPer8>
 __device__ __forceinline__ float2 chunk_p64(const uint32_t* v, float2 acc, int vis, int base,
@@ -652,71 +328,6 @@ __device__ __forceinline__ void max32(const uint32_t* sv, int vis, int base, flo
     if (kMasked && base + c > vis) x = -INFINITY;
     t[c & 7] = fmaxf(t[c & 7], x);
   }
-}
-template <bool kMasked>
-__device__ __forceinline__ float row_max(const uint32_t (&sv)[128], int vis) {
-  float t[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) t[i] = -INFINITY;
-#pragma unroll
-  for (int cc = 0; cc < 4; ++cc) max32<kMasked>(sv + 32 * cc, vis, 32 * cc, t);
-  return fmaxf(fmaxf(fmaxf(t[0], t[1]), fmaxf(t[2], t[3])), fmaxf(fmaxf(t[4], t[5]), fmaxf(t[6], t[7])));
-}
-// Row max of the tile (pass 1) with the next chunk's TMEM load in flight.
-template <bool kMasked>
-__device__ __forceinline__ float tile_max(uint32_t tS, int vis) {
-  uint32_t a[32], b[32];
-  float mx = -INFINITY;
-  tmem_ld32(tS, a);
-  tmem_wait_ld();
-  tmem_ld32(tS + 32, b);
-  mx = chunk_max<kMasked>(a, mx, vis, 0);
-  tmem_wait_ld();
-  tmem_ld32(tS + 64, a);
-  mx = chunk_max<kMasked>(b, mx, vis, 32);
-  tmem_wait_ld();
-  tmem_ld32(tS + 96, b);
-  mx = chunk_max<kMasked>(a, mx, vis, 64);
-  tmem_wait_ld();
-  return chunk_max<kMasked>(b, mx, vis, 96);
-}
-// P of the tile (pass 2): re-reads S, writes P (bf16) over S columns [0, 64) of this lane.
-template <bool kMasked, int kPolyPer8>
-__device__ __forceinline__ float tile_p(uint32_t tS, int vis, float2 sc2, float2 nm2) {
-  uint32_t a[32], b[32], pk[16];
-  float2 acc = make_float2(0.f, 0.f);
-  tmem_ld32(tS, a);
-  tmem_wait_ld();
-  tmem_ld32(tS + 32, b);
-  acc = chunk_p<kMasked, kPolyPer8>(a, acc, vis, 0, sc2, nm2, pk);
-  tmem_st16(tS, pk);
-  tmem_wait_ld();
-  tmem_ld32(tS + 64, a);
-  acc = chunk_p<kMasked, kPolyPer8>(b, acc, vis, 32, sc2, nm2, pk);
-  tmem_st16(tS + 16, pk);
-  tmem_wait_ld();
-  tmem_ld32(tS + 96, b);
-  acc = chunk_p<kMasked, kPolyPer8>(a, acc, vis, 64, sc2, nm2, pk);
-  tmem_st16(tS + 32, pk);
-  tmem_wait_ld();
-  acc = chunk_p<kMasked, kPolyPer8>(b, acc, vis, 96, sc2, nm2, pk);
-  tmem_st16(tS + 48, pk);
-  return acc.x + acc.y;
-}
-
-// Single-pass variant: the whole 128-column row is in registers (needs ~200 registers; the
-// softmax warpgroups get kRegSoftmax via setmaxnreg).
-template <bool kMasked, int kPolyPer8>
-__device__ __forceinline__ float row_p(uint32_t (&sv)[128], uint32_t tS, int vis, float2 sc2, float2 nm2) {
-  float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-  for (int cc = 0; cc < 4; ++cc) {
-    uint32_t pk[16];
-    acc = chunk_p<kMasked, kPolyPer8>(*reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc), acc, vis,
-                                      32 * cc, sc2, nm2, pk);
-    tmem_st16(tS + 16 * cc, pk);
-  }
-  return acc.x + acc.y;
 }
 
 #ifdef S2L_TRACE
@@ -973,11 +584,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
             for (int b = 0; b < 8; ++b) {
               if (b < nb_tile) {
                 const int64_t pos0 = tpos + b * p.kb;
-#ifdef S2L_EXP_FUSE_POOLREAD   // timing experiment only: chunk tiles from the pool (stale data)
-                if (false) {
-#else
                 if (fresh && pos0 >= it.q_pos) {
-#endif
                   if constexpr (kFuse) {
                     // chunk block: rows q_row + (pos0 - q_pos) .. of this layer's K or V input
                     const CUtensorMap* tin = kind ? &p.tmap_vin : &p.tmap_kin;
@@ -995,11 +602,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
           }
           __syncwarp();
         }
-#ifdef S2L_EXP_FUSE_NOWRITE    // timing experiment only: no pool writes
-        if (false) {
-#else
         if (fresh && tpos + kBN > wr_lo && tpos < wr_hi) {
-#endif
           // write this unit's chunk blocks of the tile (K and V) from the ring to the pool
 #pragma unroll
           for (int kind = 0; kind < 2; ++kind) {
@@ -1056,13 +659,11 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       auto issue_s = [&](int i, uint32_t kslot) {
         if (lane == 0) TRACE(13, i, 0);
         const uint64_t kd = dk0 + ((kslot * kTileBytes) >> 4);
-#ifndef S2L_EXP_NO_S
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
           const uint32_t off = ((kk >> 2) * kAtom + (kk & 3) * 32) >> 4;
           mma_ss_elect(tmem + i * 128, dq[i] + off, kd + off, idesc_s, kk > 0);
         }
-#endif
         mma_commit_elect(bar(WB_SF + i));
         if (lane == 0) TRACE(14, i, 0);
       };
@@ -1072,7 +673,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         mbar_wait(bar(WB_PF + i), j & 1);               // P keys 0-63 in TMEM
         tc_fence_after();
         if (lane == 0) TRACE(11, i, j);
-#ifndef S2L_EXP_NO_PV
 #pragma unroll
         for (int kk = 0; kk < kBN / 32; ++kk)
           mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
@@ -1084,7 +684,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         for (int kk = kBN / 32; kk < kBN / 16; ++kk)
           mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
                        idesc_o, 1);
-#endif
       };
       mbar_wait(bar(WB_QF), 0);
       tc_fence_after();
@@ -1181,29 +780,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
 #endif
       tc_fence_after();
       if (tr) TRACE(21, i, j);
-#ifdef S2L_EXP_MMA_ONLY   // timing experiment only: tensor-core / TMA pipeline without softmax
-      tc_fence_before();
-      mbar_arrive(bar(WB_PF + i));
-      mbar_arrive(bar(WB_PH + i));
-      continue;
-#endif
-#ifdef S2L_EXP_TMEM_ONLY  // timing experiment only: the softmax's TMEM traffic without its math
-      {
-        uint32_t tv[128];
-        tmem_ld32(tS, tv);
-        tmem_ld32(tS + 32, tv + 32);
-        tmem_ld32(tS + 64, tv + 64);
-        tmem_ld32(tS + 96, tv + 96);
-        tmem_wait_ld();
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) tmem_st16(tS + 16 * cc, tv + 16 * cc);
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(bar(WB_PF + i));
-        mbar_arrive(bar(WB_PH + i));
-          continue;
-      }
-#endif
       const int64_t key0 = (int64_t)(jb + j) * kBN;
       const int64_t vis64 = limit - key0;                 // keys c <= vis of this tile visible
       const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBN ? kBN : vis64));
@@ -1272,7 +848,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
       const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_use, -m_use);
       float2 acc = make_float2(0.f, 0.f);
-#if S2L_SM64
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         uint32_t pk[32];
@@ -1284,22 +859,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         tc_fence_before();
         mbar_arrive(bar((hh == 0 ? WB_PF : WB_PH) + i));
         if (tr) TRACE(hh == 0 ? 23 : 24, i, j);
-      }
-      if (false)
-#endif
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        uint32_t pk[16];
-        uint32_t(&v32)[32] = *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc);
-        acc = masked_tile ? chunk_p<true, 0>(v32, acc, vis, 32 * cc, sc2, nm2, pk)
-                          : chunk_p<false, kPolyPairsPer8>(v32, acc, vis, 32 * cc, sc2, nm2, pk);
-        tmem_st16(tS + 16 * cc, pk);
-        if (cc == 1 || cc == 3) {      // keys 0-63 / 64-127 of P are in TMEM
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(bar((cc == 1 ? WB_PF : WB_PH) + i));
-          if (tr) TRACE(cc == 1 ? 23 : 24, i, j);
-        }
       }
       l_run += acc.x + acc.y;
     }
@@ -1415,1312 +974,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
   }
 }
 
-// ======================================================================================
-// v4 = v2 with the softmax of each Q tile split by columns over two warps per SMSP (eight
-// warps per tile, 640 threads): a tile's exponentials are issued by two warps in parallel,
-// halving the softmax latency that bounds the ping-pong (profiles/r01: one warp per SMSP
-// needed ~2200 cycles per tile vs 1024 cycles of the other tile's MMAs).
-namespace v4 {
-constexpr int kThreads = 640;
-constexpr int kRegLaunch = 96, kRegCtrl = 64, kRegSoftmax = 104;
-static_assert(128 * kRegCtrl + 512 * kRegSoftmax <= kThreads * kRegLaunch, "register pool");
-constexpr int WNST = 4;
-constexpr uint32_t WOFF_Q0 = 0;
-constexpr uint32_t WOFF_Q1 = kTileBytes;
-constexpr uint32_t WOFF_RING = 2 * kTileBytes;
-constexpr uint32_t WOFF_RED = WOFF_RING + WNST * kTileBytes;      // 3 x [2][128][2] floats
-constexpr uint32_t WOFF_BAR = WOFF_RED + 3 * 2 * 128 * 2 * 4;
-constexpr uint32_t WB_QF = 0, WB_RF = 1, WB_RE = 1 + WNST, WB_SF = 1 + 2 * WNST, WB_PF = WB_SF + 2,
-                   WB_PH = WB_PF + 2, WB_OF = WB_PH + 2, WNBARS = WB_OF + 2;
-constexpr uint32_t WOFF_TMEM = WOFF_BAR + WNBARS * 8;
-constexpr uint32_t SMEM = WOFF_TMEM + 16 + 1024;
-constexpr int kPolyPairsPer8 = v2::kPolyPairsPer8;
-}  // namespace v4
-
-__global__ void __launch_bounds__(v4::kThreads, 1)
-    attn_tc4_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                    const __grid_constant__ CUtensorMap tmap_kv,
-                    const __grid_constant__ CUtensorMap tmap_kv4, const __grid_constant__ TcParams p) {
-  using namespace v4;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t sb = smem_u32(smem);
-  auto bar = [&](uint32_t i) { return sb + WOFF_BAR + 8u * i; };
-  uint32_t* tmem_holder = (uint32_t*)(smem + WOFF_TMEM);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#ifdef S2L_TRACE
-  uint32_t tr_n = 0;
-  const uint32_t tr_w = warp == 1 ? 0u : (warp == 4 ? 1u : (warp == 12 ? 2u : 3u));
-#endif
-
-  // ---- work unit: (item, kv head, pair of Q tiles), longest first
-  int32_t unit = blockIdx.x, piece = 0, npieces = 1;
-  if (unit >= p.split_begin) {
-    const int32_t b = unit - p.split_begin;
-    unit = p.split_begin + b / p.split_s;
-    piece = b % p.split_s;
-    npieces = p.split_s;
-  }
-  int32_t lo = 0, hi = p.n_items - 1;
-  while (lo < hi) {
-    const int32_t mid = (lo + hi + 1) >> 1;
-    if (item_at(p, mid).unit_begin <= unit) lo = mid; else hi = mid - 1;
-  }
-  const AttnItemDev it = item_at(p, lo);
-  const int32_t local = unit - it.unit_begin;
-  const int32_t pairs = (it.tiles + 1) >> 1;
-  const int32_t pair = pairs - 1 - local / p.h_kv;
-  const int32_t kvh = local % p.h_kv;
-  const int32_t G = p.group;
-  const int32_t toks = kBM / G;
-  const int32_t tok0 = pair * 2 * toks;               // first token of tile 0; tile 1 at +toks
-  const int32_t tok_last = min(tok0 + 2 * toks, it.n_q) - 1;
-  const int64_t key_last = it.q_pos + tok_last;
-  const int32_t nT_all = (int32_t)(key_last / kBN) + 1;
-  const int32_t jb = (int32_t)((int64_t)nT_all * piece / npieces);   // this CTA's KV tiles
-  const int32_t nT = (int32_t)((int64_t)nT_all * (piece + 1) / npieces) - jb;
-  const int64_t kv_len = it.q_pos + it.n_q;
-  const int32_t nblk_valid = (int32_t)((kv_len + p.kb - 1) / p.kb);
-
-  if (threadIdx.x == 0) {
-    mbar_init(bar(WB_QF), 1);
-    for (int s = 0; s < WNST; ++s) {
-      mbar_init(bar(WB_RF + s), 1);
-      mbar_init(bar(WB_RE + s), 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(bar(WB_SF + i), 1);
-      mbar_init(bar(WB_PF + i), 128);
-      mbar_init(bar(WB_PH + i), 128);
-      mbar_init(bar(WB_OF + i), 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv4) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_holder;
-
-  if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtrl));
-    if (warp == 0) {
-      // ================= TMA producer =================
-      if (lane == 0) {
-        mbar_expect_tx(bar(WB_QF), 2 * kTileBytes);
-        const int32_t z = (int32_t)(it.q_row + tok0);
-        tma_load_3d(sb + WOFF_Q0, &tmap_q, bar(WB_QF), 0, kvh * G, z);
-        tma_load_3d(sb + WOFF_Q0 + kAtom, &tmap_q, bar(WB_QF), 64, kvh * G, z);
-        tma_load_3d(sb + WOFF_Q1, &tmap_q, bar(WB_QF), 0, kvh * G, z + toks);
-        tma_load_3d(sb + WOFF_Q1 + kAtom, &tmap_q, bar(WB_QF), 64, kvh * G, z + toks);
-      }
-      const int32_t nb_tile = kBN / p.kb;               // 1..8 blocks per 128-key tile
-      const int32_t* trow = p.table + (int64_t)it.slot * p.max_blocks;
-      const int32_t rows_per_block = p.L * 2 * p.h_kv * p.kb;
-      const int32_t row_kv[2] = {((p.layer * 2 + 0) * p.h_kv + kvh) * p.kb,
-                                 ((p.layer * 2 + 1) * p.h_kv + kvh) * p.kb};
-      const int32_t lkh[2] = {(p.layer * 2 + 0) * p.h_kv + kvh, (p.layer * 2 + 1) * p.h_kv + kvh};
-      auto load_id = [&](int32_t jt) {                  // lane b < nb_tile: block b of tile jt
-        const int32_t b = (jb + jt) * nb_tile + lane;
-        return __ldg(trow + (b < nblk_valid ? b : 0));
-      };
-      int32_t next_id = (lane < nb_tile) ? load_id(0) : 0;
-      uint32_t rp = 0;
-      for (int32_t j = 0; j < nT; ++j) {
-        const int32_t cur_id = next_id;
-        if (j + 1 < nT && lane < nb_tile) next_id = load_id(j + 1);   // prefetch the next ids
-        int32_t ids[8];
-#pragma unroll
-        for (int b = 0; b < 8; ++b) ids[b] = __shfl_sync(0xffffffffu, cur_id, b);
-        bool run = (jb + j + 1) * nb_tile <= nblk_valid;   // whole tile inside the table
-#pragma unroll
-        for (int b = 1; b < 8; ++b)
-          if (b < nb_tile) run = run && (ids[b] == ids[0] + b);
-#pragma unroll
-        for (int kind = 0; kind < 2; ++kind, ++rp) {
-          const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
-          mbar_wait(bar(WB_RE + s), ph ^ 1);
-          if (lane == 0 && run) {
-            // consecutive block ids: two 4-D boxes (d halves) cover the whole 128-key tile
-            mbar_expect_tx(bar(WB_RF + s), kTileBytes);
-            const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
-            tma_load_4d(dst, &tmap_kv4, bar(WB_RF + s), 0, 0, lkh[kind], ids[0]);
-            tma_load_4d(dst + kAtom, &tmap_kv4, bar(WB_RF + s), 64, 0, lkh[kind], ids[0]);
-          } else if (lane == 0) {
-            // one lane issues the whole tile: 2 boxes {64, k} (d halves) per block
-#ifdef S2L_EXP_HALF_LOAD   // timing experiment only: load one d-half of each K/V tile
-            mbar_expect_tx(bar(WB_RF + s), kTileBytes / 2);
-#else
-            mbar_expect_tx(bar(WB_RF + s), kTileBytes);
-#endif
-            const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
-#ifdef S2L_EXP_BOX32   // timing experiment only: boxes of 2 blocks (wrong rows, same bytes)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              if (b < nb_tile / 2) {
-                const int32_t y = ids[2 * b] * rows_per_block + row_kv[kind];
-                tma_load_2d(dst + b * 2 * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
-                tma_load_2d(dst + kAtom + b * 2 * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
-              }
-            }
-            if (false)
-#endif
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-              if (b < nb_tile) {
-                const int32_t y = ids[b] * rows_per_block + row_kv[kind];
-                tma_load_2d(dst + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
-#ifndef S2L_EXP_HALF_LOAD
-                tma_load_2d(dst + kAtom + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
-#endif
-              }
-            }
-          }
-          __syncwarp();
-        }
-      }
-    } else if (warp == 1) {
-      // ================= MMA issuer (whole warp, one elected lane issues) =================
-      constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);
-      constexpr uint32_t idesc_o = idesc_bf16(kBM, kD, 0, 1);
-      // descriptors of the buffer bases; the start-address field (bits 0-13, 16-byte units)
-      // is advanced by adding (byte offset >> 4) — smem addresses stay below 256 KB
-      const uint64_t dq[2] = {sdesc(sb + WOFF_Q0, 16, 1024), sdesc(sb + WOFF_Q1, 16, 1024)};
-      const uint64_t dk0 = sdesc(sb + WOFF_RING, 16, 1024);
-      const uint64_t dv0 = sdesc(sb + WOFF_RING, kAtom, 1024);
-      uint32_t rp = 0;
-      auto next_full = [&]() {
-        const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
-        ++rp;
-        mbar_wait(bar(WB_RF + s), ph);
-        tc_fence_after();
-        return s;
-      };
-      auto issue_s = [&](int i, uint32_t kslot) {
-        const uint64_t kd = dk0 + ((kslot * kTileBytes) >> 4);
-#ifndef S2L_EXP_NO_S
-#pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint32_t off = ((kk >> 2) * kAtom + (kk & 3) * 32) >> 4;
-          mma_ss_elect(tmem + i * 128, dq[i] + off, kd + off, idesc_s, kk > 0);
-        }
-#endif
-        mma_commit_elect(bar(WB_SF + i));
-      };
-      auto issue_pv = [&](int i, uint32_t vslot, int32_t j) {
-        const uint64_t vd = dv0 + ((vslot * kTileBytes) >> 4);
-        if (lane == 0) TRACE(10, i, j);
-        mbar_wait(bar(WB_PF + i), j & 1);               // P keys 0-63 in TMEM
-        tc_fence_after();
-        if (lane == 0) TRACE(11, i, j);
-#ifndef S2L_EXP_NO_PV
-#pragma unroll
-        for (int kk = 0; kk < kBN / 32; ++kk)
-          mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
-                       idesc_o, (j > 0 || kk > 0));
-        mbar_wait(bar(WB_PH + i), j & 1);               // P keys 64-127
-        tc_fence_after();
-        if (lane == 0) TRACE(12, i, j);
-#pragma unroll
-        for (int kk = kBN / 32; kk < kBN / 16; ++kk)
-          mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
-                       idesc_o, 1);
-#endif
-      };
-      mbar_wait(bar(WB_QF), 0);
-      tc_fence_after();
-      uint32_t kslot = next_full();
-      issue_s(0, kslot);
-      issue_s(1, kslot);
-      mma_commit_elect(bar(WB_RE + kslot));
-      for (int32_t j = 0; j < nT; ++j) {
-        const uint32_t vslot = next_full();
-        issue_pv(0, vslot, j);
-        const bool more = j + 1 < nT;
-        if (more) {
-          kslot = next_full();
-          issue_s(0, kslot);
-        } else {
-          mma_commit_elect(bar(WB_OF + 0));
-        }
-        issue_pv(1, vslot, j);
-        mma_commit_elect(bar(WB_RE + vslot));
-        if (more) {
-          issue_s(1, kslot);
-          mma_commit_elect(bar(WB_RE + kslot));
-        } else {
-          mma_commit_elect(bar(WB_OF + 1));
-        }
-      }
-      __syncwarp();
-    }
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
-    // ===== softmax / correction / epilogue: tile i, column half h, lane quarter q =====
-    // Each row's 128 scores are split between two warps of the same SMSP (half h handles keys
-    // 64h .. 64h+63); the row max is exchanged through shared memory and a 64-thread named
-    // barrier; each half writes its half of P (and arrives on P_lo / P_hi), rescales and
-    // stores its 64 columns of O.
-    const int t = warp - 4;                          // 0..15
-    const int i = t >> 3;                            // Q tile
-    const int h = (t >> 2) & 1;                      // column half
-    const int q = warp & 3;                          // TMEM lane quarter
-    const int r = q * 32 + lane;                     // tile row == TMEM lane
-    const uint32_t bar_pair = 1 + i * 4 + q;         // named barrier of the two halves of rows q*32..
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const uint32_t tS = tmem + lane_off + i * 128;
-    const uint32_t tO = tmem + lane_off + TMEM_O + i * 128 + 64 * h;
-    float* red = reinterpret_cast<float*>(smem + WOFF_RED);   // [2 parity][2 tiles][128 rows][2 halves]
-    const int32_t tok = tok0 + i * toks + r / G;
-    const int32_t hq = kvh * G + r % G;
-    const bool valid = tok < it.n_q;
-    const int64_t limit = it.q_pos + (valid ? tok : tok_last);
-    const float sl2 = p.scale_log2;
-    float m_run = -INFINITY, l_run = 0.f;
-    for (int32_t j = 0; j < nT; ++j) {
-      const bool tr = (warp == 4 || warp == 12) && lane == 0;
-      if (tr) TRACE(20, i, j);
-      mbar_wait(bar(WB_SF + i), j & 1);
-      tc_fence_after();
-      if (tr) TRACE(21, i, j);
-#ifdef S2L_EXP_MMA_ONLY
-      tc_fence_before();
-      mbar_arrive(bar((h ? WB_PH : WB_PF) + i));
-      continue;
-#endif
-      const int64_t key0 = (int64_t)(jb + j) * kBN + 64 * h;
-      const int64_t vis64 = limit - key0;             // this half's columns c <= vis visible
-      const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > 64 ? 64 : vis64));
-      const bool masked = __any_sync(0xffffffffu, vis < 63);
-      uint32_t sv[64];
-      float mt[8];
-#pragma unroll
-      for (int z = 0; z < 8; ++z) mt[z] = -INFINITY;
-      tmem_ld32(tS + 64 * h, sv);
-      tmem_ld32(tS + 64 * h + 32, sv + 32);
-      tmem_wait_ld();
-      if (masked) { max32<true>(sv, vis, 0, mt); max32<true>(sv + 32, vis, 32, mt); }
-      else { max32<false>(sv, vis, 0, mt); max32<false>(sv + 32, vis, 32, mt); }
-      float pm = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])), fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7])));
-      float* slot = red + (((j & 1) * 2 + i) * 128 + r) * 2;
-      slot[h] = pm;
-      asm volatile("bar.sync %0, 64;" ::"r"(bar_pair) : "memory");
-      const float mx = fmaxf(slot[0], slot[1]) * sl2;
-      if (tr) TRACE(22, i, j);
-      const float m_new = (mx > m_run + kRescaleThresh) ? mx : m_run;
-      if (j > 0) {
-        const bool resc = m_new != m_run;
-        if (__any_sync(0xffffffffu, resc)) {
-          const float alpha = resc ? fast_exp2(m_run - m_new) : 1.f;
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            uint32_t ov[16];
-            tmem_ld16(tO + c * 16, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 16; e += 2) {
-              float2 x = __fmul2_rn(make_float2(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])),
-                                    make_float2(alpha, alpha));
-              ov[e] = __float_as_uint(x.x);
-              ov[e + 1] = __float_as_uint(x.y);
-            }
-            tmem_st16(tO + c * 16, ov);
-          }
-          l_run *= alpha;
-        }
-      }
-      m_run = m_new;
-      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_use, -m_use);
-      float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        uint32_t pk[16];
-        uint32_t(&v32)[32] = *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc);
-        acc = masked ? chunk_p<true, 0>(v32, acc, vis, 32 * cc, sc2, nm2, pk)
-                     : chunk_p<false, kPolyPairsPer8>(v32, acc, vis, 32 * cc, sc2, nm2, pk);
-        tmem_st16(tS + 32 * h + 16 * cc, pk);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(bar((h ? WB_PH : WB_PF) + i));
-      if (tr) TRACE(23, i, j);
-      l_run += acc.x + acc.y;
-    }
-    // ---- epilogue: row sum of both halves, then this half's 64 columns of O
-    mbar_wait(bar(WB_OF + i), 0);
-    tc_fence_after();
-    float* lsl = red + ((2 * 2 + i) * 128 + r) * 2;   // after the two max parities
-    lsl[h] = l_run;
-    asm volatile("bar.sync %0, 64;" ::"r"(bar_pair) : "memory");
-    const float l_tot = lsl[0] + lsl[1];
-    __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD + 64 * h;
-    if (npieces == 1) {
-      const float inv = 1.f / l_tot;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t ov[16];
-        tmem_ld16(tO + c * 16, ov);
-        tmem_wait_ld();
-        if (valid) {
-          uint32_t w[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            w[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
-          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
-          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-        }
-      }
-      if (valid && h == 0 && p.lse)
-        p.lse[(it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_tot)) * 0.69314718055994531f;
-    } else {
-      const int32_t su = unit - p.split_begin;
-      const int64_t prow = (((int64_t)su * npieces + piece) * 2 + i) * 128 + r;
-      float* wo = p.ws + prow * kD + 64 * h;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t ov[16];
-        tmem_ld16(tO + c * 16, ov);
-        tmem_wait_ld();
-        float4* dst = reinterpret_cast<float4*>(wo + c * 16);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
-                               __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
-      }
-      if (h == 0) {
-        p.ws_ml[prow * 2] = m_run;
-        p.ws_ml[prow * 2 + 1] = l_tot;
-      }
-      __threadfence();
-      asm volatile("bar.sync 9, 512;" ::: "memory");       // every softmax thread wrote
-      uint32_t* flag = (uint32_t*)(smem + WOFF_TMEM + 8);
-      if (threadIdx.x == 128) {
-        const int32_t old = atomicAdd(p.ws_cnt + su, 1);
-        const uint32_t last = (old == npieces - 1) ? 1u : 0u;
-        if (last) p.ws_cnt[su] = 0;
-        *flag = last;
-      }
-      asm volatile("bar.sync 9, 512;" ::: "memory");
-      if (*flag) {
-        __threadfence();
-        float M = -INFINITY;
-        for (int k = 0; k < npieces; ++k) {
-          const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
-          M = fmaxf(M, __ldcg(p.ws_ml + pr * 2));
-        }
-        constexpr int kMaxPieces = 8;
-        float wk[kMaxPieces];
-        float Lsum = 0.f;
-#pragma unroll
-        for (int k = 0; k < kMaxPieces; ++k) {
-          wk[k] = 0.f;
-          if (k < npieces) {
-            const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
-            wk[k] = fast_exp2(__ldcg(p.ws_ml + pr * 2) - M);
-            Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
-          }
-        }
-        const float inv = 1.f / Lsum;
-#pragma unroll 1
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          float acc[32];
-#pragma unroll
-          for (int c = 0; c < 32; ++c) acc[c] = 0.f;
-#pragma unroll
-          for (int k = 0; k < kMaxPieces; ++k) {
-            if (k < npieces) {
-              const float* po = p.ws + ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * kD + 64 * h + c0;
-#pragma unroll
-              for (int c = 0; c < 32; c += 2) {
-                const float2 x = __ldcg(reinterpret_cast<const float2*>(po + c));
-                acc[c] += wk[k] * x.x;
-                acc[c + 1] += wk[k] * x.y;
-              }
-            }
-          }
-          if (valid) {
-#pragma unroll
-            for (int c = 0; c < 32; c += 8) {
-              uint4 v4 = make_uint4(pack_bf16(acc[c] * inv, acc[c + 1] * inv), pack_bf16(acc[c + 2] * inv, acc[c + 3] * inv),
-                                    pack_bf16(acc[c + 4] * inv, acc[c + 5] * inv), pack_bf16(acc[c + 6] * inv, acc[c + 7] * inv));
-              *reinterpret_cast<uint4*>(orow + c0 + c) = v4;
-            }
-          }
-        }
-        if (valid && h == 0 && p.lse)
-          p.lse[(it.q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
-      }
-    }
-    tc_fence_before();
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS));
-  }
-}
-
-
-// ======================================================================================
-// v5: v2 with 64-key KV steps and a double-buffered S per Q tile (TMEM per tile: S[2] x 64
-// columns + O 128 = 256; two tiles = 512).  The tensor core computes S_i(j+1) while the
-// softmax works on S_i(j), so each tile's softmax runs back to back instead of waiting for its
-// own PV/S MMAs (v2's period was T_softmax + T_mma per tile); the two tiles' softmax warps share
-// each SMSP.  PV_i(j) (4 TS-MMAs, K = 64 keys) follows P_i(j); S_i(j+2) reuses S_i(j)'s buffer
-// after PV_i(j) in the in-order tensor pipe.  A rescale of O waits for PV_i(j-1) (O_done).
-namespace v5 {
-constexpr int kThreads = 384;
-constexpr int kRegLaunch = 168, kRegCtrl = 88, kRegSoftmax = 208;
-static_assert(128 * kRegCtrl + 256 * kRegSoftmax <= kThreads * kRegLaunch, "register pool");
-constexpr int kBS = 64;                                  // keys per KV step
-constexpr uint32_t kKV = kBS * kD * 2;                   // 16 KB K or V tile
-constexpr uint32_t kAtomS = kBS * 128;                   // one d-half [64 keys][64] = 8 KB
-constexpr int WNST = 10;
-constexpr uint32_t WOFF_Q0 = 0;
-constexpr uint32_t WOFF_Q1 = kTileBytes;
-constexpr uint32_t WOFF_RING = 2 * kTileBytes;
-constexpr uint32_t WOFF_BAR = WOFF_RING + WNST * kKV;
-// QF, RF[NST], RE[NST], SF[tile][buf] (4), PF[tile][buf] (4), OD[2], OF[2].  S and P are double
-// buffered by step parity (the softmax may run one step ahead of the MMA warp); O_done has a
-// single phase (after PV_i(nT-2)), so no phase of any barrier is ever skipped by a waiter.
-constexpr uint32_t WB_QF = 0, WB_RF = 1, WB_RE = 1 + WNST, WB_SF = 1 + 2 * WNST, WB_PF = WB_SF + 4,
-                   WB_OD = WB_PF + 4, WB_OF = WB_OD + 2, WNBARS = WB_OF + 2;
-constexpr uint32_t WOFF_TMEM = WOFF_BAR + WNBARS * 8;
-constexpr uint32_t SMEM = WOFF_TMEM + 16 + 1024;
-constexpr int kPolyPairsPer8 = v2::kPolyPairsPer8;
-}  // namespace v5
-
-__global__ void __launch_bounds__(v5::kThreads, 1)
-    attn_tc5_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                    const __grid_constant__ CUtensorMap tmap_kv,
-                    const __grid_constant__ CUtensorMap tmap_kv64, const __grid_constant__ TcParams p) {
-  using namespace v5;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t sb = smem_u32(smem);
-  auto bar = [&](uint32_t i) { return sb + WOFF_BAR + 8u * i; };
-  uint32_t* tmem_holder = (uint32_t*)(smem + WOFF_TMEM);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#ifdef S2L_TRACE
-  uint32_t tr_n = 0;
-  const uint32_t tr_w = warp == 1 ? 0u : (warp == 4 ? 1u : (warp == 8 ? 2u : 3u));
-#endif
-
-  // ---- work unit: (item, kv head, pair of Q tiles), longest first (same as v2)
-  int32_t unit = blockIdx.x, piece = 0, npieces = 1;
-  if (unit >= p.split_begin) {
-    const int32_t b = unit - p.split_begin;
-    unit = p.split_begin + b / p.split_s;
-    piece = b % p.split_s;
-    npieces = p.split_s;
-  }
-  int32_t lo = 0, hi = p.n_items - 1;
-  while (lo < hi) {
-    const int32_t mid = (lo + hi + 1) >> 1;
-    if (item_at(p, mid).unit_begin <= unit) lo = mid; else hi = mid - 1;
-  }
-  const AttnItemDev it = item_at(p, lo);
-  const int32_t local = unit - it.unit_begin;
-  const int32_t pairs = (it.tiles + 1) >> 1;
-  const int32_t pair = pairs - 1 - local / p.h_kv;
-  const int32_t kvh = local % p.h_kv;
-  const int32_t G = p.group;
-  const int32_t toks = kBM / G;
-  const int32_t tok0 = pair * 2 * toks;
-  const int32_t tok_last = min(tok0 + 2 * toks, it.n_q) - 1;
-  const int64_t key_last = it.q_pos + tok_last;
-  const int32_t nT_all = (int32_t)(key_last / kBS) + 1;
-  const int32_t jb = (int32_t)((int64_t)nT_all * piece / npieces);
-  const int32_t nT = (int32_t)((int64_t)nT_all * (piece + 1) / npieces) - jb;
-  const int64_t kv_len = it.q_pos + it.n_q;
-  const int32_t nblk_valid = (int32_t)((kv_len + p.kb - 1) / p.kb);
-
-  if (threadIdx.x == 0) {
-    mbar_init(bar(WB_QF), 1);
-    for (int s = 0; s < WNST; ++s) {
-      mbar_init(bar(WB_RF + s), 1);
-      mbar_init(bar(WB_RE + s), 1);
-    }
-    for (int i = 0; i < 4; ++i) {
-      mbar_init(bar(WB_SF + i), 1);
-      mbar_init(bar(WB_PF + i), 128);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(bar(WB_OD + i), 1);
-      mbar_init(bar(WB_OF + i), 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv64) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_holder;
-
-  if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtrl));
-    if (warp == 0) {
-      // ================= TMA producer: loads in the MMA's consumption order
-      //   K_0, K_1, then per step j: V_j, K_{j+2}   (one ring, released in the same order)
-      if (lane == 0) {
-        mbar_expect_tx(bar(WB_QF), 2 * kTileBytes);
-        const int32_t z = (int32_t)(it.q_row + tok0);
-        tma_load_3d(sb + WOFF_Q0, &tmap_q, bar(WB_QF), 0, kvh * G, z);
-        tma_load_3d(sb + WOFF_Q0 + kAtom, &tmap_q, bar(WB_QF), 64, kvh * G, z);
-        tma_load_3d(sb + WOFF_Q1, &tmap_q, bar(WB_QF), 0, kvh * G, z + toks);
-        tma_load_3d(sb + WOFF_Q1 + kAtom, &tmap_q, bar(WB_QF), 64, kvh * G, z + toks);
-      }
-      const int32_t nb_tile = kBS / p.kb;               // 1..4 blocks per 64-key tile
-      const int32_t* trow = p.table + (int64_t)it.slot * p.max_blocks;
-      const int32_t rows_per_block = p.L * 2 * p.h_kv * p.kb;
-      const int32_t row_kv[2] = {((p.layer * 2 + 0) * p.h_kv + kvh) * p.kb,
-                                 ((p.layer * 2 + 1) * p.h_kv + kvh) * p.kb};
-      const int32_t lkh[2] = {(p.layer * 2 + 0) * p.h_kv + kvh, (p.layer * 2 + 1) * p.h_kv + kvh};
-      uint32_t rp = 0;
-      auto load_tile = [&](int32_t jt, int kind) {
-        int32_t bid = 0;
-        if (lane < nb_tile) {
-          const int32_t b = (jb + jt) * nb_tile + lane;
-          bid = __ldg(trow + (b < nblk_valid ? b : 0));
-        }
-        int32_t ids[4];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) ids[b] = __shfl_sync(0xffffffffu, bid, b);
-        bool run = (jb + jt + 1) * nb_tile <= nblk_valid;
-#pragma unroll
-        for (int b = 1; b < 4; ++b)
-          if (b < nb_tile) run = run && (ids[b] == ids[0] + b);
-        const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
-        ++rp;
-        mbar_wait(bar(WB_RE + s), ph ^ 1);
-        if (lane == 0) {
-          mbar_expect_tx(bar(WB_RF + s), kKV);
-          const uint32_t dst = sb + WOFF_RING + s * kKV;
-          if (run) {
-            tma_load_4d(dst, &tmap_kv64, bar(WB_RF + s), 0, 0, lkh[kind], ids[0]);
-            tma_load_4d(dst + kAtomS, &tmap_kv64, bar(WB_RF + s), 64, 0, lkh[kind], ids[0]);
-          } else {
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              if (b < nb_tile) {
-                const int32_t y = ids[b] * rows_per_block + row_kv[kind];
-                tma_load_2d(dst + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
-                tma_load_2d(dst + kAtomS + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
-              }
-            }
-          }
-        }
-        __syncwarp();
-      };
-      load_tile(0, 0);
-      if (nT > 1) load_tile(1, 0);
-      for (int32_t j = 0; j < nT; ++j) {
-        load_tile(j, 1);
-        if (j + 2 < nT) load_tile(j + 2, 0);
-      }
-    } else if (warp == 1) {
-      // ================= MMA issuer (whole warp, one elected lane issues) =================
-      constexpr uint32_t idesc_s = idesc_bf16(kBM, kBS, 0, 0);  // S: M 128, N 64 keys
-      constexpr uint32_t idesc_o = idesc_bf16(kBM, kD, 0, 1);   // O: M 128, N 128 d
-      const uint64_t dq[2] = {sdesc(sb + WOFF_Q0, 16, 1024), sdesc(sb + WOFF_Q1, 16, 1024)};
-      const uint64_t dk0 = sdesc(sb + WOFF_RING, 16, 1024);
-      const uint64_t dv0 = sdesc(sb + WOFF_RING, kAtomS, 1024);
-      uint32_t rp = 0;
-      auto next_full = [&]() {
-        const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
-        ++rp;
-        mbar_wait(bar(WB_RF + s), ph);
-        tc_fence_after();
-        return s;
-      };
-      // S_i(jj) into buffer jj & 1 of tile i
-      auto issue_s = [&](int i, uint32_t kslot, int32_t jj) {
-        const uint64_t kd = dk0 + ((kslot * kKV) >> 4);
-#pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint32_t qoff = ((kk >> 2) * kAtom + (kk & 3) * 32) >> 4;
-          const uint32_t koff = ((kk >> 2) * kAtomS + (kk & 3) * 32) >> 4;
-          mma_ss_elect(tmem + i * 256 + (jj & 1) * 64, dq[i] + qoff, kd + koff, idesc_s, kk > 0);
-        }
-        mma_commit_elect(bar(WB_SF + i * 2 + (jj & 1)));
-      };
-      auto issue_pv = [&](int i, uint32_t vslot, int32_t j) {
-        const uint64_t vd = dv0 + ((vslot * kKV) >> 4);
-        if (lane == 0) TRACE(10, i, j);
-        mbar_wait(bar(WB_PF + i * 2 + (j & 1)), (j >> 1) & 1);
-        tc_fence_after();
-        if (lane == 0) TRACE(11, i, j);
-#pragma unroll
-        for (int kk = 0; kk < kBS / 16; ++kk)
-          mma_ts_elect(tmem + i * 256 + 128, tmem + i * 256 + (j & 1) * 64 + kk * 8,
-                       vd + ((kk * 16 * 128) >> 4), idesc_o, (j > 0 || kk > 0));
-        if (j + 2 == nT) mma_commit_elect(bar(WB_OD + i));   // PV_i(nT-2) done (one phase)
-      };
-      mbar_wait(bar(WB_QF), 0);
-      tc_fence_after();
-      uint32_t k0 = next_full();
-      issue_s(0, k0, 0);
-      issue_s(1, k0, 0);
-      mma_commit_elect(bar(WB_RE + k0));
-      if (nT > 1) {
-        const uint32_t k1 = next_full();
-        issue_s(0, k1, 1);
-        issue_s(1, k1, 1);
-        mma_commit_elect(bar(WB_RE + k1));
-      }
-      for (int32_t j = 0; j < nT; ++j) {
-        const uint32_t vslot = next_full();
-        const bool more = j + 2 < nT;
-        const uint32_t kslot = more ? next_full() : 0;
-        issue_pv(0, vslot, j);
-        if (more) issue_s(0, kslot, j + 2);
-        if (j + 1 == nT) mma_commit_elect(bar(WB_OF + 0));
-        issue_pv(1, vslot, j);
-        mma_commit_elect(bar(WB_RE + vslot));
-        if (more) {
-          issue_s(1, kslot, j + 2);
-          mma_commit_elect(bar(WB_RE + kslot));
-        }
-        if (j + 1 == nT) mma_commit_elect(bar(WB_OF + 1));
-      }
-    }
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
-    // ================= softmax / correction / epilogue of Q tile i =================
-    const int i = (warp - 4) >> 2;
-    const int r = (warp & 3) * 32 + lane;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t tS0 = tmem + lane_off + i * 256;
-    const uint32_t tO = tmem + lane_off + i * 256 + 128;
-    const int32_t tok = tok0 + i * toks + r / G;
-    const int32_t hq = kvh * G + r % G;
-    const bool valid = tok < it.n_q;
-    const int64_t limit = it.q_pos + (valid ? tok : tok_last);
-    const float sl2 = p.scale_log2;
-    float m_run = -INFINITY, l_run = 0.f;
-    for (int32_t j = 0; j < nT; ++j) {
-      const uint32_t tS = tS0 + (j & 1) * 64;
-      const bool tr = (warp & 3) == 0 && lane == 0;
-      if (tr) TRACE(20, i, j);
-      mbar_wait(bar(WB_SF + i * 2 + (j & 1)), (j >> 1) & 1);
-      tc_fence_after();
-      if (tr) TRACE(21, i, j);
-      const int64_t key0 = (int64_t)(jb + j) * kBS;
-      const int64_t vis64 = limit - key0;
-      const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBS ? kBS : vis64));
-      const bool masked_tile = __any_sync(0xffffffffu, vis < kBS - 1);
-      uint32_t sv[64];
-      float mt[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) mt[q] = -INFINITY;
-      tmem_ld32(tS, sv);
-      tmem_ld32(tS + 32, sv + 32);
-      tmem_wait_ld();
-      if (masked_tile) { max32<true>(sv, vis, 0, mt); max32<true>(sv + 32, vis, 32, mt); }
-      else { max32<false>(sv, vis, 0, mt); max32<false>(sv + 32, vis, 32, mt); }
-      float mx = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])), fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7])));
-      mx *= sl2;
-      if (tr) TRACE(22, i, j);
-      const float m_new = (mx > m_run + kRescaleThresh) ? mx : m_run;
-      const bool resc = j > 0 && m_new != m_run;
-      const float alpha = resc ? fast_exp2(m_run - m_new) : 1.f;
-      m_run = m_new;
-      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_use, -m_use);
-      float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        uint32_t pk[16];
-        uint32_t(&v32)[32] = *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc);
-        acc = masked_tile ? chunk_p<true, 0>(v32, acc, vis, 32 * cc, sc2, nm2, pk)
-                          : chunk_p<false, kPolyPairsPer8>(v32, acc, vis, 32 * cc, sc2, nm2, pk);
-        tmem_st16(tS + 16 * cc, pk);
-      }
-      if (j > 0 && __any_sync(0xffffffffu, resc)) {
-        // O may only be rescaled after PV_i(j-1) has landed: S_i(j+1) was issued after it
-        // (same in-order tensor pipe), and for the last step O_done marks PV_i(nT-2)
-        if (j + 1 < nT) mbar_wait(bar(WB_SF + i * 2 + ((j + 1) & 1)), ((j + 1) >> 1) & 1);
-        else mbar_wait(bar(WB_OD + i), 0);
-        tc_fence_after();
-        if (tr) TRACE(23, i, j);
-        {
-#pragma unroll 1
-          for (int c = 0; c < 8; ++c) {
-            uint32_t ov[16];
-            tmem_ld16(tO + c * 16, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 16; e += 2) {
-              float2 x = __fmul2_rn(make_float2(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])),
-                                    make_float2(alpha, alpha));
-              ov[e] = __float_as_uint(x.x);
-              ov[e + 1] = __float_as_uint(x.y);
-            }
-            tmem_st16(tO + c * 16, ov);
-          }
-          l_run *= alpha;
-        }
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(bar(WB_PF + i * 2 + (j & 1)));
-      if (tr) TRACE(24, i, j);
-      l_run += acc.x + acc.y;
-    }
-    // epilogue
-    mbar_wait(bar(WB_OF + i), 0);
-    tc_fence_after();
-    __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
-    if (npieces == 1) {
-      const float inv = 1.f / l_run;
-#pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
-        uint32_t ov[16];
-        tmem_ld16(tO + c * 16, ov);
-        tmem_wait_ld();
-        if (valid) {
-          uint32_t w[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            w[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
-          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
-          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-        }
-      }
-      if (valid && p.lse)
-        p.lse[(it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
-    } else {
-      const int32_t su = unit - p.split_begin;
-      const int64_t prow = (((int64_t)su * npieces + piece) * 2 + i) * 128 + r;
-      float* wo = p.ws + prow * kD;
-#pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
-        uint32_t ov[16];
-        tmem_ld16(tO + c * 16, ov);
-        tmem_wait_ld();
-        float4* dst = reinterpret_cast<float4*>(wo + c * 16);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
-                               __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
-      }
-      p.ws_ml[prow * 2] = m_run;
-      p.ws_ml[prow * 2 + 1] = l_run;
-      __threadfence();
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      uint32_t* flag = (uint32_t*)(smem + WOFF_TMEM + 8);
-      if (threadIdx.x == 128) {
-        const int32_t old = atomicAdd(p.ws_cnt + su, 1);
-        const uint32_t last = (old == npieces - 1) ? 1u : 0u;
-        if (last) p.ws_cnt[su] = 0;
-        *flag = last;
-      }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      if (*flag) {
-        __threadfence();
-        float M = -INFINITY;
-        for (int k = 0; k < npieces; ++k) {
-          const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
-          M = fmaxf(M, __ldcg(p.ws_ml + pr * 2));
-        }
-        constexpr int kMaxPieces = 8;
-        float wk[kMaxPieces];
-        float Lsum = 0.f;
-#pragma unroll
-        for (int k = 0; k < kMaxPieces; ++k) {
-          wk[k] = 0.f;
-          if (k < npieces) {
-            const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
-            wk[k] = fast_exp2(__ldcg(p.ws_ml + pr * 2) - M);
-            Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
-          }
-        }
-        const float inv = 1.f / Lsum;
-#pragma unroll 1
-        for (int c0 = 0; c0 < kD; c0 += 32) {
-          float acc[32];
-#pragma unroll
-          for (int c = 0; c < 32; ++c) acc[c] = 0.f;
-#pragma unroll
-          for (int k = 0; k < kMaxPieces; ++k) {
-            if (k < npieces) {
-              const float* po = p.ws + ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * kD + c0;
-#pragma unroll
-              for (int c = 0; c < 32; c += 2) {
-                const float2 x = __ldcg(reinterpret_cast<const float2*>(po + c));
-                acc[c] += wk[k] * x.x;
-                acc[c + 1] += wk[k] * x.y;
-              }
-            }
-          }
-          if (valid) {
-#pragma unroll
-            for (int c = 0; c < 32; c += 8) {
-              uint4 v4 = make_uint4(pack_bf16(acc[c] * inv, acc[c + 1] * inv), pack_bf16(acc[c + 2] * inv, acc[c + 3] * inv),
-                                    pack_bf16(acc[c + 4] * inv, acc[c + 5] * inv), pack_bf16(acc[c + 6] * inv, acc[c + 7] * inv));
-              *reinterpret_cast<uint4*>(orow + c0 + c) = v4;
-            }
-          }
-        }
-        if (valid && p.lse)
-          p.lse[(it.q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
-      }
-    }
-    tc_fence_before();
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS));
-  }
-}
-
-// ======================================================================================
-// v3 = v2 made persistent: each CTA loops over work items (whole units, then the tail-wave
-// split pieces) with a static stride of gridDim.x, so the TMEM allocation / barrier setup is
-// paid once per SM and the next item's Q load, K/V loads and first S MMAs overlap the current
-// item's epilogue.  Barrier phases run on per-CTA counters (KV steps g, items n) instead of
-// per-item indices.  Q_empty (committed after an item's last S MMAs) lets the producer load
-// the next Q; O reuse is ordered by the softmax warps themselves (their epilogue precedes
-// their next P_full arrival, which gates the next item's first PV).
-struct WorkInfo {
-  AttnItemDev it;
-  int32_t unit, piece, npieces, kvh, tok0, tok_last, jb, nT, nblk_valid;
-};
-
-__device__ __forceinline__ WorkInfo decode_work(const TcParams& p, int32_t w) {
-  WorkInfo wk;
-  wk.unit = w;
-  wk.piece = 0;
-  wk.npieces = 1;
-  if (w >= p.split_begin) {
-    const int32_t b = w - p.split_begin;
-    wk.unit = p.split_begin + b / p.split_s;
-    wk.piece = b % p.split_s;
-    wk.npieces = p.split_s;
-  }
-  int32_t lo = 0, hi = p.n_items - 1;
-  while (lo < hi) {
-    const int32_t mid = (lo + hi + 1) >> 1;
-    if (item_at(p, mid).unit_begin <= wk.unit) lo = mid; else hi = mid - 1;
-  }
-  wk.it = item_at(p, lo);
-  const int32_t local = wk.unit - wk.it.unit_begin;
-  const int32_t pairs = (wk.it.tiles + 1) >> 1;
-  const int32_t pair = pairs - 1 - local / p.h_kv;
-  wk.kvh = local % p.h_kv;
-  const int32_t toks = kBM / p.group;
-  wk.tok0 = pair * 2 * toks;
-  wk.tok_last = min(wk.tok0 + 2 * toks, wk.it.n_q) - 1;
-  const int32_t nT_all = (int32_t)((wk.it.q_pos + wk.tok_last) / kBN) + 1;
-  wk.jb = (int32_t)((int64_t)nT_all * wk.piece / wk.npieces);
-  wk.nT = (int32_t)((int64_t)nT_all * (wk.piece + 1) / wk.npieces) - wk.jb;
-  wk.nblk_valid = (int32_t)((wk.it.q_pos + wk.it.n_q + p.kb - 1) / p.kb);
-  return wk;
-}
-
-__global__ void __launch_bounds__(v2::kThreads, 1)
-    attn_tc3_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                    const __grid_constant__ CUtensorMap tmap_kv,
-                    const __grid_constant__ CUtensorMap tmap_kv4, const __grid_constant__ TcParams p) {
-  using namespace v2;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t sb = smem_u32(smem);
-  auto bar = [&](uint32_t i) { return sb + WOFF_BAR + 8u * i; };
-  uint32_t* tmem_holder = (uint32_t*)(smem + WOFF_TMEM);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t G = p.group;
-  const int32_t toks = kBM / G;
-  const int32_t W = p.n_work;
-
-  if (threadIdx.x == 0) {
-    mbar_init(bar(WB_QF), 1);
-    mbar_init(bar(WB_QE), 1);
-    for (int s = 0; s < WNST; ++s) {
-      mbar_init(bar(WB_RF + s), 1);
-      mbar_init(bar(WB_RE + s), 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(bar(WB_SF + i), 1);
-      mbar_init(bar(WB_PF + i), 128);
-      mbar_init(bar(WB_PH + i), 128);
-      mbar_init(bar(WB_OF + i), 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv4) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_holder;
-
-  if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtrl));
-    if (warp == 0) {
-      // ================= TMA producer =================
-      const int32_t nb_tile = kBN / p.kb;
-      const int32_t rows_per_block = p.L * 2 * p.h_kv * p.kb;
-      uint32_t rp = 0, n = 0;
-      for (int32_t w = blockIdx.x; w < W; w += gridDim.x, ++n) {
-        const WorkInfo wk = decode_work(p, w);
-        if (lane == 0) {
-          mbar_wait(bar(WB_QE), (n & 1) ^ 1);          // previous item's S MMAs are done
-          mbar_expect_tx(bar(WB_QF), 2 * kTileBytes);
-          const int32_t z = (int32_t)(wk.it.q_row + wk.tok0);
-          tma_load_3d(sb + WOFF_Q0, &tmap_q, bar(WB_QF), 0, wk.kvh * G, z);
-          tma_load_3d(sb + WOFF_Q0 + kAtom, &tmap_q, bar(WB_QF), 64, wk.kvh * G, z);
-          tma_load_3d(sb + WOFF_Q1, &tmap_q, bar(WB_QF), 0, wk.kvh * G, z + toks);
-          tma_load_3d(sb + WOFF_Q1 + kAtom, &tmap_q, bar(WB_QF), 64, wk.kvh * G, z + toks);
-        }
-        __syncwarp();
-        const int32_t* trow = p.table + (int64_t)wk.it.slot * p.max_blocks;
-        const int32_t row_kv[2] = {((p.layer * 2 + 0) * p.h_kv + wk.kvh) * p.kb,
-                                   ((p.layer * 2 + 1) * p.h_kv + wk.kvh) * p.kb};
-        auto load_id = [&](int32_t jt) {
-          const int32_t b = (wk.jb + jt) * nb_tile + lane;
-          return __ldg(trow + (b < wk.nblk_valid ? b : 0));
-        };
-        const int32_t lkh[2] = {(p.layer * 2 + 0) * p.h_kv + wk.kvh, (p.layer * 2 + 1) * p.h_kv + wk.kvh};
-        int32_t next_id = (lane < nb_tile) ? load_id(0) : 0;
-        for (int32_t j = 0; j < wk.nT; ++j) {
-          const int32_t cur_id = next_id;
-          if (j + 1 < wk.nT && lane < nb_tile) next_id = load_id(j + 1);
-          int32_t ids[8];
-#pragma unroll
-          for (int b = 0; b < 8; ++b) ids[b] = __shfl_sync(0xffffffffu, cur_id, b);
-          bool run = (wk.jb + j + 1) * nb_tile <= wk.nblk_valid;
-#pragma unroll
-          for (int b = 1; b < 8; ++b)
-            if (b < nb_tile) run = run && (ids[b] == ids[0] + b);
-#pragma unroll
-          for (int kind = 0; kind < 2; ++kind, ++rp) {
-            const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
-            mbar_wait(bar(WB_RE + s), ph ^ 1);
-            if (lane == 0 && run) {
-              mbar_expect_tx(bar(WB_RF + s), kTileBytes);
-              const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
-              tma_load_4d(dst, &tmap_kv4, bar(WB_RF + s), 0, 0, lkh[kind], ids[0]);
-              tma_load_4d(dst + kAtom, &tmap_kv4, bar(WB_RF + s), 64, 0, lkh[kind], ids[0]);
-            } else if (lane == 0) {
-              mbar_expect_tx(bar(WB_RF + s), kTileBytes);
-              const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
-#pragma unroll
-              for (int b = 0; b < 8; ++b) {
-                if (b < nb_tile) {
-                  const int32_t y = ids[b] * rows_per_block + row_kv[kind];
-                  tma_load_2d(dst + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 0, y);
-                  tma_load_2d(dst + kAtom + b * p.kb * 128, &tmap_kv, bar(WB_RF + s), 64, y);
-                }
-              }
-            }
-            __syncwarp();
-          }
-        }
-      }
-    } else if (warp == 1) {
-      // ================= MMA issuer (whole warp, one elected lane issues) =================
-      constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);
-      constexpr uint32_t idesc_o = idesc_bf16(kBM, kD, 0, 1);
-      const uint64_t dq[2] = {sdesc(sb + WOFF_Q0, 16, 1024), sdesc(sb + WOFF_Q1, 16, 1024)};
-      const uint64_t dk0 = sdesc(sb + WOFF_RING, 16, 1024);
-      const uint64_t dv0 = sdesc(sb + WOFF_RING, kAtom, 1024);
-      uint32_t rp = 0, g = 0, n = 0;
-      auto next_full = [&]() {
-        const uint32_t s = rp % WNST, ph = (rp / WNST) & 1;
-        ++rp;
-        mbar_wait(bar(WB_RF + s), ph);
-        tc_fence_after();
-        return s;
-      };
-      auto issue_s = [&](int i, uint32_t kslot) {
-        const uint64_t kd = dk0 + ((kslot * kTileBytes) >> 4);
-#pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint32_t off = ((kk >> 2) * kAtom + (kk & 3) * 32) >> 4;
-          mma_ss_elect(tmem + i * 128, dq[i] + off, kd + off, idesc_s, kk > 0);
-        }
-        mma_commit_elect(bar(WB_SF + i));
-      };
-      auto issue_pv = [&](int i, uint32_t vslot, int32_t j, uint32_t gj) {
-        const uint64_t vd = dv0 + ((vslot * kTileBytes) >> 4);
-        mbar_wait(bar(WB_PF + i), gj & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < kBN / 32; ++kk)
-          mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
-                       idesc_o, (j > 0 || kk > 0));
-        mbar_wait(bar(WB_PH + i), gj & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = kBN / 32; kk < kBN / 16; ++kk)
-          mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
-                       idesc_o, 1);
-      };
-      for (int32_t w = blockIdx.x; w < W; w += gridDim.x, ++n) {
-        const int32_t nT = decode_work(p, w).nT;
-        mbar_wait(bar(WB_QF), n & 1);
-        tc_fence_after();
-        uint32_t kslot = next_full();
-        issue_s(0, kslot);
-        issue_s(1, kslot);
-        mma_commit_elect(bar(WB_RE + kslot));
-        if (nT == 1) mma_commit_elect(bar(WB_QE));      // last S of this item issued
-        for (int32_t j = 0; j < nT; ++j) {
-          const uint32_t gj = g + j;
-          const uint32_t vslot = next_full();
-          issue_pv(0, vslot, j, gj);
-          const bool more = j + 1 < nT;
-          if (more) {
-            kslot = next_full();
-            issue_s(0, kslot);
-          } else {
-            mma_commit_elect(bar(WB_OF + 0));
-          }
-          issue_pv(1, vslot, j, gj);
-          mma_commit_elect(bar(WB_RE + vslot));
-          if (more) {
-            issue_s(1, kslot);
-            mma_commit_elect(bar(WB_RE + kslot));
-            if (j + 2 == nT) mma_commit_elect(bar(WB_QE));
-          } else {
-            mma_commit_elect(bar(WB_OF + 1));
-          }
-        }
-        g += nT;
-      }
-    }
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
-    // ================= softmax / correction / epilogue of Q tile i =================
-    const int i = (warp - 4) >> 2;
-    const int r = (warp & 3) * 32 + lane;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + lane_off + i * 128;
-    const uint32_t tO = tmem + lane_off + TMEM_O + i * 128;
-    const float sl2 = p.scale_log2;
-    uint32_t g = 0, n = 0;
-    for (int32_t w = blockIdx.x; w < W; w += gridDim.x, ++n) {
-      const WorkInfo wk = decode_work(p, w);
-      const int32_t tok = wk.tok0 + i * toks + r / G;
-      const int32_t hq = wk.kvh * G + r % G;
-      const bool valid = tok < wk.it.n_q;
-      const int64_t limit = wk.it.q_pos + (valid ? tok : wk.tok_last);
-      float m_run = -INFINITY, l_run = 0.f;
-      for (int32_t j = 0; j < wk.nT; ++j) {
-        mbar_wait(bar(WB_SF + i), (g + j) & 1);
-        tc_fence_after();
-#ifdef S2L_EXP_MMA_ONLY
-        tc_fence_before();
-        mbar_arrive(bar(WB_PF + i));
-        mbar_arrive(bar(WB_PH + i));
-        continue;
-#endif
-        const int64_t key0 = (int64_t)(wk.jb + j) * kBN;
-        const int64_t vis64 = limit - key0;
-        const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBN ? kBN : vis64));
-        const bool masked_tile = __any_sync(0xffffffffu, vis < kBN - 1);
-        uint32_t sv[128];
-        float mt[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) mt[q] = -INFINITY;
-        tmem_ld32(tS, sv);
-        tmem_ld32(tS + 32, sv + 32);
-        tmem_wait_ld();
-        tmem_ld32(tS + 64, sv + 64);                      // in flight during the first max half
-        tmem_ld32(tS + 96, sv + 96);
-        if (masked_tile) { max32<true>(sv, vis, 0, mt); max32<true>(sv + 32, vis, 32, mt); }
-        else { max32<false>(sv, vis, 0, mt); max32<false>(sv + 32, vis, 32, mt); }
-        tmem_wait_ld();
-        if (masked_tile) { max32<true>(sv + 64, vis, 64, mt); max32<true>(sv + 96, vis, 96, mt); }
-        else { max32<false>(sv + 64, vis, 64, mt); max32<false>(sv + 96, vis, 96, mt); }
-        float mx = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])), fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7])));
-        mx *= sl2;
-        const float m_new = (mx > m_run + kRescaleThresh) ? mx : m_run;
-        if (j > 0) {
-          const bool resc = m_new != m_run;
-          if (__any_sync(0xffffffffu, resc)) {
-            const float alpha = resc ? fast_exp2(m_run - m_new) : 1.f;
-#pragma unroll 1
-            for (int c = 0; c < 8; ++c) {
-              uint32_t ov[16];
-              tmem_ld16(tO + c * 16, ov);
-              tmem_wait_ld();
-#pragma unroll
-              for (int e = 0; e < 16; e += 2) {
-                float2 x = __fmul2_rn(make_float2(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])),
-                                      make_float2(alpha, alpha));
-                ov[e] = __float_as_uint(x.x);
-                ov[e + 1] = __float_as_uint(x.y);
-              }
-              tmem_st16(tO + c * 16, ov);
-            }
-            l_run *= alpha;
-          }
-        }
-        m_run = m_new;
-        const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-        const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_use, -m_use);
-        float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          uint32_t pk[16];
-          uint32_t(&v32)[32] = *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * cc);
-          acc = masked_tile ? chunk_p<true, 0>(v32, acc, vis, 32 * cc, sc2, nm2, pk)
-                            : chunk_p<false, kPolyPairsPer8>(v32, acc, vis, 32 * cc, sc2, nm2, pk);
-          tmem_st16(tS + 16 * cc, pk);
-          if (cc == 1 || cc == 3) {
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(bar((cc == 1 ? WB_PF : WB_PH) + i));
-          }
-        }
-        l_run += acc.x + acc.y;
-      }
-      g += wk.nT;
-      // ---- epilogue of this item (overlaps the next item's first S MMAs)
-      mbar_wait(bar(WB_OF + i), n & 1);
-      tc_fence_after();
-      __nv_bfloat16* orow = p.o + ((wk.it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
-      if (wk.npieces == 1) {
-        const float inv = 1.f / l_run;
-#pragma unroll 1
-        for (int c = 0; c < 8; ++c) {
-          uint32_t ov[16];
-          tmem_ld16(tO + c * 16, ov);
-          tmem_wait_ld();
-          if (valid) {
-            uint32_t wv[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              wv[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
-            uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
-            dst[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-            dst[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
-          }
-        }
-        if (valid && p.lse)
-          p.lse[(wk.it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
-      } else {
-        const int32_t su = wk.unit - p.split_begin;
-        const int32_t npieces = wk.npieces;
-        const int64_t prow = (((int64_t)su * npieces + wk.piece) * 2 + i) * 128 + r;
-        float* wo = p.ws + prow * kD;
-#pragma unroll 1
-        for (int c = 0; c < 8; ++c) {
-          uint32_t ov[16];
-          tmem_ld16(tO + c * 16, ov);
-          tmem_wait_ld();
-          float4* dst = reinterpret_cast<float4*>(wo + c * 16);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
-                                 __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
-        }
-        p.ws_ml[prow * 2] = m_run;
-        p.ws_ml[prow * 2 + 1] = l_run;
-        __threadfence();
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        uint32_t* flag = (uint32_t*)(smem + WOFF_TMEM + 8);
-        if (threadIdx.x == 128) {
-          const int32_t old = atomicAdd(p.ws_cnt + su, 1);
-          const uint32_t last = (old == npieces - 1) ? 1u : 0u;
-          if (last) p.ws_cnt[su] = 0;
-          *flag = last;
-        }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        const bool is_last = *flag != 0;
-        asm volatile("bar.sync 1, 256;" ::: "memory");   // flag is reused by the next item
-        if (is_last) {
-          __threadfence();
-          float M = -INFINITY;
-          for (int k = 0; k < npieces; ++k) {
-            const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
-            M = fmaxf(M, __ldcg(p.ws_ml + pr * 2));
-          }
-          constexpr int kMaxPieces = 8;
-          float wk8[kMaxPieces];
-          float Lsum = 0.f;
-#pragma unroll
-          for (int k = 0; k < kMaxPieces; ++k) {
-            wk8[k] = 0.f;
-            if (k < npieces) {
-              const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
-              wk8[k] = fast_exp2(__ldcg(p.ws_ml + pr * 2) - M);
-              Lsum += wk8[k] * __ldcg(p.ws_ml + pr * 2 + 1);
-            }
-          }
-          const float inv = 1.f / Lsum;
-#pragma unroll 1
-          for (int c0 = 0; c0 < kD; c0 += 32) {
-            float acc[32];
-#pragma unroll
-            for (int c = 0; c < 32; ++c) acc[c] = 0.f;
-#pragma unroll
-            for (int k = 0; k < kMaxPieces; ++k) {
-              if (k < npieces) {
-                const float* po = p.ws + ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * kD + c0;
-#pragma unroll
-                for (int c = 0; c < 32; c += 2) {
-                  const float2 x = __ldcg(reinterpret_cast<const float2*>(po + c));
-                  acc[c] += wk8[k] * x.x;
-                  acc[c + 1] += wk8[k] * x.y;
-                }
-              }
-            }
-            if (valid) {
-#pragma unroll
-              for (int c = 0; c < 32; c += 8) {
-                uint4 v4 = make_uint4(pack_bf16(acc[c] * inv, acc[c + 1] * inv), pack_bf16(acc[c + 2] * inv, acc[c + 3] * inv),
-                                      pack_bf16(acc[c + 4] * inv, acc[c + 5] * inv), pack_bf16(acc[c + 6] * inv, acc[c + 7] * inv));
-                *reinterpret_cast<uint4*>(orow + c0 + c) = v4;
-              }
-            }
-          }
-          if (valid && p.lse)
-            p.lse[(wk.it.q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
-        }
-      }
-      tc_fence_before();
-    }
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(TMEM_COLS));
-  }
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn(const char** err) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -2758,7 +1011,6 @@ bool make_tmap_kv(void* out, const void* pool, int64_t num_blocks, int32_t L, in
     cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)total_rows};
     cuuint64_t strides[1] = {(cuuint64_t)d * 2};
     cuuint32_t box[2] = {64, (cuuint32_t)k};
-    if (const char* e = getenv("S2L_EXP_BOX_ROWS")) box[1] = (cuuint32_t)atoi(e);   // experiments only
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn((CUtensorMap*)out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)pool, dims,
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -2782,21 +1034,6 @@ bool make_tmap_kv(void* out, const void* pool, int64_t num_blocks, int32_t L, in
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       *err = "cuTensorMapEncodeTiled(pool, block runs) failed";
-      return false;
-    }
-  }
-  // (3) 64-key run map (v5): box {64, k, 1, 64/k} (only for k <= 64)
-  if (k <= 64) {
-    const int32_t R = 64 / k;
-    cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)k, (cuuint64_t)L * 2 * h_kv, (cuuint64_t)num_blocks};
-    cuuint64_t strides[3] = {(cuuint64_t)d * 2, (cuuint64_t)k * d * 2, (cuuint64_t)L * 2 * h_kv * k * d * 2};
-    cuuint32_t box[4] = {64, (cuuint32_t)k, 1, (cuuint32_t)R};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = fn((CUtensorMap*)((char*)out + 256), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)pool,
-                    dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-      *err = "cuTensorMapEncodeTiled(pool, 64-key runs) failed";
       return false;
     }
   }
@@ -2848,13 +1085,22 @@ bool make_tmap_q(void* out, const void* q, int64_t q_rows, int32_t h_q, int32_t 
 static uint32_t* g_trace = nullptr;
 void set_attn_trace(uint32_t* buf) { g_trace = buf; }
 
-int attn_tc_tiles_per_cta() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("S2L_ATTN_V1");
-    v = (e && e[0] == '1') ? 1 : 2;
-  }
-  return v;
+// The kernels' dynamic shared-memory limit is a per-device function attribute: set it once per
+// device (a context created later on another GPU of the same process gets it too).
+static cudaError_t ensure_smem_attr() {
+  static std::mutex mu;
+  static bool done[kMaxDevices] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return cudaSuccess;
+  e = cudaFuncSetAttribute(attn_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(attn_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM);
+  if (e == cudaSuccess) done[dev] = true;
+  return e;
 }
 
 cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const AttnItemDev* items_host,
@@ -2862,35 +1108,13 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
                            int32_t total_units, int32_t split_begin, int32_t split_s,
                            float* ws, int32_t max_pieces, int32_t* ws_cnt,
                            const int32_t* table, int32_t layer, const void* tmap_q,
-                           const void* tmap_kv, void* o, float* lse, int32_t num_sms,
+                           const void* tmap_kv, void* o, float* lse,
                            int32_t flags, cudaStream_t st, const void* tmap_in, void* pool,
                            uint64_t fuse_mask) {
-  const int variant = attn_tc_tiles_per_cta();
   const bool fuse = (flags & kAttnFuseAppend) != 0;
-  if (fuse && (variant != 2 || (flags & (kAttnPersistent | kAttnSplitSoftmax | kAttnKV64)) ||
-               !tmap_in || !pool))
-    return cudaErrorInvalidValue;   // the fused append exists in attn_tc2_kernel only
-  const bool persistent = (flags & kAttnPersistent) != 0;
-  static bool attr_set[3] = {false, false, false};
-  if (!attr_set[variant]) {
-    cudaError_t e = variant == 2
-        ? cudaFuncSetAttribute(attn_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM)
-        : cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    if (variant == 2) {
-      e = cudaFuncSetAttribute(attn_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM);
-      if (e != cudaSuccess) return e;
-    }
-    if (variant == 2) {
-      e = cudaFuncSetAttribute(attn_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM);
-      if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(attn_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v4::SMEM);
-      if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(attn_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, v5::SMEM);
-      if (e != cudaSuccess) return e;
-    }
-    attr_set[variant] = true;
-  }
+  if (fuse && (!tmap_in || !pool)) return cudaErrorInvalidValue;
+  cudaError_t e = ensure_smem_attr();
+  if (e != cudaSuccess) return e;
   if (total_units <= 0) return cudaSuccess;
   TcParamsFused pf{};
   TcParams plain{};
@@ -2920,7 +1144,7 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
   p.split_begin = total_units;
   p.split_s = 1;
   int32_t grid = total_units;
-  if (variant == 2 && split_s > 1 && split_begin < total_units) {
+  if (split_s > 1 && split_begin < total_units) {
     p.split_begin = split_begin;
     p.split_s = split_s;
     grid = split_begin + (total_units - split_begin) * split_s;
@@ -2938,24 +1162,8 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
   p.ws = ws;
   p.ws_ml = ws ? ws + (int64_t)max_pieces * 2 * 128 * kD : nullptr;
   p.ws_cnt = ws_cnt;
-  p.n_work = grid;
-  if (variant == 2 && (flags & kAttnKV64) && g.k <= 64) {
-    CUtensorMap tkv64;
-    memcpy(&tkv64, (const char*)tmap_kv + 256, sizeof(CUtensorMap));
-    attn_tc5_kernel<<<grid, v5::kThreads, v5::SMEM, st>>>(tq, tkv, tkv64, p);
-  } else if (variant == 2 && (flags & kAttnSplitSoftmax)) {
-    attn_tc4_kernel<<<grid, v4::kThreads, v4::SMEM, st>>>(tq, tkv, tkv4, p);
-  } else if (variant == 2 && persistent) {
-    const int32_t g = grid < num_sms ? grid : num_sms;
-    attn_tc3_kernel<<<g, v2::kThreads, v2::SMEM, st>>>(tq, tkv, tkv4, p);
-  } else if (variant == 2)
-  {
-    if (fuse) return launch_k(attn_tc2_kernel<true>, dim3(grid), dim3(v2::kThreads), v2::SMEM, st, tq, tkv, tkv4, pf);
-    return launch_k(attn_tc2_kernel<false>, dim3(grid), dim3(v2::kThreads), v2::SMEM, st, tq, tkv, tkv4, p);
-  }
-  else
-    attn_tc_kernel<<<total_units, kThreads, SMEM_BYTES, st>>>(tq, tkv, p);
-  return cudaGetLastError();
+  if (fuse) return launch_k(attn_tc2_kernel<true>, dim3(grid), dim3(v2::kThreads), v2::SMEM, st, tq, tkv, tkv4, pf);
+  return launch_k(attn_tc2_kernel<false>, dim3(grid), dim3(v2::kThreads), v2::SMEM, st, tq, tkv, tkv4, p);
 }
 
 }  // namespace s2l

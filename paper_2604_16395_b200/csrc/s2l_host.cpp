@@ -195,16 +195,13 @@ struct s2l_ctx {
   // All per-block marks are cleared when the block is allocated again.
   EventRing compute_ring, out_ring, in_ring;
   std::vector<uint64_t> freed_use, quar_out, quar_in, cpu_quar_in;
-  unsigned char tmap_kv[384] __attribute__((aligned(64)));
+  unsigned char tmap_kv[256] __attribute__((aligned(64)));
   int32_t num_sms = 148;
   float* split_ws = nullptr;          // tail-wave split partials (num_sms pieces)
   int32_t* split_cnt = nullptr;       // per split unit arrival counters (self-resetting)
   bool split_enabled = true;
-  bool persistent = false;            // persistent attention kernel (S2L_PERSIST=1)
-  bool split_softmax = false;         // v4 kernel (S2L_ATTN_V4=1)
-  bool kv64 = false;                  // v5 kernel (S2L_ATTN_V5=1)
   uint32_t* trace_buf = nullptr;      // S2L_TRACE=1: device buffer for kernel timelines (experiments)
-  int64_t trace_launch = -1, attn_launch_no = 0;  // which attention launch to trace (S2L_TRACE_LAUNCH)            // persistent attention kernel (S2L_PERSIST=1); off: measured slower
+  int64_t trace_launch = -1, attn_launch_no = 0;  // which attention launch to trace (S2L_TRACE_LAUNCH)
   bool tc_ok = false;
   s2l::Geometry geo{};
 };
@@ -614,12 +611,6 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
     CK(cudaMemsetAsync(c->split_cnt, 0, (size_t)c->num_sms * sizeof(int32_t), c->compute));
     const char* e = getenv("S2L_NO_SPLIT");
     c->split_enabled = !(e && e[0] == '1');
-    e = getenv("S2L_PERSIST");
-    c->persistent = (e && e[0] == '1');
-    e = getenv("S2L_ATTN_V4");
-    c->split_softmax = (e && e[0] == '1');
-    e = getenv("S2L_ATTN_V5");
-    c->kv64 = (e && e[0] == '1');
     e = getenv("S2L_TRACE");
     if (e && e[0] == '1') {
       CK(cudaMalloc(&c->trace_buf, (16 + 4 * 4096 * 2) * sizeof(uint32_t)));
@@ -956,8 +947,7 @@ static s2l_status prefill_impl(s2l_ctx* c, int32_t layer, int32_t n_items,
   if (append) {
     if (!v) return fail(S2L_E_INVAL, "k/v is NULL");
     std::unordered_set<int64_t> seen;
-    const bool kern = c->tc_ok && s2l::attn_tc_tiles_per_cta() == 2 && !c->persistent &&
-                      !c->split_softmax && !c->kv64;
+    const bool kern = c->tc_ok;
     int32_t aligned = 0;
     for (int32_t i = 0; i < n_items; ++i) {
       if (!seen.insert(items[i].req_id).second)
@@ -1001,7 +991,7 @@ static s2l_status prefill_impl(s2l_ctx* c, int32_t layer, int32_t n_items,
     for (int32_t i = 0; i < n_items; ++i)
       if (in_kernel[order[i]]) fuse_mask |= 1ull << i;
   }
-  const int64_t tiles_per_cta = c->tc_ok ? s2l::attn_tc_tiles_per_cta() : 1;
+  const int64_t tiles_per_cta = c->tc_ok ? 2 : 1;   // tensor-core kernel: a pair of Q tiles per CTA
   int64_t units = 0, total_q = 0;
   for (int32_t i = 0; i < n_items; ++i) {
     const s2l_prefill_item& it = items[order[i]];
@@ -1044,7 +1034,7 @@ static s2l_status prefill_impl(s2l_ctx* c, int32_t layer, int32_t n_items,
     const int64_t P = c->num_sms;
     const int64_t rem = units % P;
     int32_t split_begin = (int32_t)units, split_s = 1;
-    if (tiles_per_cta == 2 && c->split_enabled && rem > 0 && rem * 2 <= P) {
+    if (c->split_enabled && rem > 0 && rem * 2 <= P) {
       int64_t s_want = std::min<int64_t>(P / rem, 8);
       // no piece may be empty: s <= the smallest KV-tile count among the split units
       const int64_t first = units - rem;
@@ -1076,11 +1066,8 @@ static s2l_status prefill_impl(s2l_ctx* c, int32_t layer, int32_t n_items,
     CK(s2l::launch_attn_tc(c->geo, dv, inl ? dev.data() : nullptr, n_items, (int32_t)units,
                            split_begin, split_s,
                            c->split_ws, c->num_sms, c->split_cnt, c->d_table, layer, tq,
-                           c->tmap_kv, o, lse, c->num_sms,
-                           (c->persistent ? s2l::kAttnPersistent : 0) |
-                               (c->split_softmax ? s2l::kAttnSplitSoftmax : 0) |
-                               (c->kv64 ? s2l::kAttnKV64 : 0) |
-                               (fused ? s2l::kAttnFuseAppend : 0),
+                           c->tmap_kv, o, lse,
+                           fused ? s2l::kAttnFuseAppend : 0,
                            c->compute, fused ? tin : nullptr, c->gpu_pool, fuse_mask));
   } else {
     CK(s2l::launch_attn_generic(c->geo, dv, n_items, total_q, c->d_table, layer, q, o, lse,

@@ -128,9 +128,9 @@ cudaError_t launch_attn_generic(const Geometry& g, const AttnItemDev* items, int
 
 // tcgen05 / TMEM / TMA attention (head_dim 128, 16 <= k <= 128, 128 % (h_q/h_kv) == 0).
 // tmap_q points to one host CUtensorMap (128 bytes), tmap_kv to the two pool maps (256 bytes).
+// One work unit (CTA) = one (item, kv head, pair of 128-row Q tiles).
 bool attn_tc_supported(const Geometry& g);
-// Q tiles per CTA of the tensor-core kernel (2 = ping-pong v2, default; 1 = v1 via S2L_ATTN_V1=1).
-int attn_tc_tiles_per_cta();
+constexpr int kMaxDevices = 64;
 // Grid = split_begin + (total_units - split_begin) * split_s CTAs: units below split_begin
 // run whole, the remaining (tail-wave) units run as split_s KV-range pieces whose partials
 // (ws: O partials of max_pieces pieces, then their (m, l)) are merged by the last piece (ws_cnt).
@@ -141,32 +141,28 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
                            int32_t total_units, int32_t split_begin, int32_t split_s,
                            float* ws, int32_t max_pieces, int32_t* ws_cnt,
                            const int32_t* table, int32_t layer, const void* tmap_q,
-                           const void* tmap_kv, void* o, float* lse, int32_t num_sms,
+                           const void* tmap_kv, void* o, float* lse,
                            int32_t flags, cudaStream_t st, const void* tmap_in = nullptr,
                            void* pool = nullptr, uint64_t fuse_mask = ~0ull);
 // fuse_mask (kAttnFuseAppend, items inline): bit i set = item i (in the items array's order)
 // has its append fused; the others were appended before the launch and read from the pool.
 // flags of launch_attn_tc
-constexpr int32_t kAttnPersistent = 1;   // v2 only: grid = min(work items, SMs), CTAs loop
-constexpr int32_t kAttnSplitSoftmax = 2; // v4: each tile's softmax split over two warps per SMSP
-constexpr int32_t kAttnKV64 = 4;         // v5: 64-key steps, double-buffered S per tile
-// v2 only: fused append (NEXT-2).  For every item selected by fuse_mask (q_pos a multiple of
+// Fused append (NEXT-2).  For every item selected by fuse_mask (q_pos a multiple of
 // the block size) the chunk rows [q_pos, q_pos+n_q) of this layer are read from tmap_in
 // (make_tmap_in) and written to the pool by the kernel.  No two items may share a request.
 constexpr int32_t kAttnFuseAppend = 8;
 // Experiments: device buffer receiving kernel timeline stamps (S2L_TRACE builds); nullptr = off.
-void set_attn_trace(uint32_t* buf);   // v2 only: grid = min(work items, SMs), CTAs loop
+void set_attn_trace(uint32_t* buf);
 constexpr int64_t kSplitPieceFloats = 2 * 128 * 130;   // O [2][128][128] + (m, l) [2][128][2]
 // TMA descriptors (host).  Returns false on failure (message in *err).
 bool make_tmap_q(void* out128, const void* q, int64_t q_rows, int32_t h_q, int32_t d,
                  int32_t group, const char** err);
-// Maps of the pool into out384: [0,128) per-block boxes, [128,256) 128-key block runs,
-// [256,384) 64-key block runs (k <= 64).
 // One layer's K and V input rows ([rows][h_kv][d] bf16) into out512: per-block boxes (K at 0,
 // V at 128) and whole-tile boxes (K at 256, V at 384).
 bool make_tmap_in(void* out512, const void* k, const void* v, int64_t rows, int32_t h_kv,
                   int32_t d, int32_t kb, const char** err);
-bool make_tmap_kv(void* out384, const void* pool, int64_t num_blocks, int32_t L, int32_t h_kv,
+// Maps of the pool into out256: [0,128) per-block boxes, [128,256) 128-key block runs.
+bool make_tmap_kv(void* out256, const void* pool, int64_t num_blocks, int32_t L, int32_t h_kv,
                   int32_t d, int32_t k, const char** err);
 
 }  // namespace s2l
