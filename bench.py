@@ -1,25 +1,29 @@
-"""Benchmark of the streaming-prefill hot path (BASELINE.json metric, config C2 at N=1).
+"""Benchmark of the streaming-prefill hot path (BASELINE.json metric; headline config C2 at N=1).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl s2l|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl s2l|reference] [--workload c2|c4]
 
-Workload (BJ:L8, C2): Llama-3-8B attention shape (32 q / 8 kv heads, d 128, block 16), one
+Headline (BJ:L8, C2): Llama-3-8B attention shape (32 q / 8 kv heads, d 128, block 16), one
 layer, 8 concurrent requests streamed in 512-token chunks from 0 to 16K context.  One STEP =
 the whole stream: 32 x (s2l_append_chunk of 8 x 512 tokens + s2l_prefill_batch of 8 x 512
 query rows), plus new_request / release of the 8 requests.  Inputs for every chunk are
 resident in HBM before timing (1.6 GB per step: larger than the 126 MB L2, so no L2 flush
 is needed).  value = algorithmic attention FLOPs of all ranks / max-over-ranks device time.
 
-The same JSON line also reports (measured in the same run, rank 0):
-  * prefill tokens/s (new tokens / step time, per layer);
-  * a1/a2 LCP + invalidation latency on C3 token pairs (update mode, host);
-  * a5/a6 KV swap GB/s (s2l_swap_out / s2l_swap_in of 1 GiB at M_block = 2 MiB, L = 32)
-    against the measured host link (1 GiB pinned cudaMemcpyAsync, best of 3);
+The same JSON line also reports (measured in the same run):
   * roofline of the dominant kernel (tcgen05 attention) from per-launch CUDA events;
   * e2e: the same metric through the C ABI with Q/K/V in pinned HOST memory, H2D copies and
-    the D2H read of O inside the timed region (copies overlapped with compute);
-  * cpu_baseline: the fp64 oracle on a bounded sample of the same workload.
-Multi-GPU (torchrun): each rank runs its own 8 requests (sharded by request, no collective
-on the hot path); NCCL only for the barrier, the max-time reduction and the parity gather.
+    the D2H read of O inside the timed region (every rank, max over ranks);
+  * c2_steps: per-step times (median of 10 replays) and the long-step (p0 >= 4K) aggregate;
+  * c5: the long-chunk config (BJ:L11: 128K context, 2K chunks, 64q/8kv), sharded by KV head
+    across ranks, with roofline frac and sampled-row parity;
+  * c3: the update-mode config (BJ:L9: 32 x 8K, LCP 20-80 %), with roofline frac and parity;
+  * rank 0: NEXT-2 fused path, a5/a6 KV swap GB/s vs the measured host link, a1/a2 LCP
+    latency, and cpu_baseline (the fp64 oracle on a bounded sample).
+--workload c4: the memory-pressure mix (BJ:L10) sharded by request, with swap GB/s and the
+concurrent host-link aggregate.
+Multi-GPU: `--gpus N` spawns N ranks (torch.distributed.run, 127.0.0.1) unless launched under
+torchrun; one process per GPU, sharded by request (C2-C4) or KV head (C5), no collective on
+the hot path; NCCL only for the barrier, the max-time reduction and the parity gathers.
 """
 from __future__ import annotations
 
@@ -431,47 +435,460 @@ def parity_check(S, data, rank, world, dist):
             "pass": worst <= 2e-2}
 
 
+# ---------------------------------------------------------------------------- extra workloads
+def _randn_bf16(g, *shape, scale=1.0):
+    import torch
+    x = torch.randn(*shape, generator=g, device="cuda", dtype=torch.float32)
+    return (x * scale).to(torch.bfloat16) if scale != 1.0 else x.to(torch.bfloat16)
+
+
+def _bits(t):
+    import torch
+    return t.detach().contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def _reduce_max(x, dist):
+    """max over ranks of a host float (CUDA-event times are per rank)."""
+    if not dist:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _gather(x, dist, world):
+    """all_gather of a float32 tensor (device) -> list of host tensors (rank order)."""
+    import torch
+    if not dist:
+        return [x.cpu()]
+    y = x if dist.get_backend() == "nccl" else x.cpu()
+    bufs = [torch.empty_like(y) for _ in range(world)]
+    dist.all_gather(bufs, y)
+    return [b.cpu() for b in bufs]
+
+
+def _normwise(got, ref):
+    return np.abs(got - ref).max(-1) / np.maximum(np.abs(ref).max(-1), 1e-6)
+
+
+def c2_breakdown(ctx, S, reps=10):
+    """per-step times of the C2 stream (CUDA events around each chunk's append
+    + attention on the compute stream), median of `reps` replays; aggregates over the long steps
+    (p0 >= 4K) and the early ones (the piecewise-linear 'bandwidth saturation' regime of
+    PAPER.md L188)."""
+    import torch
+    per = [[] for _ in range(S.steps)]
+    for _ in range(reps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(S.steps + 1)]
+        for r, t in zip(S.rids, S.toks):
+            ctx.new_request(r, t)
+        ev[0].record()
+        for j in range(S.steps):
+            ctx.append_chunk(S.items_a[j], S.k[j], S.v[j])
+            ctx.prefill_batch(0, S.items_p[j], S.q[j], S.o[j])
+            ev[j + 1].record()
+        for r in S.rids:
+            ctx.release(r)
+        torch.cuda.synchronize()
+        for j in range(S.steps):
+            per[j].append(ev[j].elapsed_time(ev[j + 1]))
+    med = [statistics.median(x) for x in per]
+    fl = [NREQ * attn_flops(CHUNK, j * CHUNK) for j in range(S.steps)]
+    long_j = [j for j in range(S.steps) if j * CHUNK >= 4096]
+    short_j = [j for j in range(S.steps) if j * CHUNK < 4096]
+    agg = lambda js: sum(fl[j] for j in js) / (sum(med[j] for j in js) * 1e-3) / 1e12
+    return {"replays": reps, "stat": "median per step",
+            "step_ms": [round(m, 4) for m in med],
+            "step_tflops": [round(f / (m * 1e-3) / 1e12, 1) for f, m in zip(fl, med)],
+            "long_steps_p0_ge_4k_tflops": agg(long_j), "early_steps_p0_lt_4k_tflops": agg(short_j),
+            "whole_stream_tflops": agg(range(S.steps))}
+
+
+def c5_field(rank, world, dist, dev_index, pk, steps=3, warmup=1):
+    """C5 (BJ:L11): one 128K request of Llama-3-70B attention shape (64 q / 8 kv heads), 2K-token
+    chunks.  Sharded by KV head across ranks: rank g owns kv heads
+    [8g/N, 8(g+1)/N) and their q heads; no collective on the hot path, outputs are disjoint.
+    Inputs: seeded device randn (N(0,1) bf16), identical on every rank, each rank keeps its
+    heads.  value = all heads' algorithmic FLOPs / max-over-ranks stream time (strong scaling)."""
+    import torch
+    from paper_2604_16395_b200 import s2l
+    T, chunk, HQ, HKV, G = 131072, 2048, 64, 8, 8
+    h0, h1 = HKV * rank // world, HKV * (rank + 1) // world
+    hkv = h1 - h0
+    seed = 1005
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    K = _randn_bf16(g, T, HKV, D)
+    V = _randn_bf16(g, T, HKV, D)
+    Q = _randn_bf16(g, T, HQ, D)
+    nch = T // chunk
+    total_flops = sum(attn_flops(chunk, j * chunk, h_q=HQ) for j in range(nch))
+    res = {"workload": "C5 (BJ:L11): 1 request, 128K context, 2K-token chunks, 64q/8kv, d128, block 16",
+           "sharding": f"kv heads {HKV}/{world} per rank", "attn_flops": total_flops}
+    if hkv > 0:
+        Ks = [K[j * chunk:(j + 1) * chunk, h0:h1].contiguous().unsqueeze(0) for j in range(nch)]
+        Vs = [V[j * chunk:(j + 1) * chunk, h0:h1].contiguous().unsqueeze(0) for j in range(nch)]
+        Qs = [Q[j * chunk:(j + 1) * chunk, h0 * G:h1 * G].contiguous() for j in range(nch)]
+        Os = [torch.empty_like(x) for x in Qs]
+        cfg = s2l.make_config(1, hkv * G, hkv, D, KB, T // KB + 64, 0, max_requests=1, max_blocks_per_request=T // KB)
+        pool = torch.empty(cfg.num_gpu_blocks * s2l.block_bytes(cfg) // 2, dtype=torch.bfloat16,
+                           device=f"cuda:{dev_index}")
+        ctx = s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None)
+        toks = np.zeros(T, np.int32)
+
+        def stream(ev=None):
+            ctx.new_request(0, toks)
+            for j in range(nch):
+                ctx.append_chunk([(0, None, chunk, 0)], Ks[j], Vs[j])
+                ctx.prefill_batch(0, [(0, j * chunk, chunk, 0)], Qs[j], Os[j])
+                if ev is not None:
+                    ev[j + 1].record()
+            ctx.release(0)
+    for _ in range(warmup):
+        if hkv > 0:
+            stream()
+    torch.cuda.synchronize()
+    times, per = [], [[] for _ in range(nch)]
+    attn_ms = 0.0
+    for _ in range(steps):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ms = 0.0
+        if hkv > 0:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(nch + 1)]
+            ctx.set_timing(True)
+            ev[0].record()
+            stream(ev)
+            torch.cuda.synchronize()
+            attn_ms += ctx.timing_read()["attn_ms"]
+            ctx.set_timing(False)
+            ms = ev[0].elapsed_time(ev[nch])
+            for j in range(nch):
+                per[j].append(ev[j].elapsed_time(ev[j + 1]))
+        times.append(_reduce_max(ms, dist))
+    ms = statistics.median(times)
+    res.update(ms_per_stream=ms, value=total_flops / (ms * 1e-3) / 1e12, unit="TFLOP/s",
+               pct_bf16_peak=100.0 * total_flops / (ms * 1e-3) / 1e12 / world / pk["bf16"],
+               prefill_tokens_per_s=T / (ms * 1e-3), replays=steps, stat="median of replays, max over ranks")
+    if hkv > 0:
+        flops_rank = total_flops * hkv / HKV
+        ach = flops_rank * steps / (attn_ms * 1e-3) / 1e12
+        res["roofline"] = {"bound": "tensor", "achieved_rank0": ach, "peak": pk["bf16"], "unit": "TFLOP/s",
+                           "frac": ach / pk["bf16"], "kernel": "attn_tc2_kernel", "heads_rank0": [h0 * G, h1 * G]}
+        med = [statistics.median(x) for x in per]
+        fl = [attn_flops(chunk, j * chunk, h_q=hkv * G) for j in range(nch)]
+        lj = [j for j in range(nch) if j * chunk >= 32768]
+        res["long_chunks_p0_ge_32k_tflops_rank0"] = sum(fl[j] for j in lj) / (sum(med[j] for j in lj) * 1e-3) / 1e12
+        res["last_chunk_ms_rank0"] = med[-1]
+    # sampled-row parity: rows of chunks 0 and 63 (all 64 heads gathered from the ranks) vs the
+    # fp64 oracle (oracle.attention.attention_rows over the full K/V)
+    checks = [(0, [0, 1, 2047]), (nch - 1, [0, 1023, 2047])]
+    worst = 0.0
+    for j, rows in checks:
+        o = torch.zeros(len(rows), HQ, D, dtype=torch.float32, device="cuda")
+        if hkv > 0:
+            o[:, h0 * G:h1 * G] = Os[j][rows].float()
+        parts = _gather(o, dist, world)
+        if rank == 0:
+            from oracle.attention import attention_rows
+            full = sum(p for p in parts)                     # disjoint head ranges
+            a = j * chunk
+            ref, _ = attention_rows(_bits(Q[a:a + chunk]), _bits(K[:a + chunk]), _bits(V[:a + chunk]), a, rows)
+            worst = max(worst, float(_normwise(full.numpy().astype(np.float64), ref).max()))
+    if rank == 0:
+        res["parity"] = {"rows": {str(j): r for j, r in checks}, "heads": HQ, "max_normwise_err": worst,
+                         "tol": 2e-2, "pass": worst <= 2e-2}
+    if hkv > 0:
+        ctx.close()
+    return res
+
+
+def c3_field(rank, world, dist, dev_index, pk, steps=5):
+    """C3 (BJ:L9) update mode at full size, 32 requests x 8192 tokens per rank (sharded by
+    request): prefill as 2 x 4096 chunks, then update rounds -- s2l_invalidate_lcp with the LCP
+    drawn in 20-80 % (Z14), one s2l_append_chunk of all 32 suffixes, one s2l_prefill_batch of
+    all 32 suffixes.  Replays alternate the input between the new and the old token sequence
+    (both share exactly the first p tokens), so every replay is an update round with the same
+    LCP.  Inputs: seeded device randn."""
+    import torch
+    from paper_2604_16395_b200 import s2l
+    from synth import workloads as W
+    R, T, HQ, HKV = 32, 8192, H_Q, H_KV
+    seed = W.seed_of(3)
+    cfg = s2l.make_config(1, HQ, HKV, D, KB, R * T // KB + 64, 0, max_requests=R, max_blocks_per_request=T // KB)
+    pool = torch.empty(cfg.num_gpu_blocks * s2l.block_bytes(cfg) // 2, dtype=torch.bfloat16, device=f"cuda:{dev_index}")
+    ctx = s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None)
+    g = torch.Generator(device="cuda").manual_seed(seed + rank)
+    toks = [W.request_tokens(seed, rank * R + r, T) for r in range(R)]
+    ps = W.c3_lcp_draws(seed + rank, R, T)
+    news = [W.updated_tokens(seed, rank * R + r, toks[r], int(ps[r]), T, 0) for r in range(R)]
+    for r in range(R):
+        ctx.new_request(r, toks[r])
+    init = []                                               # the initial chunks' K/V (inputs)
+    for c in range(2):
+        kk, vv = _randn_bf16(g, 1, R * 4096, HKV, D), _randn_bf16(g, 1, R * 4096, HKV, D)
+        qq = _randn_bf16(g, R * 4096, HQ, D)
+        ctx.append_chunk([(r, None, 4096, r * 4096) for r in range(R)], kk, vv)
+        ctx.prefill_batch(0, [(r, c * 4096, 4096, r * 4096) for r in range(R)], qq, torch.empty_like(qq))
+        init.append((kk, vv))
+    n = [T - int(p) for p in ps]
+    off = np.concatenate([[0], np.cumsum(n)]).astype(int)
+    Rn = int(off[-1])
+    Kn, Vn, Qn = _randn_bf16(g, 1, Rn, HKV, D), _randn_bf16(g, 1, Rn, HKV, D), _randn_bf16(g, Rn, HQ, D)
+    On = torch.empty_like(Qn)
+    app = [(r, None, n[r], int(off[r])) for r in range(R)]
+    pre = [(r, int(ps[r]), n[r], int(off[r])) for r in range(R)]
+    flops = sum(attn_flops(n[r], int(ps[r])) for r in range(R))
+    cur = [0]
+
+    def round_():
+        seqs = news if cur[0] % 2 == 0 else toks
+        cur[0] += 1
+        for r in range(R):
+            ctx.invalidate_lcp(r, seqs[r])
+        ctx.append_chunk(app, Kn, Vn)
+        ctx.prefill_batch(0, pre, Qn, On)
+
+    round_()
+    round_()
+    torch.cuda.synchronize()
+    times, attn_ms, app_ms = [], 0.0, 0.0
+    for _ in range(steps):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx.set_timing(True)
+        e0.record()
+        round_()
+        e1.record()
+        torch.cuda.synchronize()
+        ti = ctx.timing_read()
+        ctx.set_timing(False)
+        attn_ms += ti["attn_ms"]
+        app_ms += ti["append_ms"]
+        times.append(_reduce_max(e0.elapsed_time(e1), dist))
+    ms = statistics.median(times)
+    ach = flops * steps / (attn_ms * 1e-3) / 1e12
+    res = {"workload": "C3 (BJ:L9): update round, 32 requests x 8192 tokens per GPU, LCP ~ U[20%, 80%]",
+           "ms_per_round": ms, "value": flops * world / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+           "pct_bf16_peak": 100.0 * flops / (ms * 1e-3) / 1e12 / pk["bf16"],
+           "tokens_recomputed_per_round": int(Rn) * world, "replays": steps,
+           "stat": "median of rounds, max over ranks",
+           "roofline": {"bound": "tensor", "achieved_rank0": ach, "peak": pk["bf16"], "unit": "TFLOP/s",
+                        "frac": ach / pk["bf16"], "kernel": "attn_tc2_kernel"},
+           "append_ms_per_round": app_ms / steps}
+    # parity: after the last round a request's K/V are the initial chunks' rows for positions
+    # < p and this round's appended rows (Kn/Vn) from p on (the inputs, not the pool); the pool
+    # read back through the block table must equal them bit for bit, and sampled attention rows
+    # are compared with the fp64 oracle over them
+    if rank == 0:
+        from oracle.attention import attention_rows
+        gp = _bits(pool).reshape(cfg.num_gpu_blocks, 1, 2, HKV, KB, D)
+        rng = np.random.default_rng(3)
+        worst, pool_ok = 0.0, True
+        for r in (0, int(np.argmin(n)), int(np.argmax(n))):
+            p0 = int(ps[r])
+            kin = np.concatenate([_bits(init[c][0][0, r * 4096:(r + 1) * 4096]) for c in range(2)])
+            vin = np.concatenate([_bits(init[c][1][0, r * 4096:(r + 1) * 4096]) for c in range(2)])
+            kin[p0:] = _bits(Kn[0, off[r]:off[r + 1]])
+            vin[p0:] = _bits(Vn[0, off[r]:off[r + 1]])
+            ids = np.array(ctx.block_table(r))
+            pos = np.arange(T)
+            pool_ok &= bool(np.array_equal(gp[ids[pos // KB], 0, 0, :, pos % KB, :], kin) and
+                            np.array_equal(gp[ids[pos // KB], 0, 1, :, pos % KB, :], vin))
+            rows = sorted(set([0, 1, n[r] - 1] + rng.integers(0, n[r], 3).tolist()))
+            ref, _ = attention_rows(_bits(Qn[off[r]:off[r + 1]]), kin, vin, p0, rows)
+            got = On[off[r]:off[r + 1]][rows].float().cpu().numpy().astype(np.float64)
+            worst = max(worst, float(_normwise(got, ref).max()))
+        res["parity"] = {"requests_checked": 3, "max_normwise_err": worst, "tol": 2e-2,
+                         "pool_bytes_bit_exact": pool_ok, "pass": worst <= 2e-2 and pool_ok}
+    ctx.close()
+    return res
+
+
+def concurrent_link(dev, dist):
+    """Host-link aggregate with every rank copying at the same time (C4's scaling
+    roofline): 1 GiB per rank per direction, barrier-started, bytes of all ranks / max time."""
+    import torch
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    out = {}
+    world = dist.get_world_size() if dist else 1
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        best = 0.0
+        for _ in range(3):
+            if dist:
+                dist.barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(); s.record(); fn(); e.record(); torch.cuda.synchronize()
+            ms = _reduce_max(s.elapsed_time(e), dist)
+            best = max(best, world * n / (ms * 1e-3) / 1e9)
+        out[name] = best
+    del h, d
+    return out
+
+
+def c4_mode(args, rank, world, dist, dev_index, pk):
+    """--workload c4 (BJ:L10): the memory-pressure mix -- 128 append / update requests
+    (paper_2604_16395_b200.pressure recipe), sharded by request across ranks (128/N each, request
+    r on rank r mod N); each rank's GPU pool holds 50 % of its shard's working set, the CPU pool
+    all of it; L = 8 layers (M_block 512 KiB).  The round-robin driver swaps the requests due
+    furthest in the future out to pinned host memory and back in, the swaps of step s+1 issued
+    on the copy streams while step s computes.  value = prefill tokens (all layers' work, all
+    ranks) / max-over-ranks stream time; swap GB/s per direction aggregated over ranks, against
+    the concurrent host-link aggregate."""
+    import torch
+    from paper_2604_16395_b200 import pressure, s2l
+    from synth import workloads as W
+    L, budget = 8, 8192
+    seed = W.seed_of(4)
+    plans = [p for p in pressure.c4_plans(seed, 128, budget=budget) if p.rid % world == rank]
+    ws = pressure.working_set_blocks(plans, KB)
+    ng, ncpu = ws // 2, ws
+    cfg = s2l.make_config(L, H_Q, H_KV, D, KB, ng, ncpu, max_requests=len(plans),
+                          max_blocks_per_request=16384 // KB, alloc_cooling=1)
+    mb = s2l.block_bytes(cfg)
+    gpool = torch.empty(ng * mb // 2, dtype=torch.bfloat16, device=f"cuda:{dev_index}")
+    cpool = torch.empty(ncpu * mb // 2, dtype=torch.bfloat16, pin_memory=True)
+    g = torch.Generator(device="cuda").manual_seed(seed + rank)
+    src_k, src_v = _randn_bf16(g, L, budget, H_KV, D), _randn_bf16(g, L, budget, H_KV, D)
+    src_q = _randn_bf16(g, budget, H_Q, D)
+    out = torch.empty_like(src_q)
+    cs, cs_in = torch.cuda.Stream(), torch.cuda.Stream()
+    runs = []
+    for it in range(1 + args.steps):                       # first run = warm-up
+        ctx = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), cs, swap_in_stream=cs_in)
+        wrap = pressure.SwapTimer(ctx, copy_stream=cs, swap_in_stream=cs_in)
+        drv = pressure.PressureDriver(wrap, plans, KB, budget, evict_ahead=2)
+        flops = [0.0]
+
+        def on_step(sel, app, pre, rows, flops=flops):
+            for (_, q_pos, n, _) in pre:
+                flops[0] += L * attn_flops(n, q_pos)
+        ex = pressure.device_executor(wrap, src_q, src_k, src_v, out, L, on_step)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        drv.run(ex)
+        for st in (cs, cs_in):
+            ev = torch.cuda.Event()
+            ev.record(st)
+            torch.cuda.current_stream().wait_event(ev)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        cm = wrap.copy_ms()
+        ctx.close()
+        if it:
+            runs.append((ms, drv.tokens, drv.swapped_out_bytes, drv.swapped_in_bytes, flops[0],
+                         cm.get("out", (0, 0.0))[1], cm.get("in", (0, 0.0))[1]))
+    ms = statistics.median([r[0] for r in runs])
+    ms_max = _reduce_max(ms, dist)
+    tok, b_out, b_in, fl = runs[0][1], runs[0][2], runs[0][3], runs[0][4]
+    tot = torch.tensor([tok, b_out, b_in, fl], dtype=torch.float64)
+    if dist:
+        tt = tot.cuda() if dist.get_backend() == "nccl" else tot
+        dist.all_reduce(tt)
+        tot = tt.cpu()
+    link1 = measure_link(f"cuda:{dev_index}") if rank == 0 else None
+    agg = concurrent_link(f"cuda:{dev_index}", dist)
+    tok_all, out_all, in_all, fl_all = [float(x) for x in tot]
+    line = {"metric": METRIC, "value": tok_all / (ms_max * 1e-3), "unit": "prefill tokens/s (x L=8 layers)",
+            "n_gpus": world, "steps": args.steps, "warmup": 1, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "C4 (BJ:L10) memory-pressure mix: 128 append/update requests sharded by request, "
+                                   "GPU pool 50% of the working set, KV swap to pinned host", "requests": 128,
+                       "layers": L, "m_block": mb, "parallelism": f"request-sharded x{world}"},
+            "attn_tflops": fl_all / (ms_max * 1e-3) / 1e12,
+            "swap": {"out_bytes": out_all, "in_bytes": in_all,
+                     "out_gbs_aggregate": out_all / (ms_max * 1e-3) / 1e9,
+                     "in_gbs_aggregate": in_all / (ms_max * 1e-3) / 1e9,
+                     "copy_stream_ms_rank0": {"out": runs[0][5], "in": runs[0][6]}},
+            "host_link_concurrent_aggregate_gbs": agg, "host_link_single_gpu_gbs": link1,
+            "stat": "median of steps (one step = the whole 128-request stream), max over ranks"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------------------- main
+def spawn(args) -> int:
+    """`--gpus N` without a torchrun environment: launch N ranks of this script under
+    torch.distributed.run (127.0.0.1) and return its exit code."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="s2l", choices=["s2l", "reference"])
-    ap.add_argument("--no-side", action="store_true", help="skip swap / LCP / e2e / cpu_baseline")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4"],
+                    help="c2: the headline line (C2, with C3 / C5 fields); c4: the memory-pressure mix")
+    ap.add_argument("--no-side", action="store_true", help="skip the side measurements (timing experiments)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return
 
     import torch
-    # S2L_BENCH_DEVICE overrides the device (test plumbing: several ranks on one GPU with gloo)
-    local = int(os.environ.get("S2L_BENCH_DEVICE", local))
-    torch.cuda.set_device(local)
-    dev = f"cuda:{local}"
+    ndev = torch.cuda.device_count()
+    if ndev < 1:
+        raise SystemExit("bench.py: no CUDA device (there is no CPU path)")
+    # one rank per GPU; with more ranks than GPUs (plumbing checks on a 1-GPU box) ranks share
+    # devices round-robin and the process group falls back to gloo (NCCL needs distinct GPUs)
+    dev_index = int(os.environ.get("S2L_BENCH_DEVICE", local % ndev))
+    torch.cuda.set_device(dev_index)
+    dev = f"cuda:{dev_index}"
     dist = None
+    shared = world > ndev
     if world > 1:
         import torch.distributed as dist
-        backend = os.environ.get("S2L_DIST_BACKEND", "nccl")
+        backend = os.environ.get("S2L_DIST_BACKEND", "gloo" if shared else "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device(dev))
         else:
             dist.init_process_group(backend)
     from paper_2604_16395_b200 import build
-    if rank == 0:
+    if local == 0:
         build.build()
     if dist:
         dist.barrier()
-    from paper_2604_16395_b200 import s2l
+    from paper_2604_16395_b200 import s2l  # noqa: F401  (fails loudly if libs2l is missing)
+    pk = peaks()
+    placement = {"ranks": world, "devices_used": min(world, ndev), "ranks_share_devices": shared,
+                 "backend": dist.get_backend() if dist else None}
+
+    if args.workload == "c4":
+        c4_mode(args, rank, world, dist, dev_index, pk)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
 
     rids, toks, data = make_stream_data(rank)
     S = Stream(rids, toks, data, dev)
-    ctx, pool = make_ctx(local)
+    ctx, pool = make_ctx(dev_index)
 
     fn = lambda: run_step(ctx, S)
     l0 = ctx.kernel_launches()
@@ -484,7 +901,7 @@ def main():
         for _ in range(args.warmup):
             fn()
         torch.cuda.synchronize()
-        with Clocks(local) as ck:
+        with Clocks(dev_index) as ck:
             ctx.set_timing(True)
             ms = timed(fn, args.steps, 0, dist)
             tinfo = ctx.timing_read()
@@ -495,7 +912,6 @@ def main():
     ms_step = ms / args.steps
     flops_rank = step_flops()
     value = flops_rank * world / (ms_step * 1e-3) / 1e12
-    pk = peaks()
     attn_launches = tinfo["attn_launches"]
     attn_ms_avg = tinfo["attn_ms"] / max(1, attn_launches)
     achieved = flops_rank * args.steps / (tinfo["attn_ms"] * 1e-3) / 1e12
@@ -517,6 +933,7 @@ def main():
                                "8 requests x 512-token chunks to 16K per GPU, append + chunked-prefill attention",
                    "global_batch": NREQ * world, "seq_len": TOTAL, "chunk": CHUNK,
                    "parallelism": f"request-sharded x{world}", "l2": "inputs 1.6 GB/step > 126 MB L2 (no flush needed)"},
+        "placement": placement,
         "pct_bf16_peak": 100.0 * value / world / pk["bf16"],
         "prefill_tokens_per_s": new_tokens / (ms_step * 1e-3),
         "gpu_launches": launches_per_step * args.steps,
@@ -539,8 +956,32 @@ def main():
                           "peak": pk.get("hbm"), "frac": (app_bytes / (app_ms * 1e-3) / 1e9) / pk["hbm"]
                           if pk.get("hbm") else None, "bytes_per_step": app_bytes,
                           "launches": tinfo.get("append_launches")}
-    # parity gather (NCCL) after timing
+    # parity gather after timing
     line["parity"] = parity_check(S, data, rank, world, dist)
+
+    # e2e through the C ABI with host buffers, every rank (max over ranks)
+    S_host = Stream(rids, toks, data, dev, pinned=True)
+    dev_bufs = tuple([torch.empty_like(S.q[0] if i in (0, 3) else S.k[0]) for _ in range(E2E_BUFS)]
+                     for i in range(4))
+    streams = (torch.cuda.Stream(), torch.cuda.Stream())
+    efn = lambda: e2e_run(ctx, S_host, dev_bufs, streams)
+    ke = max(2, args.steps // 2)
+    ems = timed(efn, ke, 1, dist) / ke
+    h2d = sum(x.numel() * 2 for L_ in (S_host.q, S_host.k, S_host.v) for x in L_)
+    d2h = sum(x.numel() * 2 for x in S_host.o)
+    line["e2e"] = {"value": flops_rank * world / (ems * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ems,
+                   "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+                   "path": "pinned host Q/K/V -> H2D (side stream) -> s2l_append_chunk + s2l_prefill_batch -> D2H O",
+                   "stat": "max over ranks"}
+    del S_host
+
+    # per-step breakdown of the C2 stream (rank 0), long-chunk C5 and update-mode C3 fields
+    if rank == 0:
+        line["c2_steps"] = c2_breakdown(ctx, S, reps=10)
+    line["c5"] = c5_field(rank, world, dist, dev_index, pk)
+    torch.cuda.empty_cache()
+    line["c3"] = c3_field(rank, world, dist, dev_index, pk)
+    torch.cuda.empty_cache()
 
     if not args.no_side and rank == 0:
         # NEXT-2: the same step through the fused append + attention path (s2l_prefill_append),
@@ -560,29 +1001,14 @@ def main():
         ffn()
         torch.cuda.synchronize()
         line["next2_fused"]["parity"] = parity_check(S, data, 0, 1, None)
-        # e2e through the C ABI with host buffers
-        S_host = Stream(rids, toks, data, dev, pinned=True)
-        dev_bufs = tuple([torch.empty_like(S.q[0] if i in (0, 3) else S.k[0]) for _ in range(E2E_BUFS)]
-                         for i in range(4))
-        streams = (torch.cuda.Stream(), torch.cuda.Stream())
-        efn = lambda: e2e_run(ctx, S_host, dev_bufs, streams)
-        ems = timed(efn, max(2, args.steps // 2), 1, None) / max(2, args.steps // 2)
-        h2d = sum(x.numel() * 2 for L_ in (S_host.q, S_host.k, S_host.v) for x in L_)
-        d2h = sum(x.numel() * 2 for x in S_host.o)
-        line["e2e"] = {"value": flops_rank / (ems * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ems,
-                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                       "path": "pinned host Q/K/V -> H2D (side stream) -> s2l_append_chunk + s2l_prefill_batch -> D2H O"}
-        del S_host
         link = measure_link(dev)
-        line["kv_swap"] = {**measure_swap(local, link), "link_h2d_gbs": link["h2d"], "link_d2h_gbs": link["d2h"]}
+        line["kv_swap"] = {**measure_swap(dev_index, link), "link_h2d_gbs": link["h2d"], "link_d2h_gbs": link["d2h"]}
         line["kv_swap_gbs"] = {"out": line["kv_swap"]["out_gbs"], "in": line["kv_swap"]["in_gbs"]}
         line["lcp_invalidate"] = measure_lcp()
-        if world == 1:
-            v, desc, thr = oracle_sample(data)
-            line["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": thr, "kind": "oracle", "sample": desc}
-    elif rank == 0:
-        line["e2e"] = None
     if rank == 0:
+        # the oracle on the host cores (bounded sample), after all device timing
+        v, desc, thr = oracle_sample(data)
+        line["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": thr, "kind": "oracle", "sample": desc}
         print(json.dumps(line), flush=True)
     ctx.close()
     if dist:

@@ -11,8 +11,9 @@ Recipe (reading Z10):
   * prefix hash H_i = splitmix64(H_{i-1} xor token_i), H_{-1} = splitmix64(seed);
     so K/V/Q of position i depend on tokens[0..i] only and an update that keeps the
     first p tokens reproduces the first p rows bit for bit (P:L170, P:L182);
-  * each Q/K/V element = Irwin-Hall(4) draw (sum of four 16-bit uniforms, centred,
-    scaled by sqrt(3) to unit variance) from splitmix64(H_i xor key(kind, layer, head, c)),
+  * each Q/K/V element = an N(0,1) draw by Box-Muller from the 64-bit
+    word x = splitmix64(H_i xor key(kind, layer, head, c)): u1 = (x>>32 + 0.5)/2^32,
+    u2 = (x & 0xffffffff)/2^32, z = sqrt(-2 ln u1) cos(2 pi u2) (|z| <= 6.8),
     then scaled by `scale` (1 normally, 4 for the "peaky" variant that exercises the
     running-max rescale), rounded float64 -> float32 (RNE) -> bf16 (RNE).
 """
@@ -87,10 +88,9 @@ def _keys(seed: int, kind: int, layer: int, heads: np.ndarray, d: int) -> np.nda
 def _rows_chunk(h: np.ndarray, keys: np.ndarray, scale: float) -> np.ndarray:
     with np.errstate(over="ignore"):
         x = splitmix64(h[:, None, None] ^ keys[None, :, :])
-    m = np.uint64(0xFFFF)
-    s = ((x & m).astype(np.float64) + ((x >> np.uint64(16)) & m).astype(np.float64)
-         + ((x >> np.uint64(32)) & m).astype(np.float64) + (x >> np.uint64(48)).astype(np.float64))
-    z = (s / 65536.0 - 2.0) * np.sqrt(3.0) * scale
+    u1 = ((x >> np.uint64(32)).astype(np.float64) + 0.5) * (1.0 / 4294967296.0)
+    u2 = (x & np.uint64(0xFFFFFFFF)).astype(np.float64) * (1.0 / 4294967296.0)
+    z = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2) * scale
     return f64_to_bf16_bits(z)
 
 

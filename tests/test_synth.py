@@ -38,8 +38,12 @@ def test_rows_distribution():
     H = synth.prefix_hashes(9, synth.tokens(9, 0, 4096))
     r = synth.rows(9, synth.KIND_V, 0, H, range(8), 128)
     x = (r.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    # N(0,1): mean, variance, Gaussian kurtosis and tails
     assert abs(x.mean()) < 0.01 and abs(x.std() - 1.0) < 0.01
-    assert np.abs(x).max() <= np.sqrt(3) * 2 + 0.05
+    kurt = ((x - x.mean()) ** 4).mean() / x.var() ** 2
+    assert abs(kurt - 3.0) < 0.05, kurt
+    assert abs((np.abs(x) > 3.0).mean() - 0.0027) < 0.0006       # 2 * (1 - Phi(3)) = 0.0027
+    assert 4.0 < np.abs(x).max() <= 6.8
     # multithreaded path == single chunk
     r1 = synth.rows(9, synth.KIND_V, 0, H[:7], range(8), 128)
     assert np.array_equal(r1, r[:7])
