@@ -40,8 +40,9 @@
 #define S2L_POLY_PAIRS 1
 #endif
 #ifndef S2L_SPLIT_S
-#define S2L_SPLIT_S 1      // v2: 1 = S(j+1) in two N=64 halves, keys 64-127 issued as soon as the
-                           // softmax has read S(j)'s upper half (overlaps the softmax)
+#define S2L_SPLIT_S 0      // 1 = S(j+1) in two N=64 halves, keys 64-127 issued as soon as the
+                           // softmax has read S(j)'s upper half (round 1); 0 = whole N=128 S
+                           // MMAs and the stale-max pipelined softmax (round 2)
 #endif
 
 namespace s2l {
@@ -318,6 +319,29 @@ __device__ __forceinline__ float2 chunk_p64(const uint32_t* v, float2 acc, int v
     pk[c] = pack_p(x[c].x, x[c].y);
   }
   return __fadd2_rn(__fadd2_rn(a[0], a[1]), __fadd2_rn(a[2], a[3]));
+}
+// p = 2^(s*scale - m) for 32 columns of an unmasked tile (16 pairs), the FMA-pipe polynomial
+// on kPolyPer8 of every 8 pairs, spread evenly (pair c is polynomial iff (c*kPolyPer8) mod 8 <
+// kPolyPer8); returns the running pair sum, writes 16 packed bf16x2.
+template <int kPolyPer8>
+__device__ __forceinline__ float2 chunk_p32(const uint32_t* v, float2 acc, float2 sc2, float2 nm2,
+                                            uint32_t (&pk)[16]) {
+  float2 x[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    x[c] = __ffma2_rn(make_float2(__uint_as_float(v[2 * c]), __uint_as_float(v[2 * c + 1])), sc2, nm2);
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    if (((c * kPolyPer8) & 7) < kPolyPer8) x[c] = exp2_poly2(x[c]);
+    else x[c] = make_float2(fast_exp2(x[c].x), fast_exp2(x[c].y));
+  }
+  float2 a[2] = {acc, make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    a[c & 1] = __fadd2_rn(a[c & 1], x[c]);
+    pk[c] = pack_p(x[c].x, x[c].y);
+  }
+  return __fadd2_rn(a[0], a[1]);
 }
 // Row max of 32 columns with 8 independent chains (short dependency latency).
 template <bool kMasked>
@@ -807,16 +831,65 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       if (masked_tile) { max32<true>(sv, vis, 0, mt); max32<true>(sv + 32, vis, 32, mt); }
       else { max32<false>(sv, vis, 0, mt); max32<false>(sv + 32, vis, 32, mt); }
 #else
-      tmem_ld32(tS, sv);
-      tmem_ld32(tS + 32, sv + 32);
-      tmem_wait_ld();
-      tmem_ld32(tS + 64, sv + 64);                      // in flight during the first max half
-      tmem_ld32(tS + 96, sv + 96);
-      if (masked_tile) { max32<true>(sv, vis, 0, mt); max32<true>(sv + 32, vis, 32, mt); }
-      else { max32<false>(sv, vis, 0, mt); max32<false>(sv + 32, vis, 32, mt); }
-      tmem_wait_ld();
-      if (masked_tile) { max32<true>(sv + 64, vis, 64, mt); max32<true>(sv + 96, vis, 96, mt); }
-      else { max32<false>(sv + 64, vis, 64, mt); max32<false>(sv + 96, vis, 96, mt); }
+      // Steady state (stale-max fast path): a tile after the first one of this CTA, with no
+      // masked key and a finite running max in every row, is exponentiated against the running
+      // max m_run straight away, chunk by chunk as its scores arrive from TMEM (p <= 2^8 as long
+      // as the tile max stays within kRescaleThresh of m_run, the same bound the lazy rescale
+      // keeps).  P of keys 0-63 is released to the PV MMAs only once the whole tile's max is
+      // known to be within that bound; otherwise (rare) the tile falls through to the exact
+      // path below, which rescales O and recomputes P with the new max (S is still in sv).
+      const bool fast = j > 0 && !masked_tile && __all_sync(0xffffffffu, m_run != -INFINITY);
+      bool loaded = false;
+      if (fast) {
+        const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_run, -m_run);
+        uint32_t pk[16];
+        tmem_ld32(tS, sv);
+        tmem_wait_ld();
+        tmem_ld32(tS + 32, sv + 32);
+        tmem_ld32(tS + 64, sv + 64);
+        tmem_ld32(tS + 96, sv + 96);
+        float2 acc = chunk_p32<kPolyPairsPer8>(sv, make_float2(0.f, 0.f), sc2, nm2, pk);
+        tmem_st16(tS, pk);
+        tmem_wait_ld();
+        acc = chunk_p32<kPolyPairsPer8>(sv + 32, acc, sc2, nm2, pk);
+        tmem_st16(tS + 16, pk);
+        max32<false>(sv, 0, 0, mt);
+        max32<false>(sv + 32, 0, 32, mt);
+        max32<false>(sv + 64, 0, 64, mt);
+        max32<false>(sv + 96, 0, 96, mt);
+        const float mxf = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])),
+                                fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7]))) * sl2;
+        if (!__any_sync(0xffffffffu, mxf > m_run + kRescaleThresh)) {
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(bar(WB_PF + i));                  // P keys 0-63
+          if (tr) TRACE(23, i, j);
+          acc = chunk_p32<kPolyPairsPer8>(sv + 64, acc, sc2, nm2, pk);
+          tmem_st16(tS + 32, pk);
+          acc = chunk_p32<kPolyPairsPer8>(sv + 96, acc, sc2, nm2, pk);
+          tmem_st16(tS + 48, pk);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(bar(WB_PH + i));                  // P keys 64-127
+          if (tr) TRACE(24, i, j);
+          l_run += acc.x + acc.y;
+          continue;
+        }
+        tmem_wait_st();                                 // speculative P lands before the rewrite
+        loaded = true;
+      }
+      if (!loaded) {
+        tmem_ld32(tS, sv);
+        tmem_ld32(tS + 32, sv + 32);
+        tmem_wait_ld();
+        tmem_ld32(tS + 64, sv + 64);                    // in flight during the first max half
+        tmem_ld32(tS + 96, sv + 96);
+        if (masked_tile) { max32<true>(sv, vis, 0, mt); max32<true>(sv + 32, vis, 32, mt); }
+        else { max32<false>(sv, vis, 0, mt); max32<false>(sv + 32, vis, 32, mt); }
+        tmem_wait_ld();
+        if (masked_tile) { max32<true>(sv + 64, vis, 64, mt); max32<true>(sv + 96, vis, 96, mt); }
+        else { max32<false>(sv + 64, vis, 64, mt); max32<false>(sv + 96, vis, 96, mt); }
+      }
 #endif
       float mx = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])), fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7])));
       mx *= sl2;

@@ -55,9 +55,17 @@ def main():
         for path, fn, (ctx, _) in zip(libs, step_fn, ctxs):
             ms = bench.timed(lambda: fn(ctx, S), 3, 1)
             res[path].append(flops * 3 / (ms * 1e-3) / 1e12)
+    kern = {}
+    for path, fn, (ctx, _) in zip(libs, step_fn, ctxs):   # attention-kernel-only (per-launch events)
+        ctx.set_timing(True)
+        bench.timed(lambda: fn(ctx, S), 3, 0)
+        ti = ctx.timing_read()
+        ctx.set_timing(False)
+        kern[path] = flops * 3 / (ti["attn_ms"] * 1e-3) / 1e12
     for path in libs:
         v = res[path]
-        print(f"{path.split('/')[-1]:40s} median {statistics.median(v):8.1f}  min {min(v):8.1f}  max {max(v):8.1f} TFLOP/s")
+        print(f"{path.split('/')[-1]:40s} median {statistics.median(v):8.1f}  min {min(v):8.1f}  max {max(v):8.1f} "
+              f"TFLOP/s (step)  attn kernel {kern[path]:8.1f}")
 
 
 if __name__ == "__main__":
