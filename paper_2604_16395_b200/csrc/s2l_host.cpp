@@ -611,6 +611,7 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
     CK(cudaMemsetAsync(c->split_cnt, 0, (size_t)c->num_sms * sizeof(int32_t), c->compute));
     const char* e = getenv("S2L_NO_SPLIT");
     c->split_enabled = !(e && e[0] == '1');
+
     e = getenv("S2L_TRACE");
     if (e && e[0] == '1') {
       CK(cudaMalloc(&c->trace_buf, (16 + 4 * 4096 * 2) * sizeof(uint32_t)));

@@ -72,6 +72,25 @@ __device__ __forceinline__ float tile_sw(const float (&s)[128], float2 sc, float
   return a.x + a.y;
 }
 
+// pure MUFU.EX2 throughput: 128 independent ex2 per thread per iteration
+__global__ void mufu_only(const float* __restrict__ in, uint32_t* out, int iters, long long* cycles) {
+  float s[128];
+#pragma unroll
+  for (int c = 0; c < 128; ++c) s[c] = in[(threadIdx.x * 7 + c) & 1023];
+  float acc = 0.f;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < 128; ++c) s[c] = ex2(s[c]);
+  }
+  long long t1 = clock64();
+#pragma unroll
+  for (int c = 0; c < 128; ++c) acc += s[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __float_as_uint(acc);
+  if (threadIdx.x == 0 && blockIdx.x == 0) *cycles = (t1 - t0) / iters;
+}
+
 template <int V, int CH, int P, int MODE>
 __global__ void k(const float* __restrict__ in, uint32_t* out, int iters, long long* cycles) {
   float s[128];
@@ -106,6 +125,14 @@ int main() {
   float* in; cudaMalloc(&in, 4096); cudaMemset(in, 0, 4096);
   uint32_t* out; cudaMalloc(&out, 148 * 256 * 4);
   long long* cyc; cudaMalloc(&cyc, 8);
+  for (int w = 1; w <= 2; ++w) {
+    mufu_only<<<148, 128 * w>>>(in, out, 200, cyc);
+    cudaDeviceSynchronize();
+    long long h;
+    cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("%-28s %d warp(s)/SMSP: %5lld cycles per 128 ex2 per warp\n", "MUFU.EX2 only", w, h);
+  }
+  run<0, 32, 1, 1>("phases of 32 pairs (kernel)", in, out, cyc);
   run<0, 16, 2, 0>("phases of 16 pairs", in, out, cyc);
   run<0, 16, 2, 1>("phases of 16 pairs", in, out, cyc);
   run<0, 32, 2, 1>("phases of 32 pairs", in, out, cyc);
