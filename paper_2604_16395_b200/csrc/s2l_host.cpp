@@ -593,6 +593,11 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
   c->quar_out.assign((size_t)cfg->num_gpu_blocks, 0);
   c->quar_in.assign((size_t)cfg->num_gpu_blocks, 0);
   c->cpu_quar_in.assign((size_t)cfg->num_cpu_blocks, 0);
+  {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
   c->tc_ok = s2l::attn_tc_supported(c->geo);
   if (c->tc_ok && cfg->num_gpu_blocks > 0) {
     const char* err = nullptr;
@@ -603,9 +608,6 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
     c->tc_ok = false;
   }
   if (c->tc_ok) {
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev));
     CK(cudaMalloc(&c->split_ws, (size_t)c->num_sms * s2l::kSplitPieceFloats * sizeof(float)));
     CK(cudaMalloc(&c->split_cnt, (size_t)c->num_sms * sizeof(int32_t)));
     CK(cudaMemsetAsync(c->split_cnt, 0, (size_t)c->num_sms * sizeof(int32_t), c->compute));
