@@ -315,6 +315,54 @@ def measure_swap(dev_index, link):
     return res
 
 
+def swap_cell(dev_index, L, B, scattered, reps=3, seed=0):
+    """a5/a6 microbench cell: B blocks of M_block = 2*L*16*8*128*2 B swapped
+    out and back in.  scattered: the request's GPU ids are a random subset of 2B ids (B one-block
+    filler requests, a random half released first; the lowest-free allocator hands the freed ids
+    out ascending), else one contiguous run.  Best of `reps`; GB/s per direction."""
+    import torch
+    from paper_2604_16395_b200 import s2l
+    ng = 2 * B + 8
+    cfg = s2l.make_config(L, H_Q, H_KV, D, KB, ng, B + 8, max_requests=2 * B + 4, max_blocks_per_request=B + 8)
+    mb = s2l.block_bytes(cfg)
+    gp = torch.empty(ng * mb // 2, dtype=torch.bfloat16, device=f"cuda:{dev_index}")
+    cp = torch.empty((B + 8) * mb // 2, dtype=torch.bfloat16).pin_memory()
+    cs, cs_in = torch.cuda.Stream(), torch.cuda.Stream()
+    ctx = s2l.Context(cfg, gp, cp, torch.cuda.current_stream(), cs, swap_in_stream=cs_in)
+    kv = torch.zeros(L, KB * B, H_KV, D, dtype=torch.bfloat16, device=f"cuda:{dev_index}")
+    rid = 10 ** 6
+    if scattered:
+        rng = np.random.default_rng(seed)
+        for f in range(2 * B):
+            ctx.new_request(f, np.zeros(KB, np.int32))
+        one = kv[:, :KB].contiguous()
+        ctx.append_chunk([(f, None, KB, 0) for f in range(2 * B)], one, one)
+        for f in sorted(rng.permutation(2 * B)[:B]):
+            ctx.release(int(f))
+    ctx.new_request(rid, np.zeros(KB * B, np.int32))
+    ctx.append_chunk([(rid, None, KB * B, 0)], kv, kv)
+    ctx.sync()
+    ids = ctx.block_table(rid)
+    runs = 1 + sum(1 for a, b in zip(ids, ids[1:]) if b != a + 1)
+    best = {"out": 0.0, "in": 0.0}
+    for _ in range(reps):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize()
+        e[0].record(cs)
+        b = ctx.swap_out([rid])
+        e[1].record(cs)
+        ctx.sync()
+        e[2].record(cs_in)
+        ctx.swap_in([rid])
+        e[3].record(cs_in)
+        ctx.sync()
+        best["out"] = max(best["out"], b / (e[0].elapsed_time(e[1]) * 1e-3) / 1e9)
+        best["in"] = max(best["in"], b / (e[2].elapsed_time(e[3]) * 1e-3) / 1e9)
+    ctx.close()
+    return {"L": L, "m_block": mb, "blocks": B, "ids": "scattered" if scattered else "contiguous", "gpu_id_runs": runs,
+            "out_gbs": best["out"], "in_gbs": best["in"]}
+
+
 def measure_lcp():
     """a1/a2 on C3 shapes (BJ:L9): 32 requests x 8192 tokens, LCP 20-80%, host-only bookkeeping."""
     from paper_2604_16395_b200 import s2l
@@ -1004,6 +1052,12 @@ def main():
         link = measure_link(dev)
         line["kv_swap"] = {**measure_swap(dev_index, link), "link_h2d_gbs": link["h2d"], "link_d2h_gbs": link["d2h"]}
         line["kv_swap_gbs"] = {"out": line["kv_swap"]["out_gbs"], "in": line["kv_swap"]["in_gbs"]}
+        # scattered / small blocks (SURVEY d.2: random ids, 64 KiB blocks at L = 1)
+        cells = [swap_cell(dev_index, 1, B, True) for B in (8, 64, 512)]
+        for cl in cells:
+            cl["out_frac_link"] = cl["out_gbs"] / link["d2h"]
+            cl["in_frac_link"] = cl["in_gbs"] / link["h2d"]
+        line["kv_swap_scattered"] = cells
         line["lcp_invalidate"] = measure_lcp()
     if rank == 0:
         # the oracle on the host cores (bounded sample), after all device timing

@@ -202,3 +202,41 @@ cudaError_t launch_append_inline(const Geometry& g, const InlineBlob& blob, int3
 }
 
 }  // namespace s2l
+
+// ---- swap gather / scatter (a5 / a6 with scattered GPU block ids) --------------------------
+// The copy engines move each contiguous run of blocks as one DMA; when the GPU ids of a swap
+// are scattered (short runs), the runs are staged: swap-out gathers the blocks of a CPU-id run
+// into a contiguous device staging buffer (HBM -> HBM) and moves it with one D2H; swap-in
+// moves a CPU run into staging with one H2D and scatters it to its GPU blocks.  One CTA moves
+// one block (16-byte vectors); block ids travel by value (<= kSwapIdsPerLaunch per launch).
+namespace s2l {
+namespace {
+struct SwapIds {
+  int32_t id[kSwapIdsPerLaunch];
+};
+__global__ void __launch_bounds__(256) swap_stage_kernel(const __grid_constant__ SwapIds ids, int32_t n,
+                                                          uint4* __restrict__ pool, uint4* __restrict__ stage,
+                                                          int64_t vec_per_block, int32_t to_stage) {
+  pdl_prologue();
+  for (int32_t b = blockIdx.x; b < n; b += gridDim.x) {
+    uint4* g = pool + (int64_t)ids.id[b] * vec_per_block;
+    uint4* s = stage + (int64_t)b * vec_per_block;
+    if (to_stage) {
+      for (int64_t i = threadIdx.x; i < vec_per_block; i += blockDim.x) s[i] = __ldcs(g + i);
+    } else {
+      for (int64_t i = threadIdx.x; i < vec_per_block; i += blockDim.x) g[i] = s[i];
+    }
+  }
+}
+}  // namespace
+
+cudaError_t launch_swap_stage(const int32_t* host_ids, int32_t n, void* pool, void* stage, int64_t block_bytes,
+                              bool to_stage, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (n > kSwapIdsPerLaunch || block_bytes % 16) return cudaErrorInvalidValue;
+  SwapIds ids;
+  memcpy(ids.id, host_ids, (size_t)n * sizeof(int32_t));
+  return launch_k(swap_stage_kernel, dim3(n), dim3(256), 0, st, ids, n, (uint4*)pool, (uint4*)stage,
+                  block_bytes / 16, to_stage ? 1 : 0);
+}
+}  // namespace s2l

@@ -120,6 +120,12 @@ cudaError_t launch_append_inline(const Geometry& g, const InlineBlob& blob, int3
                                  const void* k, const void* v, int64_t kv_rows, void* pool,
                                  cudaStream_t st, int32_t layer0 = 0, int32_t nl = 0);
 
+// Swap staging (a5 / a6 with scattered GPU ids): copies GPU blocks ids[0..n) of the pool
+// into consecutive block slots of `stage` (to_stage) or back (scatter), on stream st.
+constexpr int kSwapIdsPerLaunch = 1024;
+cudaError_t launch_swap_stage(const int32_t* host_ids, int32_t n, void* pool, void* stage, int64_t block_bytes,
+                              bool to_stage, cudaStream_t st);
+
 // CUDA-core attention for any geometry (one warp per (query row, q head)).
 cudaError_t launch_attn_generic(const Geometry& g, const AttnItemDev* items, int32_t n_items,
                                 int64_t total_q, const int32_t* table, int32_t layer,

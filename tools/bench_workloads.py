@@ -149,43 +149,27 @@ def c5():
 
 
 def c4():
+    """C4 swap microbench: B in {1, 8, 64, 512} blocks x M_block at L in
+    {1, 8, 32} (64 KiB, 512 KiB, 2 MiB), contiguous and scattered (random) GPU ids, with the
+    staged path for scattered ids on and off (S2L_SWAP_STAGE), vs the measured link."""
+    from bench import swap_cell
     link = measure_link("cuda")
     out = {"workload": "C4 swap microbench (BJ:L10)", "link_h2d_gbs": link["h2d"], "link_d2h_gbs": link["d2h"], "cells": []}
-    for L in (1, 8, 32):
-        for B in (1, 8, 64, 512):
-            cfg = s2l.make_config(L, 32, 8, 128, 16, 2 * B + 8, 2 * B + 8, max_requests=4, max_blocks_per_request=2 * B + 8)
-            mb = s2l.block_bytes(cfg)
-            if B * mb > (1 << 30) + 1:
-                continue
-            gp = torch.empty((2 * B + 8) * mb // 2, dtype=torch.bfloat16, device="cuda")
-            cp = torch.empty((2 * B + 8) * mb // 2, dtype=torch.bfloat16).pin_memory()
-            cs, cs_in = torch.cuda.Stream(), torch.cuda.Stream()     # swap-out / swap-in streams
-            ctx = s2l.Context(cfg, gp, cp, torch.cuda.current_stream(), cs, swap_in_stream=cs_in)
-            # two interleaved requests -> scattered ids for request 0 (B blocks)
-            kv = torch.zeros(L, 32, 8, 128, dtype=torch.bfloat16, device="cuda")
-            ctx.new_request(0, np.zeros(B * 16, np.int32))
-            ctx.new_request(1, np.zeros(B * 16, np.int32))
-            for _ in range(B // 2 if B > 1 else 1):
-                ctx.append_chunk([(0, None, min(32, B * 16 - ctx.query(0)["num_computed"]), 0),
-                                  (1, None, min(32, B * 16 - ctx.query(1)["num_computed"]), 0)], kv, kv)
-            ctx.sync()
-            nblk = ctx.query(0)["num_blocks"]
-            best = {}
-            for _ in range(3):
-                e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
-                e0.record(cs)
-                b_out = ctx.swap_out([0])
-                e1.record(cs)
-                ctx.sync()
-                e2.record(cs_in)
-                ctx.swap_in([0])
-                e3.record(cs_in)
-                ctx.sync()
-                for key, ms in (("out", e0.elapsed_time(e1)), ("in", e2.elapsed_time(e3))):
-                    best[key] = max(best.get(key, 0), b_out / (ms * 1e-3) / 1e9)
-            out["cells"].append({"L": L, "m_block": mb, "blocks": nblk, "bytes": b_out, "out_gbs": best["out"],
-                                 "in_gbs": best["in"], "out_frac": best["out"] / link["d2h"], "in_frac": best["in"] / link["h2d"]})
-            ctx.close()
+    for stage in ("1", "0"):
+        os.environ["S2L_SWAP_STAGE"] = stage
+        for L in (1, 8, 32):
+            for B in (1, 8, 64, 512):
+                if B * 2 * L * 16 * 8 * 128 * 2 > (1 << 30):
+                    continue
+                for scattered in (False, True):
+                    if stage == "0" and not scattered:
+                        continue
+                    cl = swap_cell(0, L, B, scattered)
+                    cl["staged_path"] = stage == "1"
+                    cl["out_frac"] = cl["out_gbs"] / link["d2h"]
+                    cl["in_frac"] = cl["in_gbs"] / link["h2d"]
+                    out["cells"].append(cl)
+    os.environ.pop("S2L_SWAP_STAGE", None)
     return out
 
 
