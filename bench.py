@@ -793,7 +793,8 @@ def c4_mode(args, rank, world, dist, dev_index, pk):
     from synth import workloads as W
     L, budget = 8, 8192
     seed = W.seed_of(4)
-    plans = [p for p in pressure.c4_plans(seed, 128, budget=budget) if p.rid % world == rank]
+    n_req = int(os.environ.get("S2L_C4_REQUESTS", "128"))   # 128 = BJ:L10; smaller for plumbing tests
+    plans = [p for p in pressure.c4_plans(seed, n_req, budget=budget) if p.rid % world == rank]
     ws = pressure.working_set_blocks(plans, KB)
     ng, ncpu = ws // 2, ws
     cfg = s2l.make_config(L, H_Q, H_KV, D, KB, ng, ncpu, max_requests=len(plans),
@@ -850,7 +851,7 @@ def c4_mode(args, rank, world, dist, dev_index, pk):
             "n_gpus": world, "steps": args.steps, "warmup": 1, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "C4 (BJ:L10) memory-pressure mix: 128 append/update requests sharded by request, "
-                                   "GPU pool 50% of the working set, KV swap to pinned host", "requests": 128,
+                                   "GPU pool 50% of the working set, KV swap to pinned host", "requests": n_req,
                        "layers": L, "m_block": mb, "parallelism": f"request-sharded x{world}"},
             "attn_tflops": fl_all / (ms_max * 1e-3) / 1e12,
             "swap": {"out_bytes": out_all, "in_bytes": in_all,

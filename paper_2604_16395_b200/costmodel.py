@@ -24,8 +24,10 @@ from dataclasses import dataclass, field
 
 @dataclass
 class PiecewiseLinear:
-    """y(x) through measured points (x sorted ascending): linear interpolation inside, the end
-    segments' slopes outside ("fit a piecewise-linear model")."""
+    """y(x) through measured points (x sorted ascending): linear interpolation inside
+    ("fit a piecewise-linear model"), the last segment's slope above the last sample,
+    and below the first sample the line through the origin to it (a zero-length
+    recompute or swap costs nothing; the paper profiles 1K-128K tokens only)."""
     xs: list
     ys: list
 
@@ -40,6 +42,8 @@ class PiecewiseLinear:
 
     def __call__(self, x: float) -> float:
         xs, ys = self.xs, self.ys
+        if x < xs[0] and xs[0] > 0:
+            return ys[0] * max(x, 0.0) / xs[0]
         i = bisect.bisect_right(xs, x) - 1
         i = min(max(i, 0), len(xs) - 2)
         x0, x1, y0, y1 = xs[i], xs[i + 1], ys[i], ys[i + 1]

@@ -5,9 +5,15 @@ Host side, like the paper's (a vLLM scheduler extension).  One `step()`:
   Phase 1 — priority ordering and feasibility: the policy (§4.4) ranks every
   unfinished request that has pending tokens; walking that order, each request gets
   min(pending, budget left) tokens (budget-clamped partial chunks) if its block estimate fits.
-  Reading Z18: "sufficient free GPU blocks remain" counts blocks that are free or held by
-  requests Phase 2 may preempt, i.e. the selected requests' total demand must fit the pool;
-  requests that do not fit, or that the token budget leaves out, go to `not_scheduled` in
+  What "sufficient free GPU blocks remain" counts is a reading (`feasibility=`):
+    "pool" (Z18, default): blocks that are free or held by requests Phase 2 may preempt, i.e.
+           the selected requests' total demand must fit the pool;
+    "free" (the SPEC's rule): projected free blocks start at the pool's free
+           count and each candidate's NEW blocks (+ its CPU blocks if it needs a swap-in) are
+           taken from them; preemption opportunities are left to Phase 2.  When nothing fits
+           (every block held by requests that all need more -- a deadlock under this rule
+           alone) the highest-priority request that fits the pool goes to Phase 2.
+  Requests that do not fit, or that the token budget leaves out, go to `not_scheduled` in
   priority order.  No state changes.
   Phase 2 — resource acquisition with adaptive preemption: for each selected request
   in priority order, while the GPU pool is short, preempt the lowest-priority request of
@@ -21,7 +27,9 @@ with tokens and no K/V); an update-mode chunk replaces it (s2l_invalidate_lcp: L
 invalidation, also on the CPU tier).  Non-streaming (vLLM-NS) requests become
 visible only when their whole input has arrived.
 
-Policies (§4.4; eviction is always reverse priority among `not_scheduled`):
+Policies (§4.4; eviction is reverse priority among `not_scheduled` -- except DEFAULT with
+`default_lifo=True` (§4.4.1 "LIFO eviction"): the last request of the running order
+that holds GPU blocks and is not being placed this step):
   DEFAULT  vLLM: running requests in their execution order, then waiting requests FIFO by
            arrival with preempted ones re-queued at the front (P:L217-L219);
   FCFS     two tiers, complete inputs first, each by arrival time (P:L223);
@@ -67,13 +75,17 @@ class SReq:
 
 class StreamingScheduler:
     def __init__(self, ctx, policy: str, block_size: int, budget: int, num_gpu_blocks: int,
-                 cost_model=None, preemption: str = "cost", streaming: bool = True):
+                 cost_model=None, preemption: str = "cost", streaming: bool = True,
+                 feasibility: str = "pool", default_lifo: bool = False):
         if policy not in POLICIES:
             raise ValueError(f"policy {policy} not in {POLICIES}")
         if preemption not in ("cost", "recompute", "swap"):
             raise ValueError("preemption must be cost | recompute | swap")
         if preemption == "cost" and cost_model is None:
             raise ValueError("cost-based preemption needs a cost model")
+        if feasibility not in ("pool", "free"):
+            raise ValueError("feasibility must be pool | free")
+        self.feasibility, self.default_lifo = feasibility, default_lifo
         self.ctx, self.policy, self.k, self.budget = ctx, policy, block_size, budget
         self.num_gpu_blocks = num_gpu_blocks
         self.cm, self.preemption, self.streaming = cost_model, preemption, streaming
@@ -158,18 +170,40 @@ class StreamingScheduler:
         selected, not_sched = [], []
         budget = self.budget
         reserved = 0
+        free = self._free_now()                   # "free": projected free blocks
         for r in order:
             n = min(self._pending(r, info[r]), budget)
-            total = self._blocks(info[r]["num_computed"] + n) if n > 0 else 0
-            if n > 0 and reserved + total <= self.num_gpu_blocks:
+            if self.feasibility == "pool":
+                total = self._blocks(info[r]["num_computed"] + n) if n > 0 else 0
+                fits = reserved + total <= self.num_gpu_blocks
+            else:
+                q = info[r]
+                total = (self._blocks(q["num_computed"] + n) - q["num_blocks"] +
+                         (q["num_blocks"] if q["tier"] == TIER_CPU else 0)) if n > 0 else 0
+                fits = total <= free
+            if n > 0 and fits:
                 selected.append((r, n))
                 reserved += total
+                free -= total if self.feasibility == "free" else 0
                 budget -= n
             else:
                 not_sched.append(r)
+        if not selected and self.feasibility == "free":
+            # the free-block rule alone can deadlock (every block held by requests that all
+            # need more); Phase 2 is given the highest-priority request that fits the pool
+            for i, r in enumerate(not_sched):
+                n = min(self._pending(r, info[r]), self.budget)
+                if n > 0 and self._blocks(info[r]["num_computed"] + n) <= self.num_gpu_blocks:
+                    selected.append((r, n))
+                    del not_sched[i]
+                    break
         # ---- Phase 2: acquisition with preemption (victims: not_sched, lowest priority first)
         out = []
         victims = list(reversed(not_sched))
+        if self.policy == "DEFAULT" and self.default_lifo:
+            # LIFO over the running order, never a request placed in this step
+            placing = {r for r, _ in selected}
+            victims = [x for x in reversed(self.running) if x not in placing]
         claimed = 0                      # new blocks the appends of placed requests will take
         for r, n in selected:
             q = self.ctx.query(r)

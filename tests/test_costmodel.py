@@ -12,7 +12,8 @@ def test_piecewise_linear_interpolates_and_extrapolates():
     f = PiecewiseLinear([1000, 2000, 4000], [1.0, 3.0, 4.0])
     assert f(1000) == 1.0 and f(2000) == 3.0 and f(4000) == 4.0
     assert f(1500) == 2.0 and f(3000) == 3.5
-    assert f(500) == 0.0           # first segment's slope
+    assert f(500) == 0.5           # below the first sample: through the origin
+    assert f(0) == 0.0
     assert f(6000) == 5.0          # last segment's slope
     with pytest.raises(ValueError):
         PiecewiseLinear([1, 1], [0, 0])

@@ -88,3 +88,66 @@ def test_kv_head_shard_reproduces_unsharded_oracle():
         assert np.array_equal(np.concatenate(parts, axis=1), full)
     with pytest.raises(ValueError):
         shard.kv_head_shard(0, 3, h_q, h_kv)
+
+
+def _c4_worker(rank, world, port, q):
+    """One rank of the request-sharded C4 mix: its requests (rid % world == rank) through the
+    pressure driver on a host-only libs2l context, every library call mirrored into the oracle
+    (tests.harness.Twin asserts bit-exact agreement); results gathered over gloo."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2604_16395_b200 import pressure, s2l
+        from tests.harness import Twin
+        k, budget = 16, 512
+        plans = [p for p in pressure.c4_plans(21, 24, lo=64, hi=1024, budget=budget) if p.rid % world == rank]
+        ws = pressure.working_set_blocks(plans, k)
+        biggest = max(-(-p.total // k) for p in plans)
+        ng = max(ws // 2, 3 * biggest + budget // k + 2)
+        nc = ws + 8
+        cfg = s2l.make_config(1, 1, 1, 8, k, ng, nc, max_requests=len(plans), max_blocks_per_request=biggest + 1,
+                              alloc_cooling=1)
+        lib = s2l.Context(cfg, host_only=True)
+        tw = Twin(lib, k, ng, nc, len(plans), biggest + 1)
+        drv = pressure.PressureDriver(tw, plans, k, budget)
+
+        def execute(sel, app, pre, rows):
+            assert all(r % world == rank for r in sel)      # a rank only touches its own shard
+            tw.append_chunk(app, None, None, kv_rows=rows)
+
+        steps = drv.run(execute)
+        stats = torch.tensor([float(drv.tokens), float(drv.swapped_out_bytes), float(steps)])
+        parts = [torch.zeros(3) for _ in range(world)]
+        dist.all_gather(parts, stats)
+        done = torch.zeros(24)
+        for p in plans:
+            done[p.rid] = 1.0
+        dist.all_reduce(done)
+        q.put((rank, [x.tolist() for x in parts], done.tolist(), ng < ws, tw.ops))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_c4_request_sharding_on_the_library():
+    """C4 sharded by request across 2 ranks (BJ:L10) with the library's host-only
+    contexts: each rank's shard is under memory pressure, every call agrees with the oracle, the
+    shards partition the 24 requests and the gathered token totals equal the workload's."""
+    from paper_2604_16395_b200 import pressure
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_c4_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    plans = pressure.c4_plans(21, 24, lo=64, hi=1024, budget=512)
+    want_tokens = sum(w.n_kv for p in plans for w in p.work)
+    for rank, parts, done, pressured, ops in res:
+        assert pressured and ops > 0
+        assert done == [1.0] * 24                         # every request on exactly one rank
+        assert sum(x[0] for x in parts) == want_tokens
+        assert sum(x[1] for x in parts) > 0               # swaps happened on the shards
+    assert res[0][1] == res[1][1]                         # both ranks gathered the same stats

@@ -189,3 +189,76 @@ def test_trace_marginals():
     assert np.mean([c <= 3 for c in cnt.values()]) > 0.5     # majority 1-3 chunks (Fig. 7)
     tot = [len(e[4]) for e in an if e[4] is not None]
     assert 7000 < np.median(tot) < 13000                      # median ~10K (Table 2)
+
+
+def test_spec_free_block_feasibility_example():
+    """S:L325 / S:L330 (feasibility="free"): projected free blocks start at the pool's free
+    count; a request needing 10 blocks with 9 projected free goes to not_scheduled, a later
+    one needing 9 is still a candidate.  Under the default Z18 reading ("pool") both are
+    selected and Phase 2 preempts the idle holder to place the first."""
+    for rule in ("free", "pool"):
+        ng = 20
+        ctx = _ctx(ng, 64)
+        sch = S.StreamingScheduler(ctx, "FCFS", 16, 1 << 20, ng, preemption="swap", feasibility=rule)
+        run = _exec(ctx)
+        sch.on_chunk(0.0, 0, 2, tokens=np.arange(16 * 11))   # holder: 11 blocks, then waits for input
+        items = sch.step(0.1)
+        run(items)
+        sch.finish_step(0.1, items)
+        assert ctx.free_blocks()[0] == 9
+        sch.on_chunk(0.2, 1, 1, tokens=np.arange(16 * 10))   # needs 10 (complete, earlier)
+        sch.on_chunk(0.3, 2, 1, tokens=np.arange(16 * 9))    # needs 9
+        items = sch.step(0.4)
+        if rule == "free":
+            assert [r for r, _, _ in items] == [2]
+            assert not any(e[1].startswith("PREEMPTED") for e in sch.events)
+        else:
+            assert [r for r, _, _ in items][0] == 1
+            assert any(e[1] == "PREEMPTED_SWAP" and e[2] == 0 for e in sch.events)
+
+
+def test_default_lifo_eviction_over_running_order():
+    """DEFAULT with default_lifo (§4.4.1): the victim is the LAST request of the running
+    order holding GPU blocks, not the lowest-priority entry of not_scheduled."""
+    ng = 40
+    ctx = _ctx(ng, 256)
+    sch = S.StreamingScheduler(ctx, "DEFAULT", 16, 1 << 20, ng, preemption="swap", default_lifo=True)
+    run = _exec(ctx)
+    sch.on_chunk(0.0, 0, 2, tokens=np.arange(16 * 12))
+    sch.on_chunk(0.1, 1, 2, tokens=np.arange(16 * 12))
+    items = sch.step(0.2)
+    run(items)
+    sch.finish_step(0.2, items)
+    assert sch.running == [0, 1]
+    sch.on_chunk(0.3, 0, 2, tokens=np.arange(16 * 14))      # r0 grows: needs 14 more, 16 free
+    sch.on_chunk(0.4, 2, 1, tokens=np.arange(16 * 10))      # a new request behind it
+    items = sch.step(0.5)
+    pre = [e[2] for e in sch.events if e[1] == "PREEMPTED_SWAP"]
+    assert pre and pre[0] == 1                                # last of the running order
+    assert 0 in [r for r, _, _ in items]
+
+
+@pytest.mark.parametrize("policy", ["DEFAULT", "FCFS"])
+def test_trace_under_spec_rules_completes(policy):
+    tr = traces.crawler_trace(6, 24, qps=4.0, hi=8192)
+    ctx = _ctx(900, 4096, max_req=25)
+    sch = S.StreamingScheduler(ctx, policy, 16, 2048, 900, cost_model=_cm(), preemption="cost",
+                               feasibility="free", default_lifo=True)
+    run = _exec(ctx)
+    t, i = 0.0, 0
+    while True:
+        while i < len(tr) and tr[i][0] <= t:
+            tc, rid, n, tok, new, mode = tr[i]
+            sch.on_chunk(tc, rid, n, tokens=tok, new_input=new, mode=mode)
+            i += 1
+        items = sch.step(t)
+        if not items:
+            if i >= len(tr):
+                break
+            t = tr[i][0]
+            continue
+        run(items)
+        t += 1e-3 + 1e-5 * sum(n for _, _, n in items)
+        sch.finish_step(t, items)
+    assert len(sch.ttfts()) == 24
+    assert ctx.lib.free_blocks() == (900, 4096)

@@ -97,7 +97,7 @@ def run(trace, policy, streaming, args, cm, pools):
     ctx = s2l.Context(cfg, gpool, cpool, torch.cuda.current_stream(), None)
     sch = S.StreamingScheduler(ctx, policy, K, args.budget, args.gpu_blocks, cost_model=cm,
                                preemption=args.preemption if cm is not None or args.preemption != "cost" else "recompute",
-                               streaming=streaming)
+                               streaming=streaming, feasibility=args.feasibility, default_lifo=args.default_lifo)
     model = DecoderModel(ctx, args.layers) if args.model else Model(ctx, args.layers, args.budget, args.gemm)
     t, i, steps, gpu_ms, host_s = 0.0, 0, 0, 0.0, 0.0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -145,6 +145,9 @@ def main():
     ap.add_argument("--cpu-blocks", type=int, default=8192)
     ap.add_argument("--delay-scale", type=float, default=1.0)
     ap.add_argument("--gemm", action="store_true")
+    ap.add_argument("--feasibility", choices=["pool", "free"], default="pool",
+                    help="Phase-1 rule: pool (reading Z18, the round-1 tables) or free (SPEC S:L325)")
+    ap.add_argument("--default-lifo", action="store_true", help="DEFAULT evicts LIFO over its running order (S:L335)")
     ap.add_argument("--model", action="store_true",
                     help="real decoder forward (random weights) through the per-layer fused API")
     ap.add_argument("--preemption", default="cost", choices=["cost", "recompute", "swap"])
