@@ -1199,7 +1199,7 @@ s2l_status s2l_block_table(s2l_ctx* c, int64_t id, int32_t* ids_out, int64_t cap
   if (!r) return fail(S2L_E_NO_REQUEST, "unknown request %lld", (long long)id);
   int64_t n = (int64_t)r->blocks.size();
   if (n_out) *n_out = n;
-  memcpy(ids_out, r->blocks.data(), (size_t)std::min(n, cap) * sizeof(int32_t));
+  if (n > 0 && cap > 0) memcpy(ids_out, r->blocks.data(), (size_t)std::min(n, cap) * sizeof(int32_t));
   return S2L_OK;
 }
 

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libs2l.so")
+# S2L_LIB selects another build of the same library (sanitizer builds, A/B experiments)
+LIB_PATH = os.environ.get("S2L_LIB") or os.path.join(_PKG, "libs2l.so")
 
 OK, E_INVAL, E_NO_GPU_BLOCKS, E_NO_CPU_BLOCKS, E_NO_REQUEST, E_STATE, E_CUDA, E_CAPACITY = 0, -1, -2, -3, -4, -5, -6, -7
 TIER_GPU, TIER_CPU = 0, 1
