@@ -15,6 +15,9 @@ Modules
                (P:L67-L77, P:L147-L149, P:L170-L184)                    pinned
   attention  — causal GQA softmax attention over the contiguous
                per-request K/V, fp64             pinned
+  fp8        — E4M3 codec of the optional FP8 KV cache (b = 1 instead
+               of the paper's 2), from the format's
+               definition                                               pinned
 
 Every function states the passage it follows.  Parity pins live in tests/ (-m "not gpu").
 """

@@ -41,6 +41,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import fp8 as _fp8
 from .attention import attention as _attention
 from .geometry import block_bytes, blocks_needed
 from .lcp import lcp
@@ -71,25 +72,31 @@ class Req:
 class OracleKV:
     def __init__(self, L, h_q, h_kv, d, k, num_gpu_blocks, num_cpu_blocks,
                  max_requests=1 << 30, max_blocks_per_request=1 << 30, lcp_block_aligned=False,
-                 mirror_pools=True, alloc_cooling=False):
+                 mirror_pools=True, alloc_cooling=False, kv_dtype="bf16"):
+        """kv_dtype "fp8" (the optional FP8 KV cache; not the paper's b = 2): K/V
+        are stored as E4M3 codes (oracle/fp8.py, b = 1); attention reads their exact values."""
         assert h_q % h_kv == 0
         self.L, self.h_q, self.h_kv, self.d, self.k = L, h_q, h_kv, d, k
         self.num_gpu_blocks, self.num_cpu_blocks = num_gpu_blocks, num_cpu_blocks
         self.max_requests, self.max_blocks = max_requests, max_blocks_per_request
         self.aligned = bool(lcp_block_aligned)
+        if kv_dtype not in ("bf16", "fp8"):
+            raise ValueError(kv_dtype)
+        self.fp8 = kv_dtype == "fp8"
         self.free = {GPU: set(range(num_gpu_blocks)), CPU: set(range(num_cpu_blocks))}
         self.cooling = bool(alloc_cooling)
         self.cool = set()   # alloc_cooling: GPU ids released by the latest swap-out, subset of free
         self.reqs: dict[int, Req] = {}
         self.mirror = mirror_pools
         shape = (L, 2, h_kv, k, d)
-        self.pool = {GPU: np.zeros((num_gpu_blocks,) + shape, np.uint16) if mirror_pools else None,
-                     CPU: np.zeros((num_cpu_blocks,) + shape, np.uint16) if mirror_pools else None}
+        pdt = np.uint8 if self.fp8 else np.uint16
+        self.pool = {GPU: np.zeros((num_gpu_blocks,) + shape, pdt) if mirror_pools else None,
+                     CPU: np.zeros((num_cpu_blocks,) + shape, pdt) if mirror_pools else None}
 
     # ---- helpers -------------------------------------------------------------------
     @property
     def m_block(self) -> int:
-        return block_bytes(self.L, self.k, self.h_kv, self.d)
+        return block_bytes(self.L, self.k, self.h_kv, self.d, b=1 if self.fp8 else 2)
 
     def _take_lowest(self, tier, n):
         """Z9: the n lowest free ids, ascending.  alloc_cooling variant: GPU ids released by
@@ -188,14 +195,20 @@ class OracleKV:
             r.blocks.extend(self._take_lowest(GPU, need))
             if n_kv:
                 self._ensure_cap(r, r.nc + n_kv)
-                r.Kc[:, r.nc:r.nc + n_kv] = k_rows[:, kv_row:kv_row + n_kv]
-                r.Vc[:, r.nc:r.nc + n_kv] = v_rows[:, kv_row:kv_row + n_kv]
+                kr, vr = k_rows[:, kv_row:kv_row + n_kv], v_rows[:, kv_row:kv_row + n_kv]
+                if self.fp8:                                # stored codes; attention reads their values
+                    kc, kr = _fp8.quantize_bf16_bits(kr)
+                    vc, vr = _fp8.quantize_bf16_bits(vr)
+                else:
+                    kc, vc = kr, vr
+                r.Kc[:, r.nc:r.nc + n_kv] = kr
+                r.Vc[:, r.nc:r.nc + n_kv] = vr
                 if self.mirror:
                     for t in range(n_kv):
                         pos = r.nc + t
                         blk, slot = r.blocks[pos // self.k], pos % self.k
-                        self.pool[GPU][blk, :, 0, :, slot, :] = k_rows[:, kv_row + t]
-                        self.pool[GPU][blk, :, 1, :, slot, :] = v_rows[:, kv_row + t]
+                        self.pool[GPU][blk, :, 0, :, slot, :] = kc[:, t]
+                        self.pool[GPU][blk, :, 1, :, slot, :] = vc[:, t]
             r.nc += n_kv
         return OK
 

@@ -252,3 +252,51 @@ def test_preempt_recompute_and_release():
     assert kv.free_counts() == (8, 8)
     assert kv.release(0) == O.OK and kv.release(0) == O.E_NO_REQUEST
     assert kv.new_request(0) == O.OK and kv.new_request(0) == O.E_STATE
+
+
+# ---- FP8 KV cache (the paper's b = 2, becomes 1) ----------------------
+def test_fp8_codec_pins():
+    """E4M3 (OCP FP8, 'FN'): values from the format's definition, RNE ties, saturation,
+    signed zero; the whole codec agrees with torch's float8_e4m3fn cast on in-range values."""
+    import torch
+    from oracle import fp8
+    t = fp8.decode_table()
+    assert t[0x38] == 1.0 and t[0x7E] == 448.0 and t[0xC0] == -2.0 and t[0x01] == 2.0 ** -9
+    assert t[0x08] == 2.0 ** -6 and t[0x07] == 7 * 2.0 ** -9 and np.isnan(t[0x7F]) and np.isnan(t[0xFF])
+    assert len(set(t[~np.isnan(t)].tolist())) == 253            # 254 finite codes, +0 == -0
+    x = np.array([1.0, 1.0625, 1.1875, 500.0, -1e9, 2.0 ** -10, 3 * 2.0 ** -11, -0.0, 448.0])
+    assert [int(c) for c in fp8.encode(x)] == [0x38, 0x38, 0x3A, 0x7E, 0xFE, 0x00, 0x01, 0x80, 0x7E]
+    c = np.arange(256, dtype=np.uint8)
+    fin = ~np.isnan(t)
+    assert np.array_equal(fp8.encode(t[fin]), c[fin])           # every finite code round-trips
+    rng = np.random.default_rng(0)
+    r = np.clip(rng.standard_normal(100000) * np.exp(rng.uniform(-8, 6, 100000)), -448, 448)
+    ref = torch.from_numpy(r.astype(np.float32)).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    assert np.array_equal(fp8.encode(r), ref)
+    # every E4M3 value is a bf16 value: the dequantized rows are exact bf16 bits
+    assert np.array_equal(fp8.bf16_bits_to_f64(fp8.f64_to_bf16_bits(t[fin])), t[fin])
+
+
+def test_fp8_kv_oracle_stores_codes_and_attends_on_their_values():
+    from oracle import fp8
+    rng = np.random.default_rng(3)
+    kv = OracleKV(1, 2, 1, 8, 4, 8, 8, kv_dtype="fp8")
+    assert kv.m_block == 2 * 1 * 4 * 1 * 8 * 1                   # b = 1 byte per value
+    k, v = _rows(rng, 1, 10, 1, 8), _rows(rng, 1, 10, 1, 8)
+    k = fp8.f64_to_bf16_bits(rng.standard_normal((1, 10, 1, 8)) * 3)   # finite, in range
+    v = fp8.f64_to_bf16_bits(rng.standard_normal((1, 10, 1, 8)))
+    kv.new_request(0, list(range(10)))
+    assert kv.append([(0, None, 10, 0)], k, v) == O.OK
+    kc, kd = fp8.quantize_bf16_bits(k)
+    blk = kv.block_table(0)
+    for pos in range(10):
+        assert np.array_equal(kv.pool[O.GPU][blk[pos // 4], :, 0, :, pos % 4, :], kc[:, pos])
+    assert np.array_equal(kv.reqs[0].Kc[:, :10], kd)
+    q = fp8.f64_to_bf16_bits(rng.standard_normal((10, 2, 8)))
+    st, o, _ = kv.prefill([(0, 0, 10, 0)], q)
+    from oracle.attention import attention
+    vq = fp8.quantize_bf16_bits(v)[1]
+    o_ref, _ = attention(q, kd[0], vq[0], 0)
+    assert st == O.OK and np.array_equal(o, o_ref)
+    st, b = kv.swap_out([0])
+    assert st == O.OK and b == 3 * kv.m_block
