@@ -796,7 +796,10 @@ def c4_mode(args, rank, world, dist, dev_index, pk):
     n_req = int(os.environ.get("S2L_C4_REQUESTS", "128"))   # 128 = BJ:L10; smaller for plumbing tests
     plans = [p for p in pressure.c4_plans(seed, n_req, budget=budget) if p.rid % world == rank]
     ws = pressure.working_set_blocks(plans, KB)
-    ng, ncpu = ws // 2, ws
+    # 50 % of the shard's working set, but at least what one step of its largest requests
+    # needs (small shards in plumbing runs; as tests/test_pressure.py)
+    biggest = max(-(-p.total // KB) for p in plans)
+    ng, ncpu = max(ws // 2, 3 * biggest + budget // KB + 2), ws
     cfg = s2l.make_config(L, H_Q, H_KV, D, KB, ng, ncpu, max_requests=len(plans),
                           max_blocks_per_request=16384 // KB, alloc_cooling=1)
     mb = s2l.block_bytes(cfg)

@@ -8,7 +8,8 @@
  *     PINNED host memory), both laid out as
  *         pool[block][layer][2 (0=K,1=V)][kv_head][slot (0..k-1)][head_dim]   bf16
  *     so one block is contiguous across layers and occupies
- *         M_block = 2 * L * k * h_kv * d * 2 bytes   (= P:L73 with d_model*h_kv/h = h_kv*d);
+ *         M_block = 2 * L * k * h_kv * d * b bytes   (= P:L73 with d_model*h_kv/h = h_kv*d;
+ *                                                     b = 2 for bf16, 1 for kv_dtype FP8);
  *   - a request table: per request its input tokens, num_computed_tokens (nc), tier
  *     (GPU or CPU), ordered block ids on that tier, total_tokens_invalidated;
  *   - a device block table [max_requests][max_blocks_per_request] int32 (library-owned)
@@ -80,6 +81,13 @@ typedef struct s2l_config {
                                      1 = round the kept prefix down to a block     */
   int32_t alloc_cooling;          /* 0 = plain lowest-free-id order (Z9, default);
                                      1 = GPU ids freed by the latest swap-out go last       */
+  int32_t kv_dtype;               /* 0 = bf16 K/V (b = 2 bytes per value; default);
+                                     1 = FP8 E4M3 K/V cache (b = 1, not the
+                                     paper's): s2l_append_chunk stores each bf16 value as the
+                                     nearest E4M3 code (RNE, saturating to +-448, reading
+                                     Z20), attention dequantizes it exactly to bf16 before
+                                     its MMAs; s2l_prefill_append then appends with a
+                                     separate launch (no in-kernel append)                  */
 } s2l_config;
 
 /* One request of an s2l_append_chunk call. */

@@ -7,17 +7,30 @@
 #include "s2l_internal.h"
 
 #include <cuda_bf16.h>
+#include <cuda_fp8.h>
 
 namespace s2l {
 namespace {
 
 __device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float(x); }
+// pool element e of a bf16 or an FP8 E4M3 pool (kv_dtype 1; exact dequantization)
+template <bool kFp8>
+__device__ __forceinline__ float kv_at(const void* pool, int64_t e) {
+  if constexpr (kFp8) {
+    __nv_fp8_e4m3 x;
+    x.__x = reinterpret_cast<const __nv_fp8_storage_t*>(pool)[e];
+    return float(x);
+  } else {
+    return bf2f(reinterpret_cast<const __nv_bfloat16*>(pool)[e]);
+  }
+}
 
+template <bool kFp8>
 __global__ void __launch_bounds__(128) attn_generic_kernel(
     const AttnItemDev* __restrict__ items, int32_t n_items, int64_t total_q,
     const int32_t* __restrict__ table, int32_t layer, const __nv_bfloat16* __restrict__ q,
     __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
-    const __nv_bfloat16* __restrict__ pool, int32_t L, int32_t h_q, int32_t h_kv, int32_t d,
+    const void* __restrict__ pool, int32_t L, int32_t h_q, int32_t h_kv, int32_t d,
     int32_t kb, int32_t max_blocks, float scale_log2) {
   const int32_t lane = threadIdx.x & 31;
   const int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -53,7 +66,7 @@ __global__ void __launch_bounds__(128) attn_generic_kernel(
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int dim = lane * per + c;
-      if (c < per && dim < d) s += qv[c] * bf2f(pool[kbase + dim]);
+      if (c < per && dim < d) s += qv[c] * kv_at<kFp8>(pool, kbase + dim);
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
@@ -65,7 +78,7 @@ __global__ void __launch_bounds__(128) attn_generic_kernel(
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int dim = lane * per + c;
-      const float vv = (c < per && dim < d) ? bf2f(pool[vbase + dim]) : 0.f;
+      const float vv = (c < per && dim < d) ? kv_at<kFp8>(pool, vbase + dim) : 0.f;
       acc[c] = acc[c] * alpha + p * vv;
     }
     m = m_new;
@@ -90,9 +103,14 @@ cudaError_t launch_attn_generic(const Geometry& g, const AttnItemDev* items, int
   if (blocks <= 0) return cudaSuccess;
   if (blocks > 0x7fffffffll) return cudaErrorInvalidValue;
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)g.d);
-  attn_generic_kernel<<<(unsigned)blocks, 128, 0, st>>>(
-      items, n_items, total_q, table, layer, (const __nv_bfloat16*)q, (__nv_bfloat16*)o, lse,
-      (const __nv_bfloat16*)pool, g.L, g.h_q, g.h_kv, g.d, g.k, g.max_blocks, scale_log2);
+  if (g.fp8)
+    attn_generic_kernel<true><<<(unsigned)blocks, 128, 0, st>>>(
+        items, n_items, total_q, table, layer, (const __nv_bfloat16*)q, (__nv_bfloat16*)o, lse,
+        pool, g.L, g.h_q, g.h_kv, g.d, g.k, g.max_blocks, scale_log2);
+  else
+    attn_generic_kernel<false><<<(unsigned)blocks, 128, 0, st>>>(
+        items, n_items, total_q, table, layer, (const __nv_bfloat16*)q, (__nv_bfloat16*)o, lse,
+        pool, g.L, g.h_q, g.h_kv, g.d, g.k, g.max_blocks, scale_log2);
   return cudaGetLastError();
 }
 

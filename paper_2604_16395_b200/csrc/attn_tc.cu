@@ -32,11 +32,6 @@
 #include <mutex>
 
 // Build-time variants (experiments; defaults are the measured best).
-#ifndef S2L_SPLIT_S
-#define S2L_SPLIT_S 0      // 1 = S(j+1) in two N=64 halves, keys 64-127 issued as soon as the
-                           // softmax has read S(j)'s upper half (round 1); 0 = whole N=128 S
-                           // MMAs and the stale-max pipelined softmax (round 2)
-#endif
 
 namespace s2l {
 namespace {
@@ -119,29 +114,53 @@ constexpr int kThreads = 384;
 constexpr int kRegLaunch = 168, kRegCtrl = 88, kRegSoftmax = 208;
 static_assert(128 * kRegCtrl + 256 * kRegSoftmax <= kThreads * kRegLaunch, "register pool");
 constexpr int kPolyPairsPer8 = S2L_POLY_PAIRS;   // of every 8 exp2 pairs, this many on the FMA pipe
-constexpr int WNST = 5;
-constexpr uint32_t WOFF_Q0 = 0;
-constexpr uint32_t WOFF_Q1 = kTileBytes;
-constexpr uint32_t WOFF_RING = 2 * kTileBytes;
-constexpr uint32_t WOFF_BAR = WOFF_RING + WNST * kTileBytes;
-// barriers: 0 Q_full, 1..WNST ring_full, WNST+1..2NST ring_empty, then S_full[2], P_full[2], O_fin[2]
-// P_full is split in two halves (keys 0-63 / 64-127) so the PV MMAs of the first half start
-// while the softmax still computes the second half.
-constexpr uint32_t WB_QF = 0, WB_RF = 1, WB_RE = 1 + WNST, WB_SF = 1 + 2 * WNST, WB_PF = WB_SF + 2,
-                   WB_PH = WB_PF + 2, WB_OF = WB_PH + 2, WB_QE = WB_OF + 2, WB_SR = WB_QE + 1,
-                   WB_SH = WB_SR + 2, WNBARS = WB_SH + 2;
-constexpr uint32_t WOFF_TMEM = WOFF_BAR + WNBARS * 8;
-constexpr uint32_t SMEM = WOFF_TMEM + 16 + 1024;
+// Shared-memory layout (bytes from the 1024-aligned base):
+//   Q tiles 0/1 | K/V ring of NST 32-KB bf16 tiles (K-major / MN-major SW128 images) |
+//   FP8 pools only: F8ST 16-KB staging slots for the E4M3 tiles TMA brings in (dense
+//   [128 keys][128 d] bytes), converted to the bf16 ring by warps 2-3 | mbarriers | TMEM addr.
+template <bool kFp8>
+struct Lay {
+  static constexpr int NST = kFp8 ? 4 : 5;
+  static constexpr int F8ST = kFp8 ? 2 : 0;
+  static constexpr uint32_t kF8Tile = 16384;
+  static constexpr uint32_t OFF_Q0 = 0, OFF_Q1 = kTileBytes, OFF_RING = 2 * kTileBytes;
+  static constexpr uint32_t OFF_F8 = OFF_RING + NST * kTileBytes;
+  static constexpr uint32_t OFF_BAR = OFF_F8 + F8ST * kF8Tile;
+  // barriers: Q_full, ring_full[NST], ring_empty[NST], S_full[2], P_full[2] (keys 0-63),
+  // P_half[2] (keys 64-127), O_fin[2], fp8 staging full[F8ST] / empty[F8ST]
+  static constexpr uint32_t B_QF = 0, B_RF = 1, B_RE = 1 + NST, B_SF = 1 + 2 * NST, B_PF = B_SF + 2,
+                            B_PH = B_PF + 2, B_OF = B_PH + 2, B_8F = B_OF + 2, B_8E = B_8F + F8ST,
+                            NBARS = B_8E + F8ST;
+  static constexpr uint32_t OFF_TMEM = OFF_BAR + NBARS * 8;
+  static constexpr uint32_t SMEM = OFF_TMEM + 16 + 1024;
+  static_assert(SMEM <= 232448, "shared memory");
+};
 }  // namespace v2
 
-// kFuse: the fused-append instantiation (NEXT-2); the plain one compiles without that code.
-template <bool kFuse>
+// two E4M3 codes (low byte first) -> bf16x2, exactly
+__device__ __forceinline__ uint32_t e4m3x2_to_bf16x2(uint16_t v) {
+  uint32_t h2;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(v));
+  float lo, hi;
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+      : "=f"(lo), "=f"(hi) : "r"(h2));
+  return pack_bf16(lo, hi);
+}
+
+// kFuse: the fused-append instantiation (NEXT-2); kFp8: K/V pool in FP8 E4M3 (kv_dtype 1).
+template <bool kFuse, bool kFp8>
 __global__ void __launch_bounds__(v2::kThreads, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_kv,
                     const __grid_constant__ CUtensorMap tmap_kv4,
                     const __grid_constant__ typename ParamsOf<kFuse>::T p) {
   using namespace v2;
+  using L = Lay<kFp8>;
+  constexpr int WNST = L::NST;
+  constexpr uint32_t WOFF_Q0 = L::OFF_Q0, WOFF_Q1 = L::OFF_Q1, WOFF_RING = L::OFF_RING, WOFF_BAR = L::OFF_BAR,
+                     WOFF_TMEM = L::OFF_TMEM;
+  constexpr uint32_t WB_QF = L::B_QF, WB_RF = L::B_RF, WB_RE = L::B_RE, WB_SF = L::B_SF, WB_PF = L::B_PF,
+                     WB_PH = L::B_PH, WB_OF = L::B_OF;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sb = smem_u32(smem);
@@ -192,7 +211,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(bar(WB_QF), 1);
     for (int s = 0; s < WNST; ++s) {
-      mbar_init(bar(WB_RF + s), 1);
+      mbar_init(bar(WB_RF + s), kFp8 ? 2 : 1);   // fp8: one arrival per converter warp
       mbar_init(bar(WB_RE + s), 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -201,9 +220,9 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       mbar_init(bar(WB_PH + i), 128);
       mbar_init(bar(WB_OF + i), 1);
     }
-    for (int q = 0; q < 2; ++q) {
-      mbar_init(bar(WB_SR + q), 128);   // split S: softmax q has read S keys 64-127
-      mbar_init(bar(WB_SH + q), 1);     // split S: S(j+1) keys 64-127 computed
+    for (int s = 0; s < L::F8ST; ++s) {
+      mbar_init(bar(L::B_8F + s), 1);
+      mbar_init(bar(L::B_8E + s), 2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
@@ -245,6 +264,41 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         return __ldg(trow + (b < nblk_valid ? b : 0));
       };
       int32_t next_id = (lane < nb_tile) ? load_id(0) : 0;
+      if constexpr (kFp8) {
+        // FP8 pool: E4M3 tiles (dense [128 keys][128 d] bytes) into the staging slots; warps
+        // 2-3 convert them into the bf16 ring the MMAs read
+        uint32_t r8 = 0;
+        for (int32_t j = 0; j < nT; ++j) {
+          const int32_t cur_id = next_id;
+          if (j + 1 < nT && lane < nb_tile) next_id = load_id(j + 1);
+          int32_t ids[8];
+#pragma unroll
+          for (int b = 0; b < 8; ++b) ids[b] = __shfl_sync(0xffffffffu, cur_id, b);
+          bool run = (jb + j + 1) * nb_tile <= nblk_valid;
+#pragma unroll
+          for (int b = 1; b < 8; ++b)
+            if (b < nb_tile) run = run && (ids[b] == ids[0] + b);
+#pragma unroll
+          for (int kind = 0; kind < 2; ++kind, ++r8) {
+            const uint32_t s = r8 % L::F8ST, ph = (r8 / L::F8ST) & 1;
+            mbar_wait(bar(L::B_8E + s), ph ^ 1);
+            if (lane == 0) {
+              mbar_expect_tx(bar(L::B_8F + s), L::kF8Tile);
+              const uint32_t dst = sb + L::OFF_F8 + s * L::kF8Tile;
+              if (run) {
+                tma_load_4d(dst, &tmap_kv4, bar(L::B_8F + s), 0, 0, lkh[kind], ids[0]);
+              } else {
+#pragma unroll
+                for (int b = 0; b < 8; ++b)
+                  if (b < nb_tile)
+                    tma_load_2d(dst + b * p.kb * 128, &tmap_kv, bar(L::B_8F + s), 0,
+                                ids[b] * rows_per_block + row_kv[kind]);
+              }
+            }
+            __syncwarp();
+          }
+        }
+      } else {
       uint32_t rp = 0;
       // fused append: blocks starting at or after q_pos come from the caller's rows; this unit
       // writes the blocks whose first position lies in its token range [wr_lo, wr_hi)
@@ -353,6 +407,52 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         }
       }
       if (kFuse && lane == 0) bulk_wait_all();
+      }
+    } else if (kFp8 && warp >= 2) {
+      // ================= FP8 -> bf16 converters (warps 2-3) =================
+      // Each E4M3 tile (TMA, dense [key][128 B]) becomes the bf16 K-major SW128 image the MMAs
+      // read: key r, d-half h, 16-byte chunk c at h*16 KB + r*128 + ((c ^ (r & 7)) << 4).
+      // E4M3 -> f16 -> f32 -> bf16 is exact (every E4M3 value is a bf16 value).
+      const int ct = threadIdx.x - 64;                    // 0..63
+      uint32_t r8 = 0, rp = 0;
+      for (int32_t j = 0; j < nT; ++j) {
+#pragma unroll 1
+        for (int kind = 0; kind < 2; ++kind, ++r8, ++rp) {
+          const uint32_t s8 = r8 % L::F8ST, s = rp % WNST;
+          mbar_wait(bar(L::B_8F + s8), (r8 / L::F8ST) & 1);
+          mbar_wait(bar(WB_RE + s), ((rp / WNST) & 1) ^ 1);
+          const uint32_t src = sb + L::OFF_F8 + s8 * L::kF8Tile;
+          const uint32_t dst = sb + WOFF_RING + s * kTileBytes;
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const uint32_t r = (uint32_t)(ct + 64 * i);
+#pragma unroll
+            for (uint32_t jj = 0; jj < 8; ++jj) {
+              const uint32_t jc = (jj + r) & 7;             // staggered: rows spread over banks
+              uint32_t f[4];
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(f[0]), "=r"(f[1]), "=r"(f[2]), "=r"(f[3])
+                           : "r"(src + r * 128 + jc * 16));
+              uint32_t o[8];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                o[2 * e] = e4m3x2_to_bf16x2((uint16_t)(f[e] & 0xffffu));
+                o[2 * e + 1] = e4m3x2_to_bf16x2((uint16_t)(f[e] >> 16));
+              }
+              const uint32_t h = jc >> 2, c = (jc & 3) * 2;  // d = 16 jc .. 16 jc + 15
+              const uint32_t row = dst + h * kAtom + r * 128;
+              st_shared_v4(row + ((c ^ (r & 7)) << 4), o[0], o[1], o[2], o[3]);
+              st_shared_v4(row + (((c + 1) ^ (r & 7)) << 4), o[4], o[5], o[6], o[7]);
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // visible to tcgen05
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(bar(WB_RF + s));
+            mbar_arrive(bar(L::B_8E + s8));
+          }
+        }
+      }
     } else if (warp == 1) {
       // ================= MMA issuer (whole warp, one elected lane issues) =================
       constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);
@@ -405,50 +505,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       issue_s(0, kslot);
       issue_s(1, kslot);
       mma_commit_elect(bar(WB_RE + kslot));
-#if S2L_SPLIT_S
-      // S_i(j+1) = Q_i K_{j+1}^T in two N = 64 halves.  Keys 64-127 land in S columns 64-127,
-      // which P_i(j) (bf16, columns 0-63) does not use: they are issued as soon as softmax i
-      // has read S_i(j)'s upper half, i.e. while it still works; keys 0-63 overwrite P_i(j)'s
-      // columns and follow PV_i(j) on the in-order tensor pipe.
-      constexpr uint32_t idesc_h = idesc_bf16(kBM, 64, 0, 0);
-      auto issue_s_half = [&](int i, uint32_t ks, int h, uint32_t done) {
-        const uint64_t kd = dk0 + ((ks * kTileBytes + h * 64 * 128) >> 4);   // key row 64h
-#pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint32_t off = ((kk >> 2) * kAtom + (kk & 3) * 32) >> 4;
-          mma_ss_elect(tmem + i * 128 + h * 64, dq[i] + off, kd + off, idesc_h, kk > 0);
-        }
-        mma_commit_elect(done);
-      };
-      for (int32_t j = 0; j < nT; ++j) {
-        const uint32_t vslot = next_full();
-        const bool more = j + 1 < nT;
-        uint32_t knext = 0;
-        if (more) {
-          knext = next_full();
-          mbar_wait(bar(WB_SR + 0), j & 1);
-          tc_fence_after();
-          issue_s_half(0, knext, 1, bar(WB_SH + 0));
-        }
-        issue_pv(0, vslot, j);
-        if (more) issue_s_half(0, knext, 0, bar(WB_SF + 0));
-        else mma_commit_elect(bar(WB_OF + 0));
-        if (more) {
-          mbar_wait(bar(WB_SR + 1), j & 1);
-          tc_fence_after();
-          issue_s_half(1, knext, 1, bar(WB_SH + 1));
-        }
-        issue_pv(1, vslot, j);
-        mma_commit_elect(bar(WB_RE + vslot));
-        if (more) {
-          issue_s_half(1, knext, 0, bar(WB_SF + 1));
-          mma_commit_elect(bar(WB_RE + knext));
-        } else {
-          mma_commit_elect(bar(WB_OF + 1));
-        }
-      }
-      if (false)
-#endif
       for (int32_t j = 0; j < nT; ++j) {
         const uint32_t vslot = next_full();
         issue_pv(0, vslot, j);
@@ -487,11 +543,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     for (int32_t j = 0; j < nT; ++j) {
       const bool tr = (warp & 3) == 0 && lane == 0;
       if (tr) TRACE(20, i, j);
-#if S2L_SPLIT_S
-      mbar_wait(j == 0 ? bar(WB_SF + i) : bar(WB_SH + i), j == 0 ? 0 : ((j - 1) & 1));
-#else
       mbar_wait(bar(WB_SF + i), j & 1);
-#endif
       tc_fence_after();
       if (tr) TRACE(21, i, j);
       const int64_t key0 = (int64_t)(jb + j) * kBN;
@@ -502,25 +554,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       float mt[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) mt[q] = -INFINITY;
-#if S2L_SPLIT_S
-      // upper half first: once it is in registers the MMA warp may compute S(j+1)'s upper half
-      tmem_ld32(tS + 64, sv + 64);
-      tmem_ld32(tS + 96, sv + 96);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(bar(WB_SR + i));
-      if (masked_tile) { max32<true>(sv + 64, vis, 64, mt); max32<true>(sv + 96, vis, 96, mt); }
-      else { max32<false>(sv + 64, vis, 64, mt); max32<false>(sv + 96, vis, 96, mt); }
-      if (j > 0) {
-        mbar_wait(bar(WB_SF + i), j & 1);              // lower half of S(j)
-        tc_fence_after();
-      }
-      tmem_ld32(tS, sv);
-      tmem_ld32(tS + 32, sv + 32);
-      tmem_wait_ld();
-      if (masked_tile) { max32<true>(sv, vis, 0, mt); max32<true>(sv + 32, vis, 32, mt); }
-      else { max32<false>(sv, vis, 0, mt); max32<false>(sv + 32, vis, 32, mt); }
-#else
       // Steady state (stale-max fast path): a tile after the first one of this CTA, with no
       // masked key and a finite running max in every row, is exponentiated against the running
       // max m_run straight away, chunk by chunk as its scores arrive from TMEM (p <= 2^8 as long
@@ -580,7 +613,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         if (masked_tile) { max32<true>(sv + 64, vis, 64, mt); max32<true>(sv + 96, vis, 96, mt); }
         else { max32<false>(sv + 64, vis, 64, mt); max32<false>(sv + 96, vis, 96, mt); }
       }
-#endif
       float mx = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])), fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7])));
       mx *= sl2;
       if (tr) TRACE(22, i, j);
@@ -745,7 +777,7 @@ bool attn_tc_supported(const Geometry& g) {
 }
 
 bool make_tmap_kv(void* out, const void* pool, int64_t num_blocks, int32_t L, int32_t h_kv,
-                  int32_t d, int32_t k, const char** err) {
+                  int32_t d, int32_t k, bool fp8, const char** err) {
   auto fn = encode_fn(err);
   if (!fn) return false;
   const int64_t total_rows = num_blocks * L * 2 * h_kv * k;
@@ -753,32 +785,37 @@ bool make_tmap_kv(void* out, const void* pool, int64_t num_blocks, int32_t L, in
     *err = "pool has >= 2^31 rows";
     return false;
   }
-  // (1) per-block map: the pool as [rows][d], box {64, k} = one (block, layer, K|V, head) d-half
+  // bf16 pools: boxes of one d-half (64 values = 128 B) in the SWIZZLE_128B image the MMAs
+  // read; FP8 pools: boxes of the whole row (128 values = 128 B), dense, for the converters
+  const CUtensorMapDataType dt = fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const CUtensorMapSwizzle sw = fp8 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B;
+  const cuuint64_t es = fp8 ? 1 : 2;
+  const cuuint32_t bx = fp8 ? 128 : 64;
+  // (1) per-block map: the pool as [rows][d], box {bx, k} = one (block, layer, K|V, head) row set
   {
     cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)total_rows};
-    cuuint64_t strides[1] = {(cuuint64_t)d * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)k};
+    cuuint64_t strides[1] = {(cuuint64_t)d * es};
+    cuuint32_t box[2] = {bx, (cuuint32_t)k};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn((CUtensorMap*)out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (void*)pool, dims,
-                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = fn((CUtensorMap*)out, dt, 2, (void*)pool, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       *err = "cuTensorMapEncodeTiled(pool, per block) failed";
       return false;
     }
   }
-  // (2) run map: the pool as [block][L*2*h_kv][k][d], box {64, k, 1, 128/k} = one d-half of a
-  //     whole 128-key tile when the tile's blocks have consecutive ids (the common case with
-  //     the lowest-free-id allocator): rows land contiguous, exactly like 128/k per-block boxes.
+  // (2) run map: the pool as [block][L*2*h_kv][k][d], box {bx, k, 1, 128/k} = a whole 128-key
+  //     tile (bf16: one d-half of it) when the tile's blocks have consecutive ids (the common
+  //     case with the lowest-free-id allocator): rows land exactly like 128/k per-block boxes.
   {
     const int32_t R = 128 / k;
     cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)k, (cuuint64_t)L * 2 * h_kv, (cuuint64_t)num_blocks};
-    cuuint64_t strides[3] = {(cuuint64_t)d * 2, (cuuint64_t)k * d * 2, (cuuint64_t)L * 2 * h_kv * k * d * 2};
-    cuuint32_t box[4] = {64, (cuuint32_t)k, 1, (cuuint32_t)(R > 0 ? R : 1)};
+    cuuint64_t strides[3] = {(cuuint64_t)d * es, (cuuint64_t)k * d * es, (cuuint64_t)L * 2 * h_kv * k * d * es};
+    cuuint32_t box[4] = {bx, (cuuint32_t)k, 1, (cuuint32_t)(R > 0 ? R : 1)};
     cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = fn((CUtensorMap*)((char*)out + 128), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void*)pool,
-                    dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = fn((CUtensorMap*)((char*)out + 128), dt, 4, (void*)pool, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       *err = "cuTensorMapEncodeTiled(pool, block runs) failed";
       return false;
@@ -843,9 +880,11 @@ static cudaError_t ensure_smem_attr() {
   if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
   std::lock_guard<std::mutex> lk(mu);
   if (done[dev]) return cudaSuccess;
-  e = cudaFuncSetAttribute(attn_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM);
+  e = cudaFuncSetAttribute(attn_tc2_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::Lay<false>::SMEM);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(attn_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::SMEM);
+    e = cudaFuncSetAttribute(attn_tc2_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::Lay<false>::SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(attn_tc2_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, v2::Lay<true>::SMEM);
   if (e == cudaSuccess) done[dev] = true;
   return e;
 }
@@ -909,8 +948,10 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
   p.ws = ws;
   p.ws_ml = ws ? ws + (int64_t)max_pieces * 2 * 128 * kD : nullptr;
   p.ws_cnt = ws_cnt;
-  if (fuse) return launch_k(attn_tc2_kernel<true>, dim3(grid), dim3(v2::kThreads), v2::SMEM, st, tq, tkv, tkv4, pf);
-  return launch_k(attn_tc2_kernel<false>, dim3(grid), dim3(v2::kThreads), v2::SMEM, st, tq, tkv, tkv4, p);
+  if (fuse && g.fp8) return cudaErrorInvalidValue;   // no in-kernel append into an FP8 pool
+  if (fuse) return launch_k(attn_tc2_kernel<true, false>, dim3(grid), dim3(v2::kThreads), v2::Lay<false>::SMEM, st, tq, tkv, tkv4, pf);
+  if (g.fp8) return launch_k(attn_tc2_kernel<false, true>, dim3(grid), dim3(v2::kThreads), v2::Lay<true>::SMEM, st, tq, tkv, tkv4, p);
+  return launch_k(attn_tc2_kernel<false, false>, dim3(grid), dim3(v2::kThreads), v2::Lay<false>::SMEM, st, tq, tkv, tkv4, p);
 }
 
 }  // namespace s2l

@@ -51,11 +51,28 @@ __device__ __forceinline__ int32_t find_item(const AppendItemDev* items, int32_t
 #endif
 constexpr int kRowsPerWarp = S2L_APPEND_ROWS;
 
+// 8 bf16 -> 8 E4M3 codes (FP8 KV cache, kv_dtype 1): round to nearest even, saturating to
+// +-448 (reading Z20; the same rule as oracle/fp8.py); low element in the low byte.
+__device__ __forceinline__ uint2 bf16x8_to_e4m3x8(uint4 v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  uint32_t o[2] = {0, 0};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xffff0000u);
+    uint16_t c;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(c) : "f"(hi), "f"(lo));
+    o[i >> 1] |= (uint32_t)c << (16 * (i & 1));
+  }
+  return make_uint2(o[0], o[1]);
+}
+
 // kMaxVecPerLane >= vectors per lane per row (vpt/32: 4 at Llama-3 h_kv 8, d 128).
 // kVpr = d/8 vectors per head row when known at compile time (16 at d = 128), else 0.
 // Descriptors either through device pointers (staging ring) or, when blob_mode != 0, from
 // the kernel's by-value parameter blob (items at 0, ids at off_ids, patches at off_patch).
-template <int kMaxVecPerLane, int kVpr>
+// kFp8: the pool holds E4M3 codes (1 byte per value): vector index i of 8 values is the uint2
+// at i (instead of the uint4 at i).
+template <int kMaxVecPerLane, int kVpr, bool kFp8>
 __global__ void __launch_bounds__(256) append_kernel(
     const AppendItemDev* __restrict__ items_p, int32_t n_items, int64_t total_rows,
     const int32_t* __restrict__ ids_p, int32_t n_ids, const TablePatch* __restrict__ patches_p,
@@ -121,7 +138,9 @@ __global__ void __launch_bounds__(256) append_kernel(
         if (gi < vpt) {
           const int32_t vpr = kVpr ? kVpr : vec_per_row;
           const int32_t head = gi / vpr, vec = gi - head * vpr;
-          pool[dst_row[rr] + (int64_t)head * kb * vpr + vec] = val[rr][u];
+          const int64_t di = dst_row[rr] + (int64_t)head * kb * vpr + vec;
+          if constexpr (kFp8) reinterpret_cast<uint2*>(pool)[di] = bf16x8_to_e4m3x8(val[rr][u]);
+          else pool[di] = val[rr][u];
         }
       }
     }
@@ -165,7 +184,11 @@ cudaError_t launch_append_impl(const Geometry& g, const AppendItemDev* items, in
   if (nl <= 0) nl = g.L;
   dim3 grid((unsigned)blocks, nl * 2);
 #define S2L_APPEND(MAXV, VPR)                                                                     \
-  e = launch_k(append_kernel<MAXV, VPR>, grid, dim3(256), 0, st, items, n_items, total_rows, ids,   \
+  e = g.fp8 ? launch_k(append_kernel<MAXV, VPR, true>, grid, dim3(256), 0, st, items, n_items, total_rows, ids, \
+               n_ids, patches, n_patches, table, (const uint4*)k, (const uint4*)v, kv_rows,         \
+               (uint4*)pool, g.L, g.h_kv, vec_per_row, kb_log2, blob, blob_mode, off_ids, off_patch, \
+               layer0)                                                                               \
+            : launch_k(append_kernel<MAXV, VPR, false>, grid, dim3(256), 0, st, items, n_items, total_rows, ids,   \
                n_ids, patches, n_patches, table, (const uint4*)k, (const uint4*)v, kv_rows,         \
                (uint4*)pool, g.L, g.h_kv, vec_per_row, kb_log2, blob, blob_mode, off_ids, off_patch, \
                layer0)

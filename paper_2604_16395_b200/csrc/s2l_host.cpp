@@ -265,6 +265,8 @@ s2l_status check_config(const s2l_config* cfg) {
     return fail(S2L_E_INVAL, "lcp_block_aligned must be 0 or 1");
   if (g.alloc_cooling != 0 && g.alloc_cooling != 1)
     return fail(S2L_E_INVAL, "alloc_cooling must be 0 or 1");
+  if (g.kv_dtype != 0 && g.kv_dtype != 1)
+    return fail(S2L_E_INVAL, "kv_dtype must be 0 (bf16) or 1 (fp8 e4m3)");
   return S2L_OK;
 }
 
@@ -279,7 +281,7 @@ s2l_status init_common(s2l_ctx* c, const s2l_config* cfg) {
   c->h_table.assign((size_t)cfg->max_requests * cfg->max_blocks_per_request, -1);
   c->dirty_flag.assign(c->h_table.size(), 0);
   c->geo = s2l::Geometry{cfg->num_layers, cfg->num_q_heads, cfg->num_kv_heads, cfg->head_dim,
-                         cfg->block_size, cfg->max_blocks_per_request};
+                         cfg->block_size, cfg->max_blocks_per_request, cfg->kv_dtype == 1};
   return S2L_OK;
 }
 
@@ -603,7 +605,7 @@ int64_t s2l_block_bytes(const s2l_config* cfg) {
   if (!cfg || cfg->num_layers < 1 || cfg->num_kv_heads < 1 || cfg->head_dim < 1 ||
       cfg->block_size < 1)
     return -1;
-  return 2ll * cfg->num_layers * cfg->block_size * cfg->num_kv_heads * cfg->head_dim * 2ll;
+  return 2ll * cfg->num_layers * cfg->block_size * cfg->num_kv_heads * cfg->head_dim * (cfg->kv_dtype == 1 ? 1ll : 2ll);
 }
 
 s2l_status s2l_create_host_only(const s2l_config* cfg, s2l_ctx** out) {
@@ -664,7 +666,7 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
   if (c->tc_ok && cfg->num_gpu_blocks > 0) {
     const char* err = nullptr;
     if (!s2l::make_tmap_kv(c->tmap_kv, gpu_pool, cfg->num_gpu_blocks, cfg->num_layers,
-                           cfg->num_kv_heads, cfg->head_dim, cfg->block_size, &err))
+                           cfg->num_kv_heads, cfg->head_dim, cfg->block_size, c->geo.fp8, &err))
       return fail(S2L_E_CUDA, "tensor map (pool): %s", err ? err : "?");
   } else {
     c->tc_ok = false;
@@ -1016,7 +1018,7 @@ static s2l_status prefill_impl(s2l_ctx* c, int32_t layer, int32_t n_items,
   if (append) {
     if (!v) return fail(S2L_E_INVAL, "k/v is NULL");
     std::unordered_set<int64_t> seen;
-    const bool kern = c->tc_ok;
+    const bool kern = c->tc_ok && !c->geo.fp8;   // no in-kernel append into an FP8 pool
     int32_t aligned = 0;
     for (int32_t i = 0; i < n_items; ++i) {
       if (!seen.insert(items[i].req_id).second)

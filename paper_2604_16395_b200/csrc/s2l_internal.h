@@ -94,6 +94,7 @@ struct InlinePatches {
 struct Geometry {
   int32_t L, h_q, h_kv, d, k;
   int32_t max_blocks;  // columns of the device block table
+  bool fp8 = false;    // K/V stored as FP8 E4M3 (s2l_config.kv_dtype = 1): 1 byte per value
 };
 
 // ---- kernel launchers (kernels_*.cu) ----------------------------------------------------
@@ -169,6 +170,6 @@ bool make_tmap_in(void* out512, const void* k, const void* v, int64_t rows, int3
                   int32_t d, int32_t kb, const char** err);
 // Maps of the pool into out256: [0,128) per-block boxes, [128,256) 128-key block runs.
 bool make_tmap_kv(void* out256, const void* pool, int64_t num_blocks, int32_t L, int32_t h_kv,
-                  int32_t d, int32_t k, const char** err);
+                  int32_t d, int32_t k, bool fp8, const char** err);
 
 }  // namespace s2l

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("S2L_LIB") or os.path.join(_PKG, "libs2l.so")
 
 OK, E_INVAL, E_NO_GPU_BLOCKS, E_NO_CPU_BLOCKS, E_NO_REQUEST, E_STATE, E_CUDA, E_CAPACITY = 0, -1, -2, -3, -4, -5, -6, -7
 TIER_GPU, TIER_CPU = 0, 1
+KV_BF16, KV_FP8 = 0, 1
 STATUS_NAMES = {0: "OK", -1: "E_INVAL", -2: "E_NO_GPU_BLOCKS", -3: "E_NO_CPU_BLOCKS",
                 -4: "E_NO_REQUEST", -5: "E_STATE", -6: "E_CUDA", -7: "E_CAPACITY"}
 
@@ -33,7 +34,7 @@ class Config(C.Structure):
                 ("head_dim", C.c_int32), ("block_size", C.c_int32), ("num_gpu_blocks", C.c_int32),
                 ("num_cpu_blocks", C.c_int32), ("max_requests", C.c_int32),
                 ("max_blocks_per_request", C.c_int32), ("lcp_block_aligned", C.c_int32),
-                ("alloc_cooling", C.c_int32)]
+                ("alloc_cooling", C.c_int32), ("kv_dtype", C.c_int32)]
 
 
 class AppendItem(C.Structure):
@@ -125,12 +126,12 @@ def _stream(s):
 
 def make_config(num_layers, num_q_heads, num_kv_heads, head_dim, block_size, num_gpu_blocks,
                 num_cpu_blocks, max_requests=256, max_blocks_per_request=None, lcp_block_aligned=0,
-                alloc_cooling=0):
+                alloc_cooling=0, kv_dtype=0):
     if max_blocks_per_request is None:
         max_blocks_per_request = max(1, num_gpu_blocks + num_cpu_blocks)
     return Config(num_layers, num_q_heads, num_kv_heads, head_dim, block_size, num_gpu_blocks,
                   num_cpu_blocks, max_requests, max_blocks_per_request, int(lcp_block_aligned),
-                  int(alloc_cooling))
+                  int(alloc_cooling), int(kv_dtype))
 
 
 def block_bytes(cfg: Config) -> int:

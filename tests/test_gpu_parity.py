@@ -985,22 +985,21 @@ def test_fused_append_then_invalidate_and_swap_in_without_host_sync():
 
 
 def test_swap_scattered_ids_staged_path():
-    """a5 / a6 with scattered GPU ids (a random half of 64 one-block requests released first,
-    so the swapped request's 32 blocks form >= 16 short runs): the library stages the copies
+    """a5 / a6 with scattered GPU ids (every other one of 64 one-block requests released first,
+    so the swapped request's 32 blocks are 32 one-block runs): the library stages the copies
     through device memory (gather kernel + one DMA per CPU-id run; H2D + scatter kernel).
     Whole blocks must round-trip bit-exactly and match the oracle's pool mirrors; attention
     after the round trip matches the oracle."""
     geo = W.Geometry(L=1, h_q=8, h_kv=2, d=128, k=16)
     P = Pair(1, 8, 2, 128, 16, 96, 64, max_requests=80, max_blocks=64)
     seed = W.seed_of(27)
-    rng = np.random.default_rng(27)
     one = _stream_qkv(seed, W.request_tokens(seed, 99, 16), geo)
     for f in range(64):
         P.new(f, W.request_tokens(seed, 1000 + f, 16))
     P.append([(f, None, 16, 0) for f in range(64)], one[1], one[2])
-    for f in sorted(rng.permutation(64)[:32]):
-        P.lib.release(int(f))
-        assert P.ora.release(int(f)) == 0
+    for f in range(0, 64, 2):
+        P.lib.release(f)
+        assert P.ora.release(f) == 0
     toks = W.request_tokens(seed, 7, 512)
     q, k, v = _stream_qkv(seed, toks, geo)
     P.new(500, toks)
