@@ -34,12 +34,14 @@ class Pair:
     """A libs2l device context and an OracleKV with identical geometry."""
 
     def __init__(self, L, h_q, h_kv, d, k, ng, nc, aligned=False, max_requests=64, max_blocks=None,
-                 mirror=True, stream=None, cooling=False):
+                 mirror=True, stream=None, cooling=False, kv_dtype=0):
         self.geo = (L, h_q, h_kv, d, k)
         self.L, self.h_q, self.h_kv, self.d, self.k = L, h_q, h_kv, d, k
         cfg = s2l.make_config(L, h_q, h_kv, d, k, ng, nc, max_requests=max_requests,
                               max_blocks_per_request=max_blocks or max(ng, nc, 1),
-                              lcp_block_aligned=int(aligned), alloc_cooling=int(cooling))
+                              lcp_block_aligned=int(aligned), alloc_cooling=int(cooling),
+                              kv_dtype=int(kv_dtype))
+        self.fp8 = kv_dtype == 1
         self.m_block = s2l.block_bytes(cfg)
         self.gpu_pool = torch.empty(max(1, ng) * self.m_block // 2, dtype=torch.bfloat16, device="cuda")
         self.cpu_pool = torch.empty(max(1, nc) * self.m_block // 2, dtype=torch.bfloat16).pin_memory()
@@ -50,7 +52,8 @@ class Pair:
         self.lib = s2l.Context(cfg, self.gpu_pool, self.cpu_pool if nc else None, self.stream, None)
         self.ora = OracleKV(L, h_q, h_kv, d, k, ng, nc, max_requests=max_requests,
                             max_blocks_per_request=max_blocks or max(ng, nc, 1), lcp_block_aligned=aligned,
-                            mirror_pools=mirror, alloc_cooling=cooling)
+                            mirror_pools=mirror, alloc_cooling=cooling,
+                            kv_dtype="fp8" if kv_dtype == 1 else "bf16")
         self.ng, self.nc = ng, nc
 
     # ---- ops on both sides -----------------------------------------------------------
@@ -150,19 +153,33 @@ class Pair:
             assert self.lib.block_table(rid) == self.ora.block_table(rid)
 
     def gpu_pool_bits(self):
+        """The GPU pool as [block][L][2][h_kv][k][d] codes: bf16 bits (uint16) or E4M3 bytes."""
         torch.cuda.synchronize()
         self.lib.sync()
-        b = self.gpu_pool.view(torch.int16).cpu().numpy().view(np.uint16)
-        return b.reshape(self.ng, self.L, 2, self.h_kv, self.k, self.d)
+        dt = np.uint8 if self.fp8 else np.uint16
+        b = self.gpu_pool.view(torch.int16).cpu().numpy().view(dt)
+        return b[: self.ng * self.L * 2 * self.h_kv * self.k * self.d].reshape(self.ng, self.L, 2, self.h_kv, self.k, self.d)
 
     def cpu_pool_bits(self):
         self.lib.sync()
-        b = self.cpu_pool.view(torch.int16).numpy().view(np.uint16)
-        return b[: self.nc * self.m_block // 2].reshape(self.nc, self.L, 2, self.h_kv, self.k, self.d)
+        dt = np.uint8 if self.fp8 else np.uint16
+        b = self.cpu_pool.view(torch.int16).numpy().view(dt)
+        return b[: self.nc * self.L * 2 * self.h_kv * self.k * self.d].reshape(self.nc, self.L, 2, self.h_kv, self.k, self.d)
 
     def check_pool_valid_slots(self):
-        """GPU pool bytes at every valid slot of every GPU-tier request == oracle's rows."""
+        """GPU pool bytes at every valid slot of every GPU-tier request == oracle's rows (FP8:
+        == the oracle's E4M3 codes of those rows, its pool mirror)."""
         g = self.gpu_pool_bits()
+        if self.fp8:
+            for rid, r in self.ora.reqs.items():
+                if r.tier != O.GPU or r.nc == 0:
+                    continue
+                pos = np.arange(r.nc)
+                blk = np.array(r.blocks)[pos // self.k]
+                slot = pos % self.k
+                m = self.ora.pool[O.GPU]
+                assert np.array_equal(g[blk, :, :, :, slot, :], m[blk, :, :, :, slot, :]), rid
+            return
         for rid, r in self.ora.reqs.items():
             if r.tier != O.GPU or r.nc == 0:
                 continue

@@ -38,6 +38,8 @@ def test_block_bytes_matches_paper_formula():
     cfg = s2l.make_config(32, 32, 8, 128, 16, 1, 0)
     assert s2l.block_bytes(cfg) == 2 * 1024 * 1024
     assert s2l.block_bytes(s2l.make_config(1, 2, 1, 16, 4, 1, 0)) == 256
+    # FP8 KV cache (kv_dtype 1): b = 1 byte per value instead of P:L63's 2
+    assert s2l.block_bytes(s2l.make_config(32, 32, 8, 128, 16, 1, 0, kv_dtype=1)) == 1024 * 1024
 
 
 def test_config_validation():
@@ -45,7 +47,8 @@ def test_config_validation():
                 s2l.make_config(1, 2, 1, 12, 4, 8, 8),        # head_dim % 8
                 s2l.make_config(1, 2, 1, 16, 3, 8, 8),        # block not power of two
                 s2l.make_config(1, 2, 1, 16, 4, 8, 8, lcp_block_aligned=2),
-                s2l.make_config(1, 2, 1, 16, 4, 8, 8, alloc_cooling=2)]:
+                s2l.make_config(1, 2, 1, 16, 4, 8, 8, alloc_cooling=2),
+                s2l.make_config(1, 2, 1, 16, 4, 8, 8, kv_dtype=2)]:
         with pytest.raises(s2l.S2LError) as e:
             s2l.Context(bad, host_only=True)
         assert e.value.status == s2l.E_INVAL
