@@ -34,7 +34,7 @@ def test_bench_two_ranks_c2_c3_c5_sharded():
 
 def test_bench_two_ranks_c4_request_sharded():
     d = _bench("--gpus", "2", "--workload", "c4", "--steps", "1", "--warmup", "3",
-               env={"S2L_C4_REQUESTS": "16"})
-    assert d["n_gpus"] == 2 and d["config"]["requests"] == 16
+               env={"S2L_C4_REQUESTS": "48"})
+    assert d["n_gpus"] == 2 and d["config"]["requests"] == 48
     assert d["value"] > 0 and d["swap"]["out_bytes"] > 0 and d["swap"]["in_bytes"] > 0
     assert d["host_link_concurrent_aggregate_gbs"]["h2d"] > 0
