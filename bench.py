@@ -159,11 +159,12 @@ class Stream:
         self.items_p = [[(r, j * CHUNK, CHUNK, i * CHUNK) for i, r in enumerate(rids)] for j in range(self.steps)]
 
 
-def make_ctx(dev_index: int):
+def make_ctx(dev_index: int, kv_dtype: int = 0):
     import torch
     from paper_2604_16395_b200 import s2l
     nblk = NREQ * TOTAL // KB
-    cfg = s2l.make_config(1, H_Q, H_KV, D, KB, nblk, 0, max_requests=NREQ, max_blocks_per_request=TOTAL // KB)
+    cfg = s2l.make_config(1, H_Q, H_KV, D, KB, nblk, 0, max_requests=NREQ, max_blocks_per_request=TOTAL // KB,
+                          kv_dtype=kv_dtype)
     pool = torch.empty(nblk * s2l.block_bytes(cfg) // 2, dtype=torch.bfloat16, device=f"cuda:{dev_index}")
     ctx = s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None)
     return ctx, pool
@@ -1063,6 +1064,29 @@ def main():
             cl["in_frac_link"] = cl["in_gbs"] / link["h2d"]
         line["kv_swap_scattered"] = cells
         line["lcp_invalidate"] = measure_lcp()
+        # f4: the same C2 stream on an FP8 E4M3 KV cache (kv_dtype 1; not the paper's b = 2)
+        ctx8, pool8 = make_ctx(dev_index, kv_dtype=1)
+        f8 = lambda: run_step(ctx8, S)
+        ctx8.set_timing(True)
+        ms8 = timed(f8, max(2, args.steps // 2), 1, None) / max(2, args.steps // 2)
+        ti8 = ctx8.timing_read()
+        ctx8.set_timing(False)
+        from oracle import fp8 as ofp8
+        from oracle.attention import attention_rows
+        rows = [0, 1, 255, 510, 511]
+        q, k, v = data[0]
+        kq, vq = ofp8.quantize_bf16_bits(k[0])[1], ofp8.quantize_bf16_bits(v[0])[1]
+        ref, _ = attention_rows(q[TOTAL - CHUNK:], kq, vq, TOTAL - CHUNK, rows)
+        got = S.o[-1][rows].float().cpu().numpy().astype(np.float64)
+        err8 = float((np.abs(got - ref).max(-1) / np.maximum(np.abs(ref).max(-1), 1e-6)).max())
+        line["fp8_kv"] = {"value": flops_rank / (ms8 * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms8,
+                          "attn_kernel_tflops": flops_rank * max(2, args.steps // 2) / (ti8["attn_ms"] * 1e-3) / 1e12,
+                          "pool_bytes": pool8.numel() * 2, "bf16_pool_bytes": pool.numel() * 2,
+                          "parity": {"max_normwise_err": err8, "tol": 2e-2, "pass": err8 <= 2e-2,
+                                     "reference": "oracle on the E4M3-quantised K/V (oracle/fp8.py)"},
+                          "note": "kv_dtype=1: E4M3 storage, exact bf16 dequantisation in shared memory before the MMAs"}
+        ctx8.close()
+        del pool8
     if rank == 0:
         # the oracle on the host cores (bounded sample), after all device timing
         v, desc, thr = oracle_sample(data)
