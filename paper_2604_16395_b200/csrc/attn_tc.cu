@@ -306,6 +306,22 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       if constexpr (kFuse) fuse = p.fuse != 0 && (lo >= 64 || ((p.fuse_mask >> lo) & 1ull));
       const int64_t wr_lo = it.q_pos + tok0, wr_hi = it.q_pos + min(tok0 + 2 * toks, it.n_q);
       bool st_pending = false;                          // lane 0 has TMA stores in flight
+      if constexpr (kFuse) {
+        // the chunk's K/V rows this unit will read from the caller's input (its last KV
+        // tiles) are prefetched into L2 now, so the diagonal tiles do not wait on DRAM (the
+        // plain path reads them from L2, where the append kernel just wrote them)
+        if (fuse && lane < 2) {
+          const CUtensorMap* tin = lane ? &p.tmap_vin_t : &p.tmap_kin_t;
+          for (int64_t tpos = (int64_t)jb * kBN; tpos < (int64_t)(jb + nT) * kBN; tpos += kBN) {
+            if (tpos < it.q_pos) continue;
+            const int32_t z = (int32_t)(it.q_row + (tpos - it.q_pos));
+            asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(tin), "r"(0),
+                         "r"(kvh), "r"(z) : "memory");
+            asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(tin), "r"(64),
+                         "r"(kvh), "r"(z) : "memory");
+          }
+        }
+      }
       for (int32_t j = 0; j < nT; ++j) {
         const int32_t cur_id = next_id;
         if (j + 1 < nT && lane < nb_tile) next_id = load_id(j + 1);   // prefetch the next ids
