@@ -106,9 +106,9 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(lbo >> 4) << 16) |
          ((uint64_t)(sbo >> 4) << 32) | (1ull << 46) | (2ull << 61);
 }
-// Instruction descriptor kind::f16: D f32, A/B bf16, dense.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_mn) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+// Instruction descriptor kind::f16: D f32, A/B bf16 (or f16 with f16 = true), dense.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_mn, bool f16 = false) {
+  return (1u << 4) | (f16 ? 0u : (1u << 7) | (1u << 10)) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
@@ -208,7 +208,17 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return r;
 }
 // P -> bf16x2 (round to nearest even) for the PV MMA.
-__device__ __forceinline__ uint32_t pack_p(float lo, float hi) { return pack_bf16(lo, hi); }
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// P -> the MMA's operand type: bf16x2 (kHalf = false) or f16x2 (the FP8-KV kernel, whose MMAs
+// run on f16 operands), round to nearest even.
+template <bool kHalf = false>
+__device__ __forceinline__ uint32_t pack_p(float lo, float hi) {
+  return kHalf ? pack_f16(lo, hi) : pack_bf16(lo, hi);
+}
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                              uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
@@ -219,7 +229,7 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
  // p = 2^(s*scale - m) for 64 columns (32 pairs per phase, the FMA-pipe polynomial spread
 // over every 8/kPolyPer8-th pair): more independent work per phase for the single softmax warp of an SMSP
 // (tools/micro/softmax_bench2.cu: ~10 % fewer cycles per tile than 32-column phases).
-template <bool kMasked, int kPolyPer8>
+template <bool kMasked, int kPolyPer8, bool kHalf = false>
 __device__ __forceinline__ float2 chunk_p64(const uint32_t* v, float2 acc, int vis, int base,
                                             float2 sc2, float2 nm2, uint32_t (&pk)[32]) {
   float2 x[32];
@@ -244,14 +254,14 @@ __device__ __forceinline__ float2 chunk_p64(const uint32_t* v, float2 acc, int v
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
     a[c & 3] = __fadd2_rn(a[c & 3], x[c]);
-    pk[c] = pack_p(x[c].x, x[c].y);
+    pk[c] = pack_p<kHalf>(x[c].x, x[c].y);
   }
   return __fadd2_rn(__fadd2_rn(a[0], a[1]), __fadd2_rn(a[2], a[3]));
 }
 // p = 2^(s*scale - m) for 32 columns of an unmasked tile (16 pairs), the FMA-pipe polynomial
 // on kPolyPer8 of every 8 pairs, spread evenly (pair c is polynomial iff (c*kPolyPer8) mod 8 <
 // kPolyPer8); returns the running pair sum, writes 16 packed bf16x2.
-template <int kPolyPer8>
+template <int kPolyPer8, bool kHalf = false>
 __device__ __forceinline__ float2 chunk_p32(const uint32_t* v, float2 acc, float2 sc2, float2 nm2,
                                             uint32_t (&pk)[16]) {
   float2 x[16];
@@ -267,7 +277,7 @@ __device__ __forceinline__ float2 chunk_p32(const uint32_t* v, float2 acc, float
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
     a[c & 1] = __fadd2_rn(a[c & 1], x[c]);
-    pk[c] = pack_p(x[c].x, x[c].y);
+    pk[c] = pack_p<kHalf>(x[c].x, x[c].y);
   }
   return __fadd2_rn(a[0], a[1]);
 }
