@@ -127,24 +127,29 @@ struct Lay {
   static constexpr uint32_t OFF_F8 = OFF_RING + NST * kTileBytes;
   static constexpr uint32_t OFF_BAR = OFF_F8 + F8ST * kF8Tile;
   // barriers: Q_full, ring_full[NST], ring_empty[NST], S_full[2], P_full[2] (keys 0-63),
-  // P_half[2] (keys 64-127), O_fin[2], fp8 staging full[F8ST] / empty[F8ST]
+  // P_half[2] (keys 64-127), O_fin[2], fp8 staging full[F8ST] / empty[F8ST], fp8: Q in f16
   static constexpr uint32_t B_QF = 0, B_RF = 1, B_RE = 1 + NST, B_SF = 1 + 2 * NST, B_PF = B_SF + 2,
                             B_PH = B_PF + 2, B_OF = B_PH + 2, B_8F = B_OF + 2, B_8E = B_8F + F8ST,
-                            NBARS = B_8E + F8ST;
+                            B_QC = B_8E + F8ST, NBARS = B_QC + (kFp8 ? 1 : 0);
   static constexpr uint32_t OFF_TMEM = OFF_BAR + NBARS * 8;
   static constexpr uint32_t SMEM = OFF_TMEM + 16 + 1024;
   static_assert(SMEM <= 232448, "shared memory");
 };
 }  // namespace v2
 
-// two E4M3 codes (low byte first) -> bf16x2, exactly
-__device__ __forceinline__ uint32_t e4m3x2_to_bf16x2(uint16_t v) {
+// two E4M3 codes (low byte first) -> f16x2, exactly (every E4M3 value, 2^-9 .. 448, is an f16)
+__device__ __forceinline__ uint32_t e4m3x2_to_f16x2(uint16_t v) {
   uint32_t h2;
   asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(v));
-  float lo, hi;
-  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
-      : "=f"(lo), "=f"(hi) : "r"(h2));
-  return pack_bf16(lo, hi);
+  return h2;
+}
+// bf16x2 -> f16x2: exact for |x| in [2^-14, 65504] (f16 has the wider mantissa); beyond, the
+// nearest f16 (saturating at +-65504, subnormal / zero below) -- reading Z20 in DESIGN.md
+__device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t x) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(x & 0xffff0000u)),
+      "f"(__uint_as_float(x << 16)));
+  return r;
 }
 
 // kFuse: the fused-append instantiation (NEXT-2); kFp8: K/V pool in FP8 E4M3 (kv_dtype 1).
@@ -224,6 +229,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       mbar_init(bar(L::B_8F + s), 1);
       mbar_init(bar(L::B_8E + s), 2);
     }
+    if (kFp8) mbar_init(bar(L::B_QC), 2);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
@@ -425,11 +431,26 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       if (kFuse && lane == 0) bulk_wait_all();
       }
     } else if (kFp8 && warp >= 2) {
-      // ================= FP8 -> bf16 converters (warps 2-3) =================
-      // Each E4M3 tile (TMA, dense [key][128 B]) becomes the bf16 K-major SW128 image the MMAs
-      // read: key r, d-half h, 16-byte chunk c at h*16 KB + r*128 + ((c ^ (r & 7)) << 4).
-      // E4M3 -> f16 -> f32 -> bf16 is exact (every E4M3 value is a bf16 value).
+      // ================= FP8 -> f16 converters (warps 2-3) =================
+      // The FP8 kernel's MMAs run on f16 operands: E4M3 -> f16 is one exact conversion per two
+      // values (E4M3 -> bf16 would need three more).  First the two Q tiles are converted
+      // bf16 -> f16 in place (elementwise, so the SW128 image is unchanged); then each E4M3
+      // tile (TMA, dense [key][128 B]) becomes the f16 K-major SW128 image the MMAs read:
+      // key r, d-half h, 16-byte chunk c at h*16 KB + r*128 + ((c ^ (r & 7)) << 4).
       const int ct = threadIdx.x - 64;                    // 0..63
+      mbar_wait(bar(WB_QF), 0);
+#pragma unroll 4
+      for (int i = ct; i < 2 * (int)kTileBytes / 16; i += 64) {
+        const uint32_t a = sb + WOFF_Q0 + 16u * (uint32_t)i;   // Q0 and Q1 are contiguous
+        uint32_t f[4];
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(f[0]), "=r"(f[1]), "=r"(f[2]), "=r"(f[3]) : "r"(a));
+        st_shared_v4(a, bf16x2_to_f16x2(f[0]), bf16x2_to_f16x2(f[1]), bf16x2_to_f16x2(f[2]),
+                     bf16x2_to_f16x2(f[3]));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(L::B_QC));
       uint32_t r8 = 0, rp = 0;
       for (int32_t j = 0; j < nT; ++j) {
 #pragma unroll 1
@@ -452,8 +473,8 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
               uint32_t o[8];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                o[2 * e] = e4m3x2_to_bf16x2((uint16_t)(f[e] & 0xffffu));
-                o[2 * e + 1] = e4m3x2_to_bf16x2((uint16_t)(f[e] >> 16));
+                o[2 * e] = e4m3x2_to_f16x2((uint16_t)(f[e] & 0xffffu));
+                o[2 * e + 1] = e4m3x2_to_f16x2((uint16_t)(f[e] >> 16));
               }
               const uint32_t h = jc >> 2, c = (jc & 3) * 2;  // d = 16 jc .. 16 jc + 15
               const uint32_t row = dst + h * kAtom + r * 128;
@@ -471,8 +492,8 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       }
     } else if (warp == 1) {
       // ================= MMA issuer (whole warp, one elected lane issues) =================
-      constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);
-      constexpr uint32_t idesc_o = idesc_bf16(kBM, kD, 0, 1);
+      constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0, kFp8);   // fp8 pools: f16 operands
+      constexpr uint32_t idesc_o = idesc_bf16(kBM, kD, 0, 1, kFp8);
       // descriptors of the buffer bases; the start-address field (bits 0-13, 16-byte units)
       // is advanced by adding (byte offset >> 4) — smem addresses stay below 256 KB
       const uint64_t dq[2] = {sdesc(sb + WOFF_Q0, 16, 1024), sdesc(sb + WOFF_Q1, 16, 1024)};
@@ -515,7 +536,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
           mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
                        idesc_o, 1);
       };
-      mbar_wait(bar(WB_QF), 0);
+      mbar_wait(bar(kFp8 ? L::B_QC : WB_QF), 0);
       tc_fence_after();
       uint32_t kslot = next_full();
       issue_s(0, kslot);
@@ -587,10 +608,10 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         tmem_ld32(tS + 32, sv + 32);
         tmem_ld32(tS + 64, sv + 64);
         tmem_ld32(tS + 96, sv + 96);
-        float2 acc = chunk_p32<kPolyPairsPer8>(sv, make_float2(0.f, 0.f), sc2, nm2, pk);
+        float2 acc = chunk_p32<kPolyPairsPer8, kFp8>(sv, make_float2(0.f, 0.f), sc2, nm2, pk);
         tmem_st16(tS, pk);
         tmem_wait_ld();
-        acc = chunk_p32<kPolyPairsPer8>(sv + 32, acc, sc2, nm2, pk);
+        acc = chunk_p32<kPolyPairsPer8, kFp8>(sv + 32, acc, sc2, nm2, pk);
         tmem_st16(tS + 16, pk);
         max32<false>(sv, 0, 0, mt);
         max32<false>(sv + 32, 0, 32, mt);
@@ -603,9 +624,9 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
           tc_fence_before();
           mbar_arrive(bar(WB_PF + i));                  // P keys 0-63
           if (tr) TRACE(23, i, j);
-          acc = chunk_p32<kPolyPairsPer8>(sv + 64, acc, sc2, nm2, pk);
+          acc = chunk_p32<kPolyPairsPer8, kFp8>(sv + 64, acc, sc2, nm2, pk);
           tmem_st16(tS + 32, pk);
-          acc = chunk_p32<kPolyPairsPer8>(sv + 96, acc, sc2, nm2, pk);
+          acc = chunk_p32<kPolyPairsPer8, kFp8>(sv + 96, acc, sc2, nm2, pk);
           tmem_st16(tS + 48, pk);
           tmem_wait_st();
           tc_fence_before();
@@ -662,8 +683,8 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         uint32_t pk[32];
-        acc = masked_tile ? chunk_p64<true, 0>(sv + 64 * hh, acc, vis, 64 * hh, sc2, nm2, pk)
-                          : chunk_p64<false, kPolyPairsPer8>(sv + 64 * hh, acc, vis, 64 * hh, sc2, nm2, pk);
+        acc = masked_tile ? chunk_p64<true, 0, kFp8>(sv + 64 * hh, acc, vis, 64 * hh, sc2, nm2, pk)
+                          : chunk_p64<false, kPolyPairsPer8, kFp8>(sv + 64 * hh, acc, vis, 64 * hh, sc2, nm2, pk);
         tmem_st16(tS + 32 * hh, pk);
         tmem_st16(tS + 32 * hh + 16, pk + 16);
         tmem_wait_st();                // keys 64hh .. 64hh+63 of P are in TMEM

@@ -84,8 +84,10 @@ def main():
             saved[k] = os.environ.get(k)
             os.environ[k] = v
         nblk = bench.NREQ * bench.TOTAL // bench.KB
+        # "KV=1" in a spec's env list: that context's pool is FP8 E4M3 (kv_dtype 1)
         cfg = s2l.make_config(1, bench.H_Q, bench.H_KV, bench.D, bench.KB, nblk, 0, max_requests=bench.NREQ,
-                              max_blocks_per_request=bench.TOTAL // bench.KB)
+                              max_blocks_per_request=bench.TOTAL // bench.KB,
+                              kv_dtype=int(os.environ.get("KV", "0")))
         pool = torch.empty(nblk * s2l.block_bytes(cfg) // 2, dtype=torch.bfloat16, device="cuda")
         ctxs.append((s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None, lib_path=path), pool))
         for k, v in saved.items():
