@@ -494,17 +494,9 @@ s2l_status swap_impl(s2l_ctx* c, int32_t n_reqs, const int64_t* ids, int64_t* by
   char* gbase = (char*)c->gpu_pool;
   char* hbase = (char*)c->cpu_pool;
   const cudaMemcpyKind kind = dst == S2L_TIER_GPU ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  // One cudaMemcpyAsync per coalesced run (the batched-copy entry points are not used: they
+  // are closed on the GPU pool this build runs on); many short runs take the staged path below.
   auto dma = [&](std::vector<void*>& dsts, std::vector<void*>& srcs, std::vector<size_t>& sizes) -> bool {
-    if (sizes.empty()) return true;
-    if (sizes.size() == 1) return cuda_ok(c, cudaMemcpyAsync(dsts[0], srcs[0], sizes[0], kind, st), "swap copy");
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t attr_idx = 0, fail_idx = 0;
-    if (cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr, &attr_idx, 1, &fail_idx,
-                             st) == cudaSuccess)
-      return true;
-    cudaGetLastError();
     for (size_t i = 0; i < sizes.size(); ++i)
       if (!cuda_ok(c, cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], kind, st), "swap copy")) return false;
     return true;
