@@ -95,6 +95,25 @@ __device__ __forceinline__ void trace_ev(const TcParams& p, uint32_t& n, uint32_
 #else
 #define TRACE(ev, tile, j)
 #endif
+#ifdef S2L_CTATRACE
+// Timing experiment: every CTA stamps its phases (16 u64 slots per CTA in p.trace): 0/1
+// globaltimer at entry / exit, 2.. SM clock at entry, setup done, Q landed (MMA warp), first K/V
+// slot full (MMA warp), first S ready / loop end / epilogue done (softmax warp 4), exit; 9 =
+// smid << 32 | nT, 10 = unit << 16 | piece << 8 | npieces, 12 = barrier init done (thread 0),
+// 13 = TMEM allocated (warp 1).
+__device__ __forceinline__ void cta_stamp(uint32_t* tr, int slot, bool global = false) {
+  if (tr == nullptr) return;
+  uint64_t t;
+  if (global) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  else asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  reinterpret_cast<uint64_t*>(tr)[(int64_t)blockIdx.x * 16 + slot] = t;
+}
+#define CT(slot) cta_stamp(p.trace, slot)
+#define CTG(slot) cta_stamp(p.trace, slot, true)
+#else
+#define CT(slot)
+#define CTG(slot)
+#endif
 // ======================================================================================
 // v2: two Q tiles per CTA ping-ponged through the tensor core (the softmax of one tile runs
 // while the MMAs of the other execute), P kept in TMEM (TS-MMA: A operand = P from TMEM,
@@ -177,6 +196,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
   const uint32_t tr_w = warp == 1 ? 0u : (warp == 4 ? 1u : (warp == 8 ? 2u : 3u));
 #endif
 
+  if (threadIdx.x == 0) { CTG(0); CT(2); }
   // ---- work unit: (item, kv head, pair of Q tiles), longest first
   int32_t unit = blockIdx.x, piece = 0, npieces = 1;
   if (unit >= p.split_begin) {
@@ -231,27 +251,48 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     }
     if (kFp8) mbar_init(bar(L::B_QC), 2);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_q) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv4) : "memory");
+#if !S2L_PDL
+    // the two Q tiles start loading before the TMEM allocation and the CTA barrier (with PDL
+    // the load has to follow griddepcontrol.wait: Q may come from the previous kernel)
+    mbar_expect_tx(bar(WB_QF), 2 * kTileBytes);
+    const int32_t z = (int32_t)(it.q_row + tok0);
+    tma_load_3d(sb + WOFF_Q0, &tmap_q, bar(WB_QF), 0, kvh * G, z);
+    tma_load_3d(sb + WOFF_Q0 + kAtom, &tmap_q, bar(WB_QF), 64, kvh * G, z);
+    tma_load_3d(sb + WOFF_Q1, &tmap_q, bar(WB_QF), 0, kvh * G, z + toks);
+    tma_load_3d(sb + WOFF_Q1 + kAtom, &tmap_q, bar(WB_QF), 64, kvh * G, z + toks);
+#endif
+    CT(12);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_holder)),
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (lane == 0) CT(13);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+#ifdef S2L_CTATRACE
+  if (threadIdx.x == 0 && p.trace) {
+    CT(3);
+    int32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    reinterpret_cast<uint64_t*>(p.trace)[(int64_t)blockIdx.x * 16 + 9] = ((uint64_t)smid << 32) | (uint32_t)nT;
+    reinterpret_cast<uint64_t*>(p.trace)[(int64_t)blockIdx.x * 16 + 10] =
+        ((uint64_t)unit << 16) | ((uint64_t)piece << 8) | (uint64_t)npieces;
+  }
+#endif
   pdl_prologue();   // the item descriptors above come from the parameters or the staging ring
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtrl));
     if (warp == 0) {
       // ================= TMA producer =================
-      if (lane == 0) {
+      if (S2L_PDL && lane == 0) {
         mbar_expect_tx(bar(WB_QF), 2 * kTileBytes);
         const int32_t z = (int32_t)(it.q_row + tok0);
         tma_load_3d(sb + WOFF_Q0, &tmap_q, bar(WB_QF), 0, kvh * G, z);
@@ -538,7 +579,9 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       };
       mbar_wait(bar(kFp8 ? L::B_QC : WB_QF), 0);
       tc_fence_after();
+      if (lane == 0) CT(4);
       uint32_t kslot = next_full();
+      if (lane == 0) CT(5);
       issue_s(0, kslot);
       issue_s(1, kslot);
       mma_commit_elect(bar(WB_RE + kslot));
@@ -583,6 +626,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       mbar_wait(bar(WB_SF + i), j & 1);
       tc_fence_after();
       if (tr) TRACE(21, i, j);
+      if (j == 0 && warp == 4 && lane == 0) CT(6);
       const int64_t key0 = (int64_t)(jb + j) * kBN;
       const int64_t vis64 = limit - key0;                 // keys c <= vis of this tile visible
       const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBN ? kBN : vis64));
@@ -695,6 +739,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       l_run += acc.x + acc.y;
     }
     // epilogue
+    if (warp == 4 && lane == 0) CT(7);
     mbar_wait(bar(WB_OF + i), 0);
     tc_fence_after();
     __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
@@ -718,85 +763,119 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       if (valid && p.lse)
         p.lse[(it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
     } else {
-      // partial (unnormalised O, m, l) of this KV range -> workspace; the last piece merges
+      // Split piece: (unnormalised O, m, l) of this KV range.  The piece that finds every other
+      // piece already published merges straight from its own TMEM O; otherwise it publishes its
+      // partial (workspace, float4 [column quad][row] per (piece, tile): a warp's stores and
+      // loads are 512 contiguous bytes) and the last piece to publish merges from the workspace.
+      //   O = sum_k 2^(m_k - M) O_k / sum_k 2^(m_k - M) l_k,  M = max_k m_k.
       const int32_t su = unit - p.split_begin;                 // split-unit index
-      const int64_t prow = (((int64_t)su * npieces + piece) * 2 + i) * 128 + r;
-      float* wo = p.ws + prow * kD;
-#pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
-        uint32_t ov[16];
-        tmem_ld16(tO + c * 16, ov);
-        tmem_wait_ld();
-        float4* dst = reinterpret_cast<float4*>(wo + c * 16);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          dst[e] = make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
-                               __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3]));
-      }
-      p.ws_ml[prow * 2] = m_run;
-      p.ws_ml[prow * 2 + 1] = l_run;
-      __threadfence();
-      asm volatile("bar.sync 1, 256;" ::: "memory");       // both softmax warpgroups wrote
-      uint32_t* flag = (uint32_t*)(smem + WOFF_TMEM + 8);
+      float4* ws4 = reinterpret_cast<float4*>(p.ws);
+      auto wsi = [&](int32_t k) { return (((int64_t)su * npieces + k) * 2 + i) * 32 * 128 + r; };
+      auto mli = [&](int32_t k) { return ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * 2; };
+      volatile uint32_t* flag = (volatile uint32_t*)(smem + WOFF_TMEM + 8);
       if (threadIdx.x == 128) {
-        const int32_t old = atomicAdd(p.ws_cnt + su, 1);
-        const uint32_t last = (old == npieces - 1) ? 1u : 0u;
-        if (last) p.ws_cnt[su] = 0;                          // ready for the next launch
-        *flag = last;
+        int32_t done;
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(done) : "l"(p.ws_cnt + su) : "memory");
+        const uint32_t direct = (done == npieces - 1) ? 1u : 0u;
+        if (direct) p.ws_cnt[su] = 0;                         // ready for the next launch
+        *flag = direct;
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
-      if (*flag) {
-        __threadfence();
-        float M = -INFINITY;
-        for (int k = 0; k < npieces; ++k) {
-          const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
-          M = fmaxf(M, __ldcg(p.ws_ml + pr * 2));
+      const bool direct = *flag != 0;
+      bool merge = direct;
+      if (!direct) {
+#pragma unroll 1
+        for (int c = 0; c < 8; ++c) {
+          uint32_t ov[16];
+          tmem_ld16(tO + c * 16, ov);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            __stcg(ws4 + wsi(piece) + (int64_t)(4 * c + e) * 128,
+                   make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
+                               __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3])));
         }
+        __stcg(reinterpret_cast<float2*>(p.ws_ml + mli(piece)), make_float2(m_run, l_run));
+        __threadfence();
+        asm volatile("bar.sync 1, 256;" ::: "memory");       // both softmax warpgroups wrote
+        if (threadIdx.x == 128) {
+          const int32_t old = atomicAdd(p.ws_cnt + su, 1);
+          const uint32_t last = (old == npieces - 1) ? 1u : 0u;
+          if (last) p.ws_cnt[su] = 0;                        // ready for the next launch
+          *flag = last;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        merge = *flag != 0;
+        if (merge) __threadfence();
+      }
+      if (merge) {
         constexpr int kMaxPieces = 8;
-        float wk[kMaxPieces];
+        float mk[kMaxPieces], wk[kMaxPieces];
+        float M = direct ? m_run : -INFINITY;
+#pragma unroll
+        for (int k = 0; k < kMaxPieces; ++k) {
+          mk[k] = -INFINITY;
+          wk[k] = 0.f;
+          if (k < npieces && !(direct && k == piece)) {
+            const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + mli(k)));
+            mk[k] = ml.x;
+            wk[k] = ml.y;                                      // l_k for now
+            M = fmaxf(M, ml.x);
+          }
+        }
+        // a row no piece saw a key for keeps M = -inf (weights 0, O = 0; not reached by valid rows)
+        const float Mu = (M == -INFINITY) ? 0.f : M;
         float Lsum = 0.f;
 #pragma unroll
         for (int k = 0; k < kMaxPieces; ++k) {
-          wk[k] = 0.f;
-          if (k < npieces) {
-            const int64_t pr = (((int64_t)su * npieces + k) * 2 + i) * 128 + r;
-            wk[k] = fast_exp2(__ldcg(p.ws_ml + pr * 2) - M);
-            Lsum += wk[k] * __ldcg(p.ws_ml + pr * 2 + 1);
-          }
+          const float l = wk[k];
+          wk[k] = (mk[k] == -INFINITY) ? 0.f : fast_exp2(mk[k] - Mu);
+          Lsum += wk[k] * l;
         }
+        const float wself = (direct && m_run != -INFINITY) ? fast_exp2(m_run - Mu) : 0.f;
+        if (direct) Lsum += wself * l_run;
         const float inv = 1.f / Lsum;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kD; c0 += 32) {
-          float acc[32];
+        for (int c = 0; c < 8; ++c) {
+          float acc[16];
+          if (direct) {
+            uint32_t ov[16];
+            tmem_ld16(tO + c * 16, ov);
+            tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+            for (int e = 0; e < 16; ++e) acc[e] = wself * __uint_as_float(ov[e]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+          }
 #pragma unroll
           for (int k = 0; k < kMaxPieces; ++k) {
-            if (k < npieces) {
-              const float* po = p.ws + ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * kD + c0;
+            if (k < npieces && !(direct && k == piece)) {
+              const float4* src = ws4 + wsi(k) + (int64_t)(4 * c) * 128;
 #pragma unroll
-              for (int c = 0; c < 32; c += 2) {
-                const float2 x = __ldcg(reinterpret_cast<const float2*>(po + c));
-                acc[c] += wk[k] * x.x;
-                acc[c + 1] += wk[k] * x.y;
+              for (int e = 0; e < 4; ++e) {
+                const float4 x = __ldcg(src + e * 128);
+                acc[4 * e] += wk[k] * x.x;
+                acc[4 * e + 1] += wk[k] * x.y;
+                acc[4 * e + 2] += wk[k] * x.z;
+                acc[4 * e + 3] += wk[k] * x.w;
               }
             }
           }
           if (valid) {
+            uint32_t w[8];
 #pragma unroll
-            for (int c = 0; c < 32; c += 8) {
-              uint4 v4 = make_uint4(pack_bf16(acc[c] * inv, acc[c + 1] * inv), pack_bf16(acc[c + 2] * inv, acc[c + 3] * inv),
-                                    pack_bf16(acc[c + 4] * inv, acc[c + 5] * inv), pack_bf16(acc[c + 6] * inv, acc[c + 7] * inv));
-              *reinterpret_cast<uint4*>(orow + c0 + c) = v4;
-            }
+            for (int e = 0; e < 8; ++e) w[e] = pack_bf16(acc[2 * e] * inv, acc[2 * e + 1] * inv);
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
           }
         }
-        if (valid) {
-          if (p.lse) p.lse[(it.q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
-        }
+        if (valid && p.lse) p.lse[(it.q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
       }
     }
     tc_fence_before();
+    if (warp == 4 && lane == 0) CT(8);
   }
   __syncthreads();
   if (warp == 1) {
@@ -804,6 +883,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
   }
+  if (threadIdx.x == 0) { CT(11); CTG(1); }
 }
 
 }  // namespace
