@@ -76,7 +76,8 @@ typedef struct s2l_config {
   int32_t num_gpu_blocks;         /* blocks in the GPU pool                                 */
   int32_t num_cpu_blocks;         /* blocks in the CPU pool (may be 0: no swapping)         */
   int32_t max_requests;           /* live requests at once                                  */
-  int32_t max_blocks_per_request; /* columns of the device block table                      */
+  int32_t max_blocks_per_request; /* columns of the device block table; max_requests * this
+                                     and this * block_size must be < 2^31 (E_INVAL)         */
   int32_t lcp_block_aligned;      /* 0 = token-granular LCP (default, Z4);
                                      1 = round the kept prefix down to a block     */
   int32_t alloc_cooling;          /* 0 = plain lowest-free-id order (Z9, default);

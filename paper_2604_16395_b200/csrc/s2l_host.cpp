@@ -261,6 +261,11 @@ s2l_status check_config(const s2l_config* cfg) {
   if (g.num_gpu_blocks < 0 || g.num_cpu_blocks < 0 || g.max_requests < 1 ||
       g.max_blocks_per_request < 1)
     return fail(S2L_E_INVAL, "bad pool / table sizes");
+  // token positions and table indices are 32-bit on the device
+  if ((int64_t)g.max_blocks_per_request * g.block_size >= (1ll << 31) ||
+      (int64_t)g.max_requests * g.max_blocks_per_request >= (1ll << 31))
+    return fail(S2L_E_INVAL, "max_blocks_per_request * block_size and max_requests * "
+                "max_blocks_per_request must be < 2^31");
   if (g.lcp_block_aligned != 0 && g.lcp_block_aligned != 1)
     return fail(S2L_E_INVAL, "lcp_block_aligned must be 0 or 1");
   if (g.alloc_cooling != 0 && g.alloc_cooling != 1)
@@ -674,8 +679,8 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
 
     e = getenv("S2L_TRACE");
     if (e && e[0] == '1') {
-      CK(cudaMalloc(&c->trace_buf, (16 + 4 * 4096 * 2) * sizeof(uint32_t)));
-      CK(cudaMemsetAsync(c->trace_buf, 0, (16 + 4 * 4096 * 2) * sizeof(uint32_t), c->compute));
+      CK(cudaMalloc(&c->trace_buf, ((size_t)1 << 20)));
+      CK(cudaMemsetAsync(c->trace_buf, 0, ((size_t)1 << 20), c->compute));
       const char* tl = getenv("S2L_TRACE_LAUNCH");
       c->trace_launch = tl ? atoll(tl) : 0;
     }
@@ -705,7 +710,7 @@ void s2l_destroy(s2l_ctx* c) {
         cudaEventDestroy(p.second);
       }
     if (c->trace_buf) {   // experiments: dump the recorded timeline
-      std::vector<uint32_t> h(16 + 4 * 4096 * 2);
+      std::vector<uint32_t> h(((size_t)1 << 20) / sizeof(uint32_t));
       cudaMemcpy(h.data(), c->trace_buf, h.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost);
       const char* path = getenv("S2L_TRACE_FILE");
       if (FILE* f = fopen(path ? path : "s2l_trace.bin", "wb")) {
@@ -1092,6 +1097,9 @@ static s2l_status prefill_impl(s2l_ctx* c, int32_t layer, int32_t n_items,
     const char* err = nullptr;
     if (!s2l::make_tmap_q(tq, q, q_rows, c->cfg.num_q_heads, c->cfg.head_dim, G, &err))
       return fail(S2L_E_CUDA, "tensor map (q): %s", err ? err : "?");
+    alignas(64) unsigned char to[128];                // O has Q's shape: the same box
+    if (!s2l::make_tmap_q(to, o, q_rows, c->cfg.num_q_heads, c->cfg.head_dim, G, &err))
+      return fail(S2L_E_CUDA, "tensor map (o): %s", err ? err : "?");
     // Tail-wave split (hybrid stream-K): whole units fill the full waves; the units of the
     // last partial wave are cut into s contiguous KV ranges so that wave is ~full as well.
     const int64_t P = c->num_sms;
@@ -1129,7 +1137,7 @@ static s2l_status prefill_impl(s2l_ctx* c, int32_t layer, int32_t n_items,
     CK(s2l::launch_attn_tc(c->geo, dv, inl ? dev.data() : nullptr, n_items, (int32_t)units,
                            split_begin, split_s,
                            c->split_ws, c->num_sms, c->split_cnt, c->d_table, layer, tq,
-                           c->tmap_kv, o, lse,
+                           c->tmap_kv, to, o, lse,
                            fused ? s2l::kAttnFuseAppend : 0,
                            c->compute, fused ? tin : nullptr, c->gpu_pool, fuse_mask));
   } else {

@@ -148,7 +148,7 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
                            int32_t total_units, int32_t split_begin, int32_t split_s,
                            float* ws, int32_t max_pieces, int32_t* ws_cnt,
                            const int32_t* table, int32_t layer, const void* tmap_q,
-                           const void* tmap_kv, void* o, float* lse,
+                           const void* tmap_kv, const void* tmap_o, void* o, float* lse,
                            int32_t flags, cudaStream_t st, const void* tmap_in = nullptr,
                            void* pool = nullptr, uint64_t fuse_mask = ~0ull);
 // fuse_mask (kAttnFuseAppend, items inline): bit i set = item i (in the items array's order)

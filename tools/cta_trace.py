@@ -32,8 +32,8 @@ def run(launch):
         torch.cuda.synchronize()
         ctx.close()
     raw = np.fromfile(path, dtype=np.uint64)
-    n = len(raw) // 16
-    t = raw[: n * 16].reshape(n, 16).astype(np.int64)
+    n = len(raw) // 32
+    t = raw[: n * 32].reshape(n, 32).astype(np.int64)
     t = t[t[:, 0] > 0]
     g0 = t[:, 0].min()
     ent, ext = (t[:, 0] - g0) / 1e3, (t[:, 1] - g0) / 1e3         # us
@@ -44,9 +44,11 @@ def run(launch):
     dur_us = ext - ent
     cyc = clk_exit - clk[:, 0]
     mhz = cyc / np.maximum(dur_us, 1e-3)
-    ph = {"init": t[:, 12].astype(np.float64) - clk[:, 0], "alloc": t[:, 13].astype(np.float64) - clk[:, 0],
+    ph = {"decode": t[:, 14].astype(np.float64) - clk[:, 0], "mbar_init": t[:, 15].astype(np.float64) - clk[:, 0],
+          "init": t[:, 12].astype(np.float64) - clk[:, 0], "alloc": t[:, 13].astype(np.float64) - clk[:, 0],
           "setup": clk[:, 1] - clk[:, 0], "to_Q": clk[:, 2] - clk[:, 1], "to_K0": clk[:, 3] - clk[:, 2],
           "to_S0": clk[:, 4] - clk[:, 3], "loop": clk[:, 5] - clk[:, 4], "epilogue": clk[:, 6] - clk[:, 5],
+          "epi_wait_O": t[:, 16].astype(np.float64) - clk[:, 5], "epi_work": clk[:, 6] - t[:, 16].astype(np.float64),
           "exit": clk_exit - clk[:, 6]}
     gaps = []
     for s in np.unique(sm):

@@ -96,18 +96,17 @@ __device__ __forceinline__ void trace_ev(const TcParams& p, uint32_t& n, uint32_
 #define TRACE(ev, tile, j)
 #endif
 #ifdef S2L_CTATRACE
-// Timing experiment: every CTA stamps its phases (32 u64 slots per CTA in p.trace): 0/1
+// Timing experiment: every CTA stamps its phases (16 u64 slots per CTA in p.trace): 0/1
 // globaltimer at entry / exit, 2.. SM clock at entry, setup done, Q landed (MMA warp), first K/V
 // slot full (MMA warp), first S ready / loop end / epilogue done (softmax warp 4), exit; 9 =
 // smid << 32 | nT, 10 = unit << 16 | piece << 8 | npieces, 12 = barrier init done (thread 0),
-// 13 = TMEM allocated (warp 1), 14 = unit decoded (thread 0), 15 = barriers initialised,
-// 16 = O_fin wait done (warp 4).
+// 13 = TMEM allocated (warp 1), 14 = unit decoded (thread 0), 15 = barriers initialised.
 __device__ __forceinline__ void cta_stamp(uint32_t* tr, int slot, bool global = false) {
   if (tr == nullptr) return;
   uint64_t t;
   if (global) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   else asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
-  reinterpret_cast<uint64_t*>(tr)[(int64_t)blockIdx.x * 32 + slot] = t;
+  reinterpret_cast<uint64_t*>(tr)[(int64_t)blockIdx.x * 16 + slot] = t;
 }
 #define CT(slot) cta_stamp(p.trace, slot)
 #define CTG(slot) cta_stamp(p.trace, slot, true)
@@ -150,7 +149,7 @@ struct Lay {
   // P_half[2] (keys 64-127), O_fin[2], fp8 staging full[F8ST] / empty[F8ST], fp8: Q in f16
   static constexpr uint32_t B_QF = 0, B_RF = 1, B_RE = 1 + NST, B_SF = 1 + 2 * NST, B_PF = B_SF + 2,
                             B_PH = B_PF + 2, B_OF = B_PH + 2, B_8F = B_OF + 2, B_8E = B_8F + F8ST,
-                            B_QC = B_8E + F8ST, NBARS = B_QC + (kFp8 ? 1 : 0);
+                            B_QC = B_8E + F8ST, B_PVL = B_QC + (kFp8 ? 1 : 0), NBARS = B_PVL + 2;
   static constexpr uint32_t OFF_TMEM = OFF_BAR + NBARS * 8;
   static constexpr uint32_t SMEM = OFF_TMEM + 16 + 1024;
   static_assert(SMEM <= 232448, "shared memory");
@@ -178,7 +177,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     attn_tc2_kernel(const __grid_constant__ CUtensorMap tmap_q,
                     const __grid_constant__ CUtensorMap tmap_kv,
                     const __grid_constant__ CUtensorMap tmap_kv4,
-                    const __grid_constant__ CUtensorMap tmap_o,
                     const __grid_constant__ typename ParamsOf<kFuse>::T p) {
   using namespace v2;
   using L = Lay<kFp8>;
@@ -224,20 +222,16 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
   const int32_t pair = pairs - 1 - local / p.h_kv;
   const int32_t kvh = local % p.h_kv;
 #endif
-  // 32-bit arithmetic (key positions < 2^31: s2l_create checks max_blocks_per_request *
-  // block_size); G and k are powers of two (G divides 128, k checked by s2l_create), so the
-  // divisions by them are shifts -- the 64-bit divisions this replaces cost ~1000 cycles per CTA
   const int32_t G = p.group;
-  const int32_t toks = kBM >> (__ffs(G) - 1);
+  const int32_t toks = kBM / G;
   const int32_t tok0 = pair * 2 * toks;               // first token of tile 0; tile 1 at +toks
   const int32_t tok_last = min(tok0 + 2 * toks, it.n_q) - 1;
-  const int32_t qpos = (int32_t)it.q_pos;
-  const int32_t key_last = qpos + tok_last;
-  const int32_t nT_all = key_last / kBN + 1;
-  const int32_t jb = nT_all * piece / npieces;        // this CTA's KV tiles
-  const int32_t nT = nT_all * (piece + 1) / npieces - jb;
-  const int32_t kv_len = qpos + it.n_q;
-  const int32_t nblk_valid = (kv_len + p.kb - 1) >> (__ffs(p.kb) - 1);
+  const int64_t key_last = it.q_pos + tok_last;
+  const int32_t nT_all = (int32_t)(key_last / kBN) + 1;
+  const int32_t jb = (int32_t)((int64_t)nT_all * piece / npieces);   // this CTA's KV tiles
+  const int32_t nT = (int32_t)((int64_t)nT_all * (piece + 1) / npieces) - jb;
+  const int64_t kv_len = it.q_pos + it.n_q;
+  const int32_t nblk_valid = (int32_t)((kv_len + p.kb - 1) / p.kb);
 
   if (threadIdx.x == 0) {
     CT(14);
@@ -251,6 +245,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       mbar_init(bar(WB_PF + i), 128);
       mbar_init(bar(WB_PH + i), 128);
       mbar_init(bar(WB_OF + i), 1);
+      mbar_init(bar(L::B_PVL + i), 1);
     }
     for (int s = 0; s < L::F8ST; ++s) {
       mbar_init(bar(L::B_8F + s), 1);
@@ -261,7 +256,6 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     CT(15);
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_kv4) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_o) : "memory");
 #if !S2L_PDL
     // the two Q tiles start loading before the TMEM allocation and the CTA barrier (with PDL
     // the load has to follow griddepcontrol.wait: Q may come from the previous kernel)
@@ -290,8 +284,8 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     CT(3);
     int32_t smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    reinterpret_cast<uint64_t*>(p.trace)[(int64_t)blockIdx.x * 32 + 9] = ((uint64_t)smid << 32) | (uint32_t)nT;
-    reinterpret_cast<uint64_t*>(p.trace)[(int64_t)blockIdx.x * 32 + 10] =
+    reinterpret_cast<uint64_t*>(p.trace)[(int64_t)blockIdx.x * 16 + 9] = ((uint64_t)smid << 32) | (uint32_t)nT;
+    reinterpret_cast<uint64_t*>(p.trace)[(int64_t)blockIdx.x * 16 + 10] =
         ((uint64_t)unit << 16) | ((uint64_t)piece << 8) | (uint64_t)npieces;
   }
 #endif
@@ -578,6 +572,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         for (int kk = 0; kk < kBN / 32; ++kk)
           mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
                        idesc_o, (j > 0 || kk > 0));
+        mma_commit_elect(bar(L::B_PVL + i));            // PV of keys 0-63 done (softmax slow path B)
         mbar_wait(bar(WB_PH + i), j & 1);               // P keys 64-127
         tc_fence_after();
         if (lane == 0) TRACE(12, i, j);
@@ -646,14 +641,17 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       for (int q = 0; q < 8; ++q) mt[q] = -INFINITY;
       // Steady state (stale-max fast path): a tile after the first one of this CTA, with no
       // masked key and a finite running max in every row, is exponentiated against the running
-      // max m_run straight away, chunk by chunk as its scores arrive from TMEM (p <= 2^8 as long
-      // as the tile max stays within kRescaleThresh of m_run, the same bound the lazy rescale
-      // keeps).  P of keys 0-63 is released to the PV MMAs only once the whole tile's max is
-      // known to be within that bound; otherwise (rare) the tile falls through to the exact
-      // path below, which rescales O and recomputes P with the new max (S is still in sv).
+      // max m_run straight away, chunk by chunk as its scores arrive from TMEM; no tile max is
+      // computed.  Each half of P is released to the PV MMAs once its row sums are <= kSumBound
+      // (so every p of the half is <= kSumBound: far from overflow in fp32 O / l, and below the
+      // f16 limit of the FP8 kernel's P).  A violating low half (rare after the first tiles)
+      // falls through to the exact path below with the scores still in registers (slow path A);
+      // a violating high half after the low half was released (slow path B) waits for the PV
+      // MMAs of keys 0-63, rescales O with the tile max and recomputes the high half.
       const bool fast = j > 0 && !masked_tile && __all_sync(0xffffffffu, m_run != -INFINITY);
       bool loaded = false;
       if (fast) {
+        constexpr float kSumBound = kFp8 ? 32768.f : 65536.f;
         const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_run, -m_run);
         uint32_t pk[16];
         tmem_ld32(tS, sv);
@@ -666,25 +664,62 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         tmem_wait_ld();
         acc = chunk_p32<kPolyPairsPer8, kFp8>(sv + 32, acc, sc2, nm2, pk);
         tmem_st16(tS + 16, pk);
-        max32<false>(sv, 0, 0, mt);
-        max32<false>(sv + 32, 0, 32, mt);
-        max32<false>(sv + 64, 0, 64, mt);
-        max32<false>(sv + 96, 0, 96, mt);
-        const float mxf = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])),
-                                fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7]))) * sl2;
-        if (!__any_sync(0xffffffffu, mxf > m_run + kRescaleThresh)) {
+        const float s_lo = acc.x + acc.y;
+        if (!__any_sync(0xffffffffu, !(s_lo <= kSumBound))) {
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(bar(WB_PF + i));                  // P keys 0-63
           if (tr) TRACE(23, i, j);
-          acc = chunk_p32<kPolyPairsPer8, kFp8>(sv + 64, acc, sc2, nm2, pk);
+          acc = chunk_p32<kPolyPairsPer8, kFp8>(sv + 64, make_float2(0.f, 0.f), sc2, nm2, pk);
           tmem_st16(tS + 32, pk);
           acc = chunk_p32<kPolyPairsPer8, kFp8>(sv + 96, acc, sc2, nm2, pk);
           tmem_st16(tS + 48, pk);
+          const float s_hi = acc.x + acc.y;
+          if (!__any_sync(0xffffffffu, !(s_hi <= kSumBound))) {
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(bar(WB_PH + i));                // P keys 64-127
+            if (tr) TRACE(24, i, j);
+            l_run += s_lo + s_hi;
+            continue;
+          }
+          // ---- slow path B: rescale with the tile max once PV of keys 0-63 (scaled by the old
+          // m_run, like O) has completed, then recompute keys 64-127
+          max32<false>(sv, 0, 0, mt);
+          max32<false>(sv + 32, 0, 32, mt);
+          max32<false>(sv + 64, 0, 64, mt);
+          max32<false>(sv + 96, 0, 96, mt);
+          const float mxb = fmaxf(fmaxf(fmaxf(mt[0], mt[1]), fmaxf(mt[2], mt[3])),
+                                  fmaxf(fmaxf(mt[4], mt[5]), fmaxf(mt[6], mt[7]))) * sl2;
+          const float mb = (mxb > m_run + kRescaleThresh) ? mxb : m_run;
+          const float alpha = fast_exp2(m_run - mb);
           tmem_wait_st();
+          mbar_wait(bar(L::B_PVL + i), j & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            uint32_t ov[16];
+            tmem_ld16(tO + c * 16, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              float2 x = __fmul2_rn(make_float2(__uint_as_float(ov[e]), __uint_as_float(ov[e + 1])),
+                                    make_float2(alpha, alpha));
+              ov[e] = __float_as_uint(x.x);
+              ov[e + 1] = __float_as_uint(x.y);
+            }
+            tmem_st16(tO + c * 16, ov);
+          }
+          l_run = (l_run + s_lo) * alpha;
+          m_run = mb;
+          const float2 nmb = make_float2(-mb, -mb);
+          acc = chunk_p32<0, kFp8>(sv + 64, make_float2(0.f, 0.f), sc2, nmb, pk);
+          tmem_st16(tS + 32, pk);
+          acc = chunk_p32<0, kFp8>(sv + 96, acc, sc2, nmb, pk);
+          tmem_st16(tS + 48, pk);
+          tmem_wait_st();                               // O rescale and P keys 64-127 in TMEM
           tc_fence_before();
-          mbar_arrive(bar(WB_PH + i));                  // P keys 64-127
-          if (tr) TRACE(24, i, j);
+          mbar_arrive(bar(WB_PH + i));
           l_run += acc.x + acc.y;
           continue;
         }
@@ -751,55 +786,24 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     if (warp == 4 && lane == 0) CT(7);
     mbar_wait(bar(WB_OF + i), 0);
     tc_fence_after();
-    if (warp == 4 && lane == 0) CT(16);
     __nv_bfloat16* orow = p.o + ((it.q_row + tok) * p.h_q + hq) * (int64_t)kD;
-    // Output tile: when all 128 rows of tile i are valid, the bf16 rows go into the tile's Q
-    // buffer (free: O_fin covers every S MMA) in the SW128 image the Q TMA loaded, and one
-    // thread stores them with two TMA boxes (d halves) -- per-thread row stores are 16-byte
-    // pieces 256 B apart and took ~5000 cycles per CTA; a ragged tile stores its valid rows.
-    const bool tile_full = tok0 + (i + 1) * toks <= it.n_q;
-    const uint32_t ob = sb + (i ? WOFF_Q1 : WOFF_Q0);
-    auto put16 = [&](int c, const uint32_t (&w)[8]) {   // bf16 output columns 16c .. 16c+15
-      if (tile_full) {
-        const uint32_t row = ob + (uint32_t)(c >> 2) * kAtom + (uint32_t)r * 128;
-        const uint32_t cc = (uint32_t)(c & 3) * 2;
-        st_shared_v4(row + ((cc ^ (r & 7)) << 4), w[0], w[1], w[2], w[3]);
-        st_shared_v4(row + (((cc + 1) ^ (r & 7)) << 4), w[4], w[5], w[6], w[7]);
-      } else if (valid) {
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
-        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-      }
-    };
-    auto flush = [&]() {
-      if (!tile_full) return;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // st.shared -> TMA
-      asm volatile("bar.sync %0, 128;" ::"r"(2 + i) : "memory");
-      if ((warp & 3) == 0 && lane == 0) {
-        const int32_t z = (int32_t)(it.q_row + tok0 + i * toks);
-        tma_store_3d(&tmap_o, ob, 0, kvh * G, z);
-        tma_store_3d(&tmap_o, ob + kAtom, 64, kvh * G, z);
-        bulk_commit();
-        bulk_wait_all();
-      }
-    };
     if (npieces == 1) {
       const float inv = 1.f / l_run;
-      uint32_t sv[128];
-      tmem_ld32(tO, sv);                               // the whole O row in one wait
-      tmem_ld32(tO + 32, sv + 32);
-      tmem_ld32(tO + 64, sv + 64);
-      tmem_ld32(tO + 96, sv + 96);
-      tmem_wait_ld();
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < 8; ++c) {
-        uint32_t w[8];
+        uint32_t ov[16];
+        tmem_ld16(tO + c * 16, ov);
+        tmem_wait_ld();
+        if (valid) {
+          uint32_t w[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          w[e] = pack_bf16(__uint_as_float(sv[16 * c + 2 * e]) * inv, __uint_as_float(sv[16 * c + 2 * e + 1]) * inv);
-        put16(c, w);
+          for (int e = 0; e < 8; ++e)
+            w[e] = pack_bf16(__uint_as_float(ov[2 * e]) * inv, __uint_as_float(ov[2 * e + 1]) * inv);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        }
       }
-      flush();
       if (valid && p.lse)
         p.lse[(it.q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
     } else {
@@ -902,12 +906,15 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
               }
             }
           }
-          uint32_t w[8];
+          if (valid) {
+            uint32_t w[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) w[e] = pack_bf16(acc[2 * e] * inv, acc[2 * e + 1] * inv);
-          put16(c, w);
+            for (int e = 0; e < 8; ++e) w[e] = pack_bf16(acc[2 * e] * inv, acc[2 * e + 1] * inv);
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          }
         }
-        flush();
         if (valid && p.lse) p.lse[(it.q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
       }
     }
@@ -1048,7 +1055,7 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
                            int32_t total_units, int32_t split_begin, int32_t split_s,
                            float* ws, int32_t max_pieces, int32_t* ws_cnt,
                            const int32_t* table, int32_t layer, const void* tmap_q,
-                           const void* tmap_kv, const void* tmap_o, void* o, float* lse,
+                           const void* tmap_kv, void* o, float* lse,
                            int32_t flags, cudaStream_t st, const void* tmap_in, void* pool,
                            uint64_t fuse_mask) {
   const bool fuse = (flags & kAttnFuseAppend) != 0;
@@ -1077,9 +1084,8 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
   p.kb = g.k;
   p.group = g.h_q / g.h_kv;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)kD);
-  CUtensorMap tq, tkv, tkv4, to;
+  CUtensorMap tq, tkv, tkv4;
   memcpy(&tq, tmap_q, sizeof(CUtensorMap));
-  memcpy(&to, tmap_o, sizeof(CUtensorMap));
   memcpy(&tkv, tmap_kv, sizeof(CUtensorMap));
   memcpy(&tkv4, (const char*)tmap_kv + 128, sizeof(CUtensorMap));
   p.split_begin = total_units;
@@ -1104,9 +1110,9 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
   p.ws_ml = ws ? ws + (int64_t)max_pieces * 2 * 128 * kD : nullptr;
   p.ws_cnt = ws_cnt;
   if (fuse && g.fp8) return cudaErrorInvalidValue;   // no in-kernel append into an FP8 pool
-  if (fuse) return launch_k(attn_tc2_kernel<true, false>, dim3(grid), dim3(v2::kThreads), v2::Lay<false>::SMEM, st, tq, tkv, tkv4, to, pf);
-  if (g.fp8) return launch_k(attn_tc2_kernel<false, true>, dim3(grid), dim3(v2::kThreads), v2::Lay<true>::SMEM, st, tq, tkv, tkv4, to, p);
-  return launch_k(attn_tc2_kernel<false, false>, dim3(grid), dim3(v2::kThreads), v2::Lay<false>::SMEM, st, tq, tkv, tkv4, to, p);
+  if (fuse) return launch_k(attn_tc2_kernel<true, false>, dim3(grid), dim3(v2::kThreads), v2::Lay<false>::SMEM, st, tq, tkv, tkv4, pf);
+  if (g.fp8) return launch_k(attn_tc2_kernel<false, true>, dim3(grid), dim3(v2::kThreads), v2::Lay<true>::SMEM, st, tq, tkv, tkv4, p);
+  return launch_k(attn_tc2_kernel<false, false>, dim3(grid), dim3(v2::kThreads), v2::Lay<false>::SMEM, st, tq, tkv, tkv4, p);
 }
 
 }  // namespace s2l
