@@ -1,5 +1,6 @@
 """Timeline experiment: run the C2 stream once with an S2L_TRACE build and decode the trace of
 CTA 0 of attention launch S2L_TRACE_LAUNCH (default 31 = the last chunk)."""
+import json
 import os
 import struct
 import sys
@@ -60,6 +61,18 @@ def main():
     steps = sorted({k[1] for k in got_s})
     per = [got_s[(0, j + 1)] - got_s[(0, j)] for j in steps if (0, j + 1) in got_s]
     print("period (tile 0 got_S to got_S): mean %.0f cycles over %d steps" % (np.mean(per), len(per)))
+    # steady state (steps 10 .. last-10): per tile, the chain S ready -> P halves -> MMA -> next S
+    lo_j, hi_j = 10, max(steps) - 10
+    out = {}
+    for i in (0, 1):
+        ks = [(i, j) for j in range(lo_j, hi_j) if (i, j) in got_s and (i, j) in p_lo and (i, j) in p_hi]
+        f = lambda a, b: float(np.mean([a[k] - b[k] for k in ks if k in a and k in b]))
+        nxt = [got_s[(i, j + 1)] - m_hi[(i, j)] for (_, j) in ks if (i, j + 1) in got_s and (i, j) in m_hi]
+        out[f"tile{i}"] = {"gotS_to_Plo": f(p_lo, got_s), "gotS_to_Phi": f(p_hi, got_s),
+                           "Plo_to_mma_got": f(m_lo, p_lo), "Phi_to_mma_got": f(m_hi, p_hi),
+                           "mma_waiting_for_Plo": f(m_lo, wp), "softmax_waiting_for_S": f(got_s, w_s),
+                           "mma_gotPhi_to_next_gotS": float(np.mean(nxt)) if nxt else None}
+    print(json.dumps({"period": float(np.mean(per)), "steady": out}))
 
 
 if __name__ == "__main__":
