@@ -79,7 +79,7 @@ class Clocks:
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
         time.sleep(0.3)
@@ -94,7 +94,7 @@ class Clocks:
     def summary(self):
         if not self.proc or not os.path.exists(self.path):
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [x.strip() for x in line.split(",")]
@@ -102,6 +102,7 @@ class Clocks:
                 continue
             try:
                 sm.append(float(parts[0])); mx.append(float(parts[1]))
+                pw.append(float(parts[2]))
             except ValueError:
                 continue
             for nm, v in zip(names, parts[3:7]):
@@ -111,9 +112,15 @@ class Clocks:
             os.remove(self.path)
         except OSError:
             pass
-        busy = [s for s in sm if s > 500] or sm
+        # under load = samples drawing > 40 % of the run's peak power (idle gaps and the
+        # host-side set-up between timed launches excluded)
+        top = max(pw) if pw else 0.0
+        busy = [s for s, p in zip(sm, pw) if p > 0.4 * top] or sm
+        busy_pw = [p for p in pw if p > 0.4 * top]
         return {"sm_mhz": statistics.median(busy) if busy else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(sm)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(sm),
+                "samples_under_load": len(busy_pw),
+                "power_w_median_under_load": statistics.median(busy_pw) if busy_pw else None}
 
 
 def bad_clocks(c):
@@ -376,6 +383,48 @@ def swap_cell(dev_index, L, B, scattered, reps=3, seed=0):
     return {"L": L, "m_block": mb, "blocks": B, "ids": "scattered" if scattered else "contiguous", "gpu_id_runs": runs,
             "out_gbs": best["out"], "in_gbs": best["in"], "out_gbs_call": best["out_call"],
             "in_gbs_call": best["in_call"]}
+
+
+def measure_append_all_layers(dev_index, hbm_peak, reps=5):
+    """a3 at the launch size a whole model issues: one s2l_append_chunk of the C2 chunk
+    (8 requests x 512 tokens) into a 32-layer Llama-3-8B pool writes all 32 layers' K and V in
+    one launch (1 GiB read + 1 GiB written; the headline C2 stream holds one layer, so its
+    launches move 32 MiB).  Two distinct 1 GiB input sets alternate (reads from HBM, not L2);
+    per-launch device time from the library's timing events, median of `reps`."""
+    import torch
+    from paper_2604_16395_b200 import s2l
+    L = 32
+    nblk = NREQ * 2 * CHUNK // KB
+    cfg = s2l.make_config(L, H_Q, H_KV, D, KB, nblk, 0, max_requests=NREQ, max_blocks_per_request=2 * CHUNK // KB)
+    pool = torch.empty(nblk * s2l.block_bytes(cfg) // 2, dtype=torch.bfloat16, device=f"cuda:{dev_index}")
+    ctx = s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None)
+    g = torch.Generator(device=f"cuda:{dev_index}").manual_seed(11)
+    kv = [torch.randn(L, NREQ * CHUNK, H_KV, D, device=f"cuda:{dev_index}", generator=g).to(torch.bfloat16)
+          for _ in range(2)]
+    items = [(r, None, CHUNK, r * CHUNK) for r in range(NREQ)]
+    ms = []
+    for rep in range(reps + 1):
+        for r in range(NREQ):
+            ctx.new_request(r, list(range(2 * CHUNK)))
+        ctx.append_chunk(items, kv[0], kv[1])           # chunk 0 (warm the tables)
+        torch.cuda.synchronize()
+        ctx.set_timing(True)
+        ctx.append_chunk(items, kv[1], kv[0])           # chunk 1: the timed launch
+        torch.cuda.synchronize()
+        ti = ctx.timing_read()
+        ctx.set_timing(False)
+        if rep:
+            ms.append(ti["append_ms"])
+        for r in range(NREQ):
+            ctx.release(r)
+    ctx.close()
+    med = statistics.median(ms)
+    nbytes = 2 * 2 * L * NREQ * CHUNK * H_KV * D * 2
+    gbs = nbytes / (med * 1e-3) / 1e9
+    return {"bound": "hbm", "layers": L, "bytes_per_launch": nbytes, "ms_per_launch": med, "achieved": gbs,
+            "unit": "GB/s", "peak": hbm_peak, "frac": gbs / hbm_peak if hbm_peak else None, "reps": reps,
+            "stat": "median launch (library timing events)",
+            "workload": "one s2l_append_chunk of 8 x 512 tokens into a 32-layer Llama-3-8B pool (32 layers x K, V)"}
 
 
 def measure_lcp():
@@ -1083,6 +1132,7 @@ def main():
             cl["in_frac_link_call"] = cl["in_gbs_call"] / link["h2d"]
         line["kv_swap_scattered"] = cells
         line["lcp_invalidate"] = measure_lcp()
+        line["append_all_layers"] = measure_append_all_layers(dev_index, pk.get("hbm"))
         # f4: the same C2 stream on an FP8 E4M3 KV cache (kv_dtype 1; not the paper's b = 2)
         ctx8, pool8 = make_ctx(dev_index, kv_dtype=1)
         f8 = lambda: run_step(ctx8, S)

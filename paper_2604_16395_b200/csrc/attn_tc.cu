@@ -32,6 +32,9 @@
 #include <mutex>
 
 // Build-time variants (experiments; defaults are the measured best).
+#ifndef S2L_OUT_WAIT_READ
+#define S2L_OUT_WAIT_READ 1
+#endif
 
 namespace s2l {
 namespace {
@@ -49,6 +52,7 @@ struct TcParams {
   // tail-wave KV split (v2): CTAs >= split_begin are pieces of units split into split_s
   // contiguous KV ranges; partials go to ws, the last piece of a unit merges (ws_cnt).
   int32_t split_begin, split_s;
+  int32_t split_direct;   // 0: the last piece always merges from the workspace (tests)
   float* ws;       // [pieces][2][128][128] partial O (unnormalised, fp32)
   float* ws_ml;    // [pieces][2][128][2] running max (log2 units) and row sum
   int32_t* ws_cnt;
@@ -780,7 +784,11 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         tma_store_3d(&tmap_o, ob, 0, kvh * G, z);
         tma_store_3d(&tmap_o, ob + kAtom, 64, kvh * G, z);
         bulk_commit();
+#if S2L_OUT_WAIT_READ
+        bulk_wait_read();   // shared memory may be released; the global writes complete on their own
+#else
         bulk_wait_all();
+#endif
       }
     };
     if (npieces == 1) {
@@ -816,7 +824,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       if (threadIdx.x == 128) {
         int32_t done;
         asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(done) : "l"(p.ws_cnt + su) : "memory");
-        const uint32_t direct = (done == npieces - 1) ? 1u : 0u;
+        const uint32_t direct = (p.split_direct && done == npieces - 1) ? 1u : 0u;
         if (direct) p.ws_cnt[su] = 0;                         // ready for the next launch
         *flag = direct;
       }
@@ -1084,6 +1092,7 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
   memcpy(&tkv4, (const char*)tmap_kv + 128, sizeof(CUtensorMap));
   p.split_begin = total_units;
   p.split_s = 1;
+  p.split_direct = (flags & kAttnNoDirectMerge) ? 0 : 1;
   int32_t grid = total_units;
   if (split_s > 1 && split_begin < total_units) {
     p.split_begin = split_begin;

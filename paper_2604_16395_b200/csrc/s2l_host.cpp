@@ -204,6 +204,7 @@ struct s2l_ctx {
   float* split_ws = nullptr;          // tail-wave split partials (num_sms pieces)
   int32_t* split_cnt = nullptr;       // per split unit arrival counters (self-resetting)
   bool split_enabled = true;
+  bool split_direct = true;           // S2L_SPLIT_DIRECT=0: the last piece always merges from the workspace (tests)
   uint32_t* trace_buf = nullptr;      // S2L_TRACE=1: device buffer for kernel timelines (experiments)
   int64_t trace_launch = -1, attn_launch_no = 0;  // which attention launch to trace (S2L_TRACE_LAUNCH)
   bool tc_ok = false;
@@ -674,6 +675,8 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
     CK(cudaMemsetAsync(c->split_cnt, 0, (size_t)c->num_sms * sizeof(int32_t), c->compute));
     const char* e = getenv("S2L_NO_SPLIT");
     c->split_enabled = !(e && e[0] == '1');
+    e = getenv("S2L_SPLIT_DIRECT");
+    c->split_direct = !(e && e[0] == '0');
     e = getenv("S2L_SWAP_STAGE");
     c->swap_stage = !(e && e[0] == '0');
 
@@ -1138,7 +1141,7 @@ static s2l_status prefill_impl(s2l_ctx* c, int32_t layer, int32_t n_items,
                            split_begin, split_s,
                            c->split_ws, c->num_sms, c->split_cnt, c->d_table, layer, tq,
                            c->tmap_kv, to, o, lse,
-                           fused ? s2l::kAttnFuseAppend : 0,
+                           (fused ? s2l::kAttnFuseAppend : 0) | (c->split_direct ? 0 : s2l::kAttnNoDirectMerge),
                            c->compute, fused ? tin : nullptr, c->gpu_pool, fuse_mask));
   } else {
     CK(s2l::launch_attn_generic(c->geo, dv, n_items, total_q, c->d_table, layer, q, o, lse,

@@ -158,6 +158,7 @@ cudaError_t launch_attn_tc(const Geometry& g, const AttnItemDev* items, const At
 // the block size) the chunk rows [q_pos, q_pos+n_q) of this layer are read from tmap_in
 // (make_tmap_in) and written to the pool by the kernel.  No two items may share a request.
 constexpr int32_t kAttnFuseAppend = 8;
+constexpr int32_t kAttnNoDirectMerge = 16;   // tests: split pieces always merge through the workspace
 // Experiments: device buffer receiving kernel timeline stamps (S2L_TRACE builds); nullptr = off.
 void set_attn_trace(uint32_t* buf);
 constexpr int64_t kSplitPieceFloats = 2 * 128 * 130;   // O [2][128][128] + (m, l) [2][128][2]
