@@ -204,7 +204,8 @@ struct s2l_ctx {
   float* split_ws = nullptr;          // tail-wave split partials (num_sms pieces)
   int32_t* split_cnt = nullptr;       // per split unit arrival counters (self-resetting)
   bool split_enabled = true;
-  bool split_direct = true;           // S2L_SPLIT_DIRECT=0: the last piece always merges from the workspace (tests)
+  bool split_direct = true;
+  int64_t stage_min_runs = 4;         // staged swaps need >= this many id runs (S2L_STAGE_MIN_RUNS)           // S2L_SPLIT_DIRECT=0: the last piece always merges from the workspace (tests)
   uint32_t* trace_buf = nullptr;      // S2L_TRACE=1: device buffer for kernel timelines (experiments)
   int64_t trace_launch = -1, attn_launch_no = 0;  // which attention launch to trace (S2L_TRACE_LAUNCH)
   bool tc_ok = false;
@@ -513,11 +514,12 @@ s2l_status swap_impl(s2l_ctx* c, int32_t n_reqs, const int64_t* ids, int64_t* by
   // Scattered GPU ids (short runs): stage through device memory so that every run of
   // consecutive HOST ids is one DMA -- swap-out gathers the GPU blocks into a contiguous
   // staging buffer (one kernel, HBM -> HBM) and copies it out; swap-in copies in and scatters.
-  // Measured (profiles/r02/c4_swap_grid.jsonl): staging pays off only for many short runs
-  // (512 x 64 KiB random ids: 0.94 vs 0.86 of the link); a few runs are dominated by the fixed
-  // per-call DMA latency (~8 us) either way, and runs of >= 512 KiB blocks stream at the link rate.
+  // Measured (profiles/r02/c4_swap_grid.jsonl, profiles/r02s2/swap_stage_threshold.jsonl): with one
+  // DMA per run, 64 KiB random ids reach 0.31 / 0.42 of the link at 16 / 32 blocks; staged from 4
+  // runs on, 0.58 / 0.73; below ~8 blocks the fixed per-call latency (~8 us) bounds either way, and
+  // runs of >= 512 KiB blocks stream at the link rate.
   const int64_t kStageRunBytes = 256 << 10;
-  const bool staged = c->swap_stage && runs >= 16 &&
+  const bool staged = c->swap_stage && (int64_t)runs >= c->stage_min_runs &&
                       (int64_t)(moves.size() * c->m_block) < kStageRunBytes * (int64_t)runs && c->m_block % 16 == 0;
   if (staged) {
     const int dir = dst == S2L_TIER_GPU ? 1 : 0;
@@ -679,6 +681,8 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
     c->split_direct = !(e && e[0] == '0');
     e = getenv("S2L_SWAP_STAGE");
     c->swap_stage = !(e && e[0] == '0');
+    e = getenv("S2L_STAGE_MIN_RUNS");
+    if (e && atoll(e) > 0) c->stage_min_runs = atoll(e);
 
     e = getenv("S2L_TRACE");
     if (e && e[0] == '1') {
