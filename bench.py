@@ -820,6 +820,99 @@ def c3_field(rank, world, dist, dev_index, pk, steps=5):
     return res
 
 
+def c2t_field(rank, world, dist, dev_index, pk, steps=5):
+    """C2t: the trace-shaped variant of C2 for the crawler -- 8 requests per
+    rank of Llama-3-8B attention shape whose totals are LogNormal(ln 5800, 0.976) (the crawler's
+    median 5.8K) truncated to [512, 16384], each split into U{6..10} near-equal chunks
+    (P:L306); one chunk per request per step while it has chunks left, so every step is a
+    ragged batch (chunk lengths and positions not multiples of the block size).  Whole stream
+    per replay (new_request .. release), median of `steps`; inputs: seeded device randn."""
+    import torch
+    from paper_2604_16395_b200 import s2l
+    R, TMAX = NREQ, TOTAL
+    rng = np.random.default_rng(1002 + rank)
+    tot = np.clip(np.round(rng.lognormal(np.log(5800.0), 0.976, R)), 512, TMAX).astype(int)
+    nch = rng.integers(6, 11, R)
+    chunks = [[int(t) // c + (1 if i < int(t) % c else 0) for i in range(c)] for t, c in zip(tot, nch)]
+    g = torch.Generator(device="cuda").manual_seed(1002 + rank)
+    K = [_randn_bf16(g, int(t), H_KV, D) for t in tot]
+    V = [_randn_bf16(g, int(t), H_KV, D) for t in tot]
+    Q = [_randn_bf16(g, int(t), H_Q, D) for t in tot]
+    O = [torch.empty_like(q) for q in Q]
+    steps_in = []                                          # per step: items + concatenated inputs
+    flops = 0.0
+    for s in range(int(nch.max())):
+        act = [r for r in range(R) if s < nch[r]]
+        pos = [sum(chunks[r][:s]) for r in act]
+        ln = [chunks[r][s] for r in act]
+        off = np.concatenate([[0], np.cumsum(ln)]).astype(int)
+        kk = torch.cat([K[r][p:p + n] for r, p, n in zip(act, pos, ln)]).unsqueeze(0).contiguous()
+        vv = torch.cat([V[r][p:p + n] for r, p, n in zip(act, pos, ln)]).unsqueeze(0).contiguous()
+        qq = torch.cat([Q[r][p:p + n] for r, p, n in zip(act, pos, ln)]).contiguous()
+        app = [(r, None, n, int(o)) for r, n, o in zip(act, ln, off)]
+        pre = [(r, p, n, int(o)) for r, p, n, o in zip(act, pos, ln, off)]
+        steps_in.append((app, pre, kk, vv, qq, torch.empty_like(qq), act, pos, ln, off))
+        flops += sum(attn_flops(n, p) for p, n in zip(pos, ln))
+    cfg = s2l.make_config(1, H_Q, H_KV, D, KB, R * TMAX // KB + 64, 0, max_requests=R, max_blocks_per_request=TMAX // KB)
+    pool = torch.empty(cfg.num_gpu_blocks * s2l.block_bytes(cfg) // 2, dtype=torch.bfloat16, device=f"cuda:{dev_index}")
+    ctx = s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None)
+    toks = [np.zeros(int(t), np.int32) for t in tot]
+
+    def stream():
+        for r in range(R):
+            ctx.new_request(r, toks[r])
+        for app, pre, kk, vv, qq, oo, *_ in steps_in:
+            ctx.append_chunk(app, kk, vv)
+            ctx.prefill_batch(0, pre, qq, oo)
+        for r in range(R):
+            ctx.release(r)
+
+    stream()
+    torch.cuda.synchronize()
+    times, attn_ms = [], 0.0
+    for _ in range(steps):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx.set_timing(True)
+        e0.record()
+        stream()
+        e1.record()
+        torch.cuda.synchronize()
+        attn_ms += ctx.timing_read()["attn_ms"]
+        ctx.set_timing(False)
+        times.append(_reduce_max(e0.elapsed_time(e1), dist))
+    ms = statistics.median(times)
+    ach = flops * steps / (attn_ms * 1e-3) / 1e12
+    res = {"workload": "C2t (SURVEY d.2): 8 crawler-shaped requests per GPU, totals LogNormal(ln 5800, 0.976) "
+                       "in [512, 16384], U{6..10} chunks each, one chunk per request per step",
+           "totals": [int(t) for t in tot], "chunks": [int(c) for c in nch],
+           "ms_per_stream": ms, "value": flops * world / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+           "prefill_tokens_per_s": float(tot.sum()) * world / (ms * 1e-3), "replays": steps,
+           "stat": "median of streams, max over ranks",
+           "roofline": {"bound": "tensor", "achieved_rank0": ach, "peak": pk["bf16"], "unit": "TFLOP/s",
+                        "frac": ach / pk["bf16"], "kernel": "attn_tc2_kernel"}}
+    if rank == 0:                                          # sampled rows of every request's last chunk
+        from oracle.attention import attention_rows
+        worst = 0.0
+        last = {}
+        for st in steps_in:
+            for r, p, n, o in zip(st[6], st[7], st[8], st[9]):
+                last[r] = (st, p, n, int(o))
+        rs = np.random.default_rng(7)
+        for r in range(R):
+            st, p, n, o = last[r]
+            kin, vin = _bits(K[r][:p + n]), _bits(V[r][:p + n])
+            rows = sorted(set([0, n - 1] + rs.integers(0, n, 2).tolist()))
+            ref, _ = attention_rows(_bits(st[4][o:o + n]), kin, vin, p, rows)
+            got = st[5][o:o + n][rows].float().cpu().numpy().astype(np.float64)
+            worst = max(worst, float(_normwise(got, ref).max()))
+        res["parity"] = {"requests_checked": R, "max_normwise_err": worst, "tol": 2e-2, "pass": worst <= 2e-2}
+    ctx.close()
+    return res
+
+
 def concurrent_link(dev, dist):
     """Host-link aggregate with every rank copying at the same time (C4's scaling
     roofline): 1 GiB per rank per direction, barrier-started, bytes of all ranks / max time."""
@@ -1100,6 +1193,7 @@ def main():
     line["c5"] = c5_field(rank, world, dist, dev_index, pk)
     torch.cuda.empty_cache()
     line["c3"] = c3_field(rank, world, dist, dev_index, pk)
+    line["c2t"] = c2t_field(rank, world, dist, dev_index, pk)
     torch.cuda.empty_cache()
 
     if not args.no_side and rank == 0:
