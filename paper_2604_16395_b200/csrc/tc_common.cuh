@@ -11,7 +11,7 @@
 #include <cudaTypedefs.h>
 
 #ifndef S2L_POLY_PAIRS
-#define S2L_POLY_PAIRS 1   // of every 8 exp2 pairs, this many on the FMA pipe (polynomial)
+#define S2L_POLY_PAIRS 2   // of every 8 exp2 pairs, this many on the FMA pipe (polynomial)
 #endif
 
 namespace s2l {

@@ -124,6 +124,20 @@ def test_tc_gqa_ragged(h_q, h_kv):
     _multi_request_case(P, 77, geo, [517, 300, 129], [[200, 317], [1, 299], [128, 1]])
 
 
+def test_c2t_crawler_shaped_ragged_chunks():
+    """C2t, reduced: Llama-3-8B attention shape, 6 requests whose totals are
+    LogNormal(ln 5800, 0.976) draws scaled down to [97, 1500] tokens, each split into U{6..10}
+    near-equal chunks, one chunk per request per round -- every round is a ragged
+    batch (lengths and positions off the block size); every row of every round vs the oracle."""
+    geo = W.LLAMA3_8B
+    rng = np.random.default_rng(1002)
+    tot = np.clip(np.round(rng.lognormal(np.log(5800.0), 0.976, 6) / 10), 97, 1500).astype(int)
+    nch = rng.integers(6, 11, 6)
+    chunks = [[int(t) // c + (1 if i < int(t) % c else 0) for i in range(c)] for t, c in zip(tot, nch)]
+    P = Pair(1, 32, 8, 128, 16, 700, 0)
+    _multi_request_case(P, W.seed_of(2), geo, [int(t) for t in tot], chunks)
+
+
 @pytest.mark.parametrize("k", [32, 64, 128])
 def test_tc_block_sizes(k):
     geo = W.Geometry(L=2, h_q=8, h_kv=2, d=128, k=k)
