@@ -22,7 +22,10 @@ constexpr int kBM = 128;
 constexpr int kBN = 128;
 constexpr uint32_t kTileBytes = kBM * kD * 2;  // 32 KB: a 128 x 128 bf16 operand tile
 constexpr uint32_t kAtom = 16384;              // one [128 rows][64 cols] SW128 column of atoms
-constexpr float kRescaleThresh = 8.0f;         // log2 units: rescale when max grows 256x
+#ifndef S2L_RESCALE_THRESH
+#define S2L_RESCALE_THRESH 8.0f
+#endif
+constexpr float kRescaleThresh = S2L_RESCALE_THRESH;   // log2 units: rescale when max grows 256x
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

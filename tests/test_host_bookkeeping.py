@@ -48,10 +48,16 @@ def test_config_validation():
                 s2l.make_config(1, 2, 1, 16, 3, 8, 8),        # block not power of two
                 s2l.make_config(1, 2, 1, 16, 4, 8, 8, lcp_block_aligned=2),
                 s2l.make_config(1, 2, 1, 16, 4, 8, 8, alloc_cooling=2),
-                s2l.make_config(1, 2, 1, 16, 4, 8, 8, kv_dtype=2)]:
+                s2l.make_config(1, 2, 1, 16, 4, 8, 8, kv_dtype=2),
+                # token positions / table indices are 32-bit on the device
+                s2l.make_config(1, 2, 1, 16, 256, 8, 8, max_blocks_per_request=1 << 23),
+                s2l.make_config(1, 2, 1, 16, 4, 8, 8, max_requests=1 << 16, max_blocks_per_request=1 << 15)]:
         with pytest.raises(s2l.S2LError) as e:
             s2l.Context(bad, host_only=True)
         assert e.value.status == s2l.E_INVAL
+    # the largest accepted geometry just below both limits
+    s2l.Context(s2l.make_config(1, 2, 1, 16, 256, 8, 8, max_requests=1,
+                                max_blocks_per_request=(1 << 23) - 1), host_only=True).close()
 
 
 def _pair(L=1, h_q=2, h_kv=1, d=16, k=4, ng=8, nc=8, aligned=False, max_requests=64, max_blocks=None,
