@@ -137,7 +137,9 @@ constexpr int kThreads = 384;
 // setmaxnreg.inc waits forever.
 constexpr int kRegLaunch = 168, kRegCtrl = 88, kRegSoftmax = 208;
 static_assert(128 * kRegCtrl + 256 * kRegSoftmax <= kThreads * kRegLaunch, "register pool");
-constexpr int kPolyPairsPer8 = S2L_POLY_PAIRS;   // of every 8 exp2 pairs, this many on the FMA pipe
+// of every 8 exp2 pairs, this many on the FMA pipe: 2 for bf16 pools; 1 for FP8 pools, whose
+// converter warps already load the FMA / ALU pipes of SMSPs 2-3 (A/B in profiles/r02s2)
+template <bool kFp8> constexpr int kPolyPairsPer8 = kFp8 ? S2L_POLY_PAIRS_FP8 : S2L_POLY_PAIRS;
 // Shared-memory layout (bytes from the 1024-aligned base):
 //   Q tiles 0/1 | K/V ring of NST 32-KB bf16 tiles (K-major / MN-major SW128 images) |
 //   FP8 pools only: F8ST 16-KB staging slots for the E4M3 tiles TMA brings in (dense
@@ -665,10 +667,10 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         tmem_ld32(tS + 32, sv + 32);
         tmem_ld32(tS + 64, sv + 64);
         tmem_ld32(tS + 96, sv + 96);
-        float2 acc = chunk_p32<kPolyPairsPer8, kFp8>(sv, make_float2(0.f, 0.f), sc2, nm2, pk);
+        float2 acc = chunk_p32<kPolyPairsPer8<kFp8>, kFp8>(sv, make_float2(0.f, 0.f), sc2, nm2, pk);
         tmem_st16(tS, pk);
         tmem_wait_ld();
-        acc = chunk_p32<kPolyPairsPer8, kFp8>(sv + 32, acc, sc2, nm2, pk);
+        acc = chunk_p32<kPolyPairsPer8<kFp8>, kFp8>(sv + 32, acc, sc2, nm2, pk);
         tmem_st16(tS + 16, pk);
         max32<false>(sv, 0, 0, mt);
         max32<false>(sv + 32, 0, 32, mt);
@@ -681,9 +683,9 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
           tc_fence_before();
           mbar_arrive(bar(WB_PF + i));                  // P keys 0-63
           if (tr) TRACE(23, i, j);
-          acc = chunk_p32<kPolyPairsPer8, kFp8>(sv + 64, acc, sc2, nm2, pk);
+          acc = chunk_p32<kPolyPairsPer8<kFp8>, kFp8>(sv + 64, acc, sc2, nm2, pk);
           tmem_st16(tS + 32, pk);
-          acc = chunk_p32<kPolyPairsPer8, kFp8>(sv + 96, acc, sc2, nm2, pk);
+          acc = chunk_p32<kPolyPairsPer8<kFp8>, kFp8>(sv + 96, acc, sc2, nm2, pk);
           tmem_st16(tS + 48, pk);
           tmem_wait_st();
           tc_fence_before();
@@ -741,7 +743,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       for (int hh = 0; hh < 2; ++hh) {
         uint32_t pk[32];
         acc = masked_tile ? chunk_p64<true, 0, kFp8>(sv + 64 * hh, acc, vis, 64 * hh, sc2, nm2, pk)
-                          : chunk_p64<false, kPolyPairsPer8, kFp8>(sv + 64 * hh, acc, vis, 64 * hh, sc2, nm2, pk);
+                          : chunk_p64<false, kPolyPairsPer8<kFp8>, kFp8>(sv + 64 * hh, acc, vis, 64 * hh, sc2, nm2, pk);
         tmem_st16(tS + 32 * hh, pk);
         tmem_st16(tS + 32 * hh + 16, pk + 16);
         tmem_wait_st();                // keys 64hh .. 64hh+63 of P are in TMEM

@@ -13,6 +13,9 @@
 #ifndef S2L_POLY_PAIRS
 #define S2L_POLY_PAIRS 2   // of every 8 exp2 pairs, this many on the FMA pipe (polynomial)
 #endif
+#ifndef S2L_POLY_PAIRS_FP8
+#define S2L_POLY_PAIRS_FP8 1   // the FP8-pool kernel's share
+#endif
 
 namespace s2l {
 namespace {
