@@ -478,6 +478,66 @@ def oracle_sample(data, budget_s=15.0):
     return flops / t_tot / 1e12, desc, threads
 
 
+def oracle_extra_samples(budget_s=6.0):
+    """the fp64 oracle on bounded subsets of C3 and C5 (seeded N(0,1) rows from
+    numpy, the same distribution as the GPU fields), with the full-config time extrapolated from
+    the measured rate (labelled so), plus host LCP throughput on a C3-sized token pair."""
+    from oracle.lcp import lcp
+    rng = np.random.default_rng(5)
+    out = {}
+    bf = lambda *sh: (rng.standard_normal(sh).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    # C3: one update of one request (p = 4096 of 8192: 4096 recomputed rows); the oracle's batched
+    # path on the first R rows of the chunk, R doubling until the budget
+    from oracle.attention import attention
+    T, p0 = 8192, 4096
+    q, k, v = bf(T - p0, H_Q, D), bf(T, H_KV, D), bf(T, H_KV, D)
+    R, t, fl = 16, 0.0, 0.0
+    while True:
+        t0 = time.perf_counter()
+        attention(q[:R], k[:p0 + R], v[:p0 + R], p0)
+        t += time.perf_counter() - t0
+        fl += attn_flops(R, p0)
+        if t > budget_s or 2 * R > T - p0:
+            break
+        R *= 2
+    rate = fl / t
+    full = 32 * attn_flops(T - p0, p0)
+    out["c3"] = {"sample": f"one C3 update (p = 4096): chunk rows [0, R) for R = 16 .. {R}, 32 heads, {t:.1f} s",
+                 "gflops_fp64": rate / 1e9, "extrapolated_update_round_s": full / rate,
+                 "extrapolated_note": "32 requests x 4096 rows at the measured rate (extrapolated)"}
+    # C5: the last chunk of the 128K stream for one kv group (8 q heads, p0 = 129024)
+    T5, c5 = 131072, 2048
+    p5 = T5 - c5
+    q5, k5, v5 = bf(c5, 8, D), bf(T5, 1, D), bf(T5, 1, D)
+    R, t, fl = 8, 0.0, 0.0
+    while True:
+        t0 = time.perf_counter()
+        attention(q5[:R], k5[:p5 + R], v5[:p5 + R], p5)
+        t += time.perf_counter() - t0
+        fl += attn_flops(R, p5, h_q=8)
+        if t > budget_s or 2 * R > c5:
+            break
+        R *= 2
+    rate5 = fl / t
+    full5 = sum(attn_flops(c5, j * c5, h_q=64) for j in range(T5 // c5))
+    out["c5"] = {"sample": f"C5 last chunk, one kv group (8 q heads): rows [0, R) for R = 8 .. {R}, {t:.1f} s",
+                 "gflops_fp64": rate5 / 1e9, "extrapolated_stream_s": full5 / rate5,
+                 "extrapolated_note": "the whole 128K C5 stream, 64 q heads, at the measured rate (extrapolated)"}
+    # host LCP on a C3-sized token pair (P:L170): bytes compared per second
+    a = rng.integers(0, 128256, 8192).astype(np.int32)
+    b = a.copy()
+    b[6000:] = rng.integers(0, 128256, 8192 - 6000)
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < 0.5:
+        lcp(a, b)
+        n += 1
+    dt = time.perf_counter() - t0
+    out["lcp_oracle"] = {"pair": "8192-token C3 input, LCP 6000", "calls": n, "us_per_call": dt / n * 1e6,
+                         "gb_per_s": n * 6001 * 4 / dt / 1e9}
+    return out
+
+
 def reference_arm(args, rank, world):
     """--impl reference: the oracle timed on the host cores on this arm's workload and metric."""
     if rank != 0:
@@ -1255,6 +1315,8 @@ def main():
         # the oracle on the host cores (bounded sample), after all device timing
         v, desc, thr = oracle_sample(data)
         line["cpu_baseline"] = {"value": v, "unit": "TFLOP/s", "cores": thr, "kind": "oracle", "sample": desc}
+        if not args.no_side:
+            line["cpu_baseline"]["extra"] = oracle_extra_samples()
         print(json.dumps(line), flush=True)
     ctx.close()
     if dist:
