@@ -1,7 +1,7 @@
 """Same-window comparison of libs2l's attention with the FlashAttention-4 Blackwell forward
 kernel (CuTe-DSL, shipped inside vllm as `vllm.vllm_flash_attn.cute`) on the C2 stream.
 
-    python tools/fa4_compare.py [--reps 5] [--out gpurun_out/fa4_compare.json]
+    python tools/fa4_compare.py [--reps 5] [--c5] [--out gpurun_out/fa4_compare.json]
 
 A LIBRARY comparator (like timing cuBLAS beside a GEMM): it is not on libs2l's path and nothing
 in the product imports it.  Workload = bench.py's C2 (BJ:L8): 8 requests, 32 q / 8 kv heads,
@@ -13,6 +13,7 @@ d 128, 512-token chunks from 0 to 16K; per step the chunk's queries attend causa
   * fa4_paged: FA4 with page_table over a [pages][16][h_kv][d] K and V cache (same page ids).
   * fa4_dense: FA4 over batch-padded contiguous K/V ([8][16384][h_kv][d]) with seqused_k -- FA4's
                best case (no paging).
+--c5: the long-chunk config instead (BJ:L11: one request, 128K context, 2K chunks, 64q/8kv).
 Timing: CUDA events around each launch on the current stream, median of --reps replays per step.
 The outputs of step 31 are compared (per-row normwise difference, the parity metric of the tests).
 """
@@ -33,6 +34,8 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 
 NREQ, CHUNK, TOTAL, H_Q, H_KV, D, KB = bench.NREQ, bench.CHUNK, bench.TOTAL, bench.H_Q, bench.H_KV, bench.D, bench.KB
+if "--c5" in sys.argv:
+    NREQ, CHUNK, TOTAL, H_Q = 1, 2048, 131072, 64
 STEPS = TOTAL // CHUNK
 
 
@@ -52,6 +55,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "fa4_compare.json"))
+    ap.add_argument("--c5", action="store_true")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     torch.cuda.set_device(dev)
@@ -60,11 +64,17 @@ def main():
     q = [torch.randn(NREQ * CHUNK, H_Q, D, device=dev, generator=g).to(torch.bfloat16) for _ in range(STEPS)]
     k = [torch.randn(1, NREQ * CHUNK, H_KV, D, device=dev, generator=g).to(torch.bfloat16) for _ in range(STEPS)]
     v = [torch.randn(1, NREQ * CHUNK, H_KV, D, device=dev, generator=g).to(torch.bfloat16) for _ in range(STEPS)]
-    fl = [NREQ * bench.attn_flops(CHUNK, j * CHUNK) for j in range(STEPS)]
-    res = {"workload": "C2 (BJ:L8) stream, 8 x 512-token chunks to 16K, 32q/8kv, d 128", "reps": a.reps}
+    ap_c5 = "--c5" in sys.argv
+    fl = [NREQ * bench.attn_flops(CHUNK, j * CHUNK, h_q=H_Q) for j in range(STEPS)]
+    res = {"workload": ("C5 (BJ:L11) stream, 1 x 2048-token chunks to 128K, 64q/8kv, d 128" if ap_c5 else
+                        "C2 (BJ:L8) stream, 8 x 512-token chunks to 16K, 32q/8kv, d 128"), "reps": a.reps}
 
     # ---- libs2l
-    ctx, pool = bench.make_ctx(0)
+    from paper_2604_16395_b200 import s2l
+    nblk_all = NREQ * TOTAL // KB
+    cfg = s2l.make_config(1, H_Q, H_KV, D, KB, nblk_all, 0, max_requests=NREQ, max_blocks_per_request=TOTAL // KB)
+    pool = torch.empty(nblk_all * s2l.block_bytes(cfg) // 2, dtype=torch.bfloat16, device=dev)
+    ctx = s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None)
     rids = list(range(NREQ))
     toks = [list(range(TOTAL)) for _ in rids]
     items_a = [[(r, None, CHUNK, i * CHUNK) for i, r in enumerate(rids)] for _ in range(STEPS)]
