@@ -6,25 +6,26 @@
 // 0 .. q_pos+t of kv head g = h / G (G = h_q/h_kv), softmax scale 1/sqrt(128), K/V read from
 // the paged pool through the request's block table.
 //
-// Tiling (one CTA = one 128-row Q tile of one (item, kv head)):
+// Tiling (one CTA = one work unit: a pair of 128-row Q tiles of one (item, kv head), or a
+// KV-range piece of such a unit in the tail wave; details in DESIGN.md §6):
 //   * GQA packing: tile row r = (token t0 + r/G, q head g*G + r%G), so the G heads that share
-//     a kv head share every K/V tile (one TMA of Q: box {64, G, 128/G} over [rows][h_q][d]).
-//   * KV tiles of 128 keys; each 16-token (k-token) block is one TMA box {64, k} per d-half
-//     at row (((block*L + layer)*2 + K|V)*h_kv + g)*k of the pool viewed as [rows][128].
-//     Boxes land at 2 KB (k*128 B) offsets, giving the canonical K-major SWIZZLE_128B
-//     layout [d-half][128 keys][64] without a gather.
-//   * S = Q·K^T: 8 x tcgen05.mma M=128 N=128 K=16 (A, B K-major SW128) into TMEM
-//     (two S buffers of 128 columns, so S_{j+1} runs on the tensor core while the softmax
-//     warps work on S_j).
-//   * softmax warps (4 warps, thread = TMEM lane = row) tcgen05.ld S, mask, online softmax
-//     in fp32 with exp2 (log2 e folded into the scale), lazy rescale of O (only when the row
-//     max grows by > 2^8), write P as bf16 into shared memory in the K-major SW128 layout.
-//   * O += P·V: 8 x tcgen05.mma M=128 N=128 K=16, A = P (K-major), B = V (MN-major SW128,
-//     V is [keys][d] with d contiguous, LBO = 16 KB between d-halves) into TMEM O.
-//   * epilogue: tcgen05.ld O, divide by the row sum, bf16 store; optional LSE.
-// Warp roles: 0 = TMA producer, 1 = MMA issuer (one thread), 2 = TMEM allocator,
-// 4..7 = softmax / correction / epilogue.  Pipelines: K ring x2, V ring x2 (TMA -> MMA),
-// S x2 (MMA -> softmax), P x1 and O (softmax <-> MMA), all mbarrier-based.
+//     a kv head share every K/V tile (Q by TMA boxes {64, G, 128/G} over [rows][h_q][d]).
+//   * KV tiles of 128 keys in the canonical K-major SWIZZLE_128B layout [d-half][128 keys][64]:
+//     one 4-D TMA box per d-half when the tile's blocks have consecutive ids, else one 2-D box
+//     {64, k} per block and d-half; one ring of 5 x 32-KB slots (K_j, V_j, K_j+1, ...).
+//   * S_i = Q_i·K^T: 8 x tcgen05.mma M128 N128 K16 (SS) into TMEM S_i; O_i += P_i·V: 8 TS-MMAs
+//     with P_i in TMEM (aliasing S_i's first 64 columns) and V MN-major from shared memory.
+//     TMEM: S_0, S_1, O_0, O_1 (512 columns).  One MMA warp issues PV_0, S_0, PV_1, S_1 per KV
+//     step, which keeps the two tiles' softmaxes half a step apart on the shared SMSPs.
+//   * softmax (warpgroup per tile, thread = TMEM lane = row): stale-max exponentials against
+//     the running max as the score chunks arrive, exact path (max, lazy O rescale when the max
+//     grows by > 2^8) on the first, masked and violating tiles; exp2 on MUFU plus a
+//     polynomial share on the FMA pipe; P packed to bf16 (f16 for FP8 pools) in two halves.
+//   * epilogue: O / l from TMEM; full tiles staged in the freed Q buffer and written by TMA;
+//     split pieces merge (O_k, m_k, l_k) through a coalesced workspace or straight from TMEM.
+// Warp roles: 0 = TMA producer, 1 = MMA issuer + TMEM allocator, 2-3 = FP8 -> f16 converters
+// (FP8 pools only), 4-7 / 8-11 = softmax + epilogue of Q tile 0 / 1.  All hand-offs are
+// mbarriers; every wait traps after ~2^26 polls instead of hanging.
 #include "tc_common.cuh"
 
 #include <cstdlib>
@@ -124,9 +125,9 @@ __device__ __forceinline__ void cta_stamp(uint32_t* tr, int slot, bool global = 
 // while the MMAs of the other execute), P kept in TMEM (TS-MMA: A operand = P from TMEM,
 // aliasing the first 64 columns of that tile's S buffer), one unified K/V TMA ring of 5
 // 32-KB slots, packed f32x2 FMA / ADD in the softmax, setmaxnreg to give the two softmax
-// warpgroups 224 registers.  384 threads: warpgroup 0 = producer (warp 0), MMA issuer
-// (warp 1), TMEM allocator (warp 2); warpgroup 1 = softmax/epilogue of Q tile 0;
-// warpgroup 2 = softmax/epilogue of Q tile 1.
+// warpgroups 208 registers.  384 threads: warpgroup 0 = producer (warp 0), MMA issuer and
+// TMEM allocator (warp 1), FP8 converters (warps 2-3, FP8 pools); warpgroup 1 = softmax /
+// epilogue of Q tile 0; warpgroup 2 = softmax / epilogue of Q tile 1.
 // Hand-offs per tile i: MMA commits S_full[i] after S_i(j) (which also covers PV_i(j-1));
 // softmax_i writes P_i(j) into TMEM and arrives P_full[i]; MMA issues PV_i(j) then S_i(j+1)
 // (in-order tensor pipe: PV_i(j) reads P_i(j) before S_i(j+1) overwrites those columns).
