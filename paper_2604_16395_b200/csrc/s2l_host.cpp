@@ -205,7 +205,8 @@ struct s2l_ctx {
   int32_t* split_cnt = nullptr;       // per split unit arrival counters (self-resetting)
   bool split_enabled = true;
   bool split_direct = true;
-  int64_t stage_min_runs = 4;         // staged swaps need >= this many id runs (S2L_STAGE_MIN_RUNS)           // S2L_SPLIT_DIRECT=0: the last piece always merges from the workspace (tests)
+  int64_t stage_min_runs = 4;         // staged swaps need >= this many id runs (S2L_STAGE_MIN_RUNS)
+  int64_t stage_run_bytes = 256 << 10; // ... averaging fewer bytes than this (S2L_STAGE_RUN_BYTES)           // S2L_SPLIT_DIRECT=0: the last piece always merges from the workspace (tests)
   uint32_t* trace_buf = nullptr;      // S2L_TRACE=1: device buffer for kernel timelines (experiments)
   int64_t trace_launch = -1, attn_launch_no = 0;  // which attention launch to trace (S2L_TRACE_LAUNCH)
   bool tc_ok = false;
@@ -514,13 +515,19 @@ s2l_status swap_impl(s2l_ctx* c, int32_t n_reqs, const int64_t* ids, int64_t* by
   // Scattered GPU ids (short runs): stage through device memory so that every run of
   // consecutive HOST ids is one DMA -- swap-out gathers the GPU blocks into a contiguous
   // staging buffer (one kernel, HBM -> HBM) and copies it out; swap-in copies in and scatters.
-  // Measured (profiles/r02/c4_swap_grid.jsonl, profiles/r02s2/swap_stage_threshold.jsonl): with one
-  // DMA per run, 64 KiB random ids reach 0.31 / 0.42 of the link at 16 / 32 blocks; staged from 4
-  // runs on, 0.58 / 0.73; below ~8 blocks the fixed per-call latency (~8 us) bounds either way, and
-  // runs of >= 512 KiB blocks stream at the link rate.
-  const int64_t kStageRunBytes = 256 << 10;
-  const bool staged = c->swap_stage && (int64_t)runs >= c->stage_min_runs &&
-                      (int64_t)(moves.size() * c->m_block) < kStageRunBytes * (int64_t)runs && c->m_block % 16 == 0;
+  // Measured (profiles/r02/c4_swap_grid.jsonl, profiles/r02s2/swap_stage_*.jsonl): with one DMA per
+  // run, 64 KiB random ids reach 0.31 / 0.42 of the link at 16 / 32 blocks; staged from 4 runs on,
+  // 0.58 / 0.73; 512 KiB blocks in ~1 MiB runs: 0.82 -> 0.92-0.94 staged at 64 / 512 blocks, but
+  // 0.80 -> 0.62 at 8 blocks (4 MiB); 2 MiB blocks stream at 0.94 unstaged and lose staged.  Below
+  // ~8 x 64 KiB the fixed per-transfer latency bounds either way (a contiguous 512 KiB copy
+  // reaches 0.52-0.55 of the link).
+  // Staged when there are enough runs and they are short: avg < stage_run_bytes (256 KiB), or
+  // avg < 2 MiB for a transfer of >= 16 MiB (the gather / scatter of a small transfer costs
+  // more than the per-DMA latency it saves; large runs stream at the link rate anyway).
+  const int64_t tot_bytes = (int64_t)moves.size() * c->m_block;
+  const bool staged = c->swap_stage && (int64_t)runs >= c->stage_min_runs && c->m_block % 16 == 0 &&
+                      (tot_bytes < c->stage_run_bytes * (int64_t)runs ||
+                       (tot_bytes >= (16ll << 20) && tot_bytes < (2ll << 20) * (int64_t)runs));
   if (staged) {
     const int dir = dst == S2L_TIER_GPU ? 1 : 0;
     const size_t cap_bytes = std::max<size_t>((size_t)c->m_block, (size_t)64 << 20);
@@ -683,6 +690,8 @@ s2l_status s2l_create(const s2l_config* cfg, void* gpu_pool, void* cpu_pool_pinn
     c->swap_stage = !(e && e[0] == '0');
     e = getenv("S2L_STAGE_MIN_RUNS");
     if (e && atoll(e) > 0) c->stage_min_runs = atoll(e);
+    e = getenv("S2L_STAGE_RUN_BYTES");
+    if (e && atoll(e) > 0) c->stage_run_bytes = atoll(e);
 
     e = getenv("S2L_TRACE");
     if (e && e[0] == '1') {
