@@ -629,6 +629,16 @@ def _reduce_max(x, dist):
     return float(t.item())
 
 
+def _reduce_sum(x, dist):
+    """sum over ranks of a host float (work whose size differs per rank)."""
+    if not dist:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def _gather(x, dist, world):
     """all_gather of a float32 tensor (device) -> list of host tensors (rank order)."""
     import torch
@@ -844,9 +854,9 @@ def c3_field(rank, world, dist, dev_index, pk, steps=5):
     ms = statistics.median(times)
     ach = flops * steps / (attn_ms * 1e-3) / 1e12
     res = {"workload": "C3 (BJ:L9): update round, 32 requests x 8192 tokens per GPU, LCP ~ U[20%, 80%]",
-           "ms_per_round": ms, "value": flops * world / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+           "ms_per_round": ms, "value": _reduce_sum(flops, dist) / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
            "pct_bf16_peak": 100.0 * flops / (ms * 1e-3) / 1e12 / pk["bf16"],
-           "tokens_recomputed_per_round": int(Rn) * world, "replays": steps,
+           "tokens_recomputed_per_round": int(_reduce_sum(float(Rn), dist)), "replays": steps,
            "stat": "median of rounds, max over ranks",
            "roofline": {"bound": "tensor", "achieved_rank0": ach, "peak": pk["bf16"], "unit": "TFLOP/s",
                         "frac": ach / pk["bf16"], "kernel": "attn_tc2_kernel"},
@@ -948,8 +958,8 @@ def c2t_field(rank, world, dist, dev_index, pk, steps=5):
     res = {"workload": "C2t (SURVEY d.2): 8 crawler-shaped requests per GPU, totals LogNormal(ln 5800, 0.976) "
                        "in [512, 16384], U{6..10} chunks each, one chunk per request per step",
            "totals": [int(t) for t in tot], "chunks": [int(c) for c in nch],
-           "ms_per_stream": ms, "value": flops * world / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-           "prefill_tokens_per_s": float(tot.sum()) * world / (ms * 1e-3), "replays": steps,
+           "ms_per_stream": ms, "value": _reduce_sum(flops, dist) / (ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+           "prefill_tokens_per_s": _reduce_sum(float(tot.sum()), dist) / (ms * 1e-3), "replays": steps,
            "stat": "median of streams, max over ranks",
            "roofline": {"bound": "tensor", "achieved_rank0": ach, "peak": pk["bf16"], "unit": "TFLOP/s",
                         "frac": ach / pk["bf16"], "kernel": "attn_tc2_kernel"}}
