@@ -33,6 +33,9 @@
 #include <mutex>
 
 // Build-time variants (experiments; defaults are the measured best).
+#ifndef S2L_NST_BF16
+#define S2L_NST_BF16 5        // K/V ring slots of the bf16 kernel (32 KB each)
+#endif
 #ifndef S2L_OUT_WAIT_READ
 #define S2L_OUT_WAIT_READ 1
 #endif
@@ -147,7 +150,7 @@ template <bool kFp8> constexpr int kPolyPairsPer8 = kFp8 ? S2L_POLY_PAIRS_FP8 : 
 //   [128 keys][128 d] bytes), converted to the bf16 ring by warps 2-3 | mbarriers | TMEM addr.
 template <bool kFp8>
 struct Lay {
-  static constexpr int NST = kFp8 ? 4 : 5;
+  static constexpr int NST = kFp8 ? 4 : S2L_NST_BF16;
   static constexpr int F8ST = kFp8 ? 2 : 0;
   static constexpr uint32_t kF8Tile = 16384;
   static constexpr uint32_t OFF_Q0 = 0, OFF_Q1 = kTileBytes, OFF_RING = 2 * kTileBytes;
