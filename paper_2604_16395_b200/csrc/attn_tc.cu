@@ -36,6 +36,12 @@
 #ifndef S2L_NST_BF16
 #define S2L_NST_BF16 5        // K/V ring slots of the bf16 kernel (32 KB each)
 #endif
+#ifndef S2L_NST_FP8
+#define S2L_NST_FP8 3         // converted (f16) K/V ring slots of the FP8 kernel
+#endif
+#ifndef S2L_F8ST
+#define S2L_F8ST 4            // E4M3 staging slots of the FP8 kernel (16 KB each; 3 + 4 beat 4 + 2 by ~2 %)
+#endif
 #ifndef S2L_OUT_WAIT_READ
 #define S2L_OUT_WAIT_READ 1
 #endif
@@ -150,8 +156,8 @@ template <bool kFp8> constexpr int kPolyPairsPer8 = kFp8 ? S2L_POLY_PAIRS_FP8 : 
 //   [128 keys][128 d] bytes), converted to the bf16 ring by warps 2-3 | mbarriers | TMEM addr.
 template <bool kFp8>
 struct Lay {
-  static constexpr int NST = kFp8 ? 4 : S2L_NST_BF16;
-  static constexpr int F8ST = kFp8 ? 2 : 0;
+  static constexpr int NST = kFp8 ? S2L_NST_FP8 : S2L_NST_BF16;
+  static constexpr int F8ST = kFp8 ? S2L_F8ST : 0;
   static constexpr uint32_t kF8Tile = 16384;
   static constexpr uint32_t OFF_Q0 = 0, OFF_Q1 = kTileBytes, OFF_RING = 2 * kTileBytes;
   static constexpr uint32_t OFF_F8 = OFF_RING + NST * kTileBytes;
