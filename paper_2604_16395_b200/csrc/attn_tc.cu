@@ -12,7 +12,8 @@
 //     a kv head share every K/V tile (Q by TMA boxes {64, G, 128/G} over [rows][h_q][d]).
 //   * KV tiles of 128 keys in the canonical K-major SWIZZLE_128B layout [d-half][128 keys][64]:
 //     one 4-D TMA box per d-half when the tile's blocks have consecutive ids, else one 2-D box
-//     {64, k} per block and d-half; one ring of 5 x 32-KB slots (K_j, V_j, K_j+1, ...).
+//     {64, k} per block and d-half; one ring of 5 x 32-KB slots (K_j, V_j, K_j+1, ...) at the
+//     base of shared memory, the two Q tiles after it.
 //   * S_i = Q_i·K^T: 8 x tcgen05.mma M128 N128 K16 (SS) into TMEM S_i; O_i += P_i·V: 8 TS-MMAs
 //     with P_i in TMEM (aliasing S_i's first 64 columns) and V MN-major from shared memory.
 //     TMEM: S_0, S_1, O_0, O_1 (512 columns).  One MMA warp issues PV_0, S_0, PV_1, S_1 per KV
@@ -151,7 +152,8 @@ static_assert(128 * kRegCtrl + 256 * kRegSoftmax <= kThreads * kRegLaunch, "regi
 // converter warps already load the FMA / ALU pipes of SMSPs 2-3 (A/B in profiles/r02s2)
 template <bool kFp8> constexpr int kPolyPairsPer8 = kFp8 ? S2L_POLY_PAIRS_FP8 : S2L_POLY_PAIRS;
 // Shared-memory layout (bytes from the 1024-aligned base):
-//   Q tiles 0/1 | K/V ring of NST 32-KB bf16 tiles (K-major / MN-major SW128 images) |
+//   bf16 pools: K/V ring of NST 32-KB tiles (K-major / MN-major SW128 images) | Q tiles 0/1 |
+//   FP8 pools: Q tiles 0/1 | converted K/V ring |
 //   FP8 pools only: F8ST 16-KB staging slots for the E4M3 tiles TMA brings in (dense
 //   [128 keys][128 d] bytes), converted to the bf16 ring by warps 2-3 | mbarriers | TMEM addr.
 template <bool kFp8>
@@ -159,8 +161,13 @@ struct Lay {
   static constexpr int NST = kFp8 ? S2L_NST_FP8 : S2L_NST_BF16;
   static constexpr int F8ST = kFp8 ? S2L_F8ST : 0;
   static constexpr uint32_t kF8Tile = 16384;
-  static constexpr uint32_t OFF_Q0 = 0, OFF_Q1 = kTileBytes, OFF_RING = 2 * kTileBytes;
-  static constexpr uint32_t OFF_F8 = OFF_RING + NST * kTileBytes;
+#ifndef S2L_Q_AFTER_RING
+#define S2L_Q_AFTER_RING 1     // bf16 kernels: K/V ring at the base, Q after it (+0.5 % C2 step, +0.6 % C5
+#endif                         // over Q first, 6 alternating A/B pairs each, profiles/r02s3/ab_placement.txt)
+  static constexpr bool kQLast = S2L_Q_AFTER_RING && !kFp8;
+  static constexpr uint32_t OFF_Q0 = kQLast ? NST * kTileBytes : 0, OFF_Q1 = OFF_Q0 + kTileBytes,
+                            OFF_RING = kQLast ? 0 : 2 * kTileBytes;
+  static constexpr uint32_t OFF_F8 = (2 + NST) * kTileBytes;
   static constexpr uint32_t OFF_BAR = OFF_F8 + F8ST * kF8Tile;
   // barriers: Q_full, ring_full[NST], ring_empty[NST], S_full[2], P_full[2] (keys 0-63),
   // P_half[2] (keys 64-127), O_fin[2], fp8 staging full[F8ST] / empty[F8ST], fp8: Q in f16

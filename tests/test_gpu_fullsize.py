@@ -246,3 +246,39 @@ def test_c2_full_size_peaky_and_needles(variant):
         vj = (vj.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
         assert np.abs(o_ref[0, h] - vj).max() < 0.05
     assert worst <= 2e-2
+
+
+@pytest.mark.slow
+def test_c5_full_size_sampled_rows():
+    """C5 (BJ:L11) at full size in the bench's launch configuration: one request of
+    Llama-3-70B attention shape (64 q / 8 kv heads, d 128, block 16), 128K context streamed as
+    64 chunks of 2048 tokens (append + attention per chunk; every launch is long-chunk
+    prefill, the north_star's >= 60 % target).  Sampled rows of the first, a middle and the
+    last chunk (all 64 heads, with LSE) vs the fp64 oracle; the last chunk's rows attend to up
+    to 131072 keys, so the tail-wave KV split, the lazy rescale and the stale-max path all run
+    at their longest.  Inputs: seeded device N(0,1) bf16, host copies to the oracle."""
+    T, chunk, hq, hkv, d, kb = 131072, 2048, 64, 8, 128, 16
+    cfg = s2l.make_config(1, hq, hkv, d, kb, T // kb + 64, 0, max_requests=1, max_blocks_per_request=T // kb)
+    pool = torch.empty(cfg.num_gpu_blocks * s2l.block_bytes(cfg) // 2, dtype=torch.bfloat16, device="cuda")
+    lib = s2l.Context(cfg, pool, None, torch.cuda.current_stream(), None)
+    g = torch.Generator(device="cuda").manual_seed(W.seed_of(5))
+    K, V = _randn(g, T, hkv, d), _randn(g, T, hkv, d)
+    Q = _randn(g, T, hq, d)
+    O = torch.empty_like(Q)
+    LSE = torch.zeros(T, hq, dtype=torch.float32, device="cuda")
+    lib.new_request(0, W.request_tokens(W.seed_of(5), 0, T))
+    for j in range(T // chunk):
+        a = j * chunk
+        lib.append_chunk([(0, None, chunk, 0)], K[a:a + chunk].unsqueeze(0).contiguous(),
+                         V[a:a + chunk].unsqueeze(0).contiguous())
+        lib.prefill_batch(0, [(0, a, chunk, 0)], Q[a:a + chunk], O[a:a + chunk], LSE[a:a + chunk])
+    torch.cuda.synchronize()
+    kbits, vbits = _bits(K), _bits(V)
+    rng = np.random.default_rng(11)
+    worst = 0.0
+    for j in (0, 31, 63):
+        a = j * chunk
+        rows = _rows(rng, chunk, extra=3)
+        worst = max(worst, _check_rows(O[a:a + chunk], _bits(Q[a:a + chunk]), kbits, vbits, a, rows,
+                                       LSE[a:a + chunk], tag=f"c5 chunk {j}"))
+    assert worst <= 2e-2
