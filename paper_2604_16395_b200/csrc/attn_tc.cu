@@ -146,7 +146,13 @@ constexpr int kThreads = 384;
 // setmaxnreg moves registers inside the CTA's launch allocation (384 x 168): the control
 // warpgroup releases first, the softmax warpgroups then grow; the sums must fit the pool or
 // setmaxnreg.inc waits forever.
-constexpr int kRegLaunch = 168, kRegCtrl = 88, kRegSoftmax = 208;
+#ifndef S2L_REG_CTRL
+#define S2L_REG_CTRL 88
+#endif
+#ifndef S2L_REG_SOFTMAX
+#define S2L_REG_SOFTMAX 208
+#endif
+constexpr int kRegLaunch = 168, kRegCtrl = S2L_REG_CTRL, kRegSoftmax = S2L_REG_SOFTMAX;
 static_assert(128 * kRegCtrl + 256 * kRegSoftmax <= kThreads * kRegLaunch, "register pool");
 // of every 8 exp2 pairs, this many on the FMA pipe: 2 for bf16 pools; 1 for FP8 pools, whose
 // converter warps already load the FMA / ALU pipes of SMSPs 2-3 (A/B in profiles/r02s2)
