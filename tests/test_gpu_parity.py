@@ -204,6 +204,61 @@ def test_c3_small_update_equals_fresh():
         row += 2048 - b
 
 
+def test_c3_small_budget_split_update_round():
+    """The C3 update round in scheduling steps of <= 1536 tokens (the token budget of P:L308,
+    scaled with the 4 x 2048 case; the bench's c3.budget_8192 field at full size): suffixes packed
+    in request order, a suffix that does not fit continues as the next chunk of that request
+    (partial suffix items at q_pos = p + done).  Bookkeeping, pool bytes and every row of every
+    step's attention vs the oracle (harness), and the outputs equal a fresh prefill's rows."""
+    geo = W.LLAMA3_8B
+    seed = W.seed_of(3) + 7
+    P = Pair(1, 32, 8, 128, 16, 1024, 0)
+    toks, data = _multi_request_case(P, seed, geo, [2048] * 4, [[1024, 1024]] * 4)
+    ps = W.c3_lcp_draws(seed, 4, 2048)
+    budget, steps, cur, fill = 1536, [], [], 0
+    fresh = {}
+    for r in range(4):
+        new = W.updated_tokens(seed, r, toks[r], int(ps[r]), 2048, 0)
+        assert P.invalidate(r, new) == (int(ps[r]), 2048 - int(ps[r]))
+        fresh[r] = (new,) + tuple(_stream_qkv(seed, new, geo))
+        done, n = 0, 2048 - int(ps[r])
+        while done < n:
+            take = min(n - done, budget - fill)
+            cur.append((r, int(ps[r]) + done, take))
+            done += take
+            fill += take
+            if fill == budget:
+                steps.append(cur)
+                cur, fill = [], 0
+    if cur:
+        steps.append(cur)
+    assert len(steps) >= 2 and any(len({it[0] for it in s}) > 1 for s in steps)
+    outs = {r: [] for r in range(4)}
+    for s in steps:
+        items_a, items_p, ks, vs, qs, row = [], [], [], [], [], 0
+        for r, a, n in s:
+            _, qn, kn, vn = fresh[r]
+            items_a.append((r, None, n, row)); items_p.append((r, a, n, row))
+            ks.append(kn[:, a:a + n]); vs.append(vn[:, a:a + n]); qs.append(qn[a:a + n])
+            row += n
+        P.append(items_a, np.concatenate(ks, axis=1), np.concatenate(vs, axis=1))
+        o_gpu, _, _, _ = P.prefill(items_p, np.concatenate(qs))      # every row vs the oracle
+        row = 0
+        for r, a, n in s:
+            outs[r].append(o_gpu[row:row + n])
+            row += n
+    P.check_state()
+    P.check_pools_whole()
+    F = Pair(1, 32, 8, 128, 16, 1024, 0, mirror=False)
+    for r in range(4):
+        new, qn, kn, vn = fresh[r]
+        F.new(r, new)
+        F.append([(r, None, 2048, 0)], kn, vn)
+        o_f, _, _, _ = F.prefill([(r, 0, 2048, 0)], qn)
+        b = int(ps[r])
+        assert normwise_err(np.concatenate(outs[r]), o_f[b:]).max() <= 2e-2
+
+
 def test_chunked_equals_one_shot_and_batch_independence():
     geo = W.LLAMA3_8B
     seed = 91
