@@ -1230,33 +1230,39 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
       mma_commit_elect(bar(B_RE + kslot));
       for (uint32_t n = 0;; ++n) {
         const uint32_t b = n & 1, nb = b ^ 1;
-        bool next = false;
-        int32_t nT_next = 0;
-        for (int32_t j = 0; j < nT; ++j) {
+        // steady steps: the same loop as attn_tc2_kernel's, with this unit's Q descriptors
+        // loop-invariant (a per-step Q base kept the 8 per-MMA descriptor offsets out of
+        // registers: -3.4 % on C5, measured)
+        const uint64_t qa = dq(b, 0), qb = dq(b, 1);
+        for (int32_t j = 0; j + 1 < nT; ++j) {
           const uint32_t vslot = next_full();
           issue_pv(0, vslot, j, gb + j);
-          const bool more = j + 1 < nT;
-          uint64_t qd = dq(b, 0);                       // Q of the S MMAs issued in this step
-          if (!more) {
-            mma_commit_elect(bar(B_OF + 0));
-            mbar_wait(bar(B_QF + nb), ((n + 1) >> 1) & 1);   // the next unit: Q landed
-            tc_fence_after();
-            next = info[nb].live != 0;
-            nT_next = info[nb].nT;
-            qd = dq(nb, 0);
-          }
-          const bool do_s = more || next;
-          if (do_s) {
-            kslot = next_full();
-            issue_s(0, qd, kslot);
-          }
+          kslot = next_full();
+          issue_s(0, qa, kslot);
           issue_pv(1, vslot, j, gb + j);
           mma_commit_elect(bar(B_RE + vslot));
-          if (!more) mma_commit_elect(bar(B_OF + 1));
-          if (do_s) {
-            issue_s(1, qd + (kTileBytes >> 4), kslot);
-            mma_commit_elect(bar(B_RE + kslot));
-          }
+          issue_s(1, qb, kslot);
+          mma_commit_elect(bar(B_RE + kslot));
+        }
+        // last step: the next unit's S MMAs (its Q from the other buffer) take S_0 / S_1's places
+        const int32_t j = nT - 1;
+        const uint32_t vslot = next_full();
+        issue_pv(0, vslot, j, gb + j);
+        mma_commit_elect(bar(B_OF + 0));
+        mbar_wait(bar(B_QF + nb), ((n + 1) >> 1) & 1);   // the next unit: Q landed
+        tc_fence_after();
+        const bool next = info[nb].live != 0;
+        const int32_t nT_next = info[nb].nT;
+        if (next) {
+          kslot = next_full();
+          issue_s(0, dq(nb, 0), kslot);
+        }
+        issue_pv(1, vslot, j, gb + j);
+        mma_commit_elect(bar(B_RE + vslot));
+        mma_commit_elect(bar(B_OF + 1));
+        if (next) {
+          issue_s(1, dq(nb, 1), kslot);
+          mma_commit_elect(bar(B_RE + kslot));
         }
         gb += nT;
         if (!next) break;
@@ -1324,185 +1330,196 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     const uint32_t tS = tmem + lane_off + i * 128;
     const uint32_t tO = tmem + lane_off + TMEM_O + i * 128;
     const float sl2 = p.scale_log2;
-    uint32_t gb = 0;
-    for (uint32_t n = 0;; ++n) {
-      const uint32_t b = n & 1;
-      if (n > 0) mbar_wait(bar(B_QF + b), (n >> 1) & 1);
-      const UnitInfo* u = info + b;
-      if (!u->live) break;
-      // only what the KV loop needs stays in registers across it; the epilogue re-reads the
-      // slot (it is rewritten only after this unit's hand-over to the store warp)
-      const int32_t nT = u->nT, jb = u->jb;
-      int64_t limit;
+    // flat loop over this CTA's KV steps: the hot path has the one-unit kernel's loop shape; a
+    // unit boundary (epilogue, next unit) is the rarely taken tail of the loop body
+    uint32_t gb = 0, n = 0, b = 0;
+    const UnitInfo* u = info;
+    int32_t nT = u->nT, jb = u->jb, j = 0;
+    auto limit_of = [&](const UnitInfo* x) {
+      const int32_t tok0 = x->tok0, n_q = x->n_q;
+      const int32_t tok = tok0 + i * toks + r / G;
+      return (int64_t)(x->q_pos + (tok < n_q ? tok : min(tok0 + 2 * toks, n_q) - 1));
+    };
+    int64_t limit = limit_of(u);
+    float m_run = -INFINITY, l_run = 0.f;
+    for (;;) {
+      mbar_wait(bar(B_SF + i), (gb + j) & 1);
+      tc_fence_after();
       {
-        const int32_t tok0 = u->tok0, n_q = u->n_q;
-        const int32_t tok = tok0 + i * toks + r / G;
-        limit = u->q_pos + (tok < n_q ? tok : min(tok0 + 2 * toks, n_q) - 1);
-      }
-      float m_run = -INFINITY, l_run = 0.f;
-      for (int32_t j = 0; j < nT; ++j) {
-        mbar_wait(bar(B_SF + i), (gb + j) & 1);
-        tc_fence_after();
         const int64_t key0 = (int64_t)(jb + j) * kBN;
         const int64_t vis64 = limit - key0;
         const int32_t vis = (int32_t)(vis64 < -1 ? -1 : (vis64 > kBN ? kBN : vis64));
         softmax_step<false>(tS, tO, j, vis, sl2, m_run, l_run, bar(B_PF + i), bar(B_PH + i),
                             [](uint32_t) {});
       }
+      if (++j < nT) continue;
       gb += nT;
-      // epilogue: full tiles are staged in this unit's Q buffer (free: O_fin covers every S MMA)
-      // for warp 3's TMA store; ragged tiles store their valid rows per thread
-      mbar_wait(bar(B_OF + i), n & 1);
-      tc_fence_after();
-      const int32_t tok0 = u->tok0, n_q = u->n_q, kvh = u->kvh;
-      const int32_t npieces = u->npieces, piece = u->piece, unit = u->unit;
-      const int64_t q_row = u->q_row;
-      const int32_t tok = tok0 + i * toks + r / G;
-      const int32_t hq = kvh * G + r % G;
-      const bool valid = tok < n_q;
-      __nv_bfloat16* orow = p.o + ((q_row + tok) * p.h_q + hq) * (int64_t)kD;
-      const bool tile_full = tok0 + (i + 1) * toks <= n_q;
-      const uint32_t ob = sb + OFF_Q + (b * 2 + i) * kTileBytes;
-      auto put16 = [&](int c, const uint32_t (&w)[8]) {
-        if (tile_full) {
-          const uint32_t row = ob + (uint32_t)(c >> 2) * kAtom + (uint32_t)r * 128;
-          const uint32_t cc = (uint32_t)(c & 3) * 2;
-          st_shared_v4(row + ((cc ^ (r & 7)) << 4), w[0], w[1], w[2], w[3]);
-          st_shared_v4(row + (((cc + 1) ^ (r & 7)) << 4), w[4], w[5], w[6], w[7]);
-        } else if (valid) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
-          dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-          dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-        }
-      };
-      bool staged = false;
-      if (npieces == 1) {
-        const float inv = 1.f / l_run;
-        uint32_t sv[128];
-        tmem_ld32(tO, sv);
-        tmem_ld32(tO + 32, sv + 32);
-        tmem_ld32(tO + 64, sv + 64);
-        tmem_ld32(tO + 96, sv + 96);
-        tmem_wait_ld();
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint32_t w[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            w[e] = pack_bf16(__uint_as_float(sv[16 * c + 2 * e]) * inv, __uint_as_float(sv[16 * c + 2 * e + 1]) * inv);
-          put16(c, w);
-        }
-        staged = tile_full;
-        if (valid && p.lse)
-          p.lse[(q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
-      } else {
-        // split piece: as attn_tc2_kernel (direct merge from TMEM, or publish + last merges)
-        const int32_t su = unit - p.split_begin;
-        float4* ws4 = reinterpret_cast<float4*>(p.ws);
-        auto wsi = [&](int32_t k) { return (((int64_t)su * npieces + k) * 2 + i) * 32 * 128 + r; };
-        auto mli = [&](int32_t k) { return ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * 2; };
-        volatile uint32_t* flag = flags + 4 + b;
-        if (threadIdx.x == 128) {
-          int32_t done;
-          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(done) : "l"(p.ws_cnt + su) : "memory");
-          const uint32_t direct = (p.split_direct && done == npieces - 1) ? 1u : 0u;
-          if (direct) p.ws_cnt[su] = 0;
-          *flag = direct;
-        }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        const bool direct = *flag != 0;
-        bool merge = direct;
-        if (!direct) {
-#pragma unroll 1
+      {
+        // epilogue: full tiles are staged in this unit's Q buffer (free: O_fin covers every S MMA)
+        // for warp 3's TMA store; ragged tiles store their valid rows per thread
+        mbar_wait(bar(B_OF + i), n & 1);
+        tc_fence_after();
+        const int32_t tok0 = u->tok0, n_q = u->n_q, kvh = u->kvh;
+        const int32_t npieces = u->npieces, piece = u->piece, unit = u->unit;
+        const int64_t q_row = u->q_row;
+        const int32_t tok = tok0 + i * toks + r / G;
+        const int32_t hq = kvh * G + r % G;
+        const bool valid = tok < n_q;
+        __nv_bfloat16* orow = p.o + ((q_row + tok) * p.h_q + hq) * (int64_t)kD;
+        const bool tile_full = tok0 + (i + 1) * toks <= n_q;
+        const uint32_t ob = sb + OFF_Q + (b * 2 + i) * kTileBytes;
+        auto put16 = [&](int c, const uint32_t (&w)[8]) {
+          if (tile_full) {
+            const uint32_t row = ob + (uint32_t)(c >> 2) * kAtom + (uint32_t)r * 128;
+            const uint32_t cc = (uint32_t)(c & 3) * 2;
+            st_shared_v4(row + ((cc ^ (r & 7)) << 4), w[0], w[1], w[2], w[3]);
+            st_shared_v4(row + (((cc + 1) ^ (r & 7)) << 4), w[4], w[5], w[6], w[7]);
+          } else if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+            dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          }
+        };
+        bool staged = false;
+        if (npieces == 1) {
+          const float inv = 1.f / l_run;
+          uint32_t sv[128];
+          tmem_ld32(tO, sv);
+          tmem_ld32(tO + 32, sv + 32);
+          tmem_ld32(tO + 64, sv + 64);
+          tmem_ld32(tO + 96, sv + 96);
+          tmem_wait_ld();
+  #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            uint32_t ov[16];
-            tmem_ld16(tO + c * 16, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              __stcg(ws4 + wsi(piece) + (int64_t)(4 * c + e) * 128,
-                     make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
-                                 __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3])));
-          }
-          __stcg(reinterpret_cast<float2*>(p.ws_ml + mli(piece)), make_float2(m_run, l_run));
-          __threadfence();
-          asm volatile("bar.sync 1, 256;" ::: "memory");
-          if (threadIdx.x == 128) {
-            const int32_t old = atomicAdd(p.ws_cnt + su, 1);
-            const uint32_t last = (old == npieces - 1) ? 1u : 0u;
-            if (last) p.ws_cnt[su] = 0;
-            *flag = last;
-          }
-          asm volatile("bar.sync 1, 256;" ::: "memory");
-          merge = *flag != 0;
-          if (merge) __threadfence();
-        }
-        if (merge) {
-          constexpr int kMaxPieces = 8;
-          float mk[kMaxPieces], wk[kMaxPieces];
-          float M = direct ? m_run : -INFINITY;
-#pragma unroll
-          for (int k = 0; k < kMaxPieces; ++k) {
-            mk[k] = -INFINITY;
-            wk[k] = 0.f;
-            if (k < npieces && !(direct && k == piece)) {
-              const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + mli(k)));
-              mk[k] = ml.x;
-              wk[k] = ml.y;
-              M = fmaxf(M, ml.x);
-            }
-          }
-          const float Mu = (M == -INFINITY) ? 0.f : M;
-          float Lsum = 0.f;
-#pragma unroll
-          for (int k = 0; k < kMaxPieces; ++k) {
-            const float l = wk[k];
-            wk[k] = (mk[k] == -INFINITY) ? 0.f : fast_exp2(mk[k] - Mu);
-            Lsum += wk[k] * l;
-          }
-          const float wself = (direct && m_run != -INFINITY) ? fast_exp2(m_run - Mu) : 0.f;
-          if (direct) Lsum += wself * l_run;
-          const float inv = 1.f / Lsum;
-#pragma unroll 1
-          for (int c = 0; c < 8; ++c) {
-            float acc[16];
-            if (direct) {
-              uint32_t ov[16];
-              tmem_ld16(tO + c * 16, ov);
-              tmem_wait_ld();
-#pragma unroll
-              for (int e = 0; e < 16; ++e) acc[e] = wself * __uint_as_float(ov[e]);
-            } else {
-#pragma unroll
-              for (int e = 0; e < 16; ++e) acc[e] = 0.f;
-            }
-#pragma unroll
-            for (int k = 0; k < kMaxPieces; ++k) {
-              if (k < npieces && !(direct && k == piece)) {
-                const float4* src = ws4 + wsi(k) + (int64_t)(4 * c) * 128;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float4 x = __ldcg(src + e * 128);
-                  acc[4 * e] += wk[k] * x.x;
-                  acc[4 * e + 1] += wk[k] * x.y;
-                  acc[4 * e + 2] += wk[k] * x.z;
-                  acc[4 * e + 3] += wk[k] * x.w;
-                }
-              }
-            }
             uint32_t w[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) w[e] = pack_bf16(acc[2 * e] * inv, acc[2 * e + 1] * inv);
+  #pragma unroll
+            for (int e = 0; e < 8; ++e)
+              w[e] = pack_bf16(__uint_as_float(sv[16 * c + 2 * e]) * inv, __uint_as_float(sv[16 * c + 2 * e + 1]) * inv);
             put16(c, w);
           }
           staged = tile_full;
-          if (valid && p.lse) p.lse[(q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
+          if (valid && p.lse)
+            p.lse[(q_row + tok) * p.h_q + hq] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+        } else {
+          // split piece: as attn_tc2_kernel (direct merge from TMEM, or publish + last merges)
+          const int32_t su = unit - p.split_begin;
+          float4* ws4 = reinterpret_cast<float4*>(p.ws);
+          auto wsi = [&](int32_t k) { return (((int64_t)su * npieces + k) * 2 + i) * 32 * 128 + r; };
+          auto mli = [&](int32_t k) { return ((((int64_t)su * npieces + k) * 2 + i) * 128 + r) * 2; };
+          volatile uint32_t* flag = flags + 4 + b;
+          if (threadIdx.x == 128) {
+            int32_t done;
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(done) : "l"(p.ws_cnt + su) : "memory");
+            const uint32_t direct = (p.split_direct && done == npieces - 1) ? 1u : 0u;
+            if (direct) p.ws_cnt[su] = 0;
+            *flag = direct;
+          }
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          const bool direct = *flag != 0;
+          bool merge = direct;
+          if (!direct) {
+  #pragma unroll 1
+            for (int c = 0; c < 8; ++c) {
+              uint32_t ov[16];
+              tmem_ld16(tO + c * 16, ov);
+              tmem_wait_ld();
+  #pragma unroll
+              for (int e = 0; e < 4; ++e)
+                __stcg(ws4 + wsi(piece) + (int64_t)(4 * c + e) * 128,
+                       make_float4(__uint_as_float(ov[4 * e]), __uint_as_float(ov[4 * e + 1]),
+                                   __uint_as_float(ov[4 * e + 2]), __uint_as_float(ov[4 * e + 3])));
+            }
+            __stcg(reinterpret_cast<float2*>(p.ws_ml + mli(piece)), make_float2(m_run, l_run));
+            __threadfence();
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (threadIdx.x == 128) {
+              const int32_t old = atomicAdd(p.ws_cnt + su, 1);
+              const uint32_t last = (old == npieces - 1) ? 1u : 0u;
+              if (last) p.ws_cnt[su] = 0;
+              *flag = last;
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            merge = *flag != 0;
+            if (merge) __threadfence();
+          }
+          if (merge) {
+            constexpr int kMaxPieces = 8;
+            float mk[kMaxPieces], wk[kMaxPieces];
+            float M = direct ? m_run : -INFINITY;
+  #pragma unroll
+            for (int k = 0; k < kMaxPieces; ++k) {
+              mk[k] = -INFINITY;
+              wk[k] = 0.f;
+              if (k < npieces && !(direct && k == piece)) {
+                const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + mli(k)));
+                mk[k] = ml.x;
+                wk[k] = ml.y;
+                M = fmaxf(M, ml.x);
+              }
+            }
+            const float Mu = (M == -INFINITY) ? 0.f : M;
+            float Lsum = 0.f;
+  #pragma unroll
+            for (int k = 0; k < kMaxPieces; ++k) {
+              const float l = wk[k];
+              wk[k] = (mk[k] == -INFINITY) ? 0.f : fast_exp2(mk[k] - Mu);
+              Lsum += wk[k] * l;
+            }
+            const float wself = (direct && m_run != -INFINITY) ? fast_exp2(m_run - Mu) : 0.f;
+            if (direct) Lsum += wself * l_run;
+            const float inv = 1.f / Lsum;
+  #pragma unroll 1
+            for (int c = 0; c < 8; ++c) {
+              float acc[16];
+              if (direct) {
+                uint32_t ov[16];
+                tmem_ld16(tO + c * 16, ov);
+                tmem_wait_ld();
+  #pragma unroll
+                for (int e = 0; e < 16; ++e) acc[e] = wself * __uint_as_float(ov[e]);
+              } else {
+  #pragma unroll
+                for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+              }
+  #pragma unroll
+              for (int k = 0; k < kMaxPieces; ++k) {
+                if (k < npieces && !(direct && k == piece)) {
+                  const float4* src = ws4 + wsi(k) + (int64_t)(4 * c) * 128;
+  #pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float4 x = __ldcg(src + e * 128);
+                    acc[4 * e] += wk[k] * x.x;
+                    acc[4 * e + 1] += wk[k] * x.y;
+                    acc[4 * e + 2] += wk[k] * x.z;
+                    acc[4 * e + 3] += wk[k] * x.w;
+                  }
+                }
+              }
+              uint32_t w[8];
+  #pragma unroll
+              for (int e = 0; e < 8; ++e) w[e] = pack_bf16(acc[2 * e] * inv, acc[2 * e + 1] * inv);
+              put16(c, w);
+            }
+            staged = tile_full;
+            if (valid && p.lse) p.lse[(q_row + tok) * p.h_q + hq] = (M + __log2f(Lsum)) * 0.69314718055994531f;
+          }
         }
+        // hand the tile to the output-store warp (staged or not: the Q buffer is done with)
+        if (staged) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // st.shared -> TMA
+        if (r == 0) flags[b * 2 + i] = staged ? 1u : 0u;
+        asm volatile("bar.arrive %0, 160;" ::"r"(2 + 2 * b + i) : "memory");
       }
-      // hand the tile to the output-store warp (staged or not: the Q buffer is done with)
-      if (staged) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // st.shared -> TMA
-      if (r == 0) flags[b * 2 + i] = staged ? 1u : 0u;
-      asm volatile("bar.arrive %0, 160;" ::"r"(2 + 2 * b + i) : "memory");
+      ++n;
+      b = n & 1;
+      mbar_wait(bar(B_QF + b), (n >> 1) & 1);
+      u = info + b;
+      if (!u->live) break;
+      nT = u->nT;
+      jb = u->jb;
+      limit = limit_of(u);
+      m_run = -INFINITY;
+      l_run = 0.f;
+      j = 0;
     }
   }
   __syncthreads();
