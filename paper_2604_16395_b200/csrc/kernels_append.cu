@@ -50,6 +50,10 @@ __device__ __forceinline__ int32_t find_item(const AppendItemDev* items, int32_t
 #define S2L_APPEND_ROWS 4
 #endif
 constexpr int kRowsPerWarp = S2L_APPEND_ROWS;
+// Wide token rows (more than 4 16-byte vectors per lane, h_kv * d > 1024) go one row per warp,
+// their vectors in chunks of 16 per lane, so the values in flight stay within registers.
+template <int kMaxVecPerLane> constexpr int kRowsFor = kMaxVecPerLane <= 4 ? kRowsPerWarp : 1;
+template <int kMaxVecPerLane> constexpr int kChunkFor = kMaxVecPerLane < 16 ? kMaxVecPerLane : 16;
 
 // 8 bf16 -> 8 E4M3 codes (FP8 KV cache, kv_dtype 1): round to nearest even, saturating to
 // +-448 (reading Z20; the same rule as oracle/fp8.py); low element in the low byte.
@@ -104,43 +108,96 @@ __global__ void __launch_bounds__(256) append_kernel(
   const uint4* src = (kind ? v : k) + (int64_t)(lk >> 1) * kv_rows * h_kv * vec_per_row;
   const int32_t vpt = h_kv * vec_per_row;                 // vectors per token row
   const int32_t kb = 1 << kb_log2;
-  const int64_t row0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * kRowsPerWarp;
-  const int64_t stride_rows = (int64_t)gridDim.x * (blockDim.x >> 5) * kRowsPerWarp;
-  for (int64_t rb = row0; rb < total_rows; rb += stride_rows) {
-    uint4 val[kRowsPerWarp][kMaxVecPerLane];
-    int64_t dst_row[kRowsPerWarp];        // pool vector index of (block, layer, kind, head 0, slot)
-    int64_t src_row[kRowsPerWarp];
-#pragma unroll
-    for (int rr = 0; rr < kRowsPerWarp; ++rr) {
-      const int64_t row = rb + rr;
-      dst_row[rr] = -1;
-      if (row < total_rows) {
-        const AppendItemDev& it = items[find_item(items, n_items, row)];
-        const int64_t t = row - it.row_begin;
-        const int64_t pos = it.nc + t;
-        const int32_t blk = ids[it.id_off + (int32_t)((pos >> kb_log2) - (it.nc >> kb_log2))];
-        const int32_t slot = (int32_t)(pos & (kb - 1));
-        src_row[rr] = (it.kv_row + t) * vpt;
-        dst_row[rr] = ((((int64_t)blk * L + layer) * 2 + kind) * h_kv * kb + slot) * vec_per_row;
-#pragma unroll
+  if constexpr (kMaxVecPerLane <= 4) {
+    // narrow rows (the measured configurations): each row's loads right after its lookup
+    const int64_t row0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * kRowsPerWarp;
+    const int64_t stride_rows = (int64_t)gridDim.x * (blockDim.x >> 5) * kRowsPerWarp;
+    for (int64_t rb = row0; rb < total_rows; rb += stride_rows) {
+      uint4 val[kRowsPerWarp][kMaxVecPerLane];
+      int64_t dst_row[kRowsPerWarp];        // pool vector index of (block, layer, kind, head 0, slot)
+      int64_t src_row[kRowsPerWarp];
+  #pragma unroll
+      for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+        const int64_t row = rb + rr;
+        dst_row[rr] = -1;
+        if (row < total_rows) {
+          const AppendItemDev& it = items[find_item(items, n_items, row)];
+          const int64_t t = row - it.row_begin;
+          const int64_t pos = it.nc + t;
+          const int32_t blk = ids[it.id_off + (int32_t)((pos >> kb_log2) - (it.nc >> kb_log2))];
+          const int32_t slot = (int32_t)(pos & (kb - 1));
+          src_row[rr] = (it.kv_row + t) * vpt;
+          dst_row[rr] = ((((int64_t)blk * L + layer) * 2 + kind) * h_kv * kb + slot) * vec_per_row;
+  #pragma unroll
+          for (int u = 0; u < kMaxVecPerLane; ++u) {
+            const int32_t gi = lane + 32 * u;
+            if (gi < vpt) val[rr][u] = src[src_row[rr] + gi];
+          }
+        }
+      }
+  #pragma unroll
+      for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+        if (dst_row[rr] < 0) continue;
+  #pragma unroll
         for (int u = 0; u < kMaxVecPerLane; ++u) {
           const int32_t gi = lane + 32 * u;
-          if (gi < vpt) val[rr][u] = src[src_row[rr] + gi];
+          if (gi < vpt) {
+            const int32_t vpr = kVpr ? kVpr : vec_per_row;
+            const int32_t head = gi / vpr, vec = gi - head * vpr;
+            const int64_t di = dst_row[rr] + (int64_t)head * kb * vpr + vec;
+            if constexpr (kFp8) reinterpret_cast<uint2*>(pool)[di] = bf16x8_to_e4m3x8(val[rr][u]);
+            else pool[di] = val[rr][u];
+          }
         }
       }
     }
-#pragma unroll
-    for (int rr = 0; rr < kRowsPerWarp; ++rr) {
-      if (dst_row[rr] < 0) continue;
-#pragma unroll
-      for (int u = 0; u < kMaxVecPerLane; ++u) {
-        const int32_t gi = lane + 32 * u;
-        if (gi < vpt) {
-          const int32_t vpr = kVpr ? kVpr : vec_per_row;
-          const int32_t head = gi / vpr, vec = gi - head * vpr;
-          const int64_t di = dst_row[rr] + (int64_t)head * kb * vpr + vec;
-          if constexpr (kFp8) reinterpret_cast<uint2*>(pool)[di] = bf16x8_to_e4m3x8(val[rr][u]);
-          else pool[di] = val[rr][u];
+  } else {
+    constexpr int kRows = kRowsFor<kMaxVecPerLane>, kChunk = kChunkFor<kMaxVecPerLane>;
+    const int64_t row0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * kRows;
+    const int64_t stride_rows = (int64_t)gridDim.x * (blockDim.x >> 5) * kRows;
+    for (int64_t rb = row0; rb < total_rows; rb += stride_rows) {
+      int64_t dst_row[kRows];               // pool vector index of (block, layer, kind, head 0, slot)
+      int64_t src_row[kRows];
+  #pragma unroll
+      for (int rr = 0; rr < kRows; ++rr) {
+        const int64_t row = rb + rr;
+        dst_row[rr] = -1;
+        if (row < total_rows) {
+          const AppendItemDev& it = items[find_item(items, n_items, row)];
+          const int64_t t = row - it.row_begin;
+          const int64_t pos = it.nc + t;
+          const int32_t blk = ids[it.id_off + (int32_t)((pos >> kb_log2) - (it.nc >> kb_log2))];
+          const int32_t slot = (int32_t)(pos & (kb - 1));
+          src_row[rr] = (it.kv_row + t) * vpt;
+          dst_row[rr] = ((((int64_t)blk * L + layer) * 2 + kind) * h_kv * kb + slot) * vec_per_row;
+        }
+      }
+  #pragma unroll
+      for (int c0 = 0; c0 < kMaxVecPerLane; c0 += kChunk) {
+        uint4 val[kRows][kChunk];
+  #pragma unroll
+        for (int rr = 0; rr < kRows; ++rr) {
+          if (dst_row[rr] < 0) continue;
+  #pragma unroll
+          for (int u = 0; u < kChunk; ++u) {
+            const int32_t gi = lane + 32 * (c0 + u);
+            if (gi < vpt) val[rr][u] = src[src_row[rr] + gi];
+          }
+        }
+  #pragma unroll
+        for (int rr = 0; rr < kRows; ++rr) {
+          if (dst_row[rr] < 0) continue;
+  #pragma unroll
+          for (int u = 0; u < kChunk; ++u) {
+            const int32_t gi = lane + 32 * (c0 + u);
+            if (gi < vpt) {
+              const int32_t vpr = kVpr ? kVpr : vec_per_row;
+              const int32_t head = gi / vpr, vec = gi - head * vpr;
+              const int64_t di = dst_row[rr] + (int64_t)head * kb * vpr + vec;
+              if constexpr (kFp8) reinterpret_cast<uint2*>(pool)[di] = bf16x8_to_e4m3x8(val[rr][u]);
+              else pool[di] = val[rr][u];
+            }
+          }
         }
       }
     }
@@ -177,7 +234,8 @@ cudaError_t launch_append_impl(const Geometry& g, const AppendItemDev* items, in
   const int64_t vpt = (int64_t)g.h_kv * vec_per_row;
   int kb_log2 = 0;
   while ((1 << kb_log2) < g.k) ++kb_log2;
-  const int64_t warps = (total_rows + kRowsPerWarp - 1) / kRowsPerWarp;
+  const int32_t rows_per_warp = vpt <= 128 ? kRowsPerWarp : 1;   // kRowsFor of the dispatched MAXV
+  const int64_t warps = (total_rows + rows_per_warp - 1) / rows_per_warp;
   int64_t blocks = (warps + 7) / 8;                  // 8 warps per CTA
   if (blocks < 1) blocks = 1;
   if (blocks > 65535) blocks = 65535;

@@ -124,6 +124,18 @@ def test_tc_gqa_ragged(h_q, h_kv):
     _multi_request_case(P, 77, geo, [517, 300, 129], [[200, 317], [1, 299], [128, 1]])
 
 
+@pytest.mark.parametrize("h_kv,kv_dtype", [(32, 0), (128, 0), (32, 1)])
+def test_append_wide_token_rows(h_kv, kv_dtype):
+    """Token rows wider than 128 16-byte vectors (h_kv * d > 1024: MHA shapes, h_q = h_kv at
+    d = 128) take the append kernel's one-row-per-warp, 16-vectors-per-chunk path
+    (append_kernel<16, 16> for h_kv = 32, <64, 0> for h_kv = 128), bf16 and FP8 pools: ragged
+    chunks of two requests, pool bytes whole and every attention row vs the oracle."""
+    geo = W.Geometry(L=1, h_q=h_kv, h_kv=h_kv, d=128, k=16)
+    P = Pair(1, h_kv, h_kv, 128, 16, 24, 0, max_blocks=12, kv_dtype=kv_dtype)
+    _multi_request_case(P, 313, geo, [161, 45], [[100, 61], [1, 44]])
+    P.check_pools_whole()
+
+
 def test_c2t_crawler_shaped_ragged_chunks():
     """C2t, reduced: Llama-3-8B attention shape, 6 requests whose totals are
     LogNormal(ln 5800, 0.976) draws scaled down to [97, 1500] tokens, each split into U{6..10}
