@@ -654,6 +654,26 @@ def _normwise(got, ref):
     return np.abs(got - ref).max(-1) / np.maximum(np.abs(ref).max(-1), 1e-6)
 
 
+def _guarded(line, key, fn, world):
+    """A side field of the bench line.  With one rank a failure is recorded in the line (error
+    text; traceback on stderr) so the headline fields still print; with several ranks it
+    propagates, since one failing rank would leave the others waiting in a collective.  `fn`
+    returns the field's value, or None when it writes its fields into `line` itself."""
+    if world > 1:
+        v = fn()
+        if v is not None:
+            line[key] = v
+        return
+    try:
+        v = fn()
+        if v is not None:
+            line[key] = v
+    except Exception as e:  # noqa: BLE001 -- reported in the line, not swallowed
+        import traceback
+        traceback.print_exc()
+        line[key + "_error"] = f"{type(e).__name__}: {e}"
+
+
 def c2_breakdown(ctx, S, reps=10):
     """per-step times of the C2 stream (CUDA events around each chunk's append
     + attention on the compute stream), median of `reps` replays; aggregates over the long steps
@@ -1313,14 +1333,14 @@ def main():
 
     # per-step breakdown of the C2 stream (rank 0), long-chunk C5 and update-mode C3 fields
     if rank == 0:
-        line["c2_steps"] = c2_breakdown(ctx, S, reps=10)
-    line["c5"] = c5_field(rank, world, dist, dev_index, pk)
+        _guarded(line, "c2_steps", lambda: c2_breakdown(ctx, S, reps=10), 1)
+    _guarded(line, "c5", lambda: c5_field(rank, world, dist, dev_index, pk), world)
     torch.cuda.empty_cache()
-    line["c3"] = c3_field(rank, world, dist, dev_index, pk)
-    line["c2t"] = c2t_field(rank, world, dist, dev_index, pk)
+    _guarded(line, "c3", lambda: c3_field(rank, world, dist, dev_index, pk), world)
+    _guarded(line, "c2t", lambda: c2t_field(rank, world, dist, dev_index, pk), world)
     torch.cuda.empty_cache()
 
-    if not args.no_side and rank == 0:
+    def side():
         # NEXT-2: the same step through the fused append + attention path (s2l_prefill_append),
         # timed alternately with the plain step so clock drift affects both alike
         ffn = lambda: run_step_fused(ctx, S)
@@ -1375,6 +1395,8 @@ def main():
                           "note": "kv_dtype=1: E4M3 storage, exact f16 dequantisation in shared memory, f16-operand MMAs"}
         ctx8.close()
         del pool8
+    if not args.no_side and rank == 0:
+        _guarded(line, "side_fields", side, 1)     # rank 0 only: no collectives inside
     if rank == 0:
         # the oracle on the host cores (bounded sample), after all device timing
         v, desc, thr = oracle_sample(data)
