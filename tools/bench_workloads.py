@@ -205,7 +205,15 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
     src_q = torch.randn(R, geo_hq, D, generator=g, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(src_q)
     cs, cs_in = torch.cuda.Stream(), torch.cuda.Stream()
+    # C4_PRIO=1: compute (append + attention) on a stream of the highest priority, so the block
+    # scheduler gives SMs freed by attention CTAs to attention before the staged-swap gather /
+    # scatter kernels of the (default-priority) copy streams
+    prio = os.environ.get("C4_PRIO", "0") == "1"
+    if prio:
+        torch.cuda.set_stream(torch.cuda.Stream(priority=-100))
     res = {"workload": "C4 memory-pressure mix (BJ:L10)", "requests": n_req, "L": L, "m_block": mb,
+           "compute_stream_priority": "highest" if prio else "default",
+           "swap_stage": os.environ.get("S2L_SWAP_STAGE", "default"),
            "evict_ahead": int(os.environ.get("C4_AHEAD", "2")), "prefetch_ahead": int(os.environ.get("C4_PREFETCH", "0")),
            "working_set_blocks": ws, "gpu_pool_blocks": ng, "cpu_pool_blocks": ncpu, "budget": budget}
     flops_total = 0.0
