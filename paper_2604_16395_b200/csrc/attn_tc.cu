@@ -158,8 +158,8 @@ static_assert(128 * kRegCtrl + 256 * kRegSoftmax <= kThreads * kRegLaunch, "regi
 // converter warps already load the FMA / ALU pipes of SMSPs 2-3 (A/B in profiles/r02s2)
 template <bool kFp8> constexpr int kPolyPairsPer8 = kFp8 ? S2L_POLY_PAIRS_FP8 : S2L_POLY_PAIRS;
 // Shared-memory layout (bytes from the 1024-aligned base):
-//   bf16 pools: K/V ring of NST 32-KB tiles (K-major / MN-major SW128 images) | Q tiles 0/1 |
-//   FP8 pools: Q tiles 0/1 | converted K/V ring |
+//   K/V ring of NST 32-KB tiles (K-major / MN-major SW128 images; FP8 pools: the converted
+//   f16 tiles) | Q tiles 0/1 |
 //   FP8 pools only: F8ST 16-KB staging slots for the E4M3 tiles TMA brings in (dense
 //   [128 keys][128 d] bytes), converted to the bf16 ring by warps 2-3 | mbarriers | TMEM addr.
 template <bool kFp8>
@@ -170,7 +170,10 @@ struct Lay {
 #ifndef S2L_Q_AFTER_RING
 #define S2L_Q_AFTER_RING 1     // bf16 kernels: K/V ring at the base, Q after it (+0.5 % C2 step, +0.6 % C5
 #endif                         // over Q first, 6 alternating A/B pairs each, profiles/r02s3/ab_placement.txt)
-  static constexpr bool kQLast = S2L_Q_AFTER_RING && !kFp8;
+#ifndef S2L_Q_AFTER_RING_FP8
+#define S2L_Q_AFTER_RING_FP8 1 // the FP8-pool kernel too: +2.4 % FP8 step (6 pairs, ab_placement_fp8.txt)
+#endif
+  static constexpr bool kQLast = kFp8 ? S2L_Q_AFTER_RING_FP8 : S2L_Q_AFTER_RING;
   static constexpr uint32_t OFF_Q0 = kQLast ? NST * kTileBytes : 0, OFF_Q1 = OFF_Q0 + kTileBytes,
                             OFF_RING = kQLast ? 0 : 2 * kTileBytes;
   static constexpr uint32_t OFF_F8 = (2 + NST) * kTileBytes;
