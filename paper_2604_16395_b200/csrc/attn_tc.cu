@@ -50,8 +50,17 @@
 namespace s2l {
 namespace {
 
-constexpr uint32_t TMEM_COLS = 512;                    // S0 [0,128) S1 [128,256) O [256,384)
-constexpr uint32_t TMEM_O = 256;
+constexpr uint32_t TMEM_COLS = 512;
+#ifndef S2L_TMEM_MAP
+#define S2L_TMEM_MAP 0          // experiment: 0 = S0 S1 O0 O1, 1 = S0 O0 S1 O1, 2 = O0 O1 S0 S1
+#endif
+// TMEM columns of tile i's S (P aliases its first 64 columns) and O accumulators
+__host__ __device__ constexpr uint32_t tm_s(int i) {
+  return S2L_TMEM_MAP == 1 ? 256u * i : (S2L_TMEM_MAP == 2 ? 256u + 128u * i : 128u * i);
+}
+__host__ __device__ constexpr uint32_t tm_o(int i) {
+  return S2L_TMEM_MAP == 1 ? 256u * i + 128u : (S2L_TMEM_MAP == 2 ? 128u * i : 256u + 128u * i);
+}
 
 struct TcParams {
   const AttnItemDev* items;
@@ -595,7 +604,7 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
           const uint32_t off = ((kk >> 2) * kAtom + (kk & 3) * 32) >> 4;
-          mma_ss_elect(tmem + i * 128, dq[i] + off, kd + off, idesc_s, kk > 0);
+          mma_ss_elect(tmem + tm_s(i), dq[i] + off, kd + off, idesc_s, kk > 0);
         }
         mma_commit_elect(bar(WB_SF + i));
         if (lane == 0) TRACE(14, i, 0);
@@ -608,14 +617,14 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
         if (lane == 0) TRACE(11, i, j);
 #pragma unroll
         for (int kk = 0; kk < kBN / 32; ++kk)
-          mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
+          mma_ts_elect(tmem + tm_o(i), tmem + tm_s(i) + kk * 8, vd + ((kk * 16 * 128) >> 4),
                        idesc_o, (j > 0 || kk > 0));
         mbar_wait(bar(WB_PH + i), j & 1);               // P keys 64-127
         tc_fence_after();
         if (lane == 0) TRACE(12, i, j);
 #pragma unroll
         for (int kk = kBN / 32; kk < kBN / 16; ++kk)
-          mma_ts_elect(tmem + TMEM_O + i * 128, tmem + i * 128 + kk * 8, vd + ((kk * 16 * 128) >> 4),
+          mma_ts_elect(tmem + tm_o(i), tmem + tm_s(i) + kk * 8, vd + ((kk * 16 * 128) >> 4),
                        idesc_o, 1);
       };
       mbar_wait(bar(kFp8 ? L::B_QC : WB_QF), 0);
@@ -653,8 +662,8 @@ __global__ void __launch_bounds__(v2::kThreads, 1)
     const int i = (warp - 4) >> 2;                   // 0: warps 4-7, 1: warps 8-11
     const int r = (warp & 3) * 32 + lane;            // tile row == TMEM lane
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + lane_off + i * 128;
-    const uint32_t tO = tmem + lane_off + TMEM_O + i * 128;
+    const uint32_t tS = tmem + lane_off + tm_s(i);
+    const uint32_t tO = tmem + lane_off + tm_o(i);
     const int32_t tok = tok0 + i * toks + r / G;
     const int32_t hq = kvh * G + r % G;
     const bool valid = tok < it.n_q;
