@@ -252,6 +252,15 @@ s2l_status s2l_sync(s2l_ctx* ctx);
 /* Number of kernels this context has launched since creation (evidence counter). */
 int64_t s2l_kernel_launches(s2l_ctx* ctx);
 
+/* Evidence counters since creation: cross-stream waits the runtime inserted because the work
+ * they order after was still pending when the call was issued (orderings against finished work
+ * cost nothing and are not counted).  waits[0]: the compute stream after a swap-out D2H (an
+ * append reusing a block the D2H still reads); waits[1]: compute after a swap-in H2D (the
+ * request's K/V, or a reused block, still arriving); waits[2]: a copy stream after compute
+ * (blocks kernels may still use); waits[3]: a copy stream after the other copy stream.
+ * waits: caller-owned array of 4.  Errors: S2L_E_INVAL (NULL ctx or array). */
+s2l_status s2l_wait_counts(s2l_ctx* ctx, int64_t* waits);
+
 /* Per-kernel device timing (for the roofline in bench.py).  s2l_set_timing(ctx, 1) clears
  * and starts a window: every attention / append kernel launch is then bracketed by CUDA
  * events on compute_stream.  s2l_timing_read synchronises compute_stream and returns the

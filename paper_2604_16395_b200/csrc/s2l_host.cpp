@@ -186,6 +186,7 @@ struct s2l_ctx {
   StagingRing ring;
   s2l_status sticky = S2L_OK;
   int64_t launches = 0;
+  int64_t waits[4] = {};              // s2l_wait_counts: inserted cross-stream waits by kind
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> attn_ev, append_ev, ev_pool;
   // Stream hazards (DESIGN.md §5 "Stream hazards"), tracked per request and per block so
@@ -247,6 +248,8 @@ bool ring_wait(s2l_ctx* c, EventRing& R, cudaStream_t st, uint64_t seq) {
     return true;
   }
   if (q != cudaErrorNotReady) return cuda_ok(c, q, "event ring query");
+  const bool on_compute = st == c->compute;
+  ++c->waits[on_compute ? (&R == &c->out_ring ? 0 : 1) : (&R == &c->compute_ring ? 2 : 3)];
   return cuda_ok(c, cudaStreamWaitEvent(st, ev, 0), "event ring wait");
 }
 
@@ -1249,6 +1252,12 @@ s2l_status s2l_sync(s2l_ctx* c) {
 }
 
 int64_t s2l_kernel_launches(s2l_ctx* c) { return c ? c->launches : -1; }
+
+s2l_status s2l_wait_counts(s2l_ctx* c, int64_t* waits) {
+  if (!c || !waits) return fail(S2L_E_INVAL, "ctx or waits is NULL");
+  for (int i = 0; i < 4; ++i) waits[i] = c->waits[i];
+  return S2L_OK;
+}
 
 s2l_status s2l_set_timing(s2l_ctx* c, int32_t enable) {
   if (!c) return fail(S2L_E_INVAL, "ctx is NULL");

@@ -54,7 +54,7 @@ class ReqInfo(C.Structure):
 EXPORTS = ["s2l_block_bytes", "s2l_create", "s2l_create_host_only", "s2l_destroy", "s2l_new_request",
            "s2l_release_request", "s2l_preempt_recompute", "s2l_append_chunk", "s2l_invalidate_lcp",
            "s2l_prefill_batch", "s2l_prefill_append", "s2l_swap_out", "s2l_swap_in", "s2l_query", "s2l_block_table",
-           "s2l_free_blocks", "s2l_sync", "s2l_set_swap_in_stream", "s2l_kernel_launches", "s2l_set_timing", "s2l_timing_read",
+           "s2l_free_blocks", "s2l_sync", "s2l_set_swap_in_stream", "s2l_kernel_launches", "s2l_wait_counts", "s2l_set_timing", "s2l_timing_read",
            "s2l_last_error", "s2l_version"]
 
 _libs: dict = {}
@@ -90,6 +90,7 @@ def lib(path: str | None = None) -> C.CDLL:
         "s2l_sync": (I32, [VP]),
         "s2l_set_swap_in_stream": (I32, [VP, VP]),
         "s2l_kernel_launches": (I64, [VP]),
+        "s2l_wait_counts": (I32, [VP, P(I64)]),
         "s2l_set_timing": (I32, [VP, I32]),
         "s2l_timing_read": (I32, [VP, P(C.c_double), P(I64), P(C.c_double), P(I64)]),
         "s2l_last_error": (C.c_char_p, []),
@@ -258,6 +259,12 @@ class Context:
 
     def kernel_launches(self) -> int:
         return self._L.s2l_kernel_launches(self._h)
+
+    def wait_counts(self) -> dict:
+        """Cross-stream waits the runtime inserted (s2l_wait_counts), by kind."""
+        w = (C.c_int64 * 4)()
+        self._check(self._L.s2l_wait_counts(self._h, w))
+        return dict(compute_on_d2h=w[0], compute_on_h2d=w[1], copy_on_compute=w[2], copy_on_copy=w[3])
 
     def set_timing(self, enable: bool):
         return self._check(self._L.s2l_set_timing(self._h, int(enable)))

@@ -299,6 +299,7 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
         if mode != "warm":
             res[mode] = {"ms": ms, "host_s": host_s, "steps": steps, "tflops": flops[0] / (ms * 1e-3) / 1e12,
                          "compute_busy_ms": busy, "compute_gap_ms": gaps,
+                         "stream_waits": wrap.wait_counts(),
                          "copy_out": {"bytes": cm.get("out", (0, 0))[0], "ms": cm.get("out", (0, 0))[1]},
                          "copy_in": {"bytes": cm.get("in", (0, 0))[0], "ms": cm.get("in", (0, 0))[1]},
                          "tokens": drv.tokens, "tokens_per_s": drv.tokens / (ms * 1e-3),
