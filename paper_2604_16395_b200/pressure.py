@@ -109,7 +109,7 @@ class PressureDriver:
     """
 
     def __init__(self, ctx, plans, k: int, budget: int, evict_ahead: int = 2, cost=None,
-                 prefetch_ahead: int = 0):
+                 prefetch_ahead: int = 0, reserve: int = 0):
         """cost: None -> every victim is swapped (the C4 definition, BJ:L10); else a callable
         cost(num_computed, num_blocks) -> "recompute" | "swap" (the paper's cost-based
         preemption, P:L79 / §4.3): a recompute victim drops its blocks (no D2H) and later
@@ -119,6 +119,10 @@ class PressureDriver:
         # prefetch_ahead: also swap in the CPU-tier requests of the next `prefetch_ahead` steps
         # after sel when the room is already there, so their H2D gets several steps of compute
         self.prefetch_ahead = prefetch_ahead
+        # reserve: free GPU blocks kept beyond the look-ahead's needs (best effort), so that with
+        # the cooling allocation order a step's swap-ins and appends take blocks freed earlier
+        # rather than blocks the previous step's kernels or swap-outs may still be using
+        self.reserve = reserve
         self.prefetched = 0
         self.cost = cost
         self.recompute_preemptions = 0
@@ -244,7 +248,9 @@ class PressureDriver:
                 want += self._need(nxt, info2)
                 keep |= set(nxt)
             self.cursor = saved
-            more = self._pick(want, free_after, keep, set(protect))
+            more = self._pick(want + self.reserve, free_after, keep, set(protect))
+            if more is None and self.reserve:
+                more = self._pick(want, free_after, keep, set(protect))
             if more is not None:
                 victims += more[0]
         if victims and self.cost is not None:

@@ -215,6 +215,7 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
            "compute_stream_priority": "highest" if prio else "default",
            "swap_stage": os.environ.get("S2L_SWAP_STAGE", "default"),
            "evict_ahead": int(os.environ.get("C4_AHEAD", "2")), "prefetch_ahead": int(os.environ.get("C4_PREFETCH", "0")),
+           "reserve_frac": float(os.environ.get("C4_RESERVE", "0")),
            "working_set_blocks": ws, "gpu_pool_blocks": ng, "cpu_pool_blocks": ncpu, "budget": budget}
     flops_total = 0.0
     big = None
@@ -236,7 +237,8 @@ def c4mix(n_req=128, budget=8192, L=None, check=True):
         wrap = pressure.SwapTimer(ctx, serial=(mode == "serial"), copy_stream=cs, swap_in_stream=cs_in)
         drv = pressure.PressureDriver(wrap, plans, K, budget, evict_ahead=int(os.environ.get("C4_AHEAD", "2")),
                                       cost=cost_rule if mode == "overlap_cost" else None,
-                                      prefetch_ahead=int(os.environ.get("C4_PREFETCH", "0")))
+                                      prefetch_ahead=int(os.environ.get("C4_PREFETCH", "0")),
+                                      reserve=int(float(os.environ.get("C4_RESERVE", "0")) * ng))
         step_ev = []
         segs, snaps, flops = {}, [], [0.0]
 
