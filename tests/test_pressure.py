@@ -10,7 +10,7 @@ from synth import workloads as W
 from tests.harness import Twin
 
 
-def _run_host(seed, n_req, lo, hi, budget, frac=0.5, k=16, cost=None, prefetch=0):
+def _run_host(seed, n_req, lo, hi, budget, frac=0.5, k=16, cost=None, prefetch=0, reserve=0):
     plans = pressure.c4_plans(seed, n_req, lo=lo, hi=hi, budget=budget)
     ws = pressure.working_set_blocks(plans, k)
     biggest = max(-(-p.total // k) for p in plans)
@@ -19,7 +19,8 @@ def _run_host(seed, n_req, lo, hi, budget, frac=0.5, k=16, cost=None, prefetch=0
     cfg = s2l.make_config(1, 1, 1, 8, k, ng, nc, max_requests=n_req, max_blocks_per_request=biggest + 1)
     lib = s2l.Context(cfg, host_only=True)
     tw = Twin(lib, k, ng, nc, n_req, biggest + 1)
-    drv = pressure.PressureDriver(tw, plans, k, budget, cost=cost, prefetch_ahead=prefetch)
+    drv = pressure.PressureDriver(tw, plans, k, budget, cost=cost, prefetch_ahead=prefetch,
+                                  reserve=int(reserve * ng))
 
     def execute(sel, app, pre, rows):
         tw.append_chunk(app, None, None, kv_rows=rows)
@@ -44,6 +45,19 @@ def test_driver_bookkeeping_matches_oracle_under_pressure(seed, prefetch):
     # the op log names every library call; swaps in both directions are whole requests
     kinds = {op for op, _, _ in drv.log}
     assert {"new", "append", "prefill", "swap_out", "swap_in", "release", "invalidate"} <= kinds
+
+
+def test_driver_free_block_reserve():
+    """reserve > 0 (C4_RESERVE): the driver keeps extra GPU blocks free beyond the look-ahead's
+    needs (best effort).  Every library call still agrees with the oracle (Twin), all requests
+    finish, and it swaps out at least as many bytes as without the reserve."""
+    _, d0, _, ng, _ = _run_host(11, 24, 64, 1024, 512)
+    _, d1, _, ng1, _ = _run_host(11, 24, 64, 1024, 512, reserve=0.1)
+    assert ng1 == ng
+    assert not d1.live() and not d1.plans
+    assert d1.ctx.lib.free_blocks() == (ng, d1.ctx.ora.num_cpu_blocks)
+    assert d1.swapped_out_bytes >= d0.swapped_out_bytes
+    assert d1.tokens == d0.tokens
 
 
 def test_driver_steps_respect_budget_and_round_robin():
